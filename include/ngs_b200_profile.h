@@ -1,0 +1,55 @@
+/*
+ * ngs_b200_profile.h — measurement hooks of libngs_b200.so (not part of the
+ * reference-facing boundary in ngs_b200.h; used by bench.py).
+ *
+ * When profiling is enabled every kernel launch of the context is bracketed by
+ * CUDA events on the context's stream; ngs_profile_read resolves them into
+ * per-stage device time. Counters (launches, contributing pairs) are always on.
+ */
+#ifndef NGS_B200_PROFILE_H
+#define NGS_B200_PROFILE_H
+
+#include <stdint.h>
+
+#include "ngs_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    NGS_STAGE_PROJECT = 0,     /* K1 */
+    NGS_STAGE_SORT = 1,        /* K2-K5: depth sort, pair emission, tile sort, ranges */
+    NGS_STAGE_RASTER = 2,      /* K6 forward */
+    NGS_STAGE_LOSS = 3,        /* K7 */
+    NGS_STAGE_CONSTS = 4,      /* per-pass per-Gaussian constants */
+    NGS_STAGE_BWD_POSITION = 5,/* K8 */
+    NGS_STAGE_BWD_ROTATION = 6,
+    NGS_STAGE_BWD_SCALING = 7,
+    NGS_STAGE_BWD_OPACITY_COLOR = 8,
+    NGS_STAGE_SOLVE = 9,       /* K9 solves + commits (all attributes) */
+    NGS_STAGE_OTHER = 10,      /* memsets, copies */
+    NGS_STAGE_COUNT = 11
+};
+
+typedef struct {
+    double ms[NGS_STAGE_COUNT];             /* summed device time per stage (profiling on) */
+    int64_t launches[NGS_STAGE_COUNT];      /* kernel launches per stage */
+    int64_t total_launches;                 /* all kernel launches (always counted) */
+    int64_t contrib_pairs[4];               /* contributing (pixel, splat) records per backward pass */
+    int64_t raster_pairs;                   /* (tile, splat) pairs binned, summed over renders */
+    int64_t renders;                        /* view renders */
+} ngs_profile_stats;
+
+int32_t ngs_profile_enable(ngs_context* ctx, int32_t on);
+int32_t ngs_profile_reset(ngs_context* ctx);
+int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out);
+
+/* FP32 FFMA throughput microbenchmark on the context's device (TFLOP/s). */
+int32_t ngs_microbench_fp32(ngs_context* ctx, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NGS_B200_PROFILE_H */

@@ -1,0 +1,50 @@
+// backward.h — K8 backward-pass interface shared by backward.cu and the host.
+#pragma once
+
+#include "context.h"
+
+namespace ngsb {
+
+enum PassId { kPassPosition = 0, kPassRotation = 1, kPassScaling = 2, kPassOpacityColor = 3 };
+
+// Accumulator components per pass (FP64, component-major [c][N]).
+constexpr int kAccPosition = 9;  // grad 3, hess sym (xx, xy, xz, yy, yz, zz)
+constexpr int kAccRotation = 2;  // grad, hess
+constexpr int kAccScaling = 5;   // grad 2, hess (00, 01, 11)
+constexpr int kAccOpColor = 8;   // opacity grad, hess; colour g_acc[3], h_acc[3] (per view)
+
+// Per-(Gaussian, view) constant layouts (floats, AoS per Gaussian).
+constexpr int kPosM = 0;    // 5x3
+constexpr int kPosHu = 15;  // 5 x sym3
+constexpr int kPosJc = 45;  // 3x3 (channel, coord)
+constexpr int kPosHc = 54;  // 3 x sym3
+constexpr int kPosConsts = 72;
+constexpr int kRotConsts = 6;    // s1 (00, 01, 11), s2 (00, 01, 11)
+constexpr int kScaleConsts = 7;  // v0 (2), v1 (2), m00, m01, m11
+
+struct BackwardArgs {
+    int tiles_x, W, H;
+    const int2* ranges;
+    const int* vals;
+    const double2* pix;
+    const float4* ra;
+    const float4* rb;
+    const float4* rc;
+    const double* image;
+    const int* last;
+    const float* loss_grad;
+    const float* loss_hess;
+    const float* consts;
+    float cutoff;
+    float bg[3];
+    double* acc;
+    size_t acc_stride;
+    uint8_t* visible;                    // optional: set to 1 for kernels with >= 1 record
+    unsigned long long* contrib_pairs;   // optional: count of contributing (pixel, splat) records
+};
+
+void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s);
+void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
+                     unsigned long long* contrib_pairs, cudaStream_t s);
+
+}  // namespace ngsb

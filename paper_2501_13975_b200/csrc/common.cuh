@@ -1,0 +1,75 @@
+// common.cuh — shared device/host definitions for the sm_100a 3DGS² Newton path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "ngs_b200.h"
+
+namespace ngsb {
+
+constexpr int kTile = 16;                 // rasterizer.hpp:18 kTileSize
+constexpr int kTilePixels = kTile * kTile;
+constexpr double kNearPlaneEps = 1e-6;    // camera.hpp:11
+constexpr double kSigmaMargin = 1e-4;     // scene.hpp:10
+constexpr double kColorOffset = 0.5;      // sh.hpp:21
+
+// Error carrying an ngs_status; thrown by host code, mapped at the C-ABI edge.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        throw Error(NGS_ERR_CUDA, std::string(what) + " failed at " + file + ":" + std::to_string(line) +
+                                      ": " + cudaGetErrorString(e));
+    }
+}
+#define CUDA_CHECK(x) ::ngsb::cuda_check((x), #x, __FILE__, __LINE__)
+#define CUDA_LAUNCH_CHECK() ::ngsb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Camera constants uploaded per view (camera.hpp:17-45), FP64.
+struct CameraDev {
+    double view[16];       // row-major world->camera
+    double proj[16];       // row-major camera->clip
+    double view_proj[16];  // proj * view
+    double center[3];      // camera position in world space
+    int width, height;
+    int tiles_x, tiles_y;
+};
+
+// Device-side scene, FP32 SoA.
+struct SceneDev {
+    int n;
+    int sh_degree;
+    int n_coeffs;          // (deg+1)^2
+    float bg[3];
+    float4* pos_sigma;     // x, y, z, sigma
+    float4* scale;         // sx, sy, sz, 0
+    float4* quat;          // w, x, y, z
+    float* sh;             // [48][n] coefficient-major: sh[(16*ch + i)*n + k]
+};
+
+// Projected record of one kernel in one view (forward-pass payload), 48 B.
+//   a = (pixel.x, pixel.y, Q00, Q01), b = (Q11, sigma, c0, c1), c = (c2, cov00, cov01, cov11)
+struct ViewRecordsDev {
+    float4* a;
+    float4* b;
+    float4* c;
+    double* depth;         // camera-space depth (FP64, sort key source)
+    int4* rect;            // tile rect [tx0, ty0, tx1, ty1] inclusive; tx0 > tx1 => not binned
+    int* tiles_touched;
+    uint8_t* flags;        // bit0 projected (entry exists), bits1-3 channel clamped
+};
+
+enum RecordFlag : uint8_t { kProjected = 1, kClamp0 = 2, kClamp1 = 4, kClamp2 = 8 };
+
+// ---- small device math -----------------------------------------------------
+
+__host__ __device__ inline double mrow(const double* m, int r, int c) { return m[4 * r + c]; }
+
+}  // namespace ngsb

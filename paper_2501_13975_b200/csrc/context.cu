@@ -1,0 +1,1100 @@
+// context.cu — host side of libngs_b200.so: the C-ABI of include/ngs_b200.h.
+//
+// One ngs_context = one device + one CUDA stream + the FP32 SoA scene +
+// view slots + FP64 accumulators + trainer state. Every entry point maps the
+// reference call it replaces (cited in ngs_b200.h) onto device kernels; no
+// entry point computes on the host except one-time trainer setup (KNN of
+// camera poses, secondary.hpp:24-94) and read-back format conversion.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "backward.h"
+#include "context.h"
+#include "solve.h"
+
+namespace ngsb {
+thread_local Profiler* g_prof = nullptr;
+}
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return NGS_OK;
+    } catch (const ngsb::Error& e) {
+        return set_error(e.code, e.what());
+    } catch (const std::exception& e) {
+        return set_error(NGS_ERR_INTERNAL, e.what());
+    }
+}
+
+constexpr int kScratchSlot = NGS_MAX_VIEW_SLOTS;  // ngs_render's private slot
+
+}  // namespace
+
+using namespace ngsb;
+
+struct TrainerState {
+    bool active = false;
+    ngs_train_config cfg{};
+    std::vector<ngs_camera> cameras;
+    std::vector<ngs_camera> down_cameras;
+    std::vector<int> train_ids, probe_ids;
+    std::vector<std::vector<int>> neighbors;
+    // Targets, planar FP32: device-resident or pinned host (host_targets).
+    std::vector<DevBuf<float>> targets, down_targets;
+    std::vector<float*> host_targets, host_down_targets;
+    double barrier_weight = 1e-4;
+    int step_count = 0;
+    std::vector<ViewSlot> views;  // primary + secondaries of the current step
+    void release() {
+        for (auto& t : targets) t.release();
+        for (auto& t : down_targets) t.release();
+        for (auto* p : host_targets) cudaFreeHost(p);
+        for (auto* p : host_down_targets) cudaFreeHost(p);
+        targets.clear();
+        down_targets.clear();
+        host_targets.clear();
+        host_down_targets.clear();
+        for (auto& v : views) v.release_all();
+        views.clear();
+        active = false;
+    }
+};
+
+struct ngs_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    SceneDev scene{};
+    DevBuf<float4> pos_sigma, scale, quat;
+    DevBuf<float> sh;
+    std::array<ViewSlot, NGS_MAX_VIEW_SLOTS + 1> slots;
+    DevBuf<double> acc;
+    DevBuf<int> err;
+    DevBuf<double> norm;
+    DevBuf<unsigned long long> pairs;
+    DevBuf<uint8_t> visible;
+    DevBuf<double> out_delta;
+    DevBuf<uint8_t> out_flags;
+    TrainerState trainer;
+    Profiler prof;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    unsigned long long contrib_pairs_total = 0;
+
+    ~ngs_context() {
+        for (auto& s : slots) s.release_all();
+        trainer.release();
+        pos_sigma.release();
+        scale.release();
+        quat.release();
+        sh.release();
+        acc.release();
+        err.release();
+        norm.release();
+        pairs.release();
+        visible.release();
+        out_delta.release();
+        out_flags.release();
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void check_err() {
+        int e = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&e, err.ptr, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CUDA_CHECK(cudaStreamSynchronize(stream));
+        if (e) {
+            CUDA_CHECK(cudaMemsetAsync(err.ptr, 0, sizeof(int), stream));
+            if (e & 1) throw Error(NGS_ERR_NUMERICAL, "project_kernel: projected covariance is not positive definite");
+            if (e & 2) throw Error(NGS_ERR_DEGENERATE, "view_direction: point coincides with camera center");
+            if (e & 4) throw Error(NGS_ERR_INVALID_INPUT, "renormalize_quaternion: zero or non-finite quaternion");
+            throw Error(NGS_ERR_NUMERICAL, "device error flag " + std::to_string(e));
+        }
+    }
+
+    ViewSlot& slot(int i) {
+        if (i < 0 || i >= NGS_MAX_VIEW_SLOTS) throw Error(NGS_ERR_INVALID_INPUT, "bad view slot");
+        return slots[i];
+    }
+    ViewSlot& built(int i) {
+        ViewSlot& v = slot(i);
+        if (!v.valid) throw Error(NGS_ERR_INVALID_INPUT, "view slot " + std::to_string(i) + " is empty");
+        return v;
+    }
+    void require_scene() const {
+        if (scene.n < 0) throw Error(NGS_ERR_INVALID_INPUT, "no scene");
+    }
+};
+
+namespace {
+
+// Installs the context's profiler as the calling thread's active one.
+struct ProfInstall {
+    Profiler* prev;
+    explicit ProfInstall(ngs_context* ctx) : prev(g_prof) { g_prof = &ctx->prof; }
+    ~ProfInstall() { g_prof = prev; }
+};
+
+RasterParams to_raster(const ngs_raster_options* o) {
+    ngs_raster_options d;
+    ngs_raster_options_default(&d);
+    if (!o) o = &d;
+    RasterParams r;
+    r.lambda_lp = o->lambda_lp;
+    r.alpha_cutoff = static_cast<float>(o->alpha_cutoff);
+    r.t_min = static_cast<float>(o->t_min);
+    r.cutoff_enabled = o->alpha_cutoff > 0.0;
+    r.radius = r.cutoff_enabled ? std::max(3.0, std::sqrt(2.0 * std::log(1.0 / o->alpha_cutoff))) : 0.0;
+    return r;
+}
+
+LossParams to_loss(const ngs_loss_config* o) {
+    ngs_loss_config d;
+    ngs_loss_config_default(&d);
+    if (!o) o = &d;
+    return LossParams{o->lambda, o->c1, o->c2, o->window, o->window_sigma};
+}
+
+float float_above(double v) {
+    float f = static_cast<float>(v);
+    while (!(static_cast<double>(f) > v)) f = std::nextafter(f, 2.0f);
+    return f;
+}
+float float_below(double v) {
+    float f = static_cast<float>(v);
+    while (!(static_cast<double>(f) < v)) f = std::nextafter(f, -1.0f);
+    return f;
+}
+
+SolveParams to_solve(const ngs_newton_options* o, int commit) {
+    ngs_newton_options d;
+    ngs_newton_options_default(&d);
+    if (!o) o = &d;
+    SolveParams p;
+    p.mu_min = o->mu_min;
+    p.eig_floor_rel = o->eig_floor_rel;
+    p.step_cap_factor = o->step_cap_factor;
+    p.scale_cap_factor = o->scale_cap_factor;
+    p.color_cap = o->color_cap;
+    p.theta_cap = o->theta_cap;
+    p.barrier_weight = o->barrier_weight;
+    p.max_backtrack = o->max_backtrack;
+    p.eigengap_rel = o->eigengap_rel;
+    p.commit = commit;
+    p.sigma_lo = float_above(kSigmaMargin);
+    p.sigma_hi = float_below(1.0 - kSigmaMargin);
+    return p;
+}
+
+// Interleaved double RGB (Image, image.hpp:11-35) <-> planar FP32.
+void interleaved_to_planar(const double* src, int w, int h, std::vector<float>& out) {
+    const size_t n = static_cast<size_t>(w) * h;
+    out.resize(3 * n);
+    for (size_t i = 0; i < n; ++i)
+        for (int c = 0; c < 3; ++c) out[c * n + i] = static_cast<float>(src[3 * i + c]);
+}
+
+template <typename T>
+void download_planar(const T* d_src, int w, int h, double* dst, cudaStream_t s) {
+    const size_t n = static_cast<size_t>(w) * h;
+    std::vector<T> tmp(3 * n);
+    CUDA_CHECK(cudaMemcpyAsync(tmp.data(), d_src, sizeof(T) * 3 * n, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < n; ++i)
+        for (int c = 0; c < 3; ++c) dst[3 * i + c] = tmp[c * n + i];
+}
+
+void validate_host_scene(const ngs_scene* s) {
+    if (!s) throw Error(NGS_ERR_INVALID_INPUT, "null scene");
+    if (s->count < 0) throw Error(NGS_ERR_INVALID_INPUT, "negative kernel count");
+    if (s->sh_degree < 0 || s->sh_degree > 3) throw Error(NGS_ERR_INVALID_INPUT, "sh_degree must be in 0..3");
+    for (int c = 0; c < 3; ++c)
+        if (s->background[c] < 0.0 || s->background[c] > 1.0)
+            throw Error(NGS_ERR_INVALID_INPUT, "background channels must lie in [0,1]");
+    for (int k = 0; k < s->count; ++k) {  // validate_kernel, scene.hpp:82-92
+        const double* q = s->quaternion + 4 * k;
+        const double qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        if (std::abs(qn - 1.0) > 1e-6) throw Error(NGS_ERR_INVALID_INPUT, "kernel quaternion is not unit length");
+        const double* sc = s->scale + 3 * k;
+        if (!(std::min({sc[0], sc[1], sc[2]}) > 0.0)) throw Error(NGS_ERR_INVALID_INPUT, "kernel scale must be positive");
+        if (!(s->sigma[k] > kSigmaMargin) || !(s->sigma[k] < 1.0 - kSigmaMargin))
+            throw Error(NGS_ERR_INVALID_INPUT, "kernel opacity must lie inside (1e-4, 1 - 1e-4)");
+    }
+}
+
+// ---- host-side SH basis (read-back of dense colour terms only) ----------
+void sh_basis_host(double x, double y, double z, int degree, double v[16]) {
+    for (int i = 0; i < 16; ++i) v[i] = 0;
+    v[0] = 0.28209479177387814;
+    if (degree < 1) return;
+    const double k1 = 0.4886025119029199;
+    v[1] = -k1 * y;
+    v[2] = k1 * z;
+    v[3] = -k1 * x;
+    if (degree < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    v[4] = 1.0925484305920792 * x * y;
+    v[5] = -1.0925484305920792 * y * z;
+    v[6] = 0.31539156525252005 * (2 * zz - xx - yy);
+    v[7] = -1.0925484305920792 * x * z;
+    v[8] = 0.5462742152960396 * (xx - yy);
+    if (degree < 3) return;
+    v[9] = -0.5900435899266435 * y * (3 * xx - yy);
+    v[10] = 2.890611442640554 * x * y * z;
+    v[11] = -0.4570457994644658 * y * (4 * zz - xx - yy);
+    v[12] = 0.3731763325901154 * z * (2 * zz - 3 * xx - 3 * yy);
+    v[13] = -0.4570457994644658 * x * (4 * zz - xx - yy);
+    v[14] = 1.445305721320277 * z * (xx - yy);
+    v[15] = -0.5900435899266435 * x * (xx - 3 * yy);
+}
+
+// ---- trainer host setup (secondary.hpp:24-94, image.hpp:39-62) -----------
+
+int clamp_downsample_factor(const ngs_camera& c, int factor) {
+    int f = std::max(1, factor);
+    while (f > 1 && (c.width / f < 16 || c.height / f < 16)) --f;
+    return f;
+}
+
+void box_downsample(const double* src, int w, int h, int f, std::vector<double>& out, int& ow, int& oh) {
+    ow = std::max(1, w / f);
+    oh = std::max(1, h / f);
+    out.assign(3 * static_cast<size_t>(ow) * oh, 0.0);
+    for (int y = 0; y < oh; ++y)
+        for (int x = 0; x < ow; ++x) {
+            double acc[3] = {0, 0, 0};
+            int count = 0;
+            for (int dy = 0; dy < f; ++dy)
+                for (int dx = 0; dx < f; ++dx) {
+                    const int sx = x * f + dx, sy = y * f + dy;
+                    if (sx < w && sy < h) {
+                        for (int c = 0; c < 3; ++c) acc[c] += src[3 * (static_cast<size_t>(sy) * w + sx) + c];
+                        ++count;
+                    }
+                }
+            for (int c = 0; c < 3; ++c) out[3 * (static_cast<size_t>(y) * ow + x) + c] = acc[c] / count;
+        }
+}
+
+void camera_center(const ngs_camera& c, double out[3]) {
+    CameraDev cd;
+    upload_camera(c, cd);
+    for (int i = 0; i < 3; ++i) out[i] = cd.center[i];
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+
+extern "C" {
+
+int32_t ngs_abi_version(void) { return NGS_ABI_VERSION; }
+const char* ngs_backend(void) { return "cuda-sm_100a"; }
+const char* ngs_last_error(void) { return g_last_error.c_str(); }
+
+void ngs_raster_options_default(ngs_raster_options* out) { *out = {0.3, 1e-4, 1e-4, 1, 1}; }
+void ngs_raster_options_reference(ngs_raster_options* out) { *out = {0.3, 0.0, 0.0, 0, 1}; }
+void ngs_loss_config_default(ngs_loss_config* out) { *out = {0.2, 0.01 * 0.01, 0.03 * 0.03, 11, 1.5}; }
+void ngs_newton_options_default(ngs_newton_options* out) {
+    *out = {1e-8, 5e-2, 1.0, 2.0, 1.0, M_PI / 2, 1e-4, 8, 1e-6};
+}
+void ngs_train_config_default(ngs_train_config* out) {
+    std::memset(out, 0, sizeof(*out));
+    for (int i = 0; i < 5; ++i) out->order[i] = i;
+    out->epochs = 1;
+    out->seed = 0;
+    out->knn = 3;
+    out->secondary_downsample = 4;
+    out->threads = 1;
+    out->barrier_decay = 0.5;
+    out->barrier_floor = 1e-6;
+    ngs_newton_options_default(&out->newton);
+    ngs_raster_options_default(&out->raster);
+    ngs_loss_config_default(&out->loss);
+    out->host_targets = 0;
+}
+
+int32_t ngs_context_create(int32_t device, ngs_context** out) {
+    return guarded([&] {
+        int count = 0;
+        CUDA_CHECK(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) throw Error(NGS_ERR_CUDA, "no such CUDA device");
+        CUDA_CHECK(cudaSetDevice(device));
+        auto ctx = std::make_unique<ngs_context>();
+        ctx->device = device;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaEventCreate(&ctx->ev0));
+        CUDA_CHECK(cudaEventCreate(&ctx->ev1));
+        ctx->err.ensure(1);
+        ctx->norm.ensure(1);
+        ctx->pairs.ensure(4);
+        CUDA_CHECK(cudaMemsetAsync(ctx->err.ptr, 0, sizeof(int), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 4 * sizeof(unsigned long long), ctx->stream));
+        ctx->scene.n = 0;
+        ctx->scene.sh_degree = 0;
+        ctx->scene.n_coeffs = 1;
+        *out = ctx.release();
+    });
+}
+
+int32_t ngs_context_destroy(ngs_context* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        delete ctx;
+    });
+}
+
+int32_t ngs_set_scene(ngs_context* ctx, const ngs_scene* s) {
+    return guarded([&] {
+        validate_host_scene(s);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        const int n = s->count;
+        std::vector<float4> ps(n), sc(n), q(n);
+        std::vector<float> sh(48 * static_cast<size_t>(n));
+        for (int k = 0; k < n; ++k) {
+            ps[k] = make_float4(s->position[3 * k], s->position[3 * k + 1], s->position[3 * k + 2], s->sigma[k]);
+            sc[k] = make_float4(s->scale[3 * k], s->scale[3 * k + 1], s->scale[3 * k + 2], 0.f);
+            q[k] = make_float4(s->quaternion[4 * k], s->quaternion[4 * k + 1], s->quaternion[4 * k + 2],
+                               s->quaternion[4 * k + 3]);
+            for (int c = 0; c < 48; ++c) sh[static_cast<size_t>(c) * n + k] = static_cast<float>(s->sh[48 * k + c]);
+        }
+        ctx->pos_sigma.ensure(std::max(n, 1));
+        ctx->scale.ensure(std::max(n, 1));
+        ctx->quat.ensure(std::max(n, 1));
+        ctx->sh.ensure(48 * static_cast<size_t>(std::max(n, 1)));
+        if (n > 0) {
+            CUDA_CHECK(cudaMemcpyAsync(ctx->pos_sigma.ptr, ps.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, ctx->stream));
+            CUDA_CHECK(cudaMemcpyAsync(ctx->scale.ptr, sc.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, ctx->stream));
+            CUDA_CHECK(cudaMemcpyAsync(ctx->quat.ptr, q.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, ctx->stream));
+            CUDA_CHECK(cudaMemcpyAsync(ctx->sh.ptr, sh.data(), sizeof(float) * sh.size(), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        SceneDev& d = ctx->scene;
+        d.n = n;
+        d.sh_degree = s->sh_degree;
+        d.n_coeffs = (s->sh_degree + 1) * (s->sh_degree + 1);
+        for (int c = 0; c < 3; ++c) d.bg[c] = static_cast<float>(s->background[c]);
+        d.pos_sigma = ctx->pos_sigma.ptr;
+        d.scale = ctx->scale.ptr;
+        d.quat = ctx->quat.ptr;
+        d.sh = ctx->sh.ptr;
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        for (auto& v : ctx->slots) v.valid = false;
+    });
+}
+
+int32_t ngs_get_scene_info(ngs_context* ctx, int32_t* count, int32_t* sh_degree) {
+    return guarded([&] {
+        *count = ctx->scene.n;
+        *sh_degree = ctx->scene.sh_degree;
+    });
+}
+
+int32_t ngs_get_scene(ngs_context* ctx, ngs_scene* s) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        const int n = ctx->scene.n;
+        if (s->count != n) throw Error(NGS_ERR_INVALID_INPUT, "ngs_get_scene: count mismatch");
+        std::vector<float4> ps(n), sc(n), q(n);
+        std::vector<float> sh(48 * static_cast<size_t>(n));
+        if (n > 0) {
+            CUDA_CHECK(cudaMemcpyAsync(ps.data(), ctx->pos_sigma.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_CHECK(cudaMemcpyAsync(sc.data(), ctx->scale.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_CHECK(cudaMemcpyAsync(q.data(), ctx->quat.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_CHECK(cudaMemcpyAsync(sh.data(), ctx->sh.ptr, sizeof(float) * sh.size(), cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        }
+        s->sh_degree = ctx->scene.sh_degree;
+        for (int c = 0; c < 3; ++c) s->background[c] = ctx->scene.bg[c];
+        for (int k = 0; k < n; ++k) {
+            if (s->position) {
+                s->position[3 * k] = ps[k].x;
+                s->position[3 * k + 1] = ps[k].y;
+                s->position[3 * k + 2] = ps[k].z;
+            }
+            if (s->sigma) s->sigma[k] = ps[k].w;
+            if (s->scale) {
+                s->scale[3 * k] = sc[k].x;
+                s->scale[3 * k + 1] = sc[k].y;
+                s->scale[3 * k + 2] = sc[k].z;
+            }
+            if (s->quaternion) {
+                s->quaternion[4 * k] = q[k].x;
+                s->quaternion[4 * k + 1] = q[k].y;
+                s->quaternion[4 * k + 2] = q[k].z;
+                s->quaternion[4 * k + 3] = q[k].w;
+            }
+            if (s->sh)
+                for (int c = 0; c < 48; ++c) s->sh[48 * k + c] = sh[static_cast<size_t>(c) * n + k];
+        }
+    });
+}
+
+int32_t ngs_render(ngs_context* ctx, const ngs_camera* camera, const ngs_raster_options* options, double* rgb_out) {
+    return guarded([&] {
+        ProfInstall pi(ctx);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ViewSlot& v = ctx->slots[kScratchSlot];
+        upload_camera(*camera, v.cam);
+        v.raster = to_raster(options);
+        render_view(ctx->scene, v, false, ctx->err.ptr, ctx->stream);
+        ctx->check_err();
+        download_planar(v.image.ptr, v.W, v.H, rgb_out, ctx->stream);
+    });
+}
+
+int32_t ngs_build_view(ngs_context* ctx, int32_t slot, const ngs_camera* camera, const double* target_rgb,
+                       const ngs_raster_options* raster, const ngs_loss_config* loss, double* loss_value) {
+    return guarded([&] {
+        ProfInstall pi(ctx);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ViewSlot& v = ctx->slot(slot);
+        v.valid = false;
+        upload_camera(*camera, v.cam);
+        v.raster = to_raster(raster);
+        v.loss = to_loss(loss);
+        const size_t npx = static_cast<size_t>(camera->width) * camera->height;
+        std::vector<float> tgt;
+        interleaved_to_planar(target_rgb, camera->width, camera->height, tgt);
+        v.target.ensure(3 * npx);
+        CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, tgt.data(), sizeof(float) * 3 * npx, cudaMemcpyHostToDevice, ctx->stream));
+        render_view(ctx->scene, v, true, ctx->err.ptr, ctx->stream);
+        compute_loss(v, ctx->stream);
+        double sums[2];
+        CUDA_CHECK(cudaMemcpyAsync(sums, v.loss_sums.ptr, sizeof(sums), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->check_err();
+        const double inv3n = 1.0 / (3.0 * static_cast<double>(npx));
+        v.loss_l2 = 0.5 * inv3n * sums[0];
+        v.loss_ssim_sum = sums[1];
+        v.loss_value = v.loss_l2 + (v.loss.lambda != 0.0 ? v.loss.lambda * (1.0 - sums[1] * inv3n) : 0.0);
+        if (loss_value) *loss_value = v.loss_value;
+    });
+}
+
+int32_t ngs_get_view_info(ngs_context* ctx, int32_t slot, ngs_view_info* out) {
+    return guarded([&] {
+        ViewSlot& v = ctx->built(slot);
+        std::vector<uint8_t> flags(v.n);
+        if (v.n > 0) {
+            CUDA_CHECK(cudaMemcpyAsync(flags.data(), v.flags.ptr, v.n, cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        }
+        out->width = v.W;
+        out->height = v.H;
+        out->tiles_x = v.cam.tiles_x;
+        out->tiles_y = v.cam.tiles_y;
+        out->entries = static_cast<int32_t>(std::count_if(flags.begin(), flags.end(), [](uint8_t f) { return f & kProjected; }));
+        out->pairs = v.pairs;
+    });
+}
+
+int32_t ngs_view_splats(ngs_context* ctx, int32_t slot, ngs_splat_list* out) {
+    return guarded([&] {
+        ViewSlot& v = ctx->built(slot);
+        const int n = v.n;
+        std::vector<int> order(n);
+        std::vector<uint8_t> flags(n);
+        std::vector<double> e64(static_cast<size_t>(kEntry64) * n), depth(n);
+        std::vector<int2> ranges(v.T);
+        std::vector<int> vals(v.pairs);
+        cudaStream_t s = ctx->stream;
+        if (n > 0) {
+            CUDA_CHECK(cudaMemcpyAsync(order.data(), v.order.ptr, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(flags.data(), v.flags.ptr, n, cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(e64.data(), v.entry64.ptr, sizeof(double) * e64.size(), cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(depth.data(), v.depth.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        }
+        CUDA_CHECK(cudaMemcpyAsync(ranges.data(), v.ranges.ptr, sizeof(int2) * v.T, cudaMemcpyDeviceToHost, s));
+        if (v.pairs > 0)
+            CUDA_CHECK(cudaMemcpyAsync(vals.data(), v.pair_val_sorted.ptr, sizeof(int) * v.pairs, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        std::vector<int> entry_of(n, -1);
+        int e = 0;
+        for (int r = 0; r < n; ++r) {
+            const int k = order[r];
+            if (!(flags[k] & kProjected)) continue;
+            entry_of[k] = e;
+            const double* d = e64.data() + static_cast<size_t>(kEntry64) * k;
+            if (out->kernel) out->kernel[e] = k;
+            if (out->pixel) {
+                out->pixel[2 * e] = d[0];
+                out->pixel[2 * e + 1] = d[1];
+            }
+            if (out->depth) out->depth[e] = depth[k];
+            if (out->cov2d) {
+                out->cov2d[4 * e] = d[2];
+                out->cov2d[4 * e + 1] = d[3];
+                out->cov2d[4 * e + 2] = d[3];
+                out->cov2d[4 * e + 3] = d[4];
+            }
+            for (int c = 0; c < 3; ++c) {
+                if (out->view_color) out->view_color[3 * e + c] = d[9 + c];
+                if (out->clamped) out->clamped[3 * e + c] = (flags[k] & (kClamp0 << c)) ? 1 : 0;
+            }
+            if (out->bbox)
+                for (int i = 0; i < 4; ++i) out->bbox[4 * e + i] = d[5 + i];
+            ++e;
+        }
+        if (out->tile_offsets) {
+            int off = 0;
+            for (int t = 0; t < v.T; ++t) {
+                out->tile_offsets[t] = off;
+                off += ranges[t].y - ranges[t].x;
+            }
+            out->tile_offsets[v.T] = off;
+        }
+        if (out->tile_indices) {
+            int o = 0;
+            for (int t = 0; t < v.T; ++t)
+                for (int i = ranges[t].x; i < ranges[t].y; ++i) out->tile_indices[o++] = entry_of[vals[i]];
+        }
+    });
+}
+
+int32_t ngs_view_image(ngs_context* ctx, int32_t slot, double* rgb_out) {
+    return guarded([&] {
+        ViewSlot& v = ctx->built(slot);
+        download_planar(v.image.ptr, v.W, v.H, rgb_out, ctx->stream);
+    });
+}
+
+int32_t ngs_view_loss_derivs(ngs_context* ctx, int32_t slot, double* grad_out, double* hess_out) {
+    return guarded([&] {
+        ViewSlot& v = ctx->built(slot);
+        if (grad_out) download_planar(v.loss_grad.ptr, v.W, v.H, grad_out, ctx->stream);
+        if (hess_out) download_planar(v.loss_hess.ptr, v.W, v.H, hess_out, ctx->stream);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+int pass_of(int attr) {
+    switch (attr) {
+        case NGS_POSITION: return kPassPosition;
+        case NGS_ROTATION: return kPassRotation;
+        case NGS_SCALING: return kPassScaling;
+        default: return kPassOpacityColor;
+    }
+}
+
+int acc_components(int pass) {
+    switch (pass) {
+        case kPassPosition: return kAccPosition;
+        case kPassRotation: return kAccRotation;
+        case kPassScaling: return kAccScaling;
+        default: return kAccOpColor;
+    }
+}
+
+// Zero the accumulators and run one backward pass over views[0..nv).
+// Opacity/colour keep per-view accumulators (colour needs each view's phi).
+void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv, uint8_t* visible) {
+    const int n = ctx->scene.n;
+    const size_t stride = static_cast<size_t>(std::max(n, 1));
+    const int comps = acc_components(pass) * (pass == kPassOpacityColor ? nv : 1);
+    ctx->acc.ensure(stride * comps);
+    CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
+    for (int i = 0; i < nv; ++i) {
+        ViewSlot& v = *views[i];
+        compute_pass_consts(pass, ctx->scene, v, views[0]->cam, ctx->stream);
+        double* acc = ctx->acc.ptr + (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0);
+        launch_backward(pass, ctx->scene, v, acc, stride, visible, ctx->pairs.ptr + pass, ctx->stream);
+    }
+}
+
+ColorViews color_views(ViewSlot* const* views, int nv) {
+    if (nv > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "at most 8 views per Newton step are supported");
+    ColorViews cv{};
+    cv.n_views = nv;
+    for (int i = 0; i < nv; ++i) {
+        cv.cam[i] = views[i]->cam;
+        cv.flags[i] = views[i]->flags.ptr;
+    }
+    return cv;
+}
+
+std::vector<ViewSlot*> gather_views(ngs_context* ctx, int primary, const int32_t* secs, int nsec) {
+    std::vector<ViewSlot*> v{&ctx->built(primary)};
+    for (int i = 0; i < nsec; ++i) v.push_back(&ctx->built(secs[i]));
+    for (ViewSlot* s : v)
+        if (s->n != ctx->scene.n) throw Error(NGS_ERR_INVALID_INPUT, "view was built for a different scene");
+    return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ngs_accumulate(ngs_context* ctx, ngs_attribute attr, int32_t primary_slot, const int32_t* secondary_slots,
+                       int32_t n_secondary, const ngs_newton_options* options, ngs_terms* out) {
+    return guarded([&] {
+        ProfInstall pi(ctx);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        (void)options;
+        const auto views = gather_views(ctx, primary_slot, secondary_slots, n_secondary);
+        const int nv = static_cast<int>(views.size());
+        const int n = ctx->scene.n;
+        const size_t stride = static_cast<size_t>(std::max(n, 1));
+        const int pass = pass_of(attr);
+        ctx->visible.ensure(stride);
+        CUDA_CHECK(cudaMemsetAsync(ctx->visible.ptr, 0, stride, ctx->stream));
+        accumulate_pass(ctx, pass, views.data(), nv, ctx->visible.ptr);
+        const int comps = acc_components(pass) * (pass == kPassOpacityColor ? nv : 1);
+        std::vector<double> acc(stride * comps);
+        std::vector<uint8_t> vis(stride);
+        CUDA_CHECK(cudaMemcpyAsync(acc.data(), ctx->acc.ptr, sizeof(double) * acc.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(vis.data(), ctx->visible.ptr, stride, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->check_err();
+        auto A = [&](int c, int k) { return acc[static_cast<size_t>(c) * stride + k]; };
+        if (out->visible)
+            for (int k = 0; k < n; ++k) out->visible[k] = vis[k];
+        switch (attr) {
+            case NGS_POSITION:
+                for (int k = 0; k < n; ++k)
+                    for (int i = 0; i < 3; ++i) {
+                        if (out->grad) out->grad[3 * k + i] = A(i, k);
+                        for (int j = 0; j < 3; ++j)
+                            if (out->hess) {
+                                const int a = std::min(i, j), b = std::max(i, j);
+                                const int q = a == 0 ? b : (a == 1 ? 2 + b : 5);
+                                out->hess[9 * k + 3 * i + j] = A(3 + q, k);
+                            }
+                    }
+                break;
+            case NGS_ROTATION:
+            case NGS_OPACITY:
+                for (int k = 0; k < n; ++k) {
+                    double g = 0, h = 0;
+                    const int reps = (attr == NGS_OPACITY) ? nv : 1;
+                    const int comp_stride = (attr == NGS_OPACITY) ? kAccOpColor : 0;
+                    for (int v = 0; v < reps; ++v) {
+                        g += A(v * comp_stride + 0, k);
+                        h += A(v * comp_stride + 1, k);
+                    }
+                    if (out->grad) out->grad[k] = g;
+                    if (out->hess) out->hess[k] = h;
+                }
+                break;
+            case NGS_SCALING:
+                for (int k = 0; k < n; ++k) {
+                    if (out->grad) {
+                        out->grad[2 * k] = A(0, k);
+                        out->grad[2 * k + 1] = A(1, k);
+                    }
+                    if (out->hess) {
+                        out->hess[4 * k] = A(2, k);
+                        out->hess[4 * k + 1] = A(3, k);
+                        out->hess[4 * k + 2] = A(3, k);
+                        out->hess[4 * k + 3] = A(4, k);
+                    }
+                }
+                break;
+            case NGS_COLOR: {
+                // Dense per-channel terms from the compact per-view accumulators
+                // (color_terms newton.hpp:568-572): grad = g_acc phi, hess = h_acc phi phi^T.
+                std::vector<float4> ps(n);
+                std::vector<uint8_t> flags(static_cast<size_t>(nv) * n);
+                if (n > 0) {
+                    CUDA_CHECK(cudaMemcpy(ps.data(), ctx->pos_sigma.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+                    for (int v = 0; v < nv; ++v)
+                        CUDA_CHECK(cudaMemcpy(flags.data() + static_cast<size_t>(v) * n, views[v]->flags.ptr, n,
+                                              cudaMemcpyDeviceToHost));
+                }
+                const int nsh = ctx->scene.n_coeffs;
+                for (int k = 0; k < n; ++k) {
+                    double g[3][16] = {}, h[3][16][16] = {};
+                    for (int v = 0; v < nv; ++v) {
+                        const uint8_t f = flags[static_cast<size_t>(v) * n + k];
+                        if (!(f & kProjected)) continue;
+                        const double* c = views[v]->cam.center;
+                        double u[3] = {ps[k].x - c[0], ps[k].y - c[1], ps[k].z - c[2]};
+                        const double nr = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+                        double phi[16];
+                        sh_basis_host(u[0] / nr, u[1] / nr, u[2] / nr, ctx->scene.sh_degree, phi);
+                        for (int ch = 0; ch < 3; ++ch) {
+                            if (f & (kClamp0 << ch)) continue;
+                            const double ga = A(v * kAccOpColor + 2 + ch, k), ha = A(v * kAccOpColor + 5 + ch, k);
+                            for (int i = 0; i < nsh; ++i) {
+                                g[ch][i] += ga * phi[i];
+                                for (int j = 0; j < nsh; ++j) h[ch][i][j] += ha * phi[i] * phi[j];
+                            }
+                        }
+                    }
+                    for (int ch = 0; ch < 3; ++ch)
+                        for (int i = 0; i < 16; ++i) {
+                            if (out->grad) out->grad[48 * static_cast<size_t>(k) + 16 * ch + i] = g[ch][i];
+                            if (out->hess)
+                                for (int j = 0; j < 16; ++j)
+                                    out->hess[768 * static_cast<size_t>(k) + 256 * ch + 16 * i + j] = h[ch][i][j];
+                        }
+                }
+                break;
+            }
+        }
+    });
+}
+
+int32_t ngs_newton_step(ngs_context* ctx, ngs_attribute attr, int32_t primary_slot, const int32_t* secondary_slots,
+                        int32_t n_secondary, const ngs_newton_options* options, int32_t commit,
+                        ngs_solve_result* out) {
+    return guarded([&] {
+        ProfInstall pi(ctx);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (ctx->trainer.active && commit) {
+            // The trainer shares this context's scene; direct commits are allowed (as on the reference the
+            // caller owns the scene), but the trainer state is left untouched.
+        }
+        const auto views = gather_views(ctx, primary_slot, secondary_slots, n_secondary);
+        const int nv = static_cast<int>(views.size());
+        const int n = ctx->scene.n;
+        const size_t stride = static_cast<size_t>(std::max(n, 1));
+        const int pass = pass_of(attr);
+        accumulate_pass(ctx, pass, views.data(), nv, nullptr);
+        const SolveParams sp = to_solve(options, commit);
+        const int dsz = (attr == NGS_COLOR) ? 48 : (attr == NGS_POSITION || attr == NGS_SCALING) ? 3 : 1;
+        ctx->out_delta.ensure(stride * dsz);
+        ctx->out_flags.ensure(2 * stride);
+        SolveOutputs so{ctx->out_delta.ptr, ctx->out_flags.ptr, ctx->out_flags.ptr + stride, ctx->norm.ptr, ctx->err.ptr};
+        CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, sizeof(double), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->out_flags.ptr, 0, 2 * stride, ctx->stream));
+        launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
+                     color_views(views.data(), nv), sp, ctx->acc.ptr, stride, so, ctx->stream);
+        std::vector<double> delta(stride * dsz);
+        std::vector<uint8_t> fl(2 * stride);
+        double nsq = 0;
+        CUDA_CHECK(cudaMemcpyAsync(delta.data(), ctx->out_delta.ptr, sizeof(double) * delta.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(fl.data(), ctx->out_flags.ptr, fl.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(&nsq, ctx->norm.ptr, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->check_err();
+        if (out) {
+            if (out->delta) std::memcpy(out->delta, delta.data(), sizeof(double) * static_cast<size_t>(n) * dsz);
+            if (out->accepted) std::memcpy(out->accepted, fl.data(), n);
+            if (out->degenerate) std::memcpy(out->degenerate, fl.data() + stride, n);
+            out->delta_norm_sq = nsq;
+        }
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Trainer (trainer.hpp:128-175 setup, 299-417 newton_step)
+// ---------------------------------------------------------------------------
+
+int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32_t n_cameras,
+                              const ngs_camera* cameras, const double* const* targets, int32_t n_train,
+                              const int32_t* train_ids, int32_t n_probe, const int32_t* probe_ids,
+                              const double* const* secondary_targets, int32_t secondary_targets_downsample) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        // TrainConfig::validate, trainer.hpp:78-87
+        bool seen[5] = {};
+        for (int i = 0; i < 5; ++i) {
+            if (c->order[i] < 0 || c->order[i] > 4) throw Error(NGS_ERR_INVALID_INPUT, "train config: bad attribute");
+            seen[c->order[i]] = true;
+        }
+        for (bool s : seen)
+            if (!s) throw Error(NGS_ERR_INVALID_INPUT, "train config: order must be a permutation of all five");
+        if (c->epochs < 0) throw Error(NGS_ERR_INVALID_INPUT, "train config: epochs must be >= 0");
+        if (c->knn < 0) throw Error(NGS_ERR_INVALID_INPUT, "train config: knn must be >= 0");
+        if (n_cameras <= 0) throw Error(NGS_ERR_INVALID_INPUT, "trainer: dataset has no cameras");
+        if (n_train <= 0) throw Error(NGS_ERR_INVALID_INPUT, "trainer: no training views");
+        if (ctx->scene.n <= 0) throw Error(NGS_ERR_INVALID_INPUT, "fit_bounding_sphere: empty scene");
+        if (1 + c->knn > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "knn > 7 unsupported");
+        TrainerState& T = ctx->trainer;
+        T.release();
+        T.cfg = *c;
+        T.cameras.assign(cameras, cameras + n_cameras);
+        T.train_ids.assign(train_ids, train_ids + n_train);
+        T.probe_ids.assign(probe_ids, probe_ids + std::max(n_probe, 0));
+        T.barrier_weight = c->newton.barrier_weight;
+        T.step_count = 0;
+        // fit_bounding_sphere (secondary.hpp:24-36) over the current kernel centres.
+        const int n = ctx->scene.n;
+        std::vector<float4> ps(n);
+        CUDA_CHECK(cudaMemcpy(ps.data(), ctx->pos_sigma.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+        double ctr[3] = {0, 0, 0};
+        for (int k = 0; k < n; ++k) {
+            ctr[0] += ps[k].x;
+            ctr[1] += ps[k].y;
+            ctr[2] += ps[k].z;
+        }
+        for (double& v : ctr) v /= n;
+        double maxd = 0;
+        for (int k = 0; k < n; ++k) {
+            const double dx = ps[k].x - ctr[0], dy = ps[k].y - ctr[1], dz = ps[k].z - ctr[2];
+            maxd = std::max(maxd, std::sqrt(dx * dx + dy * dy + dz * dz));
+        }
+        const double radius = maxd > 0 ? 1.05 * maxd : 1.0;
+        // knn_views (secondary.hpp:61-81) over the training cameras.
+        auto sphere_dir = [&](const ngs_camera& cam, double out[3]) {
+            double cc[3];
+            camera_center(cam, cc);
+            double d[3] = {cc[0] - ctr[0], cc[1] - ctr[1], cc[2] - ctr[2]};
+            const double nn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+            if (!(nn > 1e-12)) throw Error(NGS_ERR_DEGENERATE, "sphere_direction: camera at the sphere center");
+            for (int i = 0; i < 3; ++i) out[i] = d[i] / nn;
+        };
+        T.neighbors.assign(n_cameras, {});
+        if (c->knn > 0 && n_train >= 2) {
+            std::vector<std::array<double, 3>> dirs(n_train);
+            for (int i = 0; i < n_train; ++i) sphere_dir(cameras[train_ids[i]], dirs[i].data());
+            for (int t = 0; t < n_train; ++t) {
+                std::vector<std::pair<double, int>> dist;
+                for (int j = 0; j < n_train; ++j) {
+                    if (j == t) continue;
+                    const double d = std::clamp(dirs[t][0] * dirs[j][0] + dirs[t][1] * dirs[j][1] + dirs[t][2] * dirs[j][2], -1.0, 1.0);
+                    dist.emplace_back(radius * std::acos(d), j);
+                }
+                std::sort(dist.begin(), dist.end());
+                const int take = std::min<int>(c->knn, static_cast<int>(dist.size()));
+                for (int i = 0; i < take; ++i) T.neighbors[train_ids[t]].push_back(train_ids[dist[i].second]);
+            }
+        }
+        // Downsampled cameras and targets (trainer.hpp:151-168).
+        const bool exact_low = secondary_targets != nullptr && secondary_targets_downsample == c->secondary_downsample;
+        T.targets.resize(n_cameras);
+        T.down_targets.resize(n_cameras);
+        for (int i = 0; i < n_cameras; ++i) {
+            const ngs_camera& cam = cameras[i];
+            const int f = clamp_downsample_factor(cam, c->secondary_downsample);
+            ngs_camera down = cam;
+            down.width = cam.width / f;
+            down.height = cam.height / f;
+            T.down_cameras.push_back(down);
+            std::vector<float> planar;
+            interleaved_to_planar(targets[i], cam.width, cam.height, planar);
+            std::vector<float> dplanar;
+            if (exact_low) {
+                const int ef = clamp_downsample_factor(cam, secondary_targets_downsample);
+                if (cam.width / ef == down.width && cam.height / ef == down.height) {
+                    interleaved_to_planar(secondary_targets[i], down.width, down.height, dplanar);
+                }
+            }
+            if (dplanar.empty()) {
+                std::vector<double> box;
+                int ow, oh;
+                box_downsample(targets[i], cam.width, cam.height, f, box, ow, oh);
+                interleaved_to_planar(box.data(), ow, oh, dplanar);
+            }
+            if (c->host_targets) {
+                float *h1 = nullptr, *h2 = nullptr;
+                CUDA_CHECK(cudaMallocHost(&h1, sizeof(float) * planar.size()));
+                CUDA_CHECK(cudaMallocHost(&h2, sizeof(float) * dplanar.size()));
+                std::memcpy(h1, planar.data(), sizeof(float) * planar.size());
+                std::memcpy(h2, dplanar.data(), sizeof(float) * dplanar.size());
+                T.host_targets.push_back(h1);
+                T.host_down_targets.push_back(h2);
+            } else {
+                T.targets[i].ensure(planar.size());
+                T.down_targets[i].ensure(dplanar.size());
+                CUDA_CHECK(cudaMemcpy(T.targets[i].ptr, planar.data(), sizeof(float) * planar.size(), cudaMemcpyHostToDevice));
+                CUDA_CHECK(cudaMemcpy(T.down_targets[i].ptr, dplanar.data(), sizeof(float) * dplanar.size(), cudaMemcpyHostToDevice));
+            }
+        }
+        T.views.resize(1 + c->knn);
+        T.active = true;
+    });
+}
+
+int32_t ngs_trainer_neighbors(ngs_context* ctx, int32_t view_id, int32_t* out, int32_t capacity, int32_t* n_out) {
+    return guarded([&] {
+        if (!ctx->trainer.active) throw Error(NGS_ERR_INVALID_INPUT, "trainer not configured");
+        const auto& nb = ctx->trainer.neighbors.at(view_id);
+        *n_out = static_cast<int32_t>(nb.size());
+        for (int i = 0; i < std::min<int>(capacity, static_cast<int>(nb.size())); ++i) out[i] = nb[i];
+    });
+}
+
+int32_t ngs_trainer_barrier_weight(ngs_context* ctx, double* out) {
+    return guarded([&] {
+        if (!ctx->trainer.active) throw Error(NGS_ERR_INVALID_INPUT, "trainer not configured");
+        *out = ctx->trainer.barrier_weight;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Render + loss for every view of the step (build_view_context x (1+K)).
+void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nbrs) {
+    TrainerState& T = ctx->trainer;
+    const int nv = 1 + static_cast<int>(nbrs.size());
+    for (int i = 0; i < nv; ++i) {
+        ViewSlot& v = T.views[i];
+        const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
+        const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
+        upload_camera(cam, v.cam);
+        v.raster = to_raster(&T.cfg.raster);
+        v.loss = to_loss(&T.cfg.loss);
+        const size_t npx = static_cast<size_t>(cam.width) * cam.height;
+        v.target.ensure(3 * npx);
+        if (T.cfg.host_targets) {
+            const float* src = (i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id];
+            CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyHostToDevice, ctx->stream));
+        } else {
+            const float* src = (i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr;
+            CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        render_view(ctx->scene, v, false, ctx->err.ptr, ctx->stream);
+        compute_loss(v, ctx->stream);
+    }
+}
+
+}  // namespace
+
+extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_iteration_report* report) {
+    return guarded([&] {
+        ProfInstall pi(ctx);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        TrainerState& T = ctx->trainer;
+        if (!T.active) throw Error(NGS_ERR_INVALID_INPUT, "trainer not configured");
+        if (view_id < 0 || view_id >= static_cast<int>(T.cameras.size()))
+            throw Error(NGS_ERR_INVALID_INPUT, "trainer: view id out of range");
+        const std::vector<int>& nbrs = T.neighbors[view_id];
+        const int nv = 1 + static_cast<int>(nbrs.size());
+        std::vector<ViewSlot*> views(nv);
+        for (int i = 0; i < nv; ++i) views[i] = &T.views[i];
+        const int n = ctx->scene.n;
+        const size_t stride = static_cast<size_t>(std::max(n, 1));
+        ngs_newton_options opts = T.cfg.newton;
+        opts.barrier_weight = T.barrier_weight;
+        const SolveParams base = to_solve(&opts, 1);
+        ctx->norm.ensure(5);
+        CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), ctx->stream));
+        render_step_views(ctx, view_id, nbrs);
+        for (int pass_i = 0; pass_i < 5; ++pass_i) {
+            const int attr = T.cfg.order[pass_i];
+            const int pass = pass_of(attr);
+            // Opacity and colour share one traversal when adjacent (same captures, trainer.hpp:412-415).
+            const bool reuse = (attr == NGS_COLOR && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_OPACITY) ||
+                               (attr == NGS_OPACITY && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_COLOR);
+            if (!reuse) accumulate_pass(ctx, pass, views.data(), nv, nullptr);
+            SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
+            launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
+                         color_views(views.data(), nv), base, ctx->acc.ptr, stride, so, ctx->stream);
+            const bool geometry = attr == NGS_POSITION || attr == NGS_ROTATION || attr == NGS_SCALING;
+            if (geometry && pass_i + 1 < 5) render_step_views(ctx, view_id, nbrs);
+        }
+        CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
+        double norms[5];
+        CUDA_CHECK(cudaMemcpyAsync(norms, ctx->norm.ptr, sizeof(norms), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->check_err();
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        T.step_count += 1;
+        for (double d : norms)
+            if (!std::isfinite(d)) throw Error(NGS_ERR_NUMERICAL, "trainer: non-finite update, aborting");
+        if (report) {
+            report->step = T.step_count;
+            report->image_id = view_id;
+            report->probe_loss = 0;
+            report->probe_psnr = 0;
+            report->probe_ssim = 0;
+            for (int i = 0; i < 5; ++i) report->delta_norms[i] = std::sqrt(norms[i]);
+            report->dt_ms = ms;
+        }
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Measurement hooks (ngs_b200_profile.h)
+// ---------------------------------------------------------------------------
+
+namespace {
+
+__global__ void ffma_peak_k(float* out, int iters) {
+    float a0 = threadIdx.x * 1e-3f, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+          a7 = a0 + 7;
+    const float b = 0.999f, c = 1e-4f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fmaf(a0, b, c);
+            a1 = fmaf(a1, b, c);
+            a2 = fmaf(a2, b, c);
+            a3 = fmaf(a3, b, c);
+            a4 = fmaf(a4, b, c);
+            a5 = fmaf(a5, b, c);
+            a6 = fmaf(a6, b, c);
+            a7 = fmaf(a7, b, c);
+        }
+    }
+    if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 12345.f) out[0] = 1.f;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ngs_profile_enable(ngs_context* ctx, int32_t on) {
+    return guarded([&] { ctx->prof.enabled = on != 0; });
+}
+
+int32_t ngs_profile_reset(ngs_context* ctx) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        ctx->prof.reset();
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 4 * sizeof(unsigned long long), ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        ctx->prof.resolve();
+        unsigned long long p[4];
+        CUDA_CHECK(cudaMemcpy(p, ctx->pairs.ptr, sizeof(p), cudaMemcpyDeviceToHost));
+        *out = ctx->prof.stats;
+        for (int i = 0; i < 4; ++i) out->contrib_pairs[i] = static_cast<int64_t>(p[i]);
+    });
+}
+
+int32_t ngs_microbench_fp32(ngs_context* ctx, double* tflops) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        int sms = 0;
+        CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        DevBuf<float> out;
+        out.ensure(1);
+        const int blocks = sms * 8, threads = 256, iters = 4096;
+        ffma_peak_k<<<blocks, threads, 0, ctx->stream>>>(out.ptr, 64);  // warm-up
+        CUDA_LAUNCH_CHECK();
+        CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
+        ffma_peak_k<<<blocks, threads, 0, ctx->stream>>>(out.ptr, iters);
+        CUDA_LAUNCH_CHECK();
+        CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * threads;
+        *tflops = flops / (ms * 1e-3) / 1e12;
+        out.release();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+// context.h — host-side state of one ngs_context (one device, one stream).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <vector>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "ngs_b200_profile.h"
+
+namespace ngsb {
+
+constexpr int kEntry64 = 12;
+
+// Raster/loss options as the kernels consume them (FP32/FP64 copies of the
+// reference structs, rasterizer.hpp:25-40, loss.hpp:11-22).
+struct RasterParams {
+    double lambda_lp;
+    float alpha_cutoff;
+    float t_min;
+    bool cutoff_enabled;  // alpha_cutoff > 0: AABB binning, else every splat in every tile
+    double radius;        // max(3, sqrt(2 ln(1/alpha_cutoff)))  rasterizer.hpp:215-216
+};
+
+struct LossParams {
+    double lambda, c1, c2;
+    int window;
+    double window_sigma;
+};
+
+template <typename T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0;
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        const size_t want = n + n / 4 + 64;
+        CUDA_CHECK(cudaMalloc(&ptr, want * sizeof(T)));
+        cap = want;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+// One rendered view: the device-resident equivalent of ViewContext
+// (newton.hpp:86-96) without the capture buffers (SURVEY.md §7 design stance).
+struct ViewSlot {
+    bool valid = false;
+    CameraDev cam{};
+    int W = 0, H = 0, T = 0;
+    int n = 0;         // kernels projected
+    int entries = 0;   // projected (non-culled) kernels
+    int pairs = 0;
+    RasterParams raster{};
+    LossParams loss{};
+    double loss_value = 0.0;
+    double loss_l2 = 0.0, loss_ssim_sum = 0.0;
+
+    // K1 projection outputs (per kernel)
+    DevBuf<float4> rec_a, rec_b, rec_c;
+    DevBuf<double2> pix;     // splat centre in pixels (FP64: re-based per tile in FP32)
+    DevBuf<double> depth;
+    DevBuf<int4> rect;
+    DevBuf<int> tiles_touched;
+    DevBuf<uint8_t> flags;
+    DevBuf<double> entry64;  // parity read-back: px, py, s00, s01, s11, bbox x0,y0,x1,y1, colour (kEntry64 per kernel)
+    // K2-K5 binning
+    DevBuf<unsigned long long> depth_key, depth_key_sorted;
+    DevBuf<int> ids, order;
+    DevBuf<int> counts_sorted, offsets;
+    DevBuf<unsigned int> pair_key, pair_key_sorted;
+    DevBuf<int> pair_val, pair_val_sorted;
+    DevBuf<int2> ranges;
+    DevBuf<unsigned char> cub_temp;
+    // K6 forward raster outputs (planar [3][H][W])
+    DevBuf<double> image;   // FP64: FP32 rounding is amplified by the (c - c^t) cancellation in the loss
+    DevBuf<float> t_final;
+    DevBuf<int> last;       // index into the tile list of the last contributing splat, -1 if none
+    // K7 loss fields
+    DevBuf<float> target;   // planar [3][H][W]
+    DevBuf<double> fields;  // 9 center fields x 3 channels x H x W
+    DevBuf<float> loss_grad, loss_hess;  // planar [3][H][W]
+    DevBuf<double> loss_sums;            // [0] sum d^2, [1] sum ssim
+    // Per-pass backward constants (per kernel, AoS)
+    DevBuf<float> consts;
+
+    void release_all();
+};
+
+// Per-context measurement state (ngs_b200_profile.h). The active profiler of
+// the calling thread is installed by each C-ABI entry point.
+struct Profiler {
+    bool enabled = false;
+    struct Rec {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    ngs_profile_stats stats{};
+
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+    void resolve() {
+        for (auto& r : pending) {
+            CUDA_CHECK(cudaEventSynchronize(r.b));
+            float ms = 0;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+            stats.ms[r.stage] += ms;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+    }
+    void reset() {
+        resolve();
+        stats = ngs_profile_stats{};
+    }
+    ~Profiler() {
+        for (auto& r : pending) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+extern thread_local Profiler* g_prof;
+
+// Brackets the kernel launches of one stage; counts `launches` kernels.
+struct StageScope {
+    Profiler* p;
+    int stage;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    StageScope(int stage_, cudaStream_t s_, int launches = 1) : p(g_prof), stage(stage_), s(s_) {
+        if (!p) return;
+        p->stats.launches[stage] += launches;
+        p->stats.total_launches += launches;
+        if (p->enabled) {
+            a = p->get();
+            CUDA_CHECK(cudaEventRecord(a, s));
+        }
+    }
+    ~StageScope() {
+        if (!p || !a) return;
+        cudaEvent_t b = p->get();
+        if (cudaEventRecord(b, s) == cudaSuccess) p->pending.push_back({stage, a, b});
+    }
+};
+
+// Launch wrappers (render.cu, loss.cu, backward.cu, solve.cu).
+void upload_camera(const ngs_camera& c, CameraDev& out);
+void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s);
+void compute_loss(ViewSlot& v, cudaStream_t s);
+
+}  // namespace ngsb

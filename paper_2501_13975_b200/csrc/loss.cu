@@ -1,0 +1,251 @@
+// loss.cu — K7: L2 + SSIM loss value and per-pixel gradient / diagonal Hessian
+// fields (total_loss_derivs, loss.hpp:342-356).
+//
+// FP64 throughout: SSIM variance/covariance are E[x^2]-E[x]^2 differences of
+// O(1) quantities whose result is O(1e-6) in flat regions; FP32 loses them
+// entirely (SURVEY.md §7 hard part 1). Two shared-memory tiled kernels, each
+// a separable valid-tap convolution (loss.hpp:81-115) with an H-halo of
+// window/2 on every side:
+//   A: 5 window statistics -> 9 window-centre fields (loss.hpp:162-214, 262-305)
+//   B: 9 field convolutions (w for grad/kw, w^2 for the rest) -> grad, hess
+//      (loss.hpp:309-329) plus the L2 terms (loss.hpp:138-156).
+#include "context.h"
+
+namespace ngsb {
+
+namespace {
+
+constexpr int kLT = 16;       // output tile edge
+constexpr int kMaxHalf = 10;  // window <= 21
+constexpr int kLS = kLT + 2 * kMaxHalf;
+
+struct Window {
+    double w[2 * kMaxHalf + 1];
+    double w2[2 * kMaxHalf + 1];
+    int half;
+};
+
+__device__ __forceinline__ double axis_norm(int x, int n, const Window& win) {
+    const int i0 = max(-win.half, -x), i1 = min(win.half, n - 1 - x);
+    double s = 0;
+    for (int i = i0; i <= i1; ++i) s += win.w[i + win.half];
+    return s;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+
+// Kernel A: window statistics and the 9 window-centre fields for one channel.
+__global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double* __restrict__ image,
+                                                     const float* __restrict__ target, Window win, double c1, double c2,
+                                                     double* __restrict__ fields, double* __restrict__ sums) {
+    __shared__ double s_x[kLS][kLS + 1], s_t[kLS][kLS + 1];
+    __shared__ double s_h[5][kLS][kLT + 1];
+    __shared__ double red[8];
+    const int ch = blockIdx.z;
+    const int ox = blockIdx.x * kLT, oy = blockIdx.y * kLT;
+    const int h = win.half, span = kLT + 2 * h;
+    const size_t plane = static_cast<size_t>(W) * H;
+    const double* img = image + ch * plane;
+    const float* tgt = target + ch * plane;
+    for (int i = threadIdx.x; i < span * span; i += blockDim.x) {
+        const int r = i / span, c = i % span;
+        const int gx = ox - h + c, gy = oy - h + r;
+        const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+        const size_t idx = static_cast<size_t>(gy) * W + gx;
+        s_x[r][c] = in ? img[idx] : 0.0;
+        s_t[r][c] = in ? static_cast<double>(tgt[idx]) : 0.0;
+    }
+    __syncthreads();
+    // Horizontal pass (out-of-image taps are zero == skipped taps).
+    for (int i = threadIdx.x; i < span * kLT; i += blockDim.x) {
+        const int r = i / kLT, c = i % kLT;
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+        for (int k = -h; k <= h; ++k) {
+            const double wk = win.w[k + h];
+            const double xv = s_x[r][c + h + k], tv = s_t[r][c + h + k];
+            a0 += wk * xv;
+            a1 += wk * (xv * xv);
+            a2 += wk * tv;
+            a3 += wk * (tv * tv);
+            a4 += wk * (xv * tv);
+        }
+        s_h[0][r][c] = a0;
+        s_h[1][r][c] = a1;
+        s_h[2][r][c] = a2;
+        s_h[3][r][c] = a3;
+        s_h[4][r][c] = a4;
+    }
+    __syncthreads();
+    const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
+    const int x = ox + lx, y = oy + ly;
+    double ssim = 0.0;
+    if (x < W && y < H) {
+        double st[5];
+        for (int f = 0; f < 5; ++f) {
+            double a = 0;
+            for (int k = -h; k <= h; ++k) a += win.w[k + h] * s_h[f][ly + h + k][lx];
+            st[f] = a;
+        }
+        const double inv_norm = 1.0 / (axis_norm(x, W, win) * axis_norm(y, H, win));
+        const double mu = st[0] * inv_norm, mu_t = st[2] * inv_norm;
+        const double var = fmax(0.0, st[1] * inv_norm - mu * mu);
+        const double var_t = fmax(0.0, st[3] * inv_norm - mu_t * mu_t);
+        const double cov = st[4] * inv_norm - mu * mu_t;
+        // loss.hpp:266-303
+        const double f0 = 2.0 * mu * mu_t + c1;
+        const double f1 = 2.0 * cov + c2;
+        const double f2 = mu * mu + mu_t * mu_t + c1;
+        const double f3 = var + var_t + c2;
+        const double nn = f0 * f1, dd = f2 * f3;
+        ssim = nn / dd;
+        const double inv_d = 1.0 / dd;
+        const double a0 = 2.0 * mu_t, a1 = -2.0 * mu_t, b1 = 2.0;
+        const double a2 = 2.0 * mu, a3 = -2.0 * mu, b3 = 2.0;
+        const double A = a0 * f1 + f0 * a1, B = f0 * b1, C = a2 * f3 + f2 * a3, E = f2 * b3;
+        const double inv_d2 = inv_d * inv_d, inv_d3 = inv_d2 * inv_d, inv_norm2 = inv_norm * inv_norm;
+        double out[9];
+        out[0] = (2.0 * mu_t * (f1 - f0) * inv_d - 2.0 * mu * nn * inv_d / f2 + 2.0 * mu * nn * inv_d / f3) * inv_norm;
+        out[1] = 2.0 * f0 * inv_d * inv_norm;
+        out[2] = -2.0 * nn * inv_d / f3 * inv_norm;
+        out[3] = -2.0 * nn / (f2 * f3 * f3) * inv_norm;
+        out[4] = (2.0 * a0 * a1 * inv_d - 2.0 * A * C * inv_d2 - nn * (2.0 * a2 * a3 + 2.0 * f3 - 2.0 * f2) * inv_d2 +
+                  2.0 * nn * C * C * inv_d3) *
+                 inv_norm2;
+        out[5] = (-2.0 * A * E * inv_d2 - 2.0 * nn * a2 * b3 * inv_d2 + 4.0 * nn * C * E * inv_d3) * inv_norm2;
+        out[6] = (2.0 * a0 * b1 * inv_d - 2.0 * B * C * inv_d2) * inv_norm2;
+        out[7] = -2.0 * B * E * inv_d2 * inv_norm2;
+        out[8] = 2.0 * nn * E * E * inv_d3 * inv_norm2;
+        const size_t idx = static_cast<size_t>(y) * W + x;
+        for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
+    }
+    const double tot = block_sum(ssim, red);
+    if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
+}
+
+// Kernel B: convolve the 9 centre fields and combine into grad / hess; also the
+// L2 part. lambda == 0 skips the SSIM fields entirely (loss.hpp:345).
+__global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double* __restrict__ image,
+                                                     const float* __restrict__ target, Window win, double lambda,
+                                                     const double* __restrict__ fields, float* __restrict__ grad,
+                                                     float* __restrict__ hess, double* __restrict__ sums) {
+    __shared__ double s_f[kLS][kLS + 1];
+    __shared__ double s_h[kLS][kLT + 1];
+    __shared__ double red[8];
+    const int ch = blockIdx.z;
+    const int ox = blockIdx.x * kLT, oy = blockIdx.y * kLT;
+    const int h = win.half, span = kLT + 2 * h;
+    const size_t plane = static_cast<size_t>(W) * H;
+    const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
+    const int x = ox + lx, y = oy + ly;
+    const bool valid = x < W && y < H;
+    const size_t idx = static_cast<size_t>(y) * W + x;
+    const double inv3n = 1.0 / (3.0 * static_cast<double>(plane));
+    double c = 0, ct = 0;
+    if (valid) {
+        c = image[ch * plane + idx];
+        ct = target[ch * plane + idx];
+    }
+    double g_ssim = 0, h_ssim = 0;
+    if (lambda != 0.0) {
+        for (int f = 0; f < 9; ++f) {
+            const double* field = fields + (static_cast<size_t>(f) * 3 + ch) * plane;
+            const double* wk = (f <= 3) ? win.w : win.w2;  // fp, fq, fr, fkw use w; the rest w^2
+            __syncthreads();
+            for (int i = threadIdx.x; i < span * span; i += blockDim.x) {
+                const int r = i / span, cc = i % span;
+                const int gx = ox - h + cc, gy = oy - h + r;
+                const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+                s_f[r][cc] = in ? field[static_cast<size_t>(gy) * W + gx] : 0.0;
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < span * kLT; i += blockDim.x) {
+                const int r = i / kLT, cc = i % kLT;
+                double a = 0;
+                for (int k = -h; k <= h; ++k) a += wk[k + h] * s_f[r][cc + h + k];
+                s_h[r][cc] = a;
+            }
+            __syncthreads();
+            double s = 0;
+            for (int k = -h; k <= h; ++k) s += wk[k + h] * s_h[ly + h + k][lx];
+            switch (f) {  // loss.hpp:323-327
+                case 0: g_ssim += s; break;
+                case 1: g_ssim += ct * s; break;
+                case 2: g_ssim += c * s; break;
+                case 3: h_ssim += s; break;
+                case 4: h_ssim += s; break;
+                case 5: h_ssim += c * s; break;
+                case 6: h_ssim += ct * s; break;
+                case 7: h_ssim += c * ct * s; break;
+                case 8: h_ssim += c * c * s; break;
+            }
+        }
+    }
+    double dsq = 0;
+    if (valid) {
+        const double d = c - ct;
+        dsq = d * d;
+        double g = inv3n * d, hh = inv3n;
+        if (lambda != 0.0) {
+            g += lambda * (-inv3n * g_ssim);
+            hh += lambda * (-inv3n * h_ssim);
+        }
+        grad[ch * plane + idx] = static_cast<float>(g);
+        hess[ch * plane + idx] = static_cast<float>(hh);
+    }
+    const double tot = block_sum(dsq, red);
+    if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
+}
+
+}  // namespace
+
+void compute_loss(ViewSlot& v, cudaStream_t s) {
+    const LossParams& L = v.loss;
+    if (L.lambda < 0.0) throw Error(NGS_ERR_INVALID_INPUT, "loss: lambda must be >= 0");
+    if (L.window < 3 || L.window % 2 == 0) throw Error(NGS_ERR_INVALID_INPUT, "loss: window must be odd and >= 3");
+    if (L.window > 2 * kMaxHalf + 1) throw Error(NGS_ERR_INVALID_INPUT, "loss: window larger than 21 unsupported");
+    const bool ssim = L.lambda != 0.0;
+    if (ssim && (v.W < L.window || v.H < L.window))
+        throw Error(NGS_ERR_INVALID_INPUT, "ssim stats: image smaller than the filter window");
+    // gaussian_window_1d, loss.hpp:66-77
+    Window win{};
+    win.half = L.window / 2;
+    double sum = 0;
+    for (int i = 0; i < L.window; ++i) {
+        const double d = i - win.half;
+        win.w[i] = std::exp(-d * d / (2.0 * L.window_sigma * L.window_sigma));
+        sum += win.w[i];
+    }
+    for (int i = 0; i < L.window; ++i) {
+        win.w[i] /= sum;
+        win.w2[i] = win.w[i] * win.w[i];
+    }
+    const size_t npx = static_cast<size_t>(v.W) * v.H;
+    v.loss_grad.ensure(3 * npx);
+    v.loss_hess.ensure(3 * npx);
+    v.loss_sums.ensure(2);
+    CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * sizeof(double), s));
+    const dim3 grid((v.W + kLT - 1) / kLT, (v.H + kLT - 1) / kLT, 3);
+    StageScope st(NGS_STAGE_LOSS, s, ssim ? 2 : 1);
+    if (ssim) {
+        v.fields.ensure(27 * npx);
+        ssim_fields_k<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
+                                           v.loss_sums.ptr);
+        CUDA_LAUNCH_CHECK();
+    }
+    ssim_derivs_k<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.lambda,
+                                       ssim ? v.fields.ptr : nullptr, v.loss_grad.ptr, v.loss_hess.ptr,
+                                       v.loss_sums.ptr);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace ngsb

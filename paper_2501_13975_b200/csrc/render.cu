@@ -1,0 +1,391 @@
+// render.cu — K1 projection, K2-K5 depth sort + tile binning, K6 forward raster.
+//
+// Reference semantics: build_splat_list (rasterizer.hpp:182-265) and
+// composite_forward / composite_pixel (rasterizer.hpp:274-442).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+
+#include "context.h"
+#include "geometry.cuh"
+#include "splat.cuh"
+
+namespace ngsb {
+
+void ViewSlot::release_all() {
+    rec_a.release();
+    rec_b.release();
+    rec_c.release();
+    pix.release();
+    depth.release();
+    rect.release();
+    tiles_touched.release();
+    flags.release();
+    entry64.release();
+    depth_key.release();
+    depth_key_sorted.release();
+    ids.release();
+    order.release();
+    counts_sorted.release();
+    offsets.release();
+    pair_key.release();
+    pair_key_sorted.release();
+    pair_val.release();
+    pair_val_sorted.release();
+    ranges.release();
+    cub_temp.release();
+    image.release();
+    t_final.release();
+    last.release();
+    target.release();
+    fields.release();
+    loss_grad.release();
+    loss_hess.release();
+    loss_sums.release();
+    consts.release();
+    valid = false;
+}
+
+// Camera(view, proj, w, h), camera.hpp:30-42.
+void upload_camera(const ngs_camera& c, CameraDev& out) {
+    if (c.width < 16 || c.height < 16) throw Error(NGS_ERR_INVALID_INPUT, "camera: width and height must be >= 16");
+    for (int i = 0; i < 16; ++i) {
+        out.view[i] = c.view[i];
+        out.proj[i] = c.proj[i];
+    }
+    for (int r = 0; r < 4; ++r)
+        for (int col = 0; col < 4; ++col) {
+            double v = 0;
+            for (int k = 0; k < 4; ++k) v += c.proj[4 * r + k] * c.view[4 * k + col];
+            out.view_proj[4 * r + col] = v;
+        }
+    const double* m = c.view;
+    auto R = [&](int i, int j) { return m[4 * i + j]; };
+    const double det = R(0, 0) * (R(1, 1) * R(2, 2) - R(2, 1) * R(1, 2)) -
+                       R(1, 0) * (R(0, 1) * R(2, 2) - R(2, 1) * R(0, 2)) +
+                       R(2, 0) * (R(0, 1) * R(1, 2) - R(1, 1) * R(0, 2));
+    if (std::abs(det) < 1e-12) throw Error(NGS_ERR_INVALID_INPUT, "camera: view rotation block is singular");
+    double inv[9];
+    inv[0] = (R(1, 1) * R(2, 2) - R(1, 2) * R(2, 1)) / det;
+    inv[1] = (R(0, 2) * R(2, 1) - R(0, 1) * R(2, 2)) / det;
+    inv[2] = (R(0, 1) * R(1, 2) - R(0, 2) * R(1, 1)) / det;
+    inv[3] = (R(1, 2) * R(2, 0) - R(1, 0) * R(2, 2)) / det;
+    inv[4] = (R(0, 0) * R(2, 2) - R(0, 2) * R(2, 0)) / det;
+    inv[5] = (R(0, 2) * R(1, 0) - R(0, 0) * R(1, 2)) / det;
+    inv[6] = (R(1, 0) * R(2, 1) - R(1, 1) * R(2, 0)) / det;
+    inv[7] = (R(0, 1) * R(2, 0) - R(0, 0) * R(2, 1)) / det;
+    inv[8] = (R(0, 0) * R(1, 1) - R(0, 1) * R(1, 0)) / det;
+    const double t[3] = {R(0, 3), R(1, 3), R(2, 3)};
+    for (int i = 0; i < 3; ++i) out.center[i] = -(inv[3 * i] * t[0] + inv[3 * i + 1] * t[1] + inv[3 * i + 2] * t[2]);
+    out.width = c.width;
+    out.height = c.height;
+    out.tiles_x = (c.width + kTile - 1) / kTile;
+    out.tiles_y = (c.height + kTile - 1) / kTile;
+}
+
+namespace {
+
+__device__ __forceinline__ unsigned long long depth_sort_key(double d) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// K1: per-kernel projection, SH colour and tile extent (FP64 math, coalesced
+// float4 SoA loads; build_splat_list per-entry block rasterizer.hpp:192-226).
+__global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev cam, RasterParams rp,
+                                                        float4* ra, float4* rb, float4* rc, double2* pix,
+                                                        double* depth, int4* rect, int* tiles_touched,
+                                                        uint8_t* flags, unsigned long long* depth_key, int* ids,
+                                                        double* entry64, int* err) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= s.n) return;
+    ids[k] = k;
+    const float4 ps = s.pos_sigma[k];
+    const D3 p = {ps.x, ps.y, ps.z};
+    Projected pr;
+    const bool ok = project_kernel(cam, p, s.quat[k], s.scale[k], rp.lambda_lp, pr);
+    double det = 0;
+    if (ok) det = pr.s00 * pr.s11 - pr.s01 * pr.s01;
+    if (!ok || !(det > 0.0)) {
+        if (ok) atomicOr(err, 1);  // project_kernel: projected covariance is not positive definite
+        tiles_touched[k] = 0;
+        flags[k] = 0;
+        rect[k] = make_int4(1, 1, 0, 0);
+        depth_key[k] = ~0ull;
+        depth[k] = 0;
+        return;
+    }
+    D3 r;
+    double rn;
+    if (!view_direction(cam, p, r, rn)) {
+        atomicOr(err, 2);  // DegenerateGeometry
+        r = d3(0, 0, 1);
+    }
+    double basis[16];
+    sh_basis(r, s.sh_degree, basis);
+    double col[3];
+    uint8_t f = kProjected;
+    for (int ch = 0; ch < 3; ++ch) {
+        double v = 0;
+        for (int i = 0; i < s.n_coeffs; ++i) v += basis[i] * static_cast<double>(s.sh[(16 * ch + i) * s.n + k]);
+        v += kColorOffset;
+        const bool clamped = v <= 0.0;
+        col[ch] = clamped ? 0.0 : v;
+        if (clamped) f |= static_cast<uint8_t>(kClamp0 << ch);
+    }
+    const double qa = pr.s11 / det, qb = -pr.s01 / det, qc = pr.s00 / det;
+    double x0, y0, x1, y1;
+    if (rp.cutoff_enabled) {
+        const double rx = rp.radius * sqrt(fmax(pr.s00, 0.0));
+        const double ry = rp.radius * sqrt(fmax(pr.s11, 0.0));
+        x0 = pr.px - rx;
+        y0 = pr.py - ry;
+        x1 = pr.px + rx;
+        y1 = pr.py + ry;
+    } else {
+        x0 = 0.0;
+        y0 = 0.0;
+        x1 = cam.width - 1.0;
+        y1 = cam.height - 1.0;
+    }
+    auto clampi = [](int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); };
+    const int tx0 = clampi(static_cast<int>(floor(x0 / kTile)), 0, cam.tiles_x - 1);
+    const int tx1 = clampi(static_cast<int>(floor(x1 / kTile)), 0, cam.tiles_x - 1);
+    const int ty0 = clampi(static_cast<int>(floor(y0 / kTile)), 0, cam.tiles_y - 1);
+    const int ty1 = clampi(static_cast<int>(floor(y1 / kTile)), 0, cam.tiles_y - 1);
+    const bool off = x1 < 0 || x0 >= cam.width || y1 < 0 || y0 >= cam.height;
+    rect[k] = off ? make_int4(1, 1, 0, 0) : make_int4(tx0, ty0, tx1, ty1);
+    tiles_touched[k] = off ? 0 : (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+    flags[k] = f;
+    depth[k] = pr.depth;
+    depth_key[k] = depth_sort_key(pr.depth);
+    pix[k] = make_double2(pr.px, pr.py);
+    ra[k] = make_float4(0.f, 0.f, static_cast<float>(qa), static_cast<float>(qb));
+    rb[k] = make_float4(static_cast<float>(qc), ps.w, static_cast<float>(col[0]), static_cast<float>(col[1]));
+    rc[k] = make_float4(static_cast<float>(col[2]), static_cast<float>(pr.s00), static_cast<float>(pr.s01),
+                        static_cast<float>(pr.s11));
+    if (entry64) {
+        double* e = entry64 + kEntry64 * static_cast<size_t>(k);
+        e[0] = pr.px;
+        e[1] = pr.py;
+        e[2] = pr.s00;
+        e[3] = pr.s01;
+        e[4] = pr.s11;
+        e[5] = x0;
+        e[6] = y0;
+        e[7] = x1;
+        e[8] = y1;
+        e[9] = col[0];
+        e[10] = col[1];
+        e[11] = col[2];
+    }
+}
+
+__global__ void gather_counts_k(int n, const int* order, const int* tiles_touched, int* counts_sorted) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) counts_sorted[r] = tiles_touched[order[r]];
+}
+
+// K3: emit (tile, kernel) pairs in depth order; a later stable sort on the
+// tile key alone keeps depth order (ties by kernel id) inside every tile.
+__global__ void emit_pairs_k(int n, int tiles_x, const int* order, const int* offsets, const int4* rect,
+                             const int* tiles_touched, unsigned int* keys, int* vals) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int k = order[r];
+    if (tiles_touched[k] == 0) return;
+    const int4 rc = rect[k];
+    int o = offsets[r];
+    for (int ty = rc.y; ty <= rc.w; ++ty)
+        for (int tx = rc.x; tx <= rc.z; ++tx) {
+            keys[o] = static_cast<unsigned int>(ty * tiles_x + tx);
+            vals[o] = k;
+            ++o;
+        }
+}
+
+// K5: per-tile [start, end) ranges from the tile-sorted key array.
+__global__ void tile_ranges_k(int pairs, const unsigned int* keys, int2* ranges) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pairs) return;
+    const unsigned int t = keys[i];
+    if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
+    if (i == pairs - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+}
+
+// K6: forward alpha-blend rasterizer. One 16x16 tile per 256-thread block;
+// the tile's depth-ordered splats are staged through shared memory in
+// batches; the block retires as soon as every pixel saturated
+// (__syncthreads_count = block-wide ballot). Pixel centres and splat centres
+// are expressed relative to the tile origin so the FP32 offsets carry
+// full precision at 4K resolutions.
+constexpr int kRasterBatch = 256;
+
+__global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int H, const int2* __restrict__ ranges,
+                                                        const int* __restrict__ vals, const double2* __restrict__ pix,
+                                                        const float4* __restrict__ ra, const float4* __restrict__ rb,
+                                                        const float4* __restrict__ rc, float bg0, float bg1, float bg2,
+                                                        float cutoff, float tmin, double* __restrict__ image,
+                                                        float* __restrict__ t_final, int* __restrict__ last_out) {
+    __shared__ float s_px[kRasterBatch], s_py[kRasterBatch], s_qa[kRasterBatch], s_qb[kRasterBatch],
+        s_qc[kRasterBatch], s_sig[kRasterBatch], s_c0[kRasterBatch], s_c1[kRasterBatch], s_c2[kRasterBatch];
+    const int tile = blockIdx.x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int x = tx * kTile + lx, y = ty * kTile + ly;
+    const bool inside = x < W && y < H;
+    const float fx = lx + 0.5f, fy = ly + 0.5f;
+    const double ox = tx * kTile, oy = ty * kTile;
+    const int2 range = ranges[tile];
+    float T = 1.0f;
+    double C0 = 0.0, C1 = 0.0, C2 = 0.0;  // FP64 colour sums (the backward's prefix uses the same)
+    int last = -1;
+    bool done = !inside;
+    for (int base = range.x; base < range.y; base += kRasterBatch) {
+        if (__syncthreads_count(done) == blockDim.x) break;
+        const int i = base + threadIdx.x;
+        if (i < range.y) {
+            const int k = vals[i];
+            const double2 p = pix[k];
+            const float4 a = ra[k], b = rb[k], c = rc[k];
+            s_px[threadIdx.x] = static_cast<float>(p.x - ox);
+            s_py[threadIdx.x] = static_cast<float>(p.y - oy);
+            s_qa[threadIdx.x] = a.z;
+            s_qb[threadIdx.x] = a.w;
+            s_qc[threadIdx.x] = b.x;
+            s_sig[threadIdx.x] = b.y;
+            s_c0[threadIdx.x] = b.z;
+            s_c1[threadIdx.x] = b.w;
+            s_c2[threadIdx.x] = c.x;
+        }
+        __syncthreads();
+        const int cnt = min(kRasterBatch, range.y - base);
+        if (!done) {
+            for (int j = 0; j < cnt; ++j) {
+                const SplatEval e = eval_splat(s_px[j], s_py[j], s_qa[j], s_qb[j], s_qc[j], s_sig[j], fx, fy);
+                if (e.alpha < cutoff) continue;
+                const double w = blend_weight(T, e.alpha);
+                C0 = __fma_rn(w, s_c0[j], C0);
+                C1 = __fma_rn(w, s_c1[j], C1);
+                C2 = __fma_rn(w, s_c2[j], C2);
+                T = next_transmittance(T, e.alpha);
+                last = base + j;
+                if (tmin > 0.f && T < tmin) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+    }
+    if (inside) {
+        const size_t plane = static_cast<size_t>(W) * H;
+        const size_t idx = static_cast<size_t>(y) * W + x;
+        image[idx] = __fma_rn(T, bg0, C0);
+        image[plane + idx] = __fma_rn(T, bg1, C1);
+        image[2 * plane + idx] = __fma_rn(T, bg2, C2);
+        t_final[idx] = T;
+        last_out[idx] = last;
+    }
+}
+
+inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
+
+}  // namespace
+
+void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s) {
+    const int n = scene.n;
+    v.n = n;
+    v.W = v.cam.width;
+    v.H = v.cam.height;
+    v.T = v.cam.tiles_x * v.cam.tiles_y;
+    v.rec_a.ensure(n);
+    v.rec_b.ensure(n);
+    v.rec_c.ensure(n);
+    v.pix.ensure(n);
+    v.depth.ensure(n);
+    v.rect.ensure(n);
+    v.tiles_touched.ensure(n);
+    v.flags.ensure(n);
+    v.depth_key.ensure(n);
+    v.depth_key_sorted.ensure(n);
+    v.ids.ensure(n);
+    v.order.ensure(n);
+    v.counts_sorted.ensure(n + 1);
+    v.offsets.ensure(n + 1);
+    v.ranges.ensure(v.T);
+    const size_t npx = static_cast<size_t>(v.W) * v.H;
+    v.image.ensure(3 * npx);
+    v.t_final.ensure(npx);
+    v.last.ensure(npx);
+    if (want_debug) v.entry64.ensure(kEntry64 * static_cast<size_t>(n));
+
+    if (n > 0) {
+        StageScope st(NGS_STAGE_PROJECT, s);
+        project_kernel_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr,
+                                                       v.pix.ptr, v.depth.ptr, v.rect.ptr, v.tiles_touched.ptr,
+                                                       v.flags.ptr, v.depth_key.ptr, v.ids.ptr,
+                                                       want_debug ? v.entry64.ptr : nullptr, d_err);
+        CUDA_LAUNCH_CHECK();
+    }
+    if (n > 0) {
+        StageScope st(NGS_STAGE_SORT, s, 13);
+        // K2: global stable depth order (ties by kernel id: keys are emitted in id order).
+        size_t temp1 = 0, temp2 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, temp1, v.depth_key.ptr, v.depth_key_sorted.ptr, v.ids.ptr,
+                                        v.order.ptr, n, 0, 64, s);
+        cub::DeviceScan::ExclusiveSum(nullptr, temp2, v.counts_sorted.ptr, v.offsets.ptr, n + 1, s);
+        v.cub_temp.ensure(std::max(temp1, temp2));
+        temp1 = v.cub_temp.cap;
+        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(v.cub_temp.ptr, temp1, v.depth_key.ptr, v.depth_key_sorted.ptr,
+                                                   v.ids.ptr, v.order.ptr, n, 0, 64, s));
+        gather_counts_k<<<blocks_for(n), 256, 0, s>>>(n, v.order.ptr, v.tiles_touched.ptr, v.counts_sorted.ptr);
+        CUDA_LAUNCH_CHECK();
+        CUDA_CHECK(cudaMemsetAsync(v.counts_sorted.ptr + n, 0, sizeof(int), s));
+        temp2 = v.cub_temp.cap;
+        CUDA_CHECK(cub::DeviceScan::ExclusiveSum(v.cub_temp.ptr, temp2, v.counts_sorted.ptr, v.offsets.ptr, n + 1, s));
+        int pairs = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&pairs, v.offsets.ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        v.pairs = pairs;
+    } else {
+        v.pairs = 0;
+    }
+    if (g_prof) {
+        g_prof->stats.raster_pairs += v.pairs;
+        g_prof->stats.renders += 1;
+    }
+    CUDA_CHECK(cudaMemsetAsync(v.ranges.ptr, 0, sizeof(int2) * v.T, s));
+    if (v.pairs > 0) {
+        StageScope st(NGS_STAGE_SORT, s, 5);
+        const int P = v.pairs;
+        v.pair_key.ensure(P);
+        v.pair_key_sorted.ensure(P);
+        v.pair_val.ensure(P);
+        v.pair_val_sorted.ensure(P);
+        emit_pairs_k<<<blocks_for(n), 256, 0, s>>>(n, v.cam.tiles_x, v.order.ptr, v.offsets.ptr, v.rect.ptr,
+                                                   v.tiles_touched.ptr, v.pair_key.ptr, v.pair_val.ptr);
+        CUDA_LAUNCH_CHECK();
+        int bits = 1;
+        while ((1 << bits) < v.T) ++bits;
+        size_t temp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, temp, v.pair_key.ptr, v.pair_key_sorted.ptr, v.pair_val.ptr,
+                                        v.pair_val_sorted.ptr, P, 0, bits, s);
+        v.cub_temp.ensure(temp);
+        temp = v.cub_temp.cap;
+        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(v.cub_temp.ptr, temp, v.pair_key.ptr, v.pair_key_sorted.ptr,
+                                                   v.pair_val.ptr, v.pair_val_sorted.ptr, P, 0, bits, s));
+        tile_ranges_k<<<blocks_for(P), 256, 0, s>>>(P, v.pair_key_sorted.ptr, v.ranges.ptr);
+        CUDA_LAUNCH_CHECK();
+    }
+    StageScope st(NGS_STAGE_RASTER, s);
+    raster_forward_k<<<v.T, 256, 0, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr,
+                                         v.pairs > 0 ? v.pair_val_sorted.ptr : nullptr, v.pix.ptr, v.rec_a.ptr,
+                                         v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1], scene.bg[2],
+                                         v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
+                                         v.last.ptr);
+    CUDA_LAUNCH_CHECK();
+    v.valid = true;
+}
+
+}  // namespace ngsb

@@ -1,0 +1,485 @@
+// solve.cu — K9: one-thread-per-Gaussian safeguarded local Newton solves and
+// commits (solve_* newton.hpp:588-811, commit_* newton.hpp:817-844).
+//
+// FP64 in registers. Each thread reads only its own kernel's accumulators and
+// parameters and writes only its own parameters, so solve+commit in one
+// kernel has exactly the reference's Jacobi semantics (trainer.hpp:331-343).
+// The spectrum repair is psd_safeguard (newton.hpp:205-238): closed-form 1x1 /
+// 2x2, and for SH colour an exact low-rank eigen-decomposition of
+// H = sum_v h_v phi_v phi_v^T (rank <= views) instead of a dense n x n Jacobi.
+#include "backward.h"
+#include "geometry.cuh"
+#include "solve.h"
+
+namespace ngsb {
+
+namespace {
+
+inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
+
+__device__ __forceinline__ void block_add(double v, double* target) {
+    __shared__ double red[8];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
+        if (t != 0.0) atomicAdd(target, t);
+    }
+}
+
+// psd_safeguard + LDLT solve for n = 1 (newton.hpp:208-214, 240-244).
+__device__ __forceinline__ double solve1(double h, double g, const SolveParams& p) {
+    const double mu = fmax(p.mu_min, p.eig_floor_rel * fabs(h));
+    const double hs = fmax(fabs(h), mu);
+    return -g / hs;
+}
+
+// psd_safeguard n = 2 (newton.hpp:215-227) + solve.
+__device__ __forceinline__ void solve2(double h00, double h01, double h11, double g0, double g1, const SolveParams& p,
+                                       double& d0, double& d1) {
+    const Eig2 e = sym2_eigen(h00, h01, h11);
+    const double lam_max = fmax(fabs(e.l0), fabs(e.l1));
+    const double mu = fmax(p.mu_min, p.eig_floor_rel * lam_max);
+    double a = h00, b = h01, c = h11;
+    if (!(e.l0 >= mu)) {
+        const double l0 = fmax(fabs(e.l0), mu), l1 = fmax(fabs(e.l1), mu);
+        a = l0 * e.v0x * e.v0x + l1 * e.v1x * e.v1x;
+        b = l0 * e.v0x * e.v0y + l1 * e.v1x * e.v1y;
+        c = l0 * e.v0y * e.v0y + l1 * e.v1y * e.v1y;
+    }
+    const double det = a * c - b * b;
+    d0 = -(c * g0 - b * g1) / det;
+    d1 = -(-b * g0 + a * g1) / det;
+}
+
+__device__ inline bool primary_dir(const CameraDev& cam, const D3& p, D3& r, int* err) {
+    double n;
+    if (!view_direction(cam, p, r, n)) {
+        atomicOr(err, 2);
+        r = d3(0, 0, 1);
+        return false;
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(256) solve_position_k(SceneDev s, CameraDev primary, SolveParams sp,
+                                                        const double* __restrict__ acc, size_t stride,
+                                                        SolveOutputs out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq = 0.0;
+    if (k < s.n) {
+        const float4 ps = s.pos_sigma[k];
+        const D3 p = {ps.x, ps.y, ps.z};
+        double g[3], H[3][3];
+        for (int i = 0; i < 3; ++i) g[i] = acc[i * stride + k];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) H[i][j] = acc[(3 + sym3(i, j)) * stride + k];
+        D3 r;
+        primary_dir(primary, p, r, out.err);
+        // build_position_subspace, newton.hpp:130-139
+        D3 seed = d3(0, 1, 0);
+        if (fabs(dot3(r, seed)) > 0.99) seed = d3(0, 0, 1);
+        D3 uy = sub3(seed, scale3(r, dot3(r, seed)));
+        uy = scale3(uy, 1.0 / sqrt(dot3(uy, uy)));
+        const D3 ux = cross3(r, uy);
+        const double U[3][2] = {{ux.x, uy.x}, {ux.y, uy.y}, {ux.z, uy.z}};
+        double H2[2][2] = {}, g2[2] = {};
+        for (int a = 0; a < 2; ++a) {
+            for (int i = 0; i < 3; ++i) g2[a] += U[i][a] * g[i];
+            for (int b = 0; b < 2; ++b)
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) H2[a][b] += U[i][a] * H[i][j] * U[j][b];
+        }
+        double d0, d1;
+        solve2(H2[0][0], 0.5 * (H2[0][1] + H2[1][0]), H2[1][1], g2[0], g2[1], sp, d0, d1);
+        double dp[3];
+        for (int i = 0; i < 3; ++i) dp[i] = U[i][0] * d0 + U[i][1] * d1;
+        if (sp.step_cap_factor > 0.0) {  // newton.hpp:612-620
+            const float4 sc = s.scale[k];
+            const double cap = sp.step_cap_factor * fmax(fmax((double)sc.x, (double)sc.y), (double)sc.z);
+            const double nrm = sqrt(dp[0] * dp[0] + dp[1] * dp[1] + dp[2] * dp[2]);
+            if (nrm > cap)
+                for (int i = 0; i < 3; ++i) dp[i] *= cap / nrm;
+        }
+        if (out.delta)
+            for (int i = 0; i < 3; ++i) out.delta[3 * k + i] = dp[i];
+        if (out.accepted) out.accepted[k] = 1;
+        nsq = dp[0] * dp[0] + dp[1] * dp[1] + dp[2] * dp[2];
+        if (sp.commit) s.pos_sigma[k] = make_float4((float)(p.x + dp[0]), (float)(p.y + dp[1]), (float)(p.z + dp[2]), ps.w);
+    }
+    block_add(nsq, out.norm_sq);
+}
+
+__global__ void __launch_bounds__(256) solve_rotation_k(SceneDev s, CameraDev primary, SolveParams sp,
+                                                        const double* __restrict__ acc, size_t stride,
+                                                        SolveOutputs out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq = 0.0;
+    if (k < s.n) {
+        const float4 ps = s.pos_sigma[k];
+        D3 r;
+        primary_dir(primary, d3(ps.x, ps.y, ps.z), r, out.err);
+        double theta = solve1(acc[stride + k], acc[k], sp);
+        if (sp.theta_cap > 0.0) theta = fmin(fmax(theta, -sp.theta_cap), sp.theta_cap);
+        if (out.delta) out.delta[k] = theta;
+        if (out.accepted) out.accepted[k] = 1;
+        nsq = theta * theta;
+        if (sp.commit) {  // commit_rotation newton.hpp:822-826
+            const double c = cos(theta), sn = sin(theta);
+            const double a0 = c, a1 = sn * r.x, a2 = sn * r.y, a3 = sn * r.z;
+            const float4 q = s.quat[k];
+            const double b0 = q.x, b1 = q.y, b2 = q.z, b3 = q.w;
+            double w = a0 * b0 - a1 * b1 - a2 * b2 - a3 * b3;
+            double x = a0 * b1 + a1 * b0 + a2 * b3 - a3 * b2;
+            double y = a0 * b2 - a1 * b3 + a2 * b0 + a3 * b1;
+            double z = a0 * b3 + a1 * b2 - a2 * b1 + a3 * b0;
+            const double nq = sqrt(w * w + x * x + y * y + z * z);
+            if (!(nq > 0.0) || !isfinite(nq)) {
+                atomicOr(out.err, 4);
+            } else {
+                w /= nq;
+                x /= nq;
+                y /= nq;
+                z /= nq;
+            }
+            s.quat[k] = make_float4((float)w, (float)x, (float)y, (float)z);
+        }
+    }
+    block_add(nsq, out.norm_sq);
+}
+
+__global__ void __launch_bounds__(256) solve_scaling_k(SceneDev s, CameraDev primary, double lambda_lp,
+                                                       const uint8_t* __restrict__ primary_flags, SolveParams sp,
+                                                       const double* __restrict__ acc, size_t stride,
+                                                       SolveOutputs out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq = 0.0;
+    if (k < s.n) {
+        const float4 ps = s.pos_sigma[k];
+        const D3 p = {ps.x, ps.y, ps.z};
+        const float4 sc = s.scale[k];
+        const double sv[3] = {sc.x, sc.y, sc.z};
+        // build_scaling_subspace (newton.hpp:152-184) on the primary entry.
+        bool degenerate = true;
+        double tp[3][2] = {};
+        if (primary_flags[k] & kProjected) {
+            Projected pr;
+            project_kernel(primary, p, s.quat[k], sc, lambda_lp, pr);
+            const Eig2 e = sym2_eigen(pr.s00, pr.s01, pr.s11);
+            degenerate = (e.l1 - e.l0) <= sp.eigengap_rel * fabs(e.l1);
+            double R[9];
+            const float4 q = s.quat[k];
+            quat_to_rot(q.x, q.y, q.z, q.w, R);
+            double JW[6];
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 3; ++j)
+                    JW[3 * i + j] = pr.J[3 * i] * mrow(primary.view, 0, j) + pr.J[3 * i + 1] * mrow(primary.view, 1, j) +
+                                    pr.J[3 * i + 2] * mrow(primary.view, 2, j);
+            double nm[6];  // n = J W R (2x3)
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 3; ++j) nm[3 * i + j] = JW[3 * i] * R[j] + JW[3 * i + 1] * R[3 + j] + JW[3 * i + 2] * R[6 + j];
+            const double vx[2] = {e.v0x, e.v1x}, vy[2] = {e.v0y, e.v1y};
+            double t[2][3];
+            for (int i = 0; i < 2; ++i)
+                for (int c = 0; c < 3; ++c) {
+                    const double vn = vx[i] * nm[c] + vy[i] * nm[3 + c];
+                    t[i][c] = 2.0 * sv[c] * vn * vn;
+                }
+            const double g00 = t[0][0] * t[0][0] + t[0][1] * t[0][1] + t[0][2] * t[0][2];
+            const double g01 = t[0][0] * t[1][0] + t[0][1] * t[1][1] + t[0][2] * t[1][2];
+            const double g11 = t[1][0] * t[1][0] + t[1][1] * t[1][1] + t[1][2] * t[1][2];
+            const Eig2 ge = sym2_eigen(g00, g01, g11);
+            const double cutoff = fmax(1e-30, 1e-12 * fabs(ge.l1));
+            double gp[2][2] = {};
+            const double gl[2] = {ge.l0, ge.l1};
+            const double gvx[2] = {ge.v0x, ge.v1x}, gvy[2] = {ge.v0y, ge.v1y};
+            for (int i = 0; i < 2; ++i)
+                if (gl[i] > cutoff) {
+                    const double inv = 1.0 / gl[i];
+                    gp[0][0] += inv * gvx[i] * gvx[i];
+                    gp[0][1] += inv * gvx[i] * gvy[i];
+                    gp[1][0] += inv * gvy[i] * gvx[i];
+                    gp[1][1] += inv * gvy[i] * gvy[i];
+                }
+            for (int c = 0; c < 3; ++c)
+                for (int j = 0; j < 2; ++j) tp[c][j] = t[0][c] * gp[0][j] + t[1][c] * gp[1][j];
+        }
+        const double g0 = acc[k], g1 = acc[stride + k];
+        const double h00 = acc[2 * stride + k], h01 = acc[3 * stride + k], h11 = acc[4 * stride + k];
+        double dl0, dl1;
+        if (degenerate) {  // newton.hpp:691-703
+            const double d = solve1(h00 + 2.0 * h01 + h11, g0 + g1, sp);
+            dl0 = dl1 = d;
+        } else {
+            solve2(h00, h01, h11, g0, g1, sp, dl0, dl1);
+        }
+        double ds[3];
+        for (int c = 0; c < 3; ++c) ds[c] = tp[c][0] * dl0 + tp[c][1] * dl1;
+        if (sp.scale_cap_factor > 1.0) {  // newton.hpp:717-726
+            double shrink = 1.0;
+            for (int c = 0; c < 3; ++c) {
+                const double lo = sv[c] / sp.scale_cap_factor - sv[c];
+                const double hi = sv[c] * sp.scale_cap_factor - sv[c];
+                if (ds[c] > hi) shrink = fmin(shrink, hi / ds[c]);
+                if (ds[c] < lo) shrink = fmin(shrink, lo / ds[c]);
+            }
+            for (int c = 0; c < 3; ++c) ds[c] *= shrink;
+        }
+        bool feasible = false;  // newton.hpp:727-738
+        for (int i = 0; i <= sp.max_backtrack; ++i) {
+            if (sv[0] + ds[0] > 0.0 && sv[1] + ds[1] > 0.0 && sv[2] + ds[2] > 0.0) {
+                feasible = true;
+                break;
+            }
+            for (int c = 0; c < 3; ++c) ds[c] *= 0.5;
+        }
+        if (!feasible) ds[0] = ds[1] = ds[2] = 0.0;
+        if (out.delta)
+            for (int c = 0; c < 3; ++c) out.delta[3 * k + c] = ds[c];
+        if (out.accepted) out.accepted[k] = feasible ? 1 : 0;
+        if (out.degenerate) out.degenerate[k] = degenerate ? 1 : 0;
+        nsq = ds[0] * ds[0] + ds[1] * ds[1] + ds[2] * ds[2];
+        if (sp.commit && feasible) {
+            float nx = (float)(sv[0] + ds[0]), ny = (float)(sv[1] + ds[1]), nz = (float)(sv[2] + ds[2]);
+            // FP32 storage must keep the reference's strict positivity invariant.
+            if (!(nx > 0.f)) nx = sc.x;
+            if (!(ny > 0.f)) ny = sc.y;
+            if (!(nz > 0.f)) nz = sc.z;
+            s.scale[k] = make_float4(nx, ny, nz, 0.f);
+        }
+    }
+    block_add(nsq, out.norm_sq);
+}
+
+__global__ void __launch_bounds__(256) solve_opacity_k(SceneDev s, SolveParams sp, const double* __restrict__ acc,
+                                                       size_t stride, int n_views, SolveOutputs out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq = 0.0;
+    if (k < s.n) {
+        const float4 ps = s.pos_sigma[k];
+        const double sig = ps.w;
+        double g = 0, h = 0;
+        for (int v = 0; v < n_views; ++v) {
+            g += acc[(static_cast<size_t>(v) * kAccOpColor + 0) * stride + k];
+            h += acc[(static_cast<size_t>(v) * kAccOpColor + 1) * stride + k];
+        }
+        // OpacityBarrier, newton.hpp:187-195
+        const double w = sp.barrier_weight;
+        const double bh = w * (1.0 / (sig * sig) + 1.0 / ((1.0 - sig) * (1.0 - sig)));
+        const double bg = -w * (1.0 / sig - 1.0 / (1.0 - sig));
+        const double d = solve1(h + bh, g + bg, sp);
+        float ns = (float)(sig + d);
+        ns = fminf(fmaxf(ns, sp.sigma_lo), sp.sigma_hi);
+        if (out.delta) out.delta[k] = ns;
+        if (out.accepted) out.accepted[k] = 1;
+        const double dd = (double)ns - sig;
+        nsq = dd * dd;
+        if (sp.commit) s.pos_sigma[k].w = ns;
+    }
+    block_add(nsq, out.norm_sq);
+}
+
+// Cyclic Jacobi for a small symmetric matrix (m <= kMaxSolveViews), ascending order not required.
+template <int MAXM>
+__device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAXM], int m) {
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) v[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        double off = 0, diag = 0;
+        for (int i = 0; i < m; ++i) {
+            diag += a[i][i] * a[i][i];
+            for (int j = i + 1; j < m; ++j) off += a[i][j] * a[i][j];
+        }
+        if (off == 0.0 || off <= 1e-32 * diag) break;
+        for (int p = 0; p < m; ++p)
+            for (int q = p + 1; q < m; ++q) {
+                if (a[p][q] == 0.0) continue;
+                const double theta = (a[q][q] - a[p][p]) / (2 * a[p][q]);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
+                const double c = 1 / sqrt(t * t + 1), sn = t * c;
+                for (int kk = 0; kk < m; ++kk) {
+                    const double akp = a[kk][p], akq = a[kk][q];
+                    a[kk][p] = c * akp - sn * akq;
+                    a[kk][q] = sn * akp + c * akq;
+                }
+                for (int kk = 0; kk < m; ++kk) {
+                    const double apk = a[p][kk], aqk = a[q][kk];
+                    a[p][kk] = c * apk - sn * aqk;
+                    a[q][kk] = sn * apk + c * aqk;
+                }
+                for (int kk = 0; kk < m; ++kk) {
+                    const double vkp = v[kk][p], vkq = v[kk][q];
+                    v[kk][p] = c * vkp - sn * vkq;
+                    v[kk][q] = sn * vkp + c * vkq;
+                }
+            }
+    }
+}
+
+// solve_color (newton.hpp:783-811) from per-view compact accumulators:
+// grad_ch = sum_v g_v phi_v, hess_ch = sum_v h_v phi_v phi_v^T (color_terms,
+// newton.hpp:538-574). Exact spectral repair through the thin SVD of
+// Phi = [phi_v]: H = U K U^T, K = L^1/2 E^T D E L^1/2, null space -> mu.
+__global__ void __launch_bounds__(128) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
+                                                     const double* __restrict__ acc, size_t stride,
+                                                     SolveOutputs out) {
+    constexpr int MV = kMaxSolveViews;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq = 0.0;
+    if (k < s.n) {
+        const int n = s.n_coeffs;
+        const float4 ps = s.pos_sigma[k];
+        const D3 p = {ps.x, ps.y, ps.z};
+        double phi[MV][16];
+        bool have[MV];
+        for (int v = 0; v < cv.n_views; ++v) {
+            have[v] = (cv.flags[v][k] & kProjected) != 0;
+            D3 r;
+            double nr;
+            if (!view_direction(cv.cam[v], p, r, nr)) r = d3(0, 0, 1);
+            sh_basis(r, s.sh_degree, phi[v]);
+        }
+        for (int ch = 0; ch < 3; ++ch) {
+            // Active views for this channel (visible, unclamped).
+            int idx[MV];
+            double gv[MV], hv[MV];
+            int m = 0;
+            for (int v = 0; v < cv.n_views; ++v) {
+                if (!have[v] || (cv.flags[v][k] & (kClamp0 << ch))) continue;
+                const double* a = acc + static_cast<size_t>(v) * kAccOpColor * stride;
+                idx[m] = v;
+                gv[m] = a[(2 + ch) * stride + k];
+                hv[m] = a[(5 + ch) * stride + k];
+                ++m;
+            }
+            double delta[16];
+            for (int i = 0; i < 16; ++i) delta[i] = 0.0;
+            if (n == 1) {
+                double g = 0, h = 0;
+                for (int j = 0; j < m; ++j) {
+                    const double f = phi[idx[j]][0];
+                    g += gv[j] * f;
+                    h += hv[j] * f * f;
+                }
+                delta[0] = solve1(h, g, sp);
+            } else {
+                double grad[16];
+                for (int i = 0; i < n; ++i) {
+                    double t = 0;
+                    for (int j = 0; j < m; ++j) t += gv[j] * phi[idx[j]][i];
+                    grad[i] = t;
+                }
+                // Gram of Phi and its eigen-decomposition.
+                double Gm[MV][MV], E[MV][MV];
+                for (int a = 0; a < m; ++a)
+                    for (int b = 0; b < m; ++b) {
+                        double t = 0;
+                        for (int i = 0; i < n; ++i) t += phi[idx[a]][i] * phi[idx[b]][i];
+                        Gm[a][b] = t;
+                    }
+                jacobi_eig<MV>(Gm, E, m);
+                double lmax = 0;
+                for (int a = 0; a < m; ++a) lmax = fmax(lmax, Gm[a][a]);
+                int keep[MV], r = 0;
+                for (int a = 0; a < m; ++a)
+                    if (Gm[a][a] > 1e-13 * lmax && Gm[a][a] > 0.0) keep[r++] = a;
+                // K (r x r) = sqrt(L_i L_j) sum_v E_vi h_v E_vj
+                double Kt[MV][MV], W[MV][MV];
+                for (int i = 0; i < r; ++i)
+                    for (int j = 0; j < r; ++j) {
+                        double t = 0;
+                        for (int v = 0; v < m; ++v) t += E[v][keep[i]] * hv[v] * E[v][keep[j]];
+                        Kt[i][j] = t * sqrt(Gm[keep[i]][keep[i]] * Gm[keep[j]][keep[j]]);
+                    }
+                jacobi_eig<MV>(Kt, W, r);
+                double lam_abs_max = 0, lam_min = 0;
+                for (int i = 0; i < r; ++i) {
+                    lam_abs_max = fmax(lam_abs_max, fabs(Kt[i][i]));
+                    lam_min = (i == 0) ? Kt[i][i] : fmin(lam_min, Kt[i][i]);
+                }
+                if (r < n) lam_min = fmin(lam_min, 0.0);
+                const double mu = fmax(sp.mu_min, sp.eig_floor_rel * lam_abs_max);
+                const bool keep_h = lam_min >= mu;  // newton.hpp:231: PD input is solved unmodified
+                // Orthonormal range basis u_i = Phi E_i / sqrt(L_i); eigenvectors y_i = sum_j W_ji u_j.
+                double resid[16];
+                for (int i = 0; i < n; ++i) resid[i] = grad[i];
+                for (int e = 0; e < r; ++e) {
+                    double y[16];
+                    for (int i = 0; i < n; ++i) {
+                        double t = 0;
+                        for (int j = 0; j < r; ++j) {
+                            const int a = keep[j];
+                            double u = 0;
+                            for (int v = 0; v < m; ++v) u += phi[idx[v]][i] * E[v][a];
+                            t += W[j][e] * u / sqrt(Gm[a][a]);
+                        }
+                        y[i] = t;
+                    }
+                    double yg = 0;
+                    for (int i = 0; i < n; ++i) yg += y[i] * grad[i];
+                    const double lam = Kt[e][e];
+                    const double l = keep_h ? lam : fmax(fabs(lam), mu);
+                    for (int i = 0; i < n; ++i) {
+                        delta[i] -= (yg / l) * y[i];
+                        resid[i] -= yg * y[i];
+                    }
+                }
+                if (!keep_h)
+                    for (int i = 0; i < n; ++i) delta[i] -= resid[i] / mu;
+            }
+            if (sp.color_cap > 0.0) {
+                double nrm = 0;
+                for (int i = 0; i < n; ++i) nrm += delta[i] * delta[i];
+                nrm = sqrt(nrm);
+                if (nrm > sp.color_cap)
+                    for (int i = 0; i < n; ++i) delta[i] *= sp.color_cap / nrm;
+            }
+            for (int i = 0; i < n; ++i) {
+                nsq += delta[i] * delta[i];
+                if (out.delta) out.delta[48 * static_cast<size_t>(k) + 16 * ch + i] = delta[i];
+                if (sp.commit) {
+                    float* c = s.sh + (static_cast<size_t>(16 * ch + i)) * s.n + k;
+                    *c = (float)((double)*c + delta[i]);
+                }
+            }
+            if (out.delta)
+                for (int i = n; i < 16; ++i) out.delta[48 * static_cast<size_t>(k) + 16 * ch + i] = 0.0;
+        }
+        if (out.accepted) out.accepted[k] = 1;
+    }
+    block_add(nsq, out.norm_sq);
+}
+
+}  // namespace
+
+void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, double lambda_lp,
+                  const uint8_t* primary_flags, const ColorViews& cv, const SolveParams& sp, const double* acc,
+                  size_t stride, const SolveOutputs& out, cudaStream_t s) {
+    const int n = scene.n;
+    if (n == 0) return;
+    StageScope st(NGS_STAGE_SOLVE, s);
+    switch (attr) {
+        case NGS_POSITION:
+            solve_position_k<<<blocks_for(n), 256, 0, s>>>(scene, primary, sp, acc, stride, out);
+            break;
+        case NGS_ROTATION:
+            solve_rotation_k<<<blocks_for(n), 256, 0, s>>>(scene, primary, sp, acc, stride, out);
+            break;
+        case NGS_SCALING:
+            solve_scaling_k<<<blocks_for(n), 256, 0, s>>>(scene, primary, lambda_lp, primary_flags, sp, acc, stride,
+                                                          out);
+            break;
+        case NGS_OPACITY:
+            solve_opacity_k<<<blocks_for(n), 256, 0, s>>>(scene, sp, acc, stride, cv.n_views, out);
+            break;
+        case NGS_COLOR:
+            solve_color_k<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+            break;
+    }
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace ngsb

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA C-ABI library against the reference oracle, stage by stage.
+
+Every comparison drives both implementations through the same C-ABI
+(include/ngs_b200.h) on the reference's own fixtures (tests/refimpl.py).
+Tolerances (SURVEY.md §8a "Parity contract"):
+  * bit-exact: splat order, tile offsets, per-tile kernel lists (rasterizer.hpp:228-263);
+  * FP32 path vs float64 reference: rel_error (fd.hpp:31-34) with an absolute
+    floor of FLOOR x max|ref| per quantity, <= TOL.
+"""
+import numpy as np
+import pytest
+
+from paper_2501_13975_b200 import capi
+from refimpl import check_fixture, random_scene, ref, synth, test_camera
+
+pytestmark = pytest.mark.gpu
+
+FLOOR = 1e-3   # absolute floor, fraction of max|ref| of the quantity
+TOL = 1e-4     # FP32 vs float64 reference
+
+
+def qerr(gpu, refv, floor_frac=FLOOR):
+    gpu = np.asarray(gpu, np.float64)
+    refv = np.asarray(refv, np.float64)
+    floor = max(floor_frac * float(np.max(np.abs(refv))) if refv.size else 0.0, 1e-300)
+    if refv.size == 0:
+        return 0.0
+    return float(np.max(np.abs(gpu - refv) / np.maximum(np.maximum(np.abs(gpu), np.abs(refv)), floor)))
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    return capi.product()
+
+
+def f32(scene):
+    """Round a fixture's parameters to FP32 so both sides see identical inputs
+    (the device stores FP32 parameters; the reference keeps float64)."""
+    s = scene.copy()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        setattr(s, f, getattr(s, f).astype(np.float32).astype(np.float64))
+    q = s.quaternion
+    assert np.all(np.abs(np.linalg.norm(q, axis=1) - 1) < 1e-6)
+    return s
+
+
+def pair(gpu, scene, quantize=True):
+    if quantize:
+        scene = f32(scene)
+    g = gpu.context()
+    r = ref().context()
+    g.set_scene(scene)
+    r.set_scene(scene)
+    return g, r
+
+
+# ---------------------------------------------------------------------------
+# K1-K6: projection, binning, forward raster
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("seed", [103, 104, 105])
+def test_render_default_cutoffs(gpu, seed):
+    scene = random_scene(seed, 60)
+    cam = test_camera((0.2, 0.1, -3.6), 64, 64)
+    g, r = pair(gpu, scene)
+    a = g.render(cam)
+    b = r.render(cam)
+    err = float(np.max(np.abs(a - b)))
+    print(f"render seed {seed}: max abs {err:.3e}")
+    assert err < 1e-4
+
+
+def test_render_reference_mode(gpu):
+    scene = random_scene(101, 40)
+    cam = test_camera((0.3, -0.2, -3.4), 64, 48)
+    g, r = pair(gpu, scene)
+    opts = gpu.reference_raster()
+    a = g.render(cam, opts)
+    b = r.render(cam, ref().reference_raster())
+    err = float(np.max(np.abs(a - b)))
+    print(f"reference-mode render: max abs {err:.3e}")
+    assert err < 1e-4
+
+
+def test_single_centered_kernel_known_answer(gpu):
+    """test_rasterizer.cpp:218-229: pixel (32, 32) == 0.8 * red."""
+    cam = test_camera((0, 0, -4), 65, 65)
+    s = capi.Scene.empty(1, 3)
+    s.scale[:] = 0.05
+    s.sigma[:] = 0.8
+    s.sh[0, :, 0] = (np.array([1.0, 0.0, 0.0]) - 0.5) / 0.28209479177387814
+    s.background[:] = 0
+    g = gpu.context()
+    g.set_scene(s)
+    img = g.render(cam)
+    assert abs(img[32, 32, 0] - 0.8) < 1e-6
+    assert img[32, 32, 1] == 0.0 and img[32, 32, 2] == 0.0
+
+
+@pytest.mark.parametrize("seed", [83, 97])
+def test_binning_bit_exact(gpu, seed):
+    scene = random_scene(seed, 40)
+    cam = test_camera((0.5, -0.3, -3.5), 80, 48)
+    g, r = pair(gpu, scene)
+    target = np.zeros((48, 80, 3))
+    g.build_view(0, cam, target)
+    r.build_view(0, cam, target)
+    sg, sr = g.view_splats(0), r.view_splats(0)
+    assert np.array_equal(sg["kernel"], sr["kernel"])
+    assert np.array_equal(sg["tile_offsets"], sr["tile_offsets"])
+    assert np.array_equal(sg["tile_indices"], sr["tile_indices"])
+    assert qerr(sg["pixel"], sr["pixel"], 0) < 1e-12
+    assert qerr(sg["cov2d"], sr["cov2d"], 0) < 1e-10
+
+
+def test_empty_scene(gpu):
+    cam = test_camera((0, 0, -4), 32, 32)
+    s = capi.Scene.empty(0, 3)
+    s.background[:] = [0.1, 0.2, 0.3]
+    g = gpu.context()
+    g.set_scene(s)
+    img = g.render(cam)
+    assert np.allclose(img, [0.1, 0.2, 0.3], atol=1e-7)
+
+
+# ---------------------------------------------------------------------------
+# K7: loss fields
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_loss_fields(gpu, seed):
+    scene, cam, target = check_fixture(seed)
+    g, r = pair(gpu, scene)
+    lg = g.build_view(0, cam, target)
+    lr = r.build_view(0, cam, target)
+    gg, hg = g.view_loss_derivs(0)
+    gr, hr = r.view_loss_derivs(0)
+    e_img = float(np.max(np.abs(g.view_image(0) - r.view_image(0))))
+    e_g, e_h = qerr(gg, gr), qerr(hg, hr)
+    print(f"loss seed {seed}: value {lg:.9g} vs {lr:.9g}; image {e_img:.2e} grad {e_g:.2e} hess {e_h:.2e}")
+    assert abs(lg - lr) <= 1e-5 * abs(lr)
+    assert e_g < 1e-3 and e_h < 1e-3
+
+
+# ---------------------------------------------------------------------------
+# K8: accumulated terms, K9: solves
+# ---------------------------------------------------------------------------
+
+def _views(lib_ctx, scene_fixture):
+    scene, cam, target, secs = scene_fixture
+    lib_ctx.build_view(0, cam, target)
+    for i, (c, t) in enumerate(secs):
+        lib_ctx.build_view(1 + i, c, t)
+    return list(range(1, 1 + len(secs)))
+
+
+@pytest.fixture(scope="module")
+def newton_fixture():
+    scene, cam, target = check_fixture(7)
+    # Two neighbour views at reduced resolution (secondaries), targets from a reference context.
+    r = ref().context()
+    r.set_scene(scene)
+    secs = []
+    for eye in [(1.0, 0.5, -3.0), (-1.2, 0.3, -2.9)]:
+        c = test_camera(eye, 32, 32)
+        secs.append((c, r.render(c)))
+    return scene, cam, target, secs
+
+
+ATTRS = [capi.POSITION, capi.ROTATION, capi.SCALING, capi.OPACITY, capi.COLOR]
+
+
+@pytest.mark.parametrize("attr", ATTRS)
+def test_accumulated_terms(gpu, newton_fixture, attr):
+    g, r = pair(gpu, newton_fixture[0])
+    sec = _views(g, newton_fixture)
+    _views(r, newton_fixture)
+    gg, hg, vg = g.accumulate(attr, 0, sec)
+    gr, hr, vr = r.accumulate(attr, 0, sec)
+    e_g, e_h = qerr(gg, gr), qerr(hg, hr)
+    print(f"{capi.ATTRIBUTES[attr]} terms: grad {e_g:.2e} hess {e_h:.2e} visible {int(vg.sum())}/{int(vr.sum())}")
+    assert np.array_equal(vg, vr)
+    assert e_g < 1e-3 and e_h < 1e-3
+
+
+@pytest.mark.parametrize("attr", ATTRS)
+def test_newton_step(gpu, newton_fixture, attr):
+    g, r = pair(gpu, newton_fixture[0])
+    sec = _views(g, newton_fixture)
+    _views(r, newton_fixture)
+    dg = g.newton_step(attr, 0, sec)
+    dr = r.newton_step(attr, 0, sec)
+    e = qerr(dg["delta"], dr["delta"])
+    print(f"{capi.ATTRIBUTES[attr]} solve: delta {e:.2e} norm {dg['delta_norm_sq']:.6g} vs {dr['delta_norm_sq']:.6g}")
+    assert e < 1e-3
+    assert np.array_equal(dg["accepted"], dr["accepted"])
+    if attr == capi.SCALING:
+        assert np.array_equal(dg["degenerate"], dr["degenerate"])
+    sg, sr = g.get_scene(), r.get_scene()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        e = qerr(getattr(sg, f), getattr(sr, f))
+        print(f"  post-commit {f}: {e:.2e}")
+        assert e < TOL, f
+
+
+# ---------------------------------------------------------------------------
+# Trainer::step
+# ---------------------------------------------------------------------------
+
+def test_trainer_step(gpu):
+    d = synth(seed=23, kernels=20, views=4, probe_views=0, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    g, r = pair(gpu, d["init"], quantize=False)
+    for ctx, lib in ((g, gpu), (r, ref())):
+        cfg = lib.default_train()
+        cfg.knn = 2
+        cfg.secondary_downsample = 2
+        ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"], d["probe"], d["secondary"],
+                              d["secondary_downsample"])
+    assert g.trainer_neighbors(0) == r.trainer_neighbors(0)
+    for view in d["train"][:2]:
+        rg = g.trainer_step(view)
+        rr = r.trainer_step(view)
+        print("delta norms", list(rg.delta_norms), list(rr.delta_norms))
+        for i in range(5):
+            assert abs(rg.delta_norms[i] - rr.delta_norms[i]) <= 1e-3 * max(abs(rr.delta_norms[i]), 1e-9)
+    sg, sr = g.get_scene(), r.get_scene()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        e = qerr(getattr(sg, f), getattr(sr, f))
+        print(f"post-step {f}: {e:.2e}")
+        assert e < 1e-4, f
