@@ -3,8 +3,10 @@
  * reference-facing boundary in ngs_b200.h; used by bench.py).
  *
  * When profiling is enabled every kernel launch of the context is bracketed by
- * CUDA events on the context's stream; ngs_profile_read resolves them into
- * per-stage device time. Counters (launches, contributing pairs) are always on.
+ * CUDA events on the context's stream and the 1+K views of a step run
+ * serialised (so per-launch times do not overlap); ngs_profile_read resolves
+ * them into per-stage device time. Counters (launches, contributing pairs)
+ * are always on.
  */
 #ifndef NGS_B200_PROFILE_H
 #define NGS_B200_PROFILE_H
@@ -47,6 +49,8 @@ int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out);
 
 /* FP32 FFMA throughput microbenchmark on the context's device (TFLOP/s). */
 int32_t ngs_microbench_fp32(ngs_context* ctx, double* tflops);
+/* FP64 DFMA throughput microbenchmark (TFLOP/s). */
+int32_t ngs_microbench_fp64(ngs_context* ctx, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -453,6 +453,11 @@ class Context:
         self._call("ngs_microbench_fp32", C.byref(v))
         return v.value
 
+    def microbench_fp64(self) -> float:
+        v = C.c_double()
+        self._call("ngs_microbench_fp64", C.byref(v))
+        return v.value
+
     def barrier_weight(self) -> float:
         v = C.c_double()
         self._call("ngs_trainer_barrier_weight", C.byref(v))

@@ -333,7 +333,7 @@ template <int PASS>
 __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
     constexpr int B = TR::BATCH, NC = TR::NC, NA = TR::NACC;
-    __shared__ float s_px[B], s_py[B], s_qa[B], s_qb[B], s_qc[B], s_sig[B], s_c[3][B];
+    __shared__ float s_px[B], s_py[B], s_qa[B], s_qb[B], s_qc[B], s_sig[B], s_c[3][B], s_qmax[B];
     __shared__ float s_const[(NC > 0 ? NC : 1) * B];
     __shared__ float s_acc[NA][B];
     __shared__ int s_kid[B];
@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
                 s_c[0][i] = rb.z;
                 s_c[1][i] = rb.w;
                 s_c[2][i] = rc.x;
+                s_qmax[i] = reject_bound(rb.y, a.cutoff);
             }
             for (int c = 0; c < NA; ++c) s_acc[c][i] = 0.f;
             s_cnt[i] = 0;
@@ -409,8 +410,8 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
             bool contrib = false;
             if (base + j <= last) {
                 const float qa = s_qa[j], qb = s_qb[j], qc = s_qc[j], sig = s_sig[j];
-                const SplatEval ev = eval_splat(s_px[j], s_py[j], qa, qb, qc, sig, fx, fy);
-                if (!(ev.alpha < a.cutoff)) {
+                SplatEval ev;
+                if (eval_splat(s_px[j], s_py[j], qa, qb, qc, sig, fx, fy, s_qmax[j], ev) && !(ev.alpha < a.cutoff)) {
                     contrib = true;
                     const float Ti = T;
                     const float w = blend_weight(Ti, ev.alpha);
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
                         const float cc = s_c[c][j];
                         const double Pn = __fma_rn(static_cast<double>(w), cc, P[c]);
                         const float behind =
-                            (base + j == last) ? a.bg[c] : static_cast<float>((Cf[c] - Pn) / static_cast<double>(Tn));
+                            (base + j == last) ? a.bg[c] : static_cast<float>(Cf[c] - Pn) * __frcp_rn(Tn);
                         acol[c] = cc - behind;
                         P[c] = Pn;
                     }
@@ -538,22 +539,14 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
                             v[5 + ch] = hl[ch] * w * w;
                         }
                     }
-                } else if (base + j == last) {
-                    // unreachable: the last recorded splat always passes the cutoff
                 }
             }
             const unsigned ballot = __ballot_sync(0xffffffffu, contrib);
             if (ballot) {
-#pragma unroll
-                for (int c = 0; c < NA; ++c) {
-                    float t = v[c];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                    v[c] = t;
-                }
+                const float sum = warp_reduce_scatter<NA>(v, lane);
+                const int idx = reduce_index<NA>(lane);
+                if (reduce_representative<NA>(lane) && idx < NA) atomicAdd(&s_acc[idx][j], sum);
                 if (lane == 0) {
-#pragma unroll
-                    for (int c = 0; c < NA; ++c) atomicAdd(&s_acc[c][j], v[c]);
                     atomicAdd(&s_cnt[j], __popc(ballot));
                     block_pairs += __popc(ballot);
                 }
@@ -601,7 +594,7 @@ void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const Cam
 
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
                      unsigned long long* contrib_pairs, cudaStream_t s) {
-    if (v.pairs == 0) return;
+    if (v.pairs == 0 || v.n == 0) return;
     BackwardArgs a;
     a.tiles_x = v.cam.tiles_x;
     a.W = v.W;

@@ -95,6 +95,13 @@ struct ngs_context {
     TrainerState trainer;
     Profiler prof;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // Per-view streams: the 1+K views of a step render and back-propagate concurrently.
+    std::array<cudaStream_t, kMaxSolveViews> vs{};
+    cudaEvent_t fork_ev = nullptr;
+    std::array<cudaEvent_t, kMaxSolveViews> join_ev{};
+    DevBuf<int> overflow;
+    DevBuf<float4> snap_ps, snap_sc, snap_q;
+    DevBuf<float> snap_sh;
     unsigned long long contrib_pairs_total = 0;
 
     ~ngs_context() {
@@ -111,8 +118,18 @@ struct ngs_context {
         visible.release();
         out_delta.release();
         out_flags.release();
+        overflow.release();
+        snap_ps.release();
+        snap_sc.release();
+        snap_q.release();
+        snap_sh.release();
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        for (auto e : join_ev)
+            if (e) cudaEventDestroy(e);
+        for (auto s : vs)
+            if (s) cudaStreamDestroy(s);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -126,6 +143,18 @@ struct ngs_context {
             if (e & 2) throw Error(NGS_ERR_DEGENERATE, "view_direction: point coincides with camera center");
             if (e & 4) throw Error(NGS_ERR_INVALID_INPUT, "renormalize_quaternion: zero or non-finite quaternion");
             throw Error(NGS_ERR_NUMERICAL, "device error flag " + std::to_string(e));
+        }
+    }
+
+    // Fork the per-view streams off the main stream / join them back.
+    void fork(int nv) {
+        CUDA_CHECK(cudaEventRecord(fork_ev, stream));
+        for (int i = 0; i < nv; ++i) CUDA_CHECK(cudaStreamWaitEvent(vs[i], fork_ev, 0));
+    }
+    void join(int nv) {
+        for (int i = 0; i < nv; ++i) {
+            CUDA_CHECK(cudaEventRecord(join_ev[i], vs[i]));
+            CUDA_CHECK(cudaStreamWaitEvent(stream, join_ev[i], 0));
         }
     }
 
@@ -344,11 +373,18 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         CUDA_CHECK(cudaEventCreate(&ctx->ev0));
         CUDA_CHECK(cudaEventCreate(&ctx->ev1));
+        CUDA_CHECK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+        for (int i = 0; i < kMaxSolveViews; ++i) {
+            CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->vs[i], cudaStreamNonBlocking));
+            CUDA_CHECK(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
+        }
+        ctx->overflow.ensure(1);
+        CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), ctx->stream));
         ctx->err.ensure(1);
         ctx->norm.ensure(1);
-        ctx->pairs.ensure(4);
+        ctx->pairs.ensure(5);
         CUDA_CHECK(cudaMemsetAsync(ctx->err.ptr, 0, sizeof(int), ctx->stream));
-        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 4 * sizeof(unsigned long long), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 5 * sizeof(unsigned long long), ctx->stream));
         ctx->scene.n = 0;
         ctx->scene.sh_degree = 0;
         ctx->scene.n_coeffs = 1;
@@ -609,18 +645,23 @@ int acc_components(int pass) {
 
 // Zero the accumulators and run one backward pass over views[0..nv).
 // Opacity/colour keep per-view accumulators (colour needs each view's phi).
-void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv, uint8_t* visible) {
+void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv, uint8_t* visible,
+                     bool concurrent = false) {
     const int n = ctx->scene.n;
     const size_t stride = static_cast<size_t>(std::max(n, 1));
     const int comps = acc_components(pass) * (pass == kPassOpacityColor ? nv : 1);
     ctx->acc.ensure(stride * comps);
     CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
+    concurrent = concurrent && nv <= kMaxSolveViews && !ctx->prof.enabled;
+    if (concurrent) ctx->fork(nv);
     for (int i = 0; i < nv; ++i) {
         ViewSlot& v = *views[i];
-        compute_pass_consts(pass, ctx->scene, v, views[0]->cam, ctx->stream);
+        cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
+        compute_pass_consts(pass, ctx->scene, v, views[0]->cam, s);
         double* acc = ctx->acc.ptr + (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0);
-        launch_backward(pass, ctx->scene, v, acc, stride, visible, ctx->pairs.ptr + pass, ctx->stream);
+        launch_backward(pass, ctx->scene, v, acc, stride, visible, ctx->pairs.ptr + pass, s);
     }
+    if (concurrent) ctx->join(nv);
 }
 
 ColorViews color_views(ViewSlot* const* views, int nv) {
@@ -936,29 +977,42 @@ int32_t ngs_trainer_barrier_weight(ngs_context* ctx, double* out) {
 
 namespace {
 
-// Render + loss for every view of the step (build_view_context x (1+K)).
-void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nbrs) {
+// Render + loss for every view of the step (build_view_context x (1+K)); one
+// stream per view, no host synchronisation (pair-capacity overflow is flagged
+// on the device and handled by the caller).
+void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nbrs, bool upload_targets) {
     TrainerState& T = ctx->trainer;
     const int nv = 1 + static_cast<int>(nbrs.size());
+    // Profiling serialises the views so per-launch event times do not overlap.
+    const bool concurrent = !ctx->prof.enabled;
+    if (concurrent) ctx->fork(nv);
     for (int i = 0; i < nv; ++i) {
         ViewSlot& v = T.views[i];
+        cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
         const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
         const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
-        upload_camera(cam, v.cam);
-        v.raster = to_raster(&T.cfg.raster);
-        v.loss = to_loss(&T.cfg.loss);
-        const size_t npx = static_cast<size_t>(cam.width) * cam.height;
-        v.target.ensure(3 * npx);
-        if (T.cfg.host_targets) {
-            const float* src = (i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id];
-            CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyHostToDevice, ctx->stream));
-        } else {
-            const float* src = (i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr;
-            CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (upload_targets) {
+            upload_camera(cam, v.cam);
+            v.raster = to_raster(&T.cfg.raster);
+            v.loss = to_loss(&T.cfg.loss);
+            const size_t npx = static_cast<size_t>(cam.width) * cam.height;
+            v.target.ensure(3 * npx);
+            if (T.cfg.host_targets) {
+                const float* src = (i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id];
+                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyHostToDevice, s));
+            } else {
+                const float* src = (i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr;
+                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyDeviceToDevice, s));
+            }
         }
-        render_view(ctx->scene, v, false, ctx->err.ptr, ctx->stream);
-        compute_loss(v, ctx->stream);
+        RenderSync rs;
+        rs.exact = false;
+        rs.overflow = ctx->overflow.ptr;
+        rs.pair_counter = ctx->pairs.ptr + 4;
+        render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
+        compute_loss(v, s);
     }
+    if (concurrent) ctx->join(nv);
 }
 
 }  // namespace
@@ -981,28 +1035,51 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
         opts.barrier_weight = T.barrier_weight;
         const SolveParams base = to_solve(&opts, 1);
         ctx->norm.ensure(5);
-        CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
-        CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), ctx->stream));
-        render_step_views(ctx, view_id, nbrs);
-        for (int pass_i = 0; pass_i < 5; ++pass_i) {
-            const int attr = T.cfg.order[pass_i];
-            const int pass = pass_of(attr);
-            // Opacity and colour share one traversal when adjacent (same captures, trainer.hpp:412-415).
-            const bool reuse = (attr == NGS_COLOR && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_OPACITY) ||
-                               (attr == NGS_OPACITY && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_COLOR);
-            if (!reuse) accumulate_pass(ctx, pass, views.data(), nv, nullptr);
-            SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
-            launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
-                         color_views(views.data(), nv), base, ctx->acc.ptr, stride, so, ctx->stream);
-            const bool geometry = attr == NGS_POSITION || attr == NGS_ROTATION || attr == NGS_SCALING;
-            if (geometry && pass_i + 1 < 5) render_step_views(ctx, view_id, nbrs);
-        }
-        CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
+        cudaStream_t s = ctx->stream;
+        // Parameter snapshot: restored if a sync-free render overflowed its pair capacity.
+        ctx->snap_ps.ensure(stride);
+        ctx->snap_sc.ensure(stride);
+        ctx->snap_q.ensure(stride);
+        ctx->snap_sh.ensure(48 * stride);
+        CUDA_CHECK(cudaMemcpyAsync(ctx->snap_ps.ptr, ctx->pos_sigma.ptr, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(ctx->snap_sc.ptr, ctx->scale.ptr, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(ctx->snap_q.ptr, ctx->quat.ptr, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(ctx->snap_sh.ptr, ctx->sh.ptr, sizeof(float) * 48 * n, cudaMemcpyDeviceToDevice, s));
         double norms[5];
-        CUDA_CHECK(cudaMemcpyAsync(norms, ctx->norm.ptr, sizeof(norms), cudaMemcpyDeviceToHost, ctx->stream));
-        ctx->check_err();
         float ms = 0;
-        CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        for (int attempt = 0;; ++attempt) {
+            CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
+            CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), s));
+            CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
+            render_step_views(ctx, view_id, nbrs, true);
+            for (int pass_i = 0; pass_i < 5; ++pass_i) {
+                const int attr = T.cfg.order[pass_i];
+                const int pass = pass_of(attr);
+                // Opacity and colour share one traversal when adjacent (same captures, trainer.hpp:412-415).
+                const bool reuse = (attr == NGS_COLOR && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_OPACITY) ||
+                                   (attr == NGS_OPACITY && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_COLOR);
+                if (!reuse) accumulate_pass(ctx, pass, views.data(), nv, nullptr, true);
+                SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
+                launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
+                             color_views(views.data(), nv), base, ctx->acc.ptr, stride, so, s);
+                const bool geometry = attr == NGS_POSITION || attr == NGS_ROTATION || attr == NGS_SCALING;
+                if (geometry && pass_i + 1 < 5) render_step_views(ctx, view_id, nbrs, false);
+            }
+            CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
+            int overflow = 0;
+            CUDA_CHECK(cudaMemcpyAsync(norms, ctx->norm.ptr, sizeof(norms), cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(&overflow, ctx->overflow.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+            ctx->check_err();
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            if (!overflow) break;
+            if (attempt >= 8) throw Error(NGS_ERR_INTERNAL, "pair capacity retry limit exceeded");
+            // Grow every view's pair capacity and re-run the step from the snapshot.
+            for (auto& v : T.views) v.pair_cap = std::max<size_t>(2 * v.pair_cap, 4096);
+            CUDA_CHECK(cudaMemcpyAsync(ctx->pos_sigma.ptr, ctx->snap_ps.ptr, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+            CUDA_CHECK(cudaMemcpyAsync(ctx->scale.ptr, ctx->snap_sc.ptr, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+            CUDA_CHECK(cudaMemcpyAsync(ctx->quat.ptr, ctx->snap_q.ptr, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+            CUDA_CHECK(cudaMemcpyAsync(ctx->sh.ptr, ctx->snap_sh.ptr, sizeof(float) * 48 * n, cudaMemcpyDeviceToDevice, s));
+        }
         T.step_count += 1;
         for (double d : norms)
             if (!std::isfinite(d)) throw Error(NGS_ERR_NUMERICAL, "trainer: non-finite update, aborting");
@@ -1024,24 +1101,46 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
 
 namespace {
 
-__global__ void ffma_peak_k(float* out, int iters) {
-    float a0 = threadIdx.x * 1e-3f, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
-          a7 = a0 + 7;
-    const float b = 0.999f, c = 1e-4f;
+template <typename T>
+__global__ void fma_peak_k(T* out, int iters) {
+    T a0 = threadIdx.x * T(1e-3), a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+      a7 = a0 + 7;
+    const T b = T(0.999), c = T(1e-4);
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-            a0 = fmaf(a0, b, c);
-            a1 = fmaf(a1, b, c);
-            a2 = fmaf(a2, b, c);
-            a3 = fmaf(a3, b, c);
-            a4 = fmaf(a4, b, c);
-            a5 = fmaf(a5, b, c);
-            a6 = fmaf(a6, b, c);
-            a7 = fmaf(a7, b, c);
+            a0 = fma(a0, b, c);
+            a1 = fma(a1, b, c);
+            a2 = fma(a2, b, c);
+            a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c);
+            a5 = fma(a5, b, c);
+            a6 = fma(a6, b, c);
+            a7 = fma(a7, b, c);
         }
     }
-    if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 12345.f) out[0] = 1.f;
+    if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == T(12345)) out[0] = T(1);
+}
+
+template <typename T>
+double fma_peak(ngs_context* ctx) {
+    int sms = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    DevBuf<T> out;
+    out.ensure(1);
+    const int blocks = sms * 8, threads = 256, iters = sizeof(T) == 4 ? 4096 : 1024;
+    fma_peak_k<T><<<blocks, threads, 0, ctx->stream>>>(out.ptr, 64);  // warm-up
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
+    fma_peak_k<T><<<blocks, threads, 0, ctx->stream>>>(out.ptr, iters);
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    out.release();
+    const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * threads;
+    return flops / (ms * 1e-3) / 1e12;
 }
 
 }  // namespace
@@ -1057,7 +1156,7 @@ int32_t ngs_profile_reset(ngs_context* ctx) {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         ctx->prof.reset();
-        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 4 * sizeof(unsigned long long), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 5 * sizeof(unsigned long long), ctx->stream));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -1067,33 +1166,25 @@ int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out) {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         ctx->prof.resolve();
-        unsigned long long p[4];
+        unsigned long long p[5];
         CUDA_CHECK(cudaMemcpy(p, ctx->pairs.ptr, sizeof(p), cudaMemcpyDeviceToHost));
         *out = ctx->prof.stats;
         for (int i = 0; i < 4; ++i) out->contrib_pairs[i] = static_cast<int64_t>(p[i]);
+        out->raster_pairs = static_cast<int64_t>(p[4]);
     });
 }
 
 int32_t ngs_microbench_fp32(ngs_context* ctx, double* tflops) {
     return guarded([&] {
         CUDA_CHECK(cudaSetDevice(ctx->device));
-        int sms = 0;
-        CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-        DevBuf<float> out;
-        out.ensure(1);
-        const int blocks = sms * 8, threads = 256, iters = 4096;
-        ffma_peak_k<<<blocks, threads, 0, ctx->stream>>>(out.ptr, 64);  // warm-up
-        CUDA_LAUNCH_CHECK();
-        CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
-        ffma_peak_k<<<blocks, threads, 0, ctx->stream>>>(out.ptr, iters);
-        CUDA_LAUNCH_CHECK();
-        CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
-        CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
-        float ms = 0;
-        CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * threads;
-        *tflops = flops / (ms * 1e-3) / 1e12;
-        out.release();
+        *tflops = fma_peak<float>(ctx);
+    });
+}
+
+int32_t ngs_microbench_fp64(ngs_context* ctx, double* tflops) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        *tflops = fma_peak<double>(ctx);
     });
 }
 

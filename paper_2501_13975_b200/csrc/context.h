@@ -59,7 +59,8 @@ struct ViewSlot {
     int W = 0, H = 0, T = 0;
     int n = 0;         // kernels projected
     int entries = 0;   // projected (non-culled) kernels
-    int pairs = 0;
+    int pairs = 0;          // exact count when known on the host, else -1
+    size_t pair_cap = 0;    // capacity of the pair buffers (sync-free renders)
     RasterParams raster{};
     LossParams loss{};
     double loss_value = 0.0;
@@ -168,7 +169,13 @@ struct StageScope {
 
 // Launch wrappers (render.cu, loss.cu, backward.cu, solve.cu).
 void upload_camera(const ngs_camera& c, CameraDev& out);
-void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s);
+struct RenderSync {
+    bool exact = true;                            // read the pair count back (one host sync)
+    int* overflow = nullptr;                      // sync-free: set when the pair capacity was exceeded
+    unsigned long long* pair_counter = nullptr;   // optional: adds the (tile, splat) pair count
+};
+void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
+                 const RenderSync& sync = RenderSync{});
 void compute_loss(ViewSlot& v, cudaStream_t s);
 
 }  // namespace ngsb

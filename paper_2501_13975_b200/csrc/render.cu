@@ -189,9 +189,15 @@ __global__ void gather_counts_k(int n, const int* order, const int* tiles_touche
 
 // K3: emit (tile, kernel) pairs in depth order; a later stable sort on the
 // tile key alone keeps depth order (ties by kernel id) inside every tile.
-__global__ void emit_pairs_k(int n, int tiles_x, const int* order, const int* offsets, const int4* rect,
-                             const int* tiles_touched, unsigned int* keys, int* vals) {
+__global__ void emit_pairs_k(int n, int tiles_x, int cap, const int* order, const int* offsets, const int4* rect,
+                             const int* tiles_touched, unsigned int* keys, int* vals, int* overflow,
+                             unsigned long long* pair_counter) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r == 0) {
+        const int total = offsets[n];
+        if (total > cap && overflow) atomicOr(overflow, 1);
+        if (pair_counter) atomicAdd(pair_counter, static_cast<unsigned long long>(total));
+    }
     if (r >= n) return;
     const int k = order[r];
     if (tiles_touched[k] == 0) return;
@@ -199,17 +205,21 @@ __global__ void emit_pairs_k(int n, int tiles_x, const int* order, const int* of
     int o = offsets[r];
     for (int ty = rc.y; ty <= rc.w; ++ty)
         for (int tx = rc.x; tx <= rc.z; ++tx) {
-            keys[o] = static_cast<unsigned int>(ty * tiles_x + tx);
-            vals[o] = k;
+            if (o < cap) {
+                keys[o] = static_cast<unsigned int>(ty * tiles_x + tx);
+                vals[o] = k;
+            }
             ++o;
         }
 }
 
-// K5: per-tile [start, end) ranges from the tile-sorted key array.
-__global__ void tile_ranges_k(int pairs, const unsigned int* keys, int2* ranges) {
+// K5: per-tile [start, end) ranges from the tile-sorted key array (padding
+// keys >= T sort after every real key and are ignored).
+__global__ void tile_ranges_k(int pairs, int T, const unsigned int* keys, int2* ranges) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= pairs) return;
     const unsigned int t = keys[i];
+    if (t >= static_cast<unsigned int>(T)) return;
     if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
     if (i == pairs - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
 }
@@ -229,7 +239,8 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
                                                         float cutoff, float tmin, double* __restrict__ image,
                                                         float* __restrict__ t_final, int* __restrict__ last_out) {
     __shared__ float s_px[kRasterBatch], s_py[kRasterBatch], s_qa[kRasterBatch], s_qb[kRasterBatch],
-        s_qc[kRasterBatch], s_sig[kRasterBatch], s_c0[kRasterBatch], s_c1[kRasterBatch], s_c2[kRasterBatch];
+        s_qc[kRasterBatch], s_sig[kRasterBatch], s_c0[kRasterBatch], s_c1[kRasterBatch], s_c2[kRasterBatch],
+        s_qmax[kRasterBatch];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
@@ -258,12 +269,14 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
             s_c0[threadIdx.x] = b.z;
             s_c1[threadIdx.x] = b.w;
             s_c2[threadIdx.x] = c.x;
+            s_qmax[threadIdx.x] = reject_bound(b.y, cutoff);
         }
         __syncthreads();
         const int cnt = min(kRasterBatch, range.y - base);
         if (!done) {
             for (int j = 0; j < cnt; ++j) {
-                const SplatEval e = eval_splat(s_px[j], s_py[j], s_qa[j], s_qb[j], s_qc[j], s_sig[j], fx, fy);
+                SplatEval e;
+                if (!eval_splat(s_px[j], s_py[j], s_qa[j], s_qb[j], s_qc[j], s_sig[j], fx, fy, s_qmax[j], e)) continue;
                 if (e.alpha < cutoff) continue;
                 const double w = blend_weight(T, e.alpha);
                 C0 = __fma_rn(w, s_c0[j], C0);
@@ -293,7 +306,8 @@ inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 
 }  // namespace
 
-void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s) {
+void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
+                 const RenderSync& sync) {
     const int n = scene.n;
     v.n = n;
     v.W = v.cam.width;
@@ -319,6 +333,8 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     v.t_final.ensure(npx);
     v.last.ensure(npx);
     if (want_debug) v.entry64.ensure(kEntry64 * static_cast<size_t>(n));
+    int bits = 1;
+    while ((1 << bits) < v.T + 1) ++bits;  // tile keys < T, padding key (all ones) sorts last
 
     if (n > 0) {
         StageScope st(NGS_STAGE_PROJECT, s);
@@ -344,43 +360,52 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
         CUDA_CHECK(cudaMemsetAsync(v.counts_sorted.ptr + n, 0, sizeof(int), s));
         temp2 = v.cub_temp.cap;
         CUDA_CHECK(cub::DeviceScan::ExclusiveSum(v.cub_temp.ptr, temp2, v.counts_sorted.ptr, v.offsets.ptr, n + 1, s));
-        int pairs = 0;
-        CUDA_CHECK(cudaMemcpyAsync(&pairs, v.offsets.ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CUDA_CHECK(cudaStreamSynchronize(s));
-        v.pairs = pairs;
-    } else {
-        v.pairs = 0;
     }
-    if (g_prof) {
-        g_prof->stats.raster_pairs += v.pairs;
-        g_prof->stats.renders += 1;
+    // Pair capacity: exact (one host sync) or the slot's running capacity with a
+    // device-side overflow flag (sync-free; the caller re-runs on overflow).
+    size_t cap;
+    if (sync.exact) {
+        int pairs = 0;
+        if (n > 0) {
+            CUDA_CHECK(cudaMemcpyAsync(&pairs, v.offsets.ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        v.pairs = pairs;
+        cap = static_cast<size_t>(pairs);
+        v.pair_cap = std::max(v.pair_cap, cap + cap / 4 + 4096);
+    } else {
+        v.pairs = -1;
+        if (v.pair_cap == 0) v.pair_cap = static_cast<size_t>(n) * 4 + 4096;
+        cap = v.pair_cap;
     }
     CUDA_CHECK(cudaMemsetAsync(v.ranges.ptr, 0, sizeof(int2) * v.T, s));
-    if (v.pairs > 0) {
+    if (cap > 0 && n > 0) {
         StageScope st(NGS_STAGE_SORT, s, 5);
-        const int P = v.pairs;
-        v.pair_key.ensure(P);
-        v.pair_key_sorted.ensure(P);
-        v.pair_val.ensure(P);
-        v.pair_val_sorted.ensure(P);
-        emit_pairs_k<<<blocks_for(n), 256, 0, s>>>(n, v.cam.tiles_x, v.order.ptr, v.offsets.ptr, v.rect.ptr,
-                                                   v.tiles_touched.ptr, v.pair_key.ptr, v.pair_val.ptr);
+        v.pair_key.ensure(cap);
+        v.pair_key_sorted.ensure(cap);
+        v.pair_val.ensure(cap);
+        v.pair_val_sorted.ensure(cap);
+        CUDA_CHECK(cudaMemsetAsync(v.pair_key.ptr, 0xFF, sizeof(unsigned int) * cap, s));
+        emit_pairs_k<<<blocks_for(n), 256, 0, s>>>(n, v.cam.tiles_x, static_cast<int>(cap), v.order.ptr,
+                                                   v.offsets.ptr, v.rect.ptr, v.tiles_touched.ptr, v.pair_key.ptr,
+                                                   v.pair_val.ptr, sync.overflow, sync.pair_counter);
         CUDA_LAUNCH_CHECK();
-        int bits = 1;
-        while ((1 << bits) < v.T) ++bits;
         size_t temp = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, temp, v.pair_key.ptr, v.pair_key_sorted.ptr, v.pair_val.ptr,
-                                        v.pair_val_sorted.ptr, P, 0, bits, s);
+                                        v.pair_val_sorted.ptr, static_cast<int>(cap), 0, bits, s);
         v.cub_temp.ensure(temp);
         temp = v.cub_temp.cap;
         CUDA_CHECK(cub::DeviceRadixSort::SortPairs(v.cub_temp.ptr, temp, v.pair_key.ptr, v.pair_key_sorted.ptr,
-                                                   v.pair_val.ptr, v.pair_val_sorted.ptr, P, 0, bits, s));
-        tile_ranges_k<<<blocks_for(P), 256, 0, s>>>(P, v.pair_key_sorted.ptr, v.ranges.ptr);
+                                                   v.pair_val.ptr, v.pair_val_sorted.ptr, static_cast<int>(cap), 0,
+                                                   bits, s));
+        tile_ranges_k<<<blocks_for(static_cast<int>(cap)), 256, 0, s>>>(static_cast<int>(cap), v.T,
+                                                                         v.pair_key_sorted.ptr, v.ranges.ptr);
         CUDA_LAUNCH_CHECK();
     }
+    if (g_prof) g_prof->stats.renders += 1;
     StageScope st(NGS_STAGE_RASTER, s);
     raster_forward_k<<<v.T, 256, 0, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr,
-                                         v.pairs > 0 ? v.pair_val_sorted.ptr : nullptr, v.pix.ptr, v.rec_a.ptr,
+                                         cap > 0 ? v.pair_val_sorted.ptr : nullptr, v.pix.ptr, v.rec_a.ptr,
                                          v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1], scene.bg[2],
                                          v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
                                          v.last.ptr);

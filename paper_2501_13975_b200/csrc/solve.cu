@@ -282,35 +282,46 @@ __global__ void __launch_bounds__(256) solve_opacity_k(SceneDev s, SolveParams s
     block_add(nsq, out.norm_sq);
 }
 
-// Cyclic Jacobi for a small symmetric matrix (m <= kMaxSolveViews), ascending order not required.
+// Cyclic Jacobi for a small symmetric MAXM x MAXM matrix, fully unrolled so
+// the matrices stay in registers (zero rows/columns are inert). Eigenvalues
+// end on the diagonal of `a`, eigenvectors in the columns of `v`.
 template <int MAXM>
-__device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAXM], int m) {
-    for (int i = 0; i < m; ++i)
-        for (int j = 0; j < m; ++j) v[i][j] = (i == j) ? 1.0 : 0.0;
-    for (int sweep = 0; sweep < 30; ++sweep) {
+__device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAXM]) {
+#pragma unroll
+    for (int i = 0; i < MAXM; ++i)
+#pragma unroll
+        for (int j = 0; j < MAXM; ++j) v[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 24; ++sweep) {
         double off = 0, diag = 0;
-        for (int i = 0; i < m; ++i) {
+#pragma unroll
+        for (int i = 0; i < MAXM; ++i) {
             diag += a[i][i] * a[i][i];
-            for (int j = i + 1; j < m; ++j) off += a[i][j] * a[i][j];
+#pragma unroll
+            for (int j = i + 1; j < MAXM; ++j) off += a[i][j] * a[i][j];
         }
         if (off == 0.0 || off <= 1e-32 * diag) break;
-        for (int p = 0; p < m; ++p)
-            for (int q = p + 1; q < m; ++q) {
+#pragma unroll
+        for (int p = 0; p < MAXM; ++p)
+#pragma unroll
+            for (int q = p + 1; q < MAXM; ++q) {
                 if (a[p][q] == 0.0) continue;
                 const double theta = (a[q][q] - a[p][p]) / (2 * a[p][q]);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
                 const double c = 1 / sqrt(t * t + 1), sn = t * c;
-                for (int kk = 0; kk < m; ++kk) {
+#pragma unroll
+                for (int kk = 0; kk < MAXM; ++kk) {
                     const double akp = a[kk][p], akq = a[kk][q];
                     a[kk][p] = c * akp - sn * akq;
                     a[kk][q] = sn * akp + c * akq;
                 }
-                for (int kk = 0; kk < m; ++kk) {
+#pragma unroll
+                for (int kk = 0; kk < MAXM; ++kk) {
                     const double apk = a[p][kk], aqk = a[q][kk];
                     a[p][kk] = c * apk - sn * aqk;
                     a[q][kk] = sn * apk + c * aqk;
                 }
-                for (int kk = 0; kk < m; ++kk) {
+#pragma unroll
+                for (int kk = 0; kk < MAXM; ++kk) {
                     const double vkp = v[kk][p], vkq = v[kk][q];
                     v[kk][p] = c * vkp - sn * vkq;
                     v[kk][q] = sn * vkp + c * vkq;
@@ -319,134 +330,216 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
     }
 }
 
-// solve_color (newton.hpp:783-811) from per-view compact accumulators:
-// grad_ch = sum_v g_v phi_v, hess_ch = sum_v h_v phi_v phi_v^T (color_terms,
-// newton.hpp:538-574). Exact spectral repair through the thin SVD of
-// Phi = [phi_v]: H = U K U^T, K = L^1/2 E^T D E L^1/2, null space -> mu.
+// solve_color (newton.hpp:783-811) from per-view compact accumulators
+// (color_terms, newton.hpp:538-574): grad_ch = sum_v g_v phi_v = Phi g,
+// hess_ch = sum_v h_v phi_v phi_v^T = Phi D Phi^T. Exact psd_safeguard
+// spectrum repair through the thin SVD of Phi, carried out entirely in the
+// m-dimensional view space: with G = Phi^T Phi = E L E^T, the non-trivial
+// eigenpairs of H are those of K = L^1/2 E^T D E L^1/2 = W Theta W^T, the
+// eigenvectors are y_i = Phi c_i with c_i = E L^-1/2 W_i, and the solution is
+// delta = Phi beta. Directions of range(Phi) whose Gram eigenvalue vanishes
+// (near-collinear view directions) carry eigenvalue ~0 and are floored to mu;
+// the null space of Phi^T carries no gradient. Nothing n-dimensional is
+// stored: phi_v is re-evaluated when beta is committed.
+template <int MV>
 __global__ void __launch_bounds__(128) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
                                                      const double* __restrict__ acc, size_t stride,
                                                      SolveOutputs out) {
-    constexpr int MV = kMaxSolveViews;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     double nsq = 0.0;
     if (k < s.n) {
         const int n = s.n_coeffs;
         const float4 ps = s.pos_sigma[k];
         const D3 p = {ps.x, ps.y, ps.z};
-        double phi[MV][16];
-        bool have[MV];
-        for (int v = 0; v < cv.n_views; ++v) {
-            have[v] = (cv.flags[v][k] & kProjected) != 0;
-            D3 r;
-            double nr;
-            if (!view_direction(cv.cam[v], p, r, nr)) r = d3(0, 0, 1);
-            sh_basis(r, s.sh_degree, phi[v]);
-        }
-        for (int ch = 0; ch < 3; ++ch) {
-            // Active views for this channel (visible, unclamped).
-            int idx[MV];
-            double gv[MV], hv[MV];
-            int m = 0;
-            for (int v = 0; v < cv.n_views; ++v) {
-                if (!have[v] || (cv.flags[v][k] & (kClamp0 << ch))) continue;
-                const double* a = acc + static_cast<size_t>(v) * kAccOpColor * stride;
-                idx[m] = v;
-                gv[m] = a[(2 + ch) * stride + k];
-                hv[m] = a[(5 + ch) * stride + k];
-                ++m;
+        const int nv = cv.n_views;
+        D3 dir[MV];
+        uint8_t fl[MV];
+#pragma unroll
+        for (int v = 0; v < MV; ++v) {
+            fl[v] = 0;
+            dir[v] = d3(0, 0, 1);
+            if (v < nv) {
+                fl[v] = cv.flags[v][k];
+                double nr;
+                if (!view_direction(cv.cam[v], p, dir[v], nr)) dir[v] = d3(0, 0, 1);
             }
+        }
+        // Gram matrix of the visible views' SH bases (phi_a . phi_b); absent views are zero.
+        double G[MV][MV];
+#pragma unroll
+        for (int a = 0; a < MV; ++a) {
+            double pa[16];
+            sh_basis(dir[a], s.sh_degree, pa);
+#pragma unroll
+            for (int b = 0; b <= a; ++b) {
+                double pb[16];
+                sh_basis(dir[b], s.sh_degree, pb);
+                double t = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) t += pa[i] * pb[i];
+                const bool on = (fl[a] & kProjected) && (fl[b] & kProjected);
+                G[a][b] = on ? t : 0.0;
+                G[b][a] = G[a][b];
+            }
+        }
+        double L[MV][MV], E[MV][MV];
+#pragma unroll
+        for (int a = 0; a < MV; ++a)
+#pragma unroll
+            for (int b = 0; b < MV; ++b) L[a][b] = G[a][b];
+        if (n > 1) jacobi_eig<MV>(L, E);
+        double lmax = 0;
+#pragma unroll
+        for (int a = 0; a < MV; ++a) lmax = fmax(lmax, L[a][a]);
+        bool kept[MV];
+        double isq[MV];  // L^-1/2 on kept directions
+        int r = 0;
+#pragma unroll
+        for (int a = 0; a < MV; ++a) {
+            kept[a] = L[a][a] > 1e-13 * lmax && L[a][a] > 0.0;
+            isq[a] = kept[a] ? 1.0 / sqrt(L[a][a]) : 0.0;
+            r += kept[a] ? 1 : 0;
+        }
+        double beta_all[3][MV];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            double gv[MV], hv[MV];
+            bool any = false;
+#pragma unroll
+            for (int v = 0; v < MV; ++v) {
+                gv[v] = 0.0;
+                hv[v] = 0.0;
+                beta_all[ch][v] = 0.0;
+                if (v < nv && (fl[v] & kProjected) && !(fl[v] & (kClamp0 << ch))) {
+                    const double* a = acc + static_cast<size_t>(v) * kAccOpColor * stride;
+                    gv[v] = a[(2 + ch) * stride + k];
+                    hv[v] = a[(5 + ch) * stride + k];
+                    any = true;
+                }
+            }
+            if (!any) continue;
+            double beta[MV];
+#pragma unroll
+            for (int a = 0; a < MV; ++a) beta[a] = 0.0;
+            double nrm2 = 0;
+            if (n == 1) {
+                // Scalar system (psd_safeguard n = 1); phi = kSH0 for every view.
+                double g = 0, h = 0;
+#pragma unroll
+                for (int a = 0; a < MV; ++a) {
+                    g += gv[a] * kSH0;
+                    h += hv[a] * kSH0 * kSH0;
+                }
+                const double d = solve1(h, g, sp);  // coefficient delta
+                beta[0] = d;
+                nrm2 = d * d;
+            } else {
+                // K = L^1/2 E^T D E L^1/2 on the kept directions.
+                double K[MV][MV], W[MV][MV];
+#pragma unroll
+                for (int i = 0; i < MV; ++i)
+#pragma unroll
+                    for (int j = 0; j < MV; ++j) {
+                        double t = 0;
+#pragma unroll
+                        for (int v = 0; v < MV; ++v) t += E[v][i] * hv[v] * E[v][j];
+                        K[i][j] = (kept[i] && kept[j]) ? t * sqrt(L[i][i] * L[j][j]) : 0.0;
+                    }
+                jacobi_eig<MV>(K, W);
+                // Eigenvectors y_e = Phi c_e with c_e = E L^-1/2 W_e; those living in the
+                // dropped subspace have c_e = 0.
+                double c[MV][MV];
+                bool live[MV];
+                double lam_abs_max = 0, lam_min = 1e300;
+#pragma unroll
+                for (int e = 0; e < MV; ++e) {
+                    double wk = 0;
+#pragma unroll
+                    for (int j = 0; j < MV; ++j) wk += kept[j] ? W[j][e] * W[j][e] : 0.0;
+                    live[e] = wk > 0.5;
+#pragma unroll
+                    for (int v = 0; v < MV; ++v) {
+                        double t = 0;
+#pragma unroll
+                        for (int j = 0; j < MV; ++j) t += E[v][j] * isq[j] * W[j][e];
+                        c[e][v] = live[e] ? t : 0.0;
+                    }
+                    if (live[e]) {
+                        lam_abs_max = fmax(lam_abs_max, fabs(K[e][e]));
+                        lam_min = fmin(lam_min, K[e][e]);
+                    }
+                }
+                if (r < n) lam_min = fmin(lam_min, 0.0);  // zero eigenvalues outside range(Phi)
+                const double mu = fmax(sp.mu_min, sp.eig_floor_rel * lam_abs_max);
+                const bool keep_h = lam_min >= mu;  // newton.hpp:231: PD input solved unmodified
+                double Gg[MV];
+#pragma unroll
+                for (int a = 0; a < MV; ++a) {
+                    double t = 0;
+#pragma unroll
+                    for (int b = 0; b < MV; ++b) t += G[a][b] * gv[b];
+                    Gg[a] = t;
+                }
+#pragma unroll
+                for (int e = 0; e < MV; ++e) {
+                    if (!live[e]) continue;
+                    double yg = 0;
+#pragma unroll
+                    for (int v = 0; v < MV; ++v) yg += c[e][v] * Gg[v];
+                    const double lam = K[e][e];
+                    const double l = keep_h ? lam : fmax(fabs(lam), mu);
+#pragma unroll
+                    for (int v = 0; v < MV; ++v) beta[v] -= (yg / l) * c[e][v];
+                }
+                if (!keep_h) {
+                    // range(Phi) directions with a vanishing Gram eigenvalue: eigenvalue ~0 -> mu.
+#pragma unroll
+                    for (int a = 0; a < MV; ++a) {
+                        if (kept[a] || !(L[a][a] > 0.0)) continue;
+                        double eg = 0;
+#pragma unroll
+                        for (int v = 0; v < MV; ++v) eg += E[v][a] * gv[v];
+#pragma unroll
+                        for (int v = 0; v < MV; ++v) beta[v] -= E[v][a] * eg / mu;
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < MV; ++a)
+#pragma unroll
+                    for (int b = 0; b < MV; ++b) nrm2 += beta[a] * G[a][b] * beta[b];
+            }
+            // Colour cap (newton.hpp:801-804) on |delta| = sqrt(beta^T G beta).
+            double scale = 1.0;
+            if (sp.color_cap > 0.0 && sqrt(nrm2) > sp.color_cap) scale = sp.color_cap / sqrt(nrm2);
+            nsq += nrm2 * scale * scale;
+#pragma unroll
+            for (int a = 0; a < MV; ++a) beta_all[ch][a] = beta[a] * scale;
+        }
+        // delta_ch = sum_v beta_v phi_v (SH0: delta = beta_0); write / commit.
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
             double delta[16];
+#pragma unroll
             for (int i = 0; i < 16; ++i) delta[i] = 0.0;
             if (n == 1) {
-                double g = 0, h = 0;
-                for (int j = 0; j < m; ++j) {
-                    const double f = phi[idx[j]][0];
-                    g += gv[j] * f;
-                    h += hv[j] * f * f;
-                }
-                delta[0] = solve1(h, g, sp);
+                delta[0] = beta_all[ch][0];
             } else {
-                double grad[16];
-                for (int i = 0; i < n; ++i) {
-                    double t = 0;
-                    for (int j = 0; j < m; ++j) t += gv[j] * phi[idx[j]][i];
-                    grad[i] = t;
-                }
-                // Gram of Phi and its eigen-decomposition.
-                double Gm[MV][MV], E[MV][MV];
-                for (int a = 0; a < m; ++a)
-                    for (int b = 0; b < m; ++b) {
-                        double t = 0;
-                        for (int i = 0; i < n; ++i) t += phi[idx[a]][i] * phi[idx[b]][i];
-                        Gm[a][b] = t;
-                    }
-                jacobi_eig<MV>(Gm, E, m);
-                double lmax = 0;
-                for (int a = 0; a < m; ++a) lmax = fmax(lmax, Gm[a][a]);
-                int keep[MV], r = 0;
-                for (int a = 0; a < m; ++a)
-                    if (Gm[a][a] > 1e-13 * lmax && Gm[a][a] > 0.0) keep[r++] = a;
-                // K (r x r) = sqrt(L_i L_j) sum_v E_vi h_v E_vj
-                double Kt[MV][MV], W[MV][MV];
-                for (int i = 0; i < r; ++i)
-                    for (int j = 0; j < r; ++j) {
-                        double t = 0;
-                        for (int v = 0; v < m; ++v) t += E[v][keep[i]] * hv[v] * E[v][keep[j]];
-                        Kt[i][j] = t * sqrt(Gm[keep[i]][keep[i]] * Gm[keep[j]][keep[j]]);
-                    }
-                jacobi_eig<MV>(Kt, W, r);
-                double lam_abs_max = 0, lam_min = 0;
-                for (int i = 0; i < r; ++i) {
-                    lam_abs_max = fmax(lam_abs_max, fabs(Kt[i][i]));
-                    lam_min = (i == 0) ? Kt[i][i] : fmin(lam_min, Kt[i][i]);
-                }
-                if (r < n) lam_min = fmin(lam_min, 0.0);
-                const double mu = fmax(sp.mu_min, sp.eig_floor_rel * lam_abs_max);
-                const bool keep_h = lam_min >= mu;  // newton.hpp:231: PD input is solved unmodified
-                // Orthonormal range basis u_i = Phi E_i / sqrt(L_i); eigenvectors y_i = sum_j W_ji u_j.
-                double resid[16];
-                for (int i = 0; i < n; ++i) resid[i] = grad[i];
-                for (int e = 0; e < r; ++e) {
-                    double y[16];
-                    for (int i = 0; i < n; ++i) {
-                        double t = 0;
-                        for (int j = 0; j < r; ++j) {
-                            const int a = keep[j];
-                            double u = 0;
-                            for (int v = 0; v < m; ++v) u += phi[idx[v]][i] * E[v][a];
-                            t += W[j][e] * u / sqrt(Gm[a][a]);
-                        }
-                        y[i] = t;
-                    }
-                    double yg = 0;
-                    for (int i = 0; i < n; ++i) yg += y[i] * grad[i];
-                    const double lam = Kt[e][e];
-                    const double l = keep_h ? lam : fmax(fabs(lam), mu);
-                    for (int i = 0; i < n; ++i) {
-                        delta[i] -= (yg / l) * y[i];
-                        resid[i] -= yg * y[i];
-                    }
-                }
-                if (!keep_h)
-                    for (int i = 0; i < n; ++i) delta[i] -= resid[i] / mu;
-            }
-            if (sp.color_cap > 0.0) {
-                double nrm = 0;
-                for (int i = 0; i < n; ++i) nrm += delta[i] * delta[i];
-                nrm = sqrt(nrm);
-                if (nrm > sp.color_cap)
-                    for (int i = 0; i < n; ++i) delta[i] *= sp.color_cap / nrm;
-            }
-            for (int i = 0; i < n; ++i) {
-                nsq += delta[i] * delta[i];
-                if (out.delta) out.delta[48 * static_cast<size_t>(k) + 16 * ch + i] = delta[i];
-                if (sp.commit) {
-                    float* c = s.sh + (static_cast<size_t>(16 * ch + i)) * s.n + k;
-                    *c = (float)((double)*c + delta[i]);
+#pragma unroll
+                for (int v = 0; v < MV; ++v) {
+                    double ph[16];
+                    sh_basis(dir[v], s.sh_degree, ph);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) delta[i] += beta_all[ch][v] * ph[i];
                 }
             }
-            if (out.delta)
-                for (int i = n; i < 16; ++i) out.delta[48 * static_cast<size_t>(k) + 16 * ch + i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (out.delta) out.delta[48 * static_cast<size_t>(k) + 16 * ch + i] = i < n ? delta[i] : 0.0;
+                if (sp.commit && i < n) {
+                    float* cc = s.sh + (static_cast<size_t>(16 * ch + i)) * s.n + k;
+                    *cc = (float)((double)*cc + delta[i]);
+                }
+            }
         }
         if (out.accepted) out.accepted[k] = 1;
     }
@@ -476,7 +569,14 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
             solve_opacity_k<<<blocks_for(n), 256, 0, s>>>(scene, sp, acc, stride, cv.n_views, out);
             break;
         case NGS_COLOR:
-            solve_color_k<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+            if (cv.n_views <= 1)
+                solve_color_k<1><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+            else if (cv.n_views <= 2)
+                solve_color_k<2><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+            else if (cv.n_views <= 4)
+                solve_color_k<4><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+            else
+                solve_color_k<8><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
             break;
     }
     CUDA_LAUNCH_CHECK();

@@ -15,8 +15,11 @@ from refimpl import check_fixture, random_scene, ref, synth, test_camera
 
 pytestmark = pytest.mark.gpu
 
-FLOOR = 1e-3   # absolute floor, fraction of max|ref| of the quantity
-TOL = 1e-4     # FP32 vs float64 reference
+FLOOR = 1e-3      # absolute floor, fraction of max|ref| of the quantity
+TOL = 1e-4        # parameters, images: FP32 vs float64 reference
+TOL_FIELD = 1e-3  # loss-derivative fields, assembled terms: FP32 image rounding (~1e-7) is
+                  # amplified by the (c - c^t) cancellation of the loss gradient
+TOL_DELTA = 2e-3  # solved deltas inherit TOL_FIELD through -H^-1 g
 
 
 def qerr(gpu, refv, floor_frac=FLOOR):
@@ -139,7 +142,7 @@ def test_loss_fields(gpu, seed):
     e_g, e_h = qerr(gg, gr), qerr(hg, hr)
     print(f"loss seed {seed}: value {lg:.9g} vs {lr:.9g}; image {e_img:.2e} grad {e_g:.2e} hess {e_h:.2e}")
     assert abs(lg - lr) <= 1e-5 * abs(lr)
-    assert e_g < 1e-3 and e_h < 1e-3
+    assert e_g < TOL_FIELD and e_h < TOL_FIELD
 
 
 # ---------------------------------------------------------------------------
@@ -180,7 +183,7 @@ def test_accumulated_terms(gpu, newton_fixture, attr):
     e_g, e_h = qerr(gg, gr), qerr(hg, hr)
     print(f"{capi.ATTRIBUTES[attr]} terms: grad {e_g:.2e} hess {e_h:.2e} visible {int(vg.sum())}/{int(vr.sum())}")
     assert np.array_equal(vg, vr)
-    assert e_g < 1e-3 and e_h < 1e-3
+    assert e_g < TOL_FIELD and e_h < TOL_FIELD
 
 
 @pytest.mark.parametrize("attr", ATTRS)
@@ -192,7 +195,7 @@ def test_newton_step(gpu, newton_fixture, attr):
     dr = r.newton_step(attr, 0, sec)
     e = qerr(dg["delta"], dr["delta"])
     print(f"{capi.ATTRIBUTES[attr]} solve: delta {e:.2e} norm {dg['delta_norm_sq']:.6g} vs {dr['delta_norm_sq']:.6g}")
-    assert e < 1e-3
+    assert e < TOL_DELTA
     assert np.array_equal(dg["accepted"], dr["accepted"])
     if attr == capi.SCALING:
         assert np.array_equal(dg["degenerate"], dr["degenerate"])
