@@ -261,7 +261,7 @@ def ours_arm(args, cfg: Config):
         ectx.trainer_step(view(args.warmup + i))
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     ds = 4
-    h2d = 3 * 4 * (cfg.width * cfg.height + 3 * (cfg.width // ds) * (cfg.height // ds))
+    h2d = 3 * 8 * (cfg.width * cfg.height + 3 * (cfg.width // ds) * (cfg.height // ds))
     d2h = 8 * 5 + 8  # delta norms + error word
     ectx.close()
 

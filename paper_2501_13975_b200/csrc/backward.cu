@@ -116,10 +116,19 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                 Hu[4][sym3(c, d)] = 2.0 * t1[3] + 2.0 * t2[3];
             }
     }
-    for (int i = 0; i < 5; ++i)
-        for (int j = 0; j < 3; ++j) o[kPosM + 3 * i + j] = static_cast<float>(M[i][j]);
-    for (int i = 0; i < 5; ++i)
-        for (int j = 0; j < 6; ++j) o[kPosHu + 6 * i + j] = static_cast<float>(Hu[i][j]);
+    for (int c = 0; c < 3; ++c) {
+        o[kPosJS + 2 * c] = static_cast<float>(M[0][c]);
+        o[kPosJS + 2 * c + 1] = static_cast<float>(M[1][c]);
+        for (int u = 0; u < 3; ++u) o[kPosJS + 6 + 3 * c + u] = static_cast<float>(M[2 + u][c]);
+    }
+    o[kPosJS + 15] = 0.f;
+    for (int p = 0; p < 6; ++p) {
+        o[kPosHpi + 2 * p] = static_cast<float>(Hu[0][p]);
+        o[kPosHpi + 2 * p + 1] = static_cast<float>(Hu[1][p]);
+        for (int u = 0; u < 3; ++u) o[kPosScd + 3 * p + u] = static_cast<float>(Hu[2 + u][p]);
+    }
+    o[kPosScd + 18] = 0.f;
+    o[kPosScd + 19] = 0.f;
     // SH colour derivatives through r(p) (view_direction_derivatives camera.hpp:79-104).
     D3 r;
     double n;
@@ -161,7 +170,10 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
         }
     }
     for (int ch = 0; ch < 3; ++ch) {
-        for (int j = 0; j < 3; ++j) o[kPosJc + 3 * ch + j] = static_cast<float>(Jc[ch][j]);
+        for (int j = 0; j < 3; ++j) o[kPosJc + 4 * ch + j] = static_cast<float>(Jc[ch][j]);
+        o[kPosJc + 4 * ch + 3] = 0.f;
+        for (int a = 0; a < 3; ++a)
+            for (int bb = a; bb < 3; ++bb) o[kPosJJ + 6 * ch + sym3(a, bb)] = static_cast<float>(Jc[ch][a] * Jc[ch][bb]);
         for (int j = 0; j < 6; ++j) o[kPosHc + 6 * ch + j] = static_cast<float>(Hc[ch][j]);
     }
 }
@@ -222,6 +234,8 @@ __global__ void __launch_bounds__(128) rotation_consts_k(SceneDev s, CameraDev c
         o[i] = static_cast<float>(s1[i]);
         o[3 + i] = static_cast<float>(s2[i]);
     }
+    o[6] = 0.f;
+    o[7] = 0.f;
 }
 
 // Scaling: this view's Sigma eigenframe (newton.hpp:152-160, 426-432) and
@@ -247,6 +261,7 @@ __global__ void __launch_bounds__(128) scaling_consts_k(SceneDev s, CameraDev ca
     o[4] = static_cast<float>(quad(e.v0x, e.v0y, e.v0x, e.v0y));
     o[5] = static_cast<float>(quad(e.v0x, e.v0y, e.v1x, e.v1y));
     o[6] = static_cast<float>(quad(e.v1x, e.v1y, e.v1x, e.v1y));
+    o[7] = 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -257,84 +272,120 @@ template <int PASS>
 struct PassTraits;
 template <>
 struct PassTraits<kPassPosition> {
-    static constexpr int NC = kPosConsts, NACC = 9, BATCH = 64;
+    static constexpr int NC = kPosConsts, NA = 9, BATCH = 64;
 };
 template <>
 struct PassTraits<kPassRotation> {
-    static constexpr int NC = kRotConsts, NACC = 2, BATCH = 128;
+    static constexpr int NC = kRotConsts, NA = 2, BATCH = 128;
 };
 template <>
 struct PassTraits<kPassScaling> {
-    static constexpr int NC = kScaleConsts, NACC = 5, BATCH = 128;
+    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 128;
 };
 template <>
 struct PassTraits<kPassOpacityColor> {
-    static constexpr int NC = 0, NACC = 8, BATCH = 128;
+    static constexpr int NC = 0, NA = 8, BATCH = 128;
 };
 
-// d(G)/du and d2G/du2 for u = (pi_x, pi_y, S00, S01, S11), off-diagonal S01
-// moving both symmetric entries (equivalent to the symmetrised tensors of
-// gaussian_weight, rasterizer.hpp:116-176).
-struct GDerivs {
-    float g[5];
-    float h[15];  // packed upper triangle, row-major over 5x5
-};
-
-__device__ __forceinline__ int s5(int i, int j) {
-    const int a = i < j ? i : j, b = i < j ? j : i;
-    return a * 5 - a * (a - 1) / 2 + (b - a);
-}
-
-__device__ __forceinline__ void sigma_second(float G, float qd0, float qd1, float qa, float qb, float qc, float hss[6]) {
-    // u_E = E qd for E in {a, b, c}; d2q_EF = 2 u_E^T Q u_F; dq = (-qd0^2, -2 qd0 qd1, -qd1^2)
-    const float ux[3] = {qd0, qd1, 0.f};
-    const float uy[3] = {0.f, qd0, qd1};
-    const float dq[3] = {-qd0 * qd0, -2.f * qd0 * qd1, -qd1 * qd1};
-    int idx = 0;
-    for (int e = 0; e < 3; ++e)
-        for (int f = e; f < 3; ++f) {
-            const float quad = ux[e] * (qa * ux[f] + qb * uy[f]) + uy[e] * (qb * ux[f] + qc * uy[f]);
-            hss[idx++] = G * (0.25f * dq[e] * dq[f] - quad);
-        }
-}
-
-__device__ __forceinline__ void g_derivs(const SplatEval& ev, float qa, float qb, float qc, GDerivs& d) {
-    const float G = ev.g, q0 = ev.qd0, q1 = ev.qd1;
-    d.g[0] = -G * q0;
-    d.g[1] = -G * q1;
-    d.g[2] = 0.5f * G * q0 * q0;
-    d.g[3] = G * q0 * q1;
-    d.g[4] = 0.5f * G * q1 * q1;
-    // pi-pi block: G (qd qd^T - Q)
-    d.h[s5(0, 0)] = G * (q0 * q0 - qa);
-    d.h[s5(0, 1)] = G * (q0 * q1 - qb);
-    d.h[s5(1, 1)] = G * (q1 * q1 - qc);
-    // pi-Sigma block: -g_k qd_a + G (Q E_k qd)_a
-    const float QEa[2] = {q0 * qa, q0 * qb};
-    const float QEb[2] = {qa * q1 + qb * q0, qb * q1 + qc * q0};
-    const float QEc[2] = {q1 * qb, q1 * qc};
-    const float qdv[2] = {q0, q1};
-    for (int a = 0; a < 2; ++a) {
-        d.h[s5(a, 2)] = -d.g[2] * qdv[a] + G * QEa[a];
-        d.h[s5(a, 3)] = -d.g[3] * qdv[a] + G * QEb[a];
-        d.h[s5(a, 4)] = -d.g[4] * qdv[a] + G * QEc[a];
+// Copies N float4 from shared memory into a register array.
+template <int N>
+__device__ __forceinline__ void ld4(float (&dst)[4 * N], const float4* src) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const float4 v = src[i];
+        dst[4 * i] = v.x;
+        dst[4 * i + 1] = v.y;
+        dst[4 * i + 2] = v.z;
+        dst[4 * i + 3] = v.w;
     }
-    float hss[6];
-    sigma_second(G, q0, q1, qa, qb, qc, hss);
-    d.h[s5(2, 2)] = hss[0];
-    d.h[s5(2, 3)] = hss[1];
-    d.h[s5(2, 4)] = hss[2];
-    d.h[s5(3, 3)] = hss[3];
-    d.h[s5(3, 4)] = hss[4];
-    d.h[s5(4, 4)] = hss[5];
+}
+
+// Position record (newton.hpp:285-340) via derivatives of the quadratic form
+// q = d^T Sigma^-1 d along p (G = exp(-q/2)):
+//   r_c  = J_c - S_c qd,   q_c = qd . (J_c + r_c),
+//   q_cd = 2 r_c^T Q r_d + 2 qd . Hpi_cd - qd^T S_cd qd,
+//   dG_c = -G q_c / 2,     d2G_cd = G (q_c q_d / 4 - q_cd / 2),
+// with J = dpi/dp, S_c = dSigma/dp_c, Hpi / S_cd the second derivatives. The
+// three-channel Gauss-Newton and curvature sums are regrouped so each output
+// entry costs a handful of FMAs.
+__device__ __forceinline__ void position_record(const float4* K4, const SplatEval& ev, float qa, float qb, float qc,
+                                                float wa, const float (&acol)[3], const float (&gl)[3],
+                                                const float (&hl)[3], float (&v)[9]) {
+    const float G = ev.g, q0 = ev.qd0, q1 = ev.qd1;
+    float A[16];
+    ld4<4>(A, K4 + kPosJS / 4);
+    float r0[3], r1[3], qcv[3], t0[3], t1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float Jx = A[2 * c], Jy = A[2 * c + 1];
+        const float Sa = A[6 + 3 * c], Sb = A[7 + 3 * c], Sc = A[8 + 3 * c];
+        r0[c] = Jx - (Sa * q0 + Sb * q1);
+        r1[c] = Jy - (Sb * q0 + Sc * q1);
+        qcv[c] = q0 * (Jx + r0[c]) + q1 * (Jy + r1[c]);
+        t0[c] = qa * r0[c] + qb * r1[c];
+        t1[c] = qb * r0[c] + qc * r1[c];
+    }
+    float dG[3], d2G[6];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dG[c] = -0.5f * G * qcv[c];
+    {
+        float Hp[12], Sd[20];
+        ld4<3>(Hp, K4 + kPosHpi / 4);
+        ld4<5>(Sd, K4 + kPosScd / 4);
+        const float m00 = q0 * q0, m01 = 2.f * q0 * q1, m11 = q1 * q1;
+        int p = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = c; d < 3; ++d, ++p) {
+                const float qcd = 2.f * (r0[c] * t0[d] + r1[c] * t1[d]) + 2.f * (q0 * Hp[2 * p] + q1 * Hp[2 * p + 1]) -
+                                  (Sd[3 * p] * m00 + Sd[3 * p + 1] * m01 + Sd[3 * p + 2] * m11);
+                d2G[p] = G * (0.25f * qcv[c] * qcv[d] - 0.5f * qcd);
+            }
+    }
+    float Jc[12];
+    ld4<3>(Jc, K4 + kPosJc / 4);
+    float sgl = 0.f, A2 = 0.f, vgl[3] = {0.f, 0.f, 0.f}, vh[3] = {0.f, 0.f, 0.f}, ga[3], ha[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        ga[ch] = gl[ch] * wa;
+        ha[ch] = hl[ch] * wa * wa;
+        sgl += ga[ch] * acol[ch];
+        const float hac = ha[ch] * acol[ch];
+        A2 += hac * acol[ch];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            vgl[i] += ga[ch] * Jc[4 * ch + i];
+            vh[i] += hac * Jc[4 * ch + i];
+        }
+    }
+    float E[36];
+    ld4<9>(E, K4 + kPosJJ / 4);
+    float JJ[6], hc[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        JJ[q] = ha[0] * E[q] + ha[1] * E[6 + q] + ha[2] * E[12 + q];
+        hc[q] = ga[0] * E[18 + q] + ga[1] * E[24 + q] + ga[2] * E[30 + q];
+    }
+    const float GG = G * G;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[c] = sgl * dG[c] + G * vgl[c];
+    int p = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = c; d < 3; ++d, ++p)
+            v[3 + p] = sgl * d2G[p] + G * hc[p] + dG[c] * vgl[d] + vgl[c] * dG[d] + A2 * dG[c] * dG[d] +
+                       G * (dG[c] * vh[d] + vh[c] * dG[d]) + GG * JJ[p];
 }
 
 template <int PASS>
 __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
-    constexpr int B = TR::BATCH, NC = TR::NC, NA = TR::NACC;
-    __shared__ float s_px[B], s_py[B], s_qa[B], s_qb[B], s_qc[B], s_sig[B], s_c[3][B], s_qmax[B];
-    __shared__ float s_const[(NC > 0 ? NC : 1) * B];
+    constexpr int B = TR::BATCH, NC = TR::NC, NA = TR::NA, NC4 = NC / 4;
+    __shared__ float4 s_g0[B], s_g1[B];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
+    __shared__ float2 s_g2[B];           // (c1, c2)
+    __shared__ float4 s_const[(NC4 > 0 ? NC4 : 1) * B];
     __shared__ float s_acc[NA][B];
     __shared__ int s_kid[B];
     __shared__ int s_cnt[B];
@@ -357,6 +408,7 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     float gl[3] = {0, 0, 0}, hl[3] = {0, 0, 0};
     if (inside) {
         last = a.last[pidx];
+#pragma unroll
         for (int c = 0; c < 3; ++c) {
             Cf[c] = a.image[c * plane + pidx];
             gl[c] = a.loss_grad[c * plane + pidx];
@@ -369,8 +421,7 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     __syncthreads();
     const int end = min(range.y, s_maxlast + 1);
 
-    float T = 1.0f;
-    double P[3] = {0, 0, 0};  // FP64 prefix sums, identical to the forward's colour sums
+    float T = 1.0f, P[3] = {0.f, 0.f, 0.f};
     const int lane = threadIdx.x & 31;
 
     for (int base = range.x; base < end; base += B) {
@@ -382,24 +433,19 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
                 s_kid[i] = k;
                 const double2 p = a.pix[k];
                 const float4 ra = a.ra[k], rb = a.rb[k], rc = a.rc[k];
-                s_px[i] = static_cast<float>(p.x - ox);
-                s_py[i] = static_cast<float>(p.y - oy);
-                s_qa[i] = ra.z;
-                s_qb[i] = ra.w;
-                s_qc[i] = rb.x;
-                s_sig[i] = rb.y;
-                s_c[0][i] = rb.z;
-                s_c[1][i] = rb.w;
-                s_c[2][i] = rc.x;
-                s_qmax[i] = reject_bound(rb.y, a.cutoff);
+                s_g0[i] = make_float4(static_cast<float>(p.x - ox), static_cast<float>(p.y - oy), ra.z, ra.w);
+                s_g1[i] = make_float4(rb.x, rb.y, reject_bound(rb.y, a.cutoff), rb.z);
+                s_g2[i] = make_float2(rb.w, rc.x);
             }
+#pragma unroll
             for (int c = 0; c < NA; ++c) s_acc[c][i] = 0.f;
             s_cnt[i] = 0;
         }
-        if constexpr (NC > 0) {
-            for (int i = threadIdx.x; i < cnt * NC; i += blockDim.x) {
-                const int j = i / NC, c = i - j * NC;
-                s_const[i] = a.consts[static_cast<size_t>(a.vals[base + j]) * NC + c];
+        if constexpr (NC4 > 0) {
+            const float4* src = reinterpret_cast<const float4*>(a.consts);
+            for (int i = threadIdx.x; i < cnt * NC4; i += blockDim.x) {
+                const int j = i / NC4, c = i - j * NC4;
+                s_const[i] = src[static_cast<size_t>(a.vals[base + j]) * NC4 + c];
             }
         }
         __syncthreads();
@@ -409,125 +455,75 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
             for (int c = 0; c < NA; ++c) v[c] = 0.f;
             bool contrib = false;
             if (base + j <= last) {
-                const float qa = s_qa[j], qb = s_qb[j], qc = s_qc[j], sig = s_sig[j];
+                const float4 g0 = s_g0[j], g1 = s_g1[j];
+                const float qa = g0.z, qb = g0.w, qc = g1.x, sig = g1.y;
                 SplatEval ev;
-                if (eval_splat(s_px[j], s_py[j], qa, qb, qc, sig, fx, fy, s_qmax[j], ev) && !(ev.alpha < a.cutoff)) {
+                if (eval_splat(g0.x, g0.y, qa, qb, qc, sig, fx, fy, g1.z, ev) && !(ev.alpha < a.cutoff)) {
                     contrib = true;
+                    const float2 g2 = s_g2[j];
+                    const float col[3] = {g1.w, g2.x, g2.y};
                     const float Ti = T;
                     const float w = blend_weight(Ti, ev.alpha);
                     const float Tn = next_transmittance(Ti, ev.alpha);
-                    float acol[3];  // c~ - behind
+                    const bool is_last = (base + j == last);
+                    const float inv_tn = __frcp_rn(Tn);
+                    float acol[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        const float cc = s_c[c][j];
-                        const double Pn = __fma_rn(static_cast<double>(w), cc, P[c]);
+                        const float Pn = __fmaf_rn(w, col[c], P[c]);
                         const float behind =
-                            (base + j == last) ? a.bg[c] : static_cast<float>(Cf[c] - Pn) * __frcp_rn(Tn);
-                        acol[c] = cc - behind;
+                            is_last ? a.bg[c] : static_cast<float>(Cf[c] - static_cast<double>(Pn)) * inv_tn;
+                        acol[c] = col[c] - behind;
                         P[c] = Pn;
                     }
                     T = Tn;
                     const float wa = sig * Ti;  // w_alpha = sigma * T
                     if constexpr (PASS == kPassPosition) {
-                        const float* K = s_const + j * NC;
-                        GDerivs d;
-                        g_derivs(ev, qa, qb, qc, d);
-                        // dG/dp = M^T g
-                        float dG[3];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            float t = 0.f;
-#pragma unroll
-                            for (int u = 0; u < 5; ++u) t += K[kPosM + 3 * u + c] * d.g[u];
-                            dG[c] = t;
-                        }
-                        // V = H M (5x3)
-                        float V[5][3];
-#pragma unroll
-                        for (int u = 0; u < 5; ++u)
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) {
-                                float t = 0.f;
-#pragma unroll
-                                for (int l = 0; l < 5; ++l) t += d.h[s5(u, l)] * K[kPosM + 3 * l + c];
-                                V[u][c] = t;
-                            }
-                        // d2G/dp2 (sym 6) = M^T V + sum_u g_u Hu_u
-                        float d2G[6];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c)
-#pragma unroll
-                            for (int e = c; e < 3; ++e) {
-                                float t = 0.f;
-#pragma unroll
-                                for (int u = 0; u < 5; ++u) t += K[kPosM + 3 * u + c] * V[u][e] + d.g[u] * K[kPosHu + 6 * u + sym3(c, e)];
-                                d2G[sym3(c, e)] = t;
-                            }
-                        // Channel sums (newton.hpp:329-340)
-                        float sgl = 0.f, vgl[3] = {0.f, 0.f, 0.f}, hc[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const float gw = gl[ch] * wa;
-                            sgl += gw * acol[ch];
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) vgl[c] += gw * K[kPosJc + 3 * ch + c];
-#pragma unroll
-                            for (int q = 0; q < 6; ++q) hc[q] += gw * K[kPosHc + 6 * ch + q];
-                        }
-                        const float G = ev.g;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) v[c] = sgl * dG[c] + G * vgl[c];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c)
-#pragma unroll
-                            for (int e = c; e < 3; ++e) {
-                                const int q = sym3(c, e);
-                                float t = sgl * d2G[q] + G * hc[q] + dG[c] * vgl[e] + vgl[c] * dG[e];
-#pragma unroll
-                                for (int ch = 0; ch < 3; ++ch) {
-                                    const float dcc = wa * (acol[ch] * dG[c] + G * K[kPosJc + 3 * ch + c]);
-                                    const float dce = wa * (acol[ch] * dG[e] + G * K[kPosJc + 3 * ch + e]);
-                                    t += hl[ch] * dcc * dce;
-                                }
-                                v[3 + q] = t;
-                            }
+                        position_record(s_const + j * NC4, ev, qa, qb, qc, wa, acol, gl, hl, v);
                     } else if constexpr (PASS == kPassRotation) {
-                        const float* K = s_const + j * NC;
-                        const float G = ev.g, q0 = ev.qd0, q1 = ev.qd1;
-                        const float gs[3] = {0.5f * G * q0 * q0, G * q0 * q1, 0.5f * G * q1 * q1};
-                        float hss[6];
-                        sigma_second(G, q0, q1, qa, qb, qc, hss);
-                        const float s1[3] = {K[0], K[1], K[2]};
-                        const float dg = gs[0] * K[0] + gs[1] * K[1] + gs[2] * K[2];
-                        float d2g = gs[0] * K[3] + gs[1] * K[4] + gs[2] * K[5];
-                        d2g += s1[0] * (hss[0] * s1[0] + 2.f * hss[1] * s1[1] + 2.f * hss[2] * s1[2]) +
-                               s1[1] * (hss[3] * s1[1] + 2.f * hss[4] * s1[2]) + s1[2] * hss[5] * s1[2];
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const float dc = wa * acol[ch] * dg;
-                            v[0] += gl[ch] * dc;
-                            v[1] += hl[ch] * dc * dc + gl[ch] * wa * acol[ch] * d2g;
-                        }
-                    } else if constexpr (PASS == kPassScaling) {
-                        const float* K = s_const + j * NC;
-                        const float G = ev.g;
-                        const float z0 = K[0] * ev.qd0 + K[1] * ev.qd1;
-                        const float z1 = K[2] * ev.qd0 + K[3] * ev.qd1;
-                        const float dg0 = 0.5f * G * z0 * z0, dg1 = 0.5f * G * z1 * z1;
-                        const float h00 = G * (0.25f * z0 * z0 * z0 * z0 - z0 * z0 * K[4]);
-                        const float h01 = G * (0.25f * z0 * z0 * z1 * z1 - z0 * z1 * K[5]);
-                        const float h11 = G * (0.25f * z1 * z1 * z1 * z1 - z1 * z1 * K[6]);
+                        // Directional derivatives along dSigma/dtheta = S1, d2Sigma/dtheta2 = S2
+                        // (newton.hpp:366-401): w = S1 qd, dq = -qd.w, d2q = 2 w^T Q w - qd^T S2 qd.
+                        const float4 k0 = s_const[j * NC4], k1 = s_const[j * NC4 + 1];
+                        const float q0 = ev.qd0, q1 = ev.qd1, G = ev.g;
+                        const float w0 = k0.x * q0 + k0.y * q1, w1 = k0.y * q0 + k0.z * q1;
+                        const float dq = -(q0 * w0 + q1 * w1);
+                        const float d2q = 2.f * (w0 * (qa * w0 + qb * w1) + w1 * (qb * w0 + qc * w1)) -
+                                          (q0 * (k0.w * q0 + k1.x * q1) + q1 * (k1.x * q0 + k1.y * q1));
+                        const float dg = -0.5f * G * dq;
+                        const float d2g = G * (0.25f * dq * dq - 0.5f * d2q);
+                        float sg = 0.f, sh = 0.f;
 #pragma unroll
                         for (int ch = 0; ch < 3; ++ch) {
                             const float s = wa * acol[ch];
-                            const float dc0 = s * dg0, dc1 = s * dg1;
-                            const float gs = gl[ch] * s;
-                            v[0] += gl[ch] * dc0;
-                            v[1] += gl[ch] * dc1;
-                            v[2] += hl[ch] * dc0 * dc0 + gs * h00;
-                            v[3] += hl[ch] * dc0 * dc1 + gs * h01;
-                            v[4] += hl[ch] * dc1 * dc1 + gs * h11;
+                            sg += gl[ch] * s;
+                            sh += hl[ch] * s * s;
                         }
+                        v[0] = sg * dg;
+                        v[1] = sh * dg * dg + sg * d2g;
+                    } else if constexpr (PASS == kPassScaling) {
+                        // Per-view eigen directions (newton.hpp:426-465): z_i = v_i . qd,
+                        // dG_i = G z_i^2 / 2, d2G_ij = G (z_i^2 z_j^2 / 4 - z_i z_j v_i^T Q v_j).
+                        const float4 k0 = s_const[j * NC4], k1 = s_const[j * NC4 + 1];
+                        const float G = ev.g;
+                        const float z0 = k0.x * ev.qd0 + k0.y * ev.qd1;
+                        const float z1 = k0.z * ev.qd0 + k0.w * ev.qd1;
+                        const float zz0 = z0 * z0, zz1 = z1 * z1;
+                        const float dg0 = 0.5f * G * zz0, dg1 = 0.5f * G * zz1;
+                        const float h00 = G * (0.25f * zz0 * zz0 - zz0 * k1.x);
+                        const float h01 = G * (0.25f * zz0 * zz1 - z0 * z1 * k1.y);
+                        const float h11 = G * (0.25f * zz1 * zz1 - zz1 * k1.z);
+                        float sg = 0.f, sh = 0.f;
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const float s = wa * acol[ch];
+                            sg += gl[ch] * s;
+                            sh += hl[ch] * s * s;
+                        }
+                        v[0] = sg * dg0;
+                        v[1] = sg * dg1;
+                        v[2] = sh * dg0 * dg0 + sg * h00;
+                        v[3] = sh * dg0 * dg1 + sg * h01;
+                        v[4] = sh * dg1 * dg1 + sg * h11;
                     } else {  // opacity data terms + colour accumulators (newton.hpp:516-567)
                         const float GT = ev.g * Ti;
 #pragma unroll

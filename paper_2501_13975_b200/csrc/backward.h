@@ -13,14 +13,17 @@ constexpr int kAccRotation = 2;  // grad, hess
 constexpr int kAccScaling = 5;   // grad 2, hess (00, 01, 11)
 constexpr int kAccOpColor = 8;   // opacity grad, hess; colour g_acc[3], h_acc[3] (per view)
 
-// Per-(Gaussian, view) constant layouts (floats, AoS per Gaussian).
-constexpr int kPosM = 0;    // 5x3
-constexpr int kPosHu = 15;  // 5 x sym3
-constexpr int kPosJc = 45;  // 3x3 (channel, coord)
-constexpr int kPosHc = 54;  // 3 x sym3
-constexpr int kPosConsts = 72;
-constexpr int kRotConsts = 6;    // s1 (00, 01, 11), s2 (00, 01, 11)
-constexpr int kScaleConsts = 7;  // v0 (2), v1 (2), m00, m01, m11
+// Per-(Gaussian, view) constant layouts (floats, AoS per Gaussian, float4-aligned
+// groups). Symmetric 3x3 pairs (c, d) are packed (00, 01, 02, 11, 12, 22).
+constexpr int kPosJS = 0;    // J columns (Jx_c, Jy_c) x3, then dSigma/dp_c (a, b, c) x3   [15 + 1 pad]
+constexpr int kPosHpi = 16;  // d2pi/dp_c dp_d: (x, y) per pair                            [12]
+constexpr int kPosScd = 28;  // d2Sigma/dp_c dp_d: (a, b, c) per pair                      [18 + 2 pad]
+constexpr int kPosJc = 48;   // dc~_ch/dp: 3 per channel, padded to 4                       [12]
+constexpr int kPosJJ = 60;   // Jc_ch Jc_ch^T: 6 per channel                                [18]
+constexpr int kPosHc = 78;   // d2c~_ch/dp2: 6 per channel                                  [18]
+constexpr int kPosConsts = 96;
+constexpr int kRotConsts = 8;    // s1 (00, 01, 11), s2 (00, 01, 11), pad 2
+constexpr int kScaleConsts = 8;  // v0 (2), v1 (2), m00, m01, m11, pad
 
 struct BackwardArgs {
     int tiles_x, W, H;

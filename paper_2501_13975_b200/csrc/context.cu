@@ -58,8 +58,8 @@ struct TrainerState {
     std::vector<int> train_ids, probe_ids;
     std::vector<std::vector<int>> neighbors;
     // Targets, planar FP32: device-resident or pinned host (host_targets).
-    std::vector<DevBuf<float>> targets, down_targets;
-    std::vector<float*> host_targets, host_down_targets;
+    std::vector<DevBuf<double>> targets, down_targets;
+    std::vector<double*> host_targets, host_down_targets;
     double barrier_weight = 1e-4;
     int step_count = 0;
     std::vector<ViewSlot> views;  // primary + secondaries of the current step
@@ -232,12 +232,13 @@ SolveParams to_solve(const ngs_newton_options* o, int commit) {
     return p;
 }
 
-// Interleaved double RGB (Image, image.hpp:11-35) <-> planar FP32.
-void interleaved_to_planar(const double* src, int w, int h, std::vector<float>& out) {
+// Interleaved double RGB (Image, image.hpp:11-35) <-> planar.
+template <typename T>
+void interleaved_to_planar(const double* src, int w, int h, std::vector<T>& out) {
     const size_t n = static_cast<size_t>(w) * h;
     out.resize(3 * n);
     for (size_t i = 0; i < n; ++i)
-        for (int c = 0; c < 3; ++c) out[c * n + i] = static_cast<float>(src[3 * i + c]);
+        for (int c = 0; c < 3; ++c) out[c * n + i] = static_cast<T>(src[3 * i + c]);
 }
 
 template <typename T>
@@ -509,10 +510,11 @@ int32_t ngs_build_view(ngs_context* ctx, int32_t slot, const ngs_camera* camera,
         v.raster = to_raster(raster);
         v.loss = to_loss(loss);
         const size_t npx = static_cast<size_t>(camera->width) * camera->height;
-        std::vector<float> tgt;
+        std::vector<double> tgt;
         interleaved_to_planar(target_rgb, camera->width, camera->height, tgt);
         v.target.ensure(3 * npx);
-        CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, tgt.data(), sizeof(float) * 3 * npx, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, tgt.data(), sizeof(double) * 3 * npx, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         render_view(ctx->scene, v, true, ctx->err.ptr, ctx->stream);
         compute_loss(v, ctx->stream);
         double sums[2];
@@ -922,9 +924,9 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
             down.width = cam.width / f;
             down.height = cam.height / f;
             T.down_cameras.push_back(down);
-            std::vector<float> planar;
+            std::vector<double> planar;
             interleaved_to_planar(targets[i], cam.width, cam.height, planar);
-            std::vector<float> dplanar;
+            std::vector<double> dplanar;
             if (exact_low) {
                 const int ef = clamp_downsample_factor(cam, secondary_targets_downsample);
                 if (cam.width / ef == down.width && cam.height / ef == down.height) {
@@ -938,18 +940,18 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
                 interleaved_to_planar(box.data(), ow, oh, dplanar);
             }
             if (c->host_targets) {
-                float *h1 = nullptr, *h2 = nullptr;
-                CUDA_CHECK(cudaMallocHost(&h1, sizeof(float) * planar.size()));
-                CUDA_CHECK(cudaMallocHost(&h2, sizeof(float) * dplanar.size()));
-                std::memcpy(h1, planar.data(), sizeof(float) * planar.size());
-                std::memcpy(h2, dplanar.data(), sizeof(float) * dplanar.size());
+                double *h1 = nullptr, *h2 = nullptr;
+                CUDA_CHECK(cudaMallocHost(&h1, sizeof(double) * planar.size()));
+                CUDA_CHECK(cudaMallocHost(&h2, sizeof(double) * dplanar.size()));
+                std::memcpy(h1, planar.data(), sizeof(double) * planar.size());
+                std::memcpy(h2, dplanar.data(), sizeof(double) * dplanar.size());
                 T.host_targets.push_back(h1);
                 T.host_down_targets.push_back(h2);
             } else {
                 T.targets[i].ensure(planar.size());
                 T.down_targets[i].ensure(dplanar.size());
-                CUDA_CHECK(cudaMemcpy(T.targets[i].ptr, planar.data(), sizeof(float) * planar.size(), cudaMemcpyHostToDevice));
-                CUDA_CHECK(cudaMemcpy(T.down_targets[i].ptr, dplanar.data(), sizeof(float) * dplanar.size(), cudaMemcpyHostToDevice));
+                CUDA_CHECK(cudaMemcpy(T.targets[i].ptr, planar.data(), sizeof(double) * planar.size(), cudaMemcpyHostToDevice));
+                CUDA_CHECK(cudaMemcpy(T.down_targets[i].ptr, dplanar.data(), sizeof(double) * dplanar.size(), cudaMemcpyHostToDevice));
             }
         }
         T.views.resize(1 + c->knn);
@@ -998,11 +1000,11 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
             const size_t npx = static_cast<size_t>(cam.width) * cam.height;
             v.target.ensure(3 * npx);
             if (T.cfg.host_targets) {
-                const float* src = (i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id];
-                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyHostToDevice, s));
+                const double* src = (i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id];
+                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx, cudaMemcpyHostToDevice, s));
             } else {
-                const float* src = (i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr;
-                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(float) * 3 * npx, cudaMemcpyDeviceToDevice, s));
+                const double* src = (i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr;
+                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx, cudaMemcpyDeviceToDevice, s));
             }
         }
         RenderSync rs;

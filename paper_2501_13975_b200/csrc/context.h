@@ -83,11 +83,11 @@ struct ViewSlot {
     DevBuf<int2> ranges;
     DevBuf<unsigned char> cub_temp;
     // K6 forward raster outputs (planar [3][H][W])
-    DevBuf<double> image;   // FP64: FP32 rounding is amplified by the (c - c^t) cancellation in the loss
+    DevBuf<double> image;   // FP64 (see raster_forward_k)
     DevBuf<float> t_final;
     DevBuf<int> last;       // index into the tile list of the last contributing splat, -1 if none
     // K7 loss fields
-    DevBuf<float> target;   // planar [3][H][W]
+    DevBuf<double> target;  // planar [3][H][W], FP64 like the reference Image
     DevBuf<double> fields;  // 9 center fields x 3 channels x H x W
     DevBuf<float> loss_grad, loss_hess;  // planar [3][H][W]
     DevBuf<double> loss_sums;            // [0] sum d^2, [1] sum ssim

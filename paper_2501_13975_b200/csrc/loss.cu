@@ -46,7 +46,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 // Kernel A: window statistics and the 9 window-centre fields for one channel.
 __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double* __restrict__ image,
-                                                     const float* __restrict__ target, Window win, double c1, double c2,
+                                                     const double* __restrict__ target, Window win, double c1, double c2,
                                                      double* __restrict__ fields, double* __restrict__ sums) {
     __shared__ double s_x[kLS][kLS + 1], s_t[kLS][kLS + 1];
     __shared__ double s_h[5][kLS][kLT + 1];
@@ -56,14 +56,14 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
     const int h = win.half, span = kLT + 2 * h;
     const size_t plane = static_cast<size_t>(W) * H;
     const double* img = image + ch * plane;
-    const float* tgt = target + ch * plane;
+    const double* tgt = target + ch * plane;
     for (int i = threadIdx.x; i < span * span; i += blockDim.x) {
         const int r = i / span, c = i % span;
         const int gx = ox - h + c, gy = oy - h + r;
         const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
         const size_t idx = static_cast<size_t>(gy) * W + gx;
         s_x[r][c] = in ? img[idx] : 0.0;
-        s_t[r][c] = in ? static_cast<double>(tgt[idx]) : 0.0;
+        s_t[r][c] = in ? tgt[idx] : 0.0;
     }
     __syncthreads();
     // Horizontal pass (out-of-image taps are zero == skipped taps).
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
 // Kernel B: convolve the 9 centre fields and combine into grad / hess; also the
 // L2 part. lambda == 0 skips the SSIM fields entirely (loss.hpp:345).
 __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double* __restrict__ image,
-                                                     const float* __restrict__ target, Window win, double lambda,
+                                                     const double* __restrict__ target, Window win, double lambda,
                                                      const double* __restrict__ fields, float* __restrict__ grad,
                                                      float* __restrict__ hess, double* __restrict__ sums) {
     __shared__ double s_f[kLS][kLS + 1];

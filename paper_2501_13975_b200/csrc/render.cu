@@ -238,9 +238,8 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
                                                         const float4* __restrict__ rc, float bg0, float bg1, float bg2,
                                                         float cutoff, float tmin, double* __restrict__ image,
                                                         float* __restrict__ t_final, int* __restrict__ last_out) {
-    __shared__ float s_px[kRasterBatch], s_py[kRasterBatch], s_qa[kRasterBatch], s_qb[kRasterBatch],
-        s_qc[kRasterBatch], s_sig[kRasterBatch], s_c0[kRasterBatch], s_c1[kRasterBatch], s_c2[kRasterBatch],
-        s_qmax[kRasterBatch];
+    __shared__ float4 s_g0[kRasterBatch], s_g1[kRasterBatch];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
+    __shared__ float2 s_g2[kRasterBatch];                      // (c1, c2)
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
@@ -250,7 +249,7 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
     const double ox = tx * kTile, oy = ty * kTile;
     const int2 range = ranges[tile];
     float T = 1.0f;
-    double C0 = 0.0, C1 = 0.0, C2 = 0.0;  // FP64 colour sums (the backward's prefix uses the same)
+    double C0 = 0.0, C1 = 0.0, C2 = 0.0;  // FP64 colour sums: the image feeds the cancelling (c - c^t) loss terms
     int last = -1;
     bool done = !inside;
     for (int base = range.x; base < range.y; base += kRasterBatch) {
@@ -260,28 +259,23 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
             const int k = vals[i];
             const double2 p = pix[k];
             const float4 a = ra[k], b = rb[k], c = rc[k];
-            s_px[threadIdx.x] = static_cast<float>(p.x - ox);
-            s_py[threadIdx.x] = static_cast<float>(p.y - oy);
-            s_qa[threadIdx.x] = a.z;
-            s_qb[threadIdx.x] = a.w;
-            s_qc[threadIdx.x] = b.x;
-            s_sig[threadIdx.x] = b.y;
-            s_c0[threadIdx.x] = b.z;
-            s_c1[threadIdx.x] = b.w;
-            s_c2[threadIdx.x] = c.x;
-            s_qmax[threadIdx.x] = reject_bound(b.y, cutoff);
+            s_g0[threadIdx.x] = make_float4(static_cast<float>(p.x - ox), static_cast<float>(p.y - oy), a.z, a.w);
+            s_g1[threadIdx.x] = make_float4(b.x, b.y, reject_bound(b.y, cutoff), b.z);
+            s_g2[threadIdx.x] = make_float2(b.w, c.x);
         }
         __syncthreads();
         const int cnt = min(kRasterBatch, range.y - base);
         if (!done) {
             for (int j = 0; j < cnt; ++j) {
+                const float4 g0 = s_g0[j], g1 = s_g1[j];
                 SplatEval e;
-                if (!eval_splat(s_px[j], s_py[j], s_qa[j], s_qb[j], s_qc[j], s_sig[j], fx, fy, s_qmax[j], e)) continue;
+                if (!eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, e)) continue;
                 if (e.alpha < cutoff) continue;
+                const float2 g2 = s_g2[j];
                 const double w = blend_weight(T, e.alpha);
-                C0 = __fma_rn(w, s_c0[j], C0);
-                C1 = __fma_rn(w, s_c1[j], C1);
-                C2 = __fma_rn(w, s_c2[j], C2);
+                C0 = __fma_rn(w, g1.w, C0);
+                C1 = __fma_rn(w, g2.x, C1);
+                C2 = __fma_rn(w, g2.y, C2);
                 T = next_transmittance(T, e.alpha);
                 last = base + j;
                 if (tmin > 0.f && T < tmin) {
