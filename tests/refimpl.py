@@ -16,7 +16,7 @@ from paper_2501_13975_b200.capi import (Camera, NgsLibrary, Scene, _dptr, _iptr,
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF_LIB = os.path.join(REPO, "oracle", "_ref", "libngs_ref.so")
-ORACLE_LIB = os.path.join(REPO, "oracle", "_ref", "libngs_oracle.so")
+
 
 
 class ngsref_synth_params(C.Structure):

@@ -1,0 +1,81 @@
+"""GPU parity against the committed golden vectors (tests/golden, produced by the
+reference itself): runs without the oracle libraries, through the C-ABI only."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2501_13975_b200 import capi
+from test_oracle import cam_from, load, scene_from
+
+pytestmark = pytest.mark.gpu
+FLOOR = 1e-3
+
+
+def qerr(a, b, floor_frac=FLOOR):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    floor = max(floor_frac * float(np.max(np.abs(b))), 1e-300)
+    return float(np.max(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)))
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    return capi.product()
+
+
+def test_golden_render_and_binning(gpu):
+    g = load("render.npz")
+    ctx = gpu.context()
+    ctx.set_scene(scene_from(g, "s_"))
+    cam = cam_from(g, "c_")
+    assert np.max(np.abs(ctx.render(cam) - g["image_default"])) < 1e-6
+    assert np.max(np.abs(ctx.render(cam, gpu.reference_raster()) - g["image_reference"])) < 1e-6
+    ctx.build_view(0, cam, np.zeros((32, 48, 3)))
+    sp = ctx.view_splats(0)
+    assert np.array_equal(sp["kernel"], g["splat_kernel"])
+    assert np.array_equal(sp["tile_offsets"], g["splat_tile_offsets"])
+    assert np.array_equal(sp["tile_indices"], g["splat_tile_indices"])
+
+
+@pytest.mark.parametrize("attr", range(5))
+def test_golden_terms_and_solves(gpu, attr):
+    g = load("newton.npz")
+    name = capi.ATTRIBUTES[attr]
+
+    def views(ctx):
+        ctx.set_scene(scene_from(g, "s_"))
+        lv = ctx.build_view(0, cam_from(g, "c_"), g["target"])
+        for i in range(2):
+            ctx.build_view(1 + i, cam_from(g, f"sec{i}_"), g[f"sec{i}_target"])
+        return lv
+
+    ctx = gpu.context()
+    lv = views(ctx)
+    assert abs(lv - float(g["loss_value"])) <= 1e-5 * abs(float(g["loss_value"]))
+    gg, hh, vis = ctx.accumulate(attr, 0, [1, 2])
+    assert np.array_equal(vis, g[f"terms_{name}_visible"])
+    assert qerr(gg, g[f"terms_{name}_grad"]) < 1e-3
+    assert qerr(hh, g[f"terms_{name}_hess"]) < 1e-3
+    ctx2 = gpu.context()
+    views(ctx2)
+    res = ctx2.newton_step(attr, 0, [1, 2])
+    assert qerr(res["delta"], g[f"solve_{name}_delta"]) < 2e-3
+    assert np.array_equal(res["accepted"], g[f"solve_{name}_accepted"])
+
+
+def test_golden_trainer_step(gpu):
+    g = load("trainer.npz")
+    ctx = gpu.context()
+    ctx.set_scene(scene_from(g, "init_"))
+    n = len([k for k in g if k.startswith("cam") and k.endswith("_view")])
+    cfg = gpu.default_train()
+    cfg.knn = 2
+    cfg.secondary_downsample = 2
+    ctx.trainer_configure(cfg, [cam_from(g, f"cam{i}_") for i in range(n)], [g[f"target{i}"] for i in range(n)],
+                          list(range(n)), [], [g[f"sec_target{i}"] for i in range(n)], 2)
+    assert ctx.trainer_neighbors(0) == list(g["neighbors0"])
+    rep = ctx.trainer_step(0)
+    assert qerr(list(rep.delta_norms), g["delta_norms"]) < 1e-3
+    post = ctx.get_scene()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        assert qerr(getattr(post, f), g["post_" + f]) < 1e-4, f
