@@ -10,8 +10,11 @@ ground-truth targets are rendered on the GPU from the truth scene.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1|c2|c3]
 
-Prints ONE JSON line (rank 0). Multi-GPU (torchrun): each rank runs its own
-Newton steps on a disjoint shard of the training views (replicas, weak scaling).
+Prints ONE JSON line (rank 0). Multi-GPU (torchrun): every rank runs the same
+sequence of Newton steps; each view of a step is split into tile-row bands
+across ranks, and the per-Gaussian FP64 accumulators are summed by an NCCL
+all-reduce after every backward pass before the replicated solve (DESIGN.md §7;
+strong scaling of one step, exact reference semantics).
 """
 from __future__ import annotations
 
@@ -196,6 +199,11 @@ def ours_arm(args, cfg: Config):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = capi.product()
     ctx = lib.context(local)
+    nccl_id = None
+    if world > 1:
+        obj = [capi.dist_unique_id(lib) if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
     truth, init = make_scenes(cfg)
     cams = cameras_for(cfg)
     ctx.set_scene(truth)
@@ -208,8 +216,10 @@ def ours_arm(args, cfg: Config):
         c.trainer_configure(tc, cams, targets, list(range(cfg.views)))
 
     configure(ctx, False)
+    if world > 1:
+        ctx.dist_init(nccl_id, rank, world)
     order = [int(v) for v in np.random.default_rng(7).permutation(cfg.views)]
-    shard = order[rank::world]
+    shard = order  # every rank steps the same views; the work of each step is sharded
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
 
     def view(i):
@@ -219,13 +229,18 @@ def ours_arm(args, cfg: Config):
         ctx.trainer_step(view(i))
     ctx.profile_reset()
     dts = []
+    prof_range = os.environ.get("NGS_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with ClockSampler(local) as clocks:
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         for i in range(args.steps):
             l2_flush(flush)
+            if prof_range:
+                torch.cuda.profiler.start()
             rep = ctx.trainer_step(view(args.warmup + i))
+            if prof_range:
+                torch.cuda.profiler.stop()
             dts.append(rep.dt_ms)
         torch.cuda.synchronize()
         if world > 1:
@@ -237,6 +252,10 @@ def ours_arm(args, cfg: Config):
     # bracketed by CUDA events on its stream) for the per-kernel roofline.
     pctx = lib.context(local)
     configure(pctx, False)
+    if world > 1:
+        obj = [capi.dist_unique_id(lib) if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        pctx.dist_init(obj[0], rank, world)
     for i in range(args.warmup):
         pctx.trainer_step(view(i))
     pctx.profile_reset()
@@ -252,6 +271,10 @@ def ours_arm(args, cfg: Config):
     ectx = lib.context(local)
     ectx.set_scene(init)
     configure(ectx, True)
+    if world > 1:
+        obj = [capi.dist_unique_id(lib) if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        ectx.dist_init(obj[0], rank, world)
     for i in range(args.warmup):
         ectx.trainer_step(view(i))
     e2e_ms = []
@@ -274,7 +297,7 @@ def ours_arm(args, cfg: Config):
 
     if rank != 0:
         return
-    views_total = args.steps * world
+    views_total = args.steps  # each step is one view, done jointly by all ranks
     value = views_total / (total_ms / 1e3)
     e2e_value = views_total / (e2e_total / 1e3)
 
@@ -293,10 +316,10 @@ def ours_arm(args, cfg: Config):
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
     line = {
         "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
         "config": {"workload": cfg.name, "desc": cfg.desc, "knn": 3, "secondary_downsample": 4,
-                   "parallelism": f"view-shard replicas x{world}", "l2": "flushed (256 MB write) between steps",
+                   "parallelism": f"tile-row bands x{world} + NCCL all-reduce of accumulators", "l2": "flushed (256 MB write) between steps",
                    "targets": "GPU-rendered from the truth scene"},
         "gaussian_solves_per_s": value * cfg.kernels,
         "e2e": {"value": e2e_value, "unit": "views/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

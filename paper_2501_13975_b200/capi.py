@@ -458,10 +458,34 @@ class Context:
         self._call("ngs_microbench_fp64", C.byref(v))
         return v.value
 
+    # multi-GPU sharding (include/ngs_b200_dist.h; CUDA library only)
+    def set_shard(self, rank: int, world: int):
+        self._call("ngs_set_shard", C.c_int32(rank), C.c_int32(world))
+
+    def dist_init(self, unique_id: bytes, rank: int, world: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self._call("ngs_dist_init", buf, C.c_int32(rank), C.c_int32(world))
+
     def barrier_weight(self) -> float:
         v = C.c_double()
         self._call("ngs_trainer_barrier_weight", C.byref(v))
         return v.value
+
+
+def dist_unique_id(lib: NgsLibrary) -> bytes:
+    """ncclGetUniqueId through the library (rank 0); broadcast the bytes to all ranks."""
+    buf = (C.c_uint8 * 128)()
+    lib.check(lib.lib.ngs_dist_unique_id(buf))
+    return bytes(buf)
+
+
+def shard_rows(tiles_y: int, rank: int, world: int):
+    """Mirror of ngsb::shard_rows (csrc/context.h): (band_y0, band_y1, own_y0, own_y1)."""
+    if world <= 1:
+        return 0, tiles_y, 0, tiles_y
+    own0 = tiles_y * rank // world
+    own1 = tiles_y * (rank + 1) // world
+    return (own0 - 1 if own0 > 0 else 0), (own1 + 1 if own1 < tiles_y else tiles_y), own0, own1
 
 
 _product = None

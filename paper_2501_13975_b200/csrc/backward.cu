@@ -15,6 +15,8 @@
 //
 // Per-(Gaussian, view) chain-rule constants are computed once per pass in FP64
 // by the *_consts kernels and staged through shared memory per batch.
+#include <algorithm>
+
 #include "backward.h"
 #include "geometry.cuh"
 #include "splat.cuh"
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     __shared__ int s_maxlast;
     unsigned long long block_pairs = 0;
 
-    const int tile = blockIdx.x;
+    const int tile = a.tile0 + blockIdx.x;  // owned tile rows only (multi-GPU shard)
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
     const int x = tx * kTile + lx, y = ty * kTile + ly;
@@ -612,12 +614,16 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     a.acc_stride = acc_stride;
     a.visible = visible;
     a.contrib_pairs = contrib_pairs;
+    const int own0 = std::max(0, v.raster.own_y0), own1 = std::min(v.cam.tiles_y, v.raster.own_y1);
+    if (own1 <= own0) return;
+    a.tile0 = own0 * v.cam.tiles_x;
+    const int blocks = (own1 - own0) * v.cam.tiles_x;
     StageScope st(NGS_STAGE_BWD_POSITION + pass, s);
     switch (pass) {
-        case kPassPosition: backward_k<kPassPosition><<<v.T, 256, 0, s>>>(a); break;
-        case kPassRotation: backward_k<kPassRotation><<<v.T, 256, 0, s>>>(a); break;
-        case kPassScaling: backward_k<kPassScaling><<<v.T, 256, 0, s>>>(a); break;
-        case kPassOpacityColor: backward_k<kPassOpacityColor><<<v.T, 256, 0, s>>>(a); break;
+        case kPassPosition: backward_k<kPassPosition><<<blocks, 256, 0, s>>>(a); break;
+        case kPassRotation: backward_k<kPassRotation><<<blocks, 256, 0, s>>>(a); break;
+        case kPassScaling: backward_k<kPassScaling><<<blocks, 256, 0, s>>>(a); break;
+        case kPassOpacityColor: backward_k<kPassOpacityColor><<<blocks, 256, 0, s>>>(a); break;
     }
     CUDA_LAUNCH_CHECK();
 }

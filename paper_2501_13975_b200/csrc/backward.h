@@ -27,6 +27,7 @@ constexpr int kScaleConsts = 8;  // v0 (2), v1 (2), m00, m01, m11, pad
 
 struct BackwardArgs {
     int tiles_x, W, H;
+    int tile0;  // first tile of the owned band
     const int2* ranges;
     const int* vals;
     const double2* pix;

@@ -6,6 +6,8 @@
 // entry point computes on the host except one-time trainer setup (KNN of
 // camera poses, secondary.hpp:24-94) and read-back format conversion.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -18,6 +20,7 @@
 #include "backward.h"
 #include "context.h"
 #include "solve.h"
+#include "ngs_b200_dist.h"
 
 namespace ngsb {
 thread_local Profiler* g_prof = nullptr;
@@ -45,6 +48,40 @@ int guarded(F&& f) {
 }
 
 constexpr int kScratchSlot = NGS_MAX_VIEW_SLOTS;  // ngs_render's private slot
+
+// NCCL is loaded at run time (dlopen) so the library has no link-time NCCL
+// dependency and shares whichever libnccl.so.2 the process already uses.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.error_string;
+        return a;
+    }();
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw ngsb::Error(NGS_ERR_NCCL, std::string(what) + ": " + nccl().error_string(r));
+}
 
 }  // namespace
 
@@ -102,9 +139,13 @@ struct ngs_context {
     DevBuf<int> overflow;
     DevBuf<float4> snap_ps, snap_sc, snap_q;
     DevBuf<float> snap_sh;
+    // Multi-GPU shard (ngs_b200_dist.h)
+    int shard_rank = 0, shard_world = 1;
+    ncclComm_t comm = nullptr;
     unsigned long long contrib_pairs_total = 0;
 
     ~ngs_context() {
+        if (comm) nccl().comm_destroy(comm);
         for (auto& s : slots) s.release_all();
         trainer.release();
         pos_sigma.release();
@@ -158,6 +199,9 @@ struct ngs_context {
         }
     }
 
+    // Raster parameters of a view with this context's shard applied.
+    RasterParams raster_for(const ngs_raster_options* o, const CameraDev& cam) const;
+
     ViewSlot& slot(int i) {
         if (i < 0 || i >= NGS_MAX_VIEW_SLOTS) throw Error(NGS_ERR_INVALID_INPUT, "bad view slot");
         return slots[i];
@@ -200,6 +244,16 @@ LossParams to_loss(const ngs_loss_config* o) {
     if (!o) o = &d;
     return LossParams{o->lambda, o->c1, o->c2, o->window, o->window_sigma};
 }
+
+}  // namespace
+
+RasterParams ngs_context::raster_for(const ngs_raster_options* o, const CameraDev& cam) const {
+    RasterParams r = to_raster(o);
+    shard_rows(cam.tiles_y, shard_rank, shard_world, r);
+    return r;
+}
+
+namespace {
 
 float float_above(double v) {
     float f = static_cast<float>(v);
@@ -492,7 +546,7 @@ int32_t ngs_render(ngs_context* ctx, const ngs_camera* camera, const ngs_raster_
         CUDA_CHECK(cudaSetDevice(ctx->device));
         ViewSlot& v = ctx->slots[kScratchSlot];
         upload_camera(*camera, v.cam);
-        v.raster = to_raster(options);
+        v.raster = to_raster(options);  // ngs_render is never sharded (full image out)
         render_view(ctx->scene, v, false, ctx->err.ptr, ctx->stream);
         ctx->check_err();
         download_planar(v.image.ptr, v.W, v.H, rgb_out, ctx->stream);
@@ -507,7 +561,7 @@ int32_t ngs_build_view(ngs_context* ctx, int32_t slot, const ngs_camera* camera,
         ViewSlot& v = ctx->slot(slot);
         v.valid = false;
         upload_camera(*camera, v.cam);
-        v.raster = to_raster(raster);
+        v.raster = ctx->raster_for(raster, v.cam);
         v.loss = to_loss(loss);
         const size_t npx = static_cast<size_t>(camera->width) * camera->height;
         std::vector<double> tgt;
@@ -664,6 +718,16 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
         launch_backward(pass, ctx->scene, v, acc, stride, visible, ctx->pairs.ptr + pass, s);
     }
     if (concurrent) ctx->join(nv);
+    if (ctx->comm) {
+        // Exchange step: per-Gaussian FP64 accumulators summed over ranks (NVLink / NVSwitch).
+        StageScope st(NGS_STAGE_OTHER, ctx->stream, 0);
+        nccl_check(nccl().all_reduce(ctx->acc.ptr, ctx->acc.ptr, stride * comps, ncclFloat64, ncclSum, ctx->comm,
+                                     ctx->stream),
+                   "ncclAllReduce(accumulators)");
+        if (visible)
+            nccl_check(nccl().all_reduce(visible, visible, stride, ncclUint8, ncclMax, ctx->comm, ctx->stream),
+                       "ncclAllReduce(visible)");
+    }
 }
 
 ColorViews color_views(ViewSlot* const* views, int nv) {
@@ -995,7 +1059,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
         if (upload_targets) {
             upload_camera(cam, v.cam);
-            v.raster = to_raster(&T.cfg.raster);
+            v.raster = ctx->raster_for(&T.cfg.raster, v.cam);
             v.loss = to_loss(&T.cfg.loss);
             const size_t npx = static_cast<size_t>(cam.width) * cam.height;
             v.target.ensure(3 * npx);
@@ -1187,6 +1251,50 @@ int32_t ngs_microbench_fp64(ngs_context* ctx, double* tflops) {
     return guarded([&] {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         *tflops = fma_peak<double>(ctx);
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-GPU (ngs_b200_dist.h)
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int32_t ngs_dist_unique_id(uint8_t out[NGS_DIST_ID_BYTES]) {
+    return guarded([&] {
+        if (!nccl().ok) throw Error(NGS_ERR_NCCL, "libnccl.so.2 not found");
+        ncclUniqueId id;
+        nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(out, id.internal, NGS_DIST_ID_BYTES);
+    });
+}
+
+int32_t ngs_dist_init(ngs_context* ctx, const uint8_t id_bytes[NGS_DIST_ID_BYTES], int32_t rank, int32_t world) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) throw Error(NGS_ERR_INVALID_INPUT, "bad rank/world");
+        if (!nccl().ok) throw Error(NGS_ERR_NCCL, "libnccl.so.2 not found");
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ncclUniqueId id;
+        std::memcpy(id.internal, id_bytes, NGS_DIST_ID_BYTES);
+        if (ctx->comm) {
+            nccl().comm_destroy(ctx->comm);
+            ctx->comm = nullptr;
+        }
+        if (world > 1) nccl_check(nccl().comm_init_rank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+        ctx->shard_rank = rank;
+        ctx->shard_world = world;
+        for (auto& v : ctx->slots) v.valid = false;
+    });
+}
+
+int32_t ngs_set_shard(ngs_context* ctx, int32_t rank, int32_t world) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) throw Error(NGS_ERR_INVALID_INPUT, "bad rank/world");
+        ctx->shard_rank = rank;
+        ctx->shard_world = world;
+        for (auto& v : ctx->slots) v.valid = false;
     });
 }
 

@@ -23,7 +23,26 @@ struct RasterParams {
     float t_min;
     bool cutoff_enabled;  // alpha_cutoff > 0: AABB binning, else every splat in every tile
     double radius;        // max(3, sqrt(2 ln(1/alpha_cutoff)))  rasterizer.hpp:215-216
+    // Multi-GPU shard of this view: tile rows [band_y0, band_y1)
+    // are projected, binned, rasterised and get loss fields (owned rows plus a
+    // one-tile-row halo, which covers the 10-px SSIM support); the backward
+    // runs over the owned rows [own_y0, own_y1) only. Full frame when unsharded.
+    int band_y0 = 0, band_y1 = 1 << 30;
+    int own_y0 = 0, own_y1 = 1 << 30;
 };
+
+// Rows of tile-row band `rank` of `world` for a view with `tiles_y` rows.
+inline void shard_rows(int tiles_y, int rank, int world, RasterParams& r) {
+    if (world <= 1) {
+        r.band_y0 = r.own_y0 = 0;
+        r.band_y1 = r.own_y1 = tiles_y;
+        return;
+    }
+    r.own_y0 = static_cast<int>(static_cast<long long>(tiles_y) * rank / world);
+    r.own_y1 = static_cast<int>(static_cast<long long>(tiles_y) * (rank + 1) / world);
+    r.band_y0 = r.own_y0 > 0 ? r.own_y0 - 1 : 0;
+    r.band_y1 = r.own_y1 < tiles_y ? r.own_y1 + 1 : tiles_y;
+}
 
 struct LossParams {
     double lambda, c1, c2;

@@ -9,6 +9,8 @@
 //   A: 5 window statistics -> 9 window-centre fields (loss.hpp:162-214, 262-305)
 //   B: 9 field convolutions (w for grad/kw, w^2 for the rest) -> grad, hess
 //      (loss.hpp:309-329) plus the L2 terms (loss.hpp:138-156).
+#include <algorithm>
+
 #include "context.h"
 
 namespace ngsb {
@@ -47,12 +49,14 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // Kernel A: window statistics and the 9 window-centre fields for one channel.
 __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double* __restrict__ image,
                                                      const double* __restrict__ target, Window win, double c1, double c2,
-                                                     double* __restrict__ fields, double* __restrict__ sums) {
+                                                     double* __restrict__ fields, double* __restrict__ sums, int row0,
+                                                     int own_y0, int own_y1) {
     __shared__ double s_x[kLS][kLS + 1], s_t[kLS][kLS + 1];
     __shared__ double s_h[5][kLS][kLT + 1];
     __shared__ double red[8];
     const int ch = blockIdx.z;
-    const int ox = blockIdx.x * kLT, oy = blockIdx.y * kLT;
+    const int ox = blockIdx.x * kLT, oy = (row0 + blockIdx.y) * kLT;
+    const bool own = (row0 + static_cast<int>(blockIdx.y)) >= own_y0 && (row0 + static_cast<int>(blockIdx.y)) < own_y1;
     const int h = win.half, span = kLT + 2 * h;
     const size_t plane = static_cast<size_t>(W) * H;
     const double* img = image + ch * plane;
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
         const size_t idx = static_cast<size_t>(y) * W + x;
         for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
     }
-    const double tot = block_sum(ssim, red);
+    const double tot = block_sum(own ? ssim : 0.0, red);
     if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
 }
 
@@ -137,12 +141,14 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
 __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double* __restrict__ image,
                                                      const double* __restrict__ target, Window win, double lambda,
                                                      const double* __restrict__ fields, float* __restrict__ grad,
-                                                     float* __restrict__ hess, double* __restrict__ sums) {
+                                                     float* __restrict__ hess, double* __restrict__ sums, int row0,
+                                                     int own_y0, int own_y1) {
     __shared__ double s_f[kLS][kLS + 1];
     __shared__ double s_h[kLS][kLT + 1];
     __shared__ double red[8];
     const int ch = blockIdx.z;
-    const int ox = blockIdx.x * kLT, oy = blockIdx.y * kLT;
+    const int ox = blockIdx.x * kLT, oy = (row0 + blockIdx.y) * kLT;
+    const bool own = (row0 + static_cast<int>(blockIdx.y)) >= own_y0 && (row0 + static_cast<int>(blockIdx.y)) < own_y1;
     const int h = win.half, span = kLT + 2 * h;
     const size_t plane = static_cast<size_t>(W) * H;
     const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
         grad[ch * plane + idx] = static_cast<float>(g);
         hess[ch * plane + idx] = static_cast<float>(hh);
     }
-    const double tot = block_sum(dsq, red);
+    const double tot = block_sum(own ? dsq : 0.0, red);
     if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
 }
 
@@ -234,17 +240,21 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     v.loss_hess.ensure(3 * npx);
     v.loss_sums.ensure(2);
     CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * sizeof(double), s));
-    const dim3 grid((v.W + kLT - 1) / kLT, (v.H + kLT - 1) / kLT, 3);
+    const int rows = (v.H + kLT - 1) / kLT;
+    const int row0 = std::max(0, v.raster.band_y0), row1 = std::min(rows, v.raster.band_y1);
+    const int own0 = std::max(0, v.raster.own_y0), own1 = std::min(rows, v.raster.own_y1);
+    if (row1 <= row0) return;
+    const dim3 grid((v.W + kLT - 1) / kLT, row1 - row0, 3);
     StageScope st(NGS_STAGE_LOSS, s, ssim ? 2 : 1);
     if (ssim) {
         v.fields.ensure(27 * npx);
         ssim_fields_k<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
-                                           v.loss_sums.ptr);
+                                           v.loss_sums.ptr, row0, own0, own1);
         CUDA_LAUNCH_CHECK();
     }
     ssim_derivs_k<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.lambda,
                                        ssim ? v.fields.ptr : nullptr, v.loss_grad.ptr, v.loss_hess.ptr,
-                                       v.loss_sums.ptr);
+                                       v.loss_sums.ptr, row0, own0, own1);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -152,9 +152,13 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
     auto clampi = [](int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); };
     const int tx0 = clampi(static_cast<int>(floor(x0 / kTile)), 0, cam.tiles_x - 1);
     const int tx1 = clampi(static_cast<int>(floor(x1 / kTile)), 0, cam.tiles_x - 1);
-    const int ty0 = clampi(static_cast<int>(floor(y0 / kTile)), 0, cam.tiles_y - 1);
-    const int ty1 = clampi(static_cast<int>(floor(y1 / kTile)), 0, cam.tiles_y - 1);
-    const bool off = x1 < 0 || x0 >= cam.width || y1 < 0 || y0 >= cam.height;
+    int ty0 = clampi(static_cast<int>(floor(y0 / kTile)), 0, cam.tiles_y - 1);
+    int ty1 = clampi(static_cast<int>(floor(y1 / kTile)), 0, cam.tiles_y - 1);
+    bool off = x1 < 0 || x0 >= cam.width || y1 < 0 || y0 >= cam.height;
+    // Multi-GPU shard: bin only into this rank's tile rows (band incl. halo).
+    ty0 = max(ty0, rp.band_y0);
+    ty1 = min(ty1, rp.band_y1 - 1);
+    off = off || ty0 > ty1;
     rect[k] = off ? make_int4(1, 1, 0, 0) : make_int4(tx0, ty0, tx1, ty1);
     tiles_touched[k] = off ? 0 : (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
     flags[k] = f;

@@ -1,0 +1,137 @@
+// C++ host path: include/ngs_b200.hpp (mirror of the reference ngs:: interface)
+// over the C-ABI of libngs_b200.so. Known answers from the reference suites.
+// Built by __graft_entry__.build(); run by tests/test_cpp_host.py on the GPU.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "ngs_b200.hpp"
+
+using namespace ngs::b200;
+
+static int failures = 0;
+#define EXPECT(c)                                                          \
+    do {                                                                   \
+        if (!(c)) {                                                        \
+            std::fprintf(stderr, "%s:%d: EXPECT(%s) failed\n", __FILE__, __LINE__, #c); \
+            ++failures;                                                    \
+        }                                                                  \
+    } while (0)
+
+static std::array<double, 16> lookat(double ex, double ey, double ez) {  // camera.hpp:288-304, target 0, up y
+    double f[3] = {-ex, -ey, -ez};
+    double fn = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    for (double& v : f) v /= fn;
+    const double up[3] = {0, 1, 0};
+    double r[3] = {up[1] * f[2] - up[2] * f[1], up[2] * f[0] - up[0] * f[2], up[0] * f[1] - up[1] * f[0]};
+    double rn = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    for (double& v : r) v /= rn;
+    double d[3] = {f[1] * r[2] - f[2] * r[1], f[2] * r[0] - f[0] * r[2], f[0] * r[1] - f[1] * r[0]};
+    const double e[3] = {ex, ey, ez};
+    auto dot = [&](const double* a) { return a[0] * e[0] + a[1] * e[1] + a[2] * e[2]; };
+    return {r[0], r[1], r[2], -dot(r), d[0], d[1], d[2], -dot(d), f[0], f[1], f[2], -dot(f), 0, 0, 0, 1};
+}
+
+static std::array<double, 16> perspective(double fov, double aspect) {  // camera.hpp:307-317
+    const double fy = 1.0 / std::tan(0.5 * fov), n = 0.05, fa = 100.0;
+    return {fy / aspect, 0, 0, 0, 0, fy, 0, 0, 0, 0, (fa + n) / (fa - n), -2 * fa * n / (fa - n), 0, 0, 1, 0};
+}
+
+int main() {
+    const double kSH0 = 0.28209479177387814;
+    // test_rasterizer.cpp:218-229 — single centred kernel, pixel (32, 32) == 0.8 red.
+    {
+        Context ctx;
+        Scene s;
+        GaussianKernel k;
+        k.scale = {0.05, 0.05, 0.05};
+        k.sigma = 0.8;
+        k.sh[0][0] = (1.0 - 0.5) / kSH0;
+        k.sh[1][0] = (0.0 - 0.5) / kSH0;
+        k.sh[2][0] = (0.0 - 0.5) / kSH0;
+        s.kernels.push_back(k);
+        ctx.set_scene(s);
+        const Camera cam(lookat(0, 0, -4), perspective(M_PI / 3, 1.0), 65, 65);
+        const Image img = ctx.render(cam);
+        const size_t i = 3 * (32 * 65 + 32);
+        EXPECT(std::abs(img.data[i] - 0.8) < 1e-6);
+        EXPECT(img.data[i + 1] == 0.0 && img.data[i + 2] == 0.0);
+    }
+    // test_rasterizer.cpp:167-174 — empty scene renders the background.
+    {
+        Context ctx;
+        Scene s;
+        s.background = {0.1, 0.2, 0.3};
+        ctx.set_scene(s);
+        const Image img = ctx.render(Camera(lookat(0, 0, -4), perspective(M_PI / 3, 1.0), 32, 32));
+        EXPECT(std::abs(img.data[3 * 40 + 1] - 0.2) < 1e-7);
+    }
+    // Exception mapping (core.hpp:30-48): camera.hpp:32-34 and scene.hpp:82-92.
+    {
+        bool thrown = false;
+        try {
+            Camera bad(lookat(0, 0, -4), perspective(1.0, 1.0), 8, 8);
+        } catch (const InvalidInput&) {
+            thrown = true;
+        }
+        EXPECT(thrown);
+        Context ctx;
+        Scene s;
+        GaussianKernel k;
+        k.sigma = 1.0;  // outside (1e-4, 1 - 1e-4)
+        s.kernels.push_back(k);
+        thrown = false;
+        try {
+            ctx.set_scene(s);
+        } catch (const InvalidInput&) {
+            thrown = true;
+        }
+        EXPECT(thrown);
+    }
+    // Trainer::step on a small fixture: the step decreases the primary loss.
+    {
+        Scene truth;
+        truth.sh_degree = 1;
+        truth.background = {0.05, 0.05, 0.08};
+        unsigned long long st = 12345;
+        auto u = [&]() { st = st * 6364136223846793005ull + 1442695040888963407ull; return (st >> 11) * 0x1.0p-53; };
+        for (int i = 0; i < 200; ++i) {
+            GaussianKernel k;
+            for (double& v : k.position) v = (u() - 0.5) * 1.2;
+            for (double& v : k.scale) v = 0.04 + 0.06 * u();
+            double q[4], n = 0;
+            for (double& v : q) { v = u() - 0.5; n += v * v; }
+            for (int j = 0; j < 4; ++j) k.quaternion[j] = q[j] / std::sqrt(n);
+            k.sigma = 0.35 + 0.35 * u();
+            for (int ch = 0; ch < 3; ++ch) { k.sh[ch][0] = (u() - 0.5) * 1.8; for (int c = 1; c < 4; ++c) k.sh[ch][c] = (u() - 0.5) * 0.2; }
+            truth.kernels.push_back(k);
+        }
+        Dataset ds;
+        Context render_ctx;
+        render_ctx.set_scene(truth);
+        for (int v = 0; v < 8; ++v) {
+            const double a = 2 * M_PI * v / 8;
+            ds.cameras.emplace_back(lookat(2.2 * std::cos(a), 0.5, 2.2 * std::sin(a)), perspective(M_PI / 3, 1.0), 64, 64);
+            ds.targets.push_back(render_ctx.render(ds.cameras.back()));
+            ds.train_ids.push_back(v);
+        }
+        Scene init = truth;
+        for (auto& k : init.kernels) { k.position[0] += 0.01 * (u() - 0.5); k.sigma = 0.5; }
+        ngs_train_config cfg = train_defaults();
+        cfg.knn = 2;
+        Trainer tr(init, ds, cfg);
+        Context probe;
+        probe.set_scene(init);
+        const double before = probe.build_view(0, ds.cameras[3], ds.targets[3]);
+        const IterationReport r = tr.step(3);
+        probe.set_scene(tr.scene());
+        const double after = probe.build_view(0, ds.cameras[3], ds.targets[3]);
+        std::printf("trainer step: loss %.6g -> %.6g, dt %.3f ms, neighbors %zu\n", before, after, r.dt_ms,
+                    tr.neighbors(3).size());
+        EXPECT(after < before);
+        EXPECT(tr.neighbors(3).size() == 2);
+        for (double d : r.delta_norms) EXPECT(std::isfinite(d));
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+    return failures ? 1 : 0;
+}

@@ -232,3 +232,29 @@ def test_trainer_step(gpu):
         e = qerr(getattr(sg, f), getattr(sr, f))
         print(f"post-step {f}: {e:.2e}")
         assert e < 1e-4, f
+
+
+# ---------------------------------------------------------------------------
+# Multi-GPU sharding, emulated on one device: the per-rank tile-row bands of
+# every view (ngs_set_shard) must sum to the unsharded accumulation — this is
+# exactly what the NCCL all-reduce of the trainer computes across ranks.
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("attr", ATTRS)
+def test_sharded_accumulate_sums_to_full(gpu, newton_fixture, world, attr):
+    full = gpu.context()
+    full.set_scene(f32(newton_fixture[0]))
+    sec = _views(full, newton_fixture)
+    gf, hf, vf = full.accumulate(attr, 0, sec)
+    gs, hs, vs = 0.0, 0.0, np.zeros_like(vf)
+    for rank in range(world):
+        c = gpu.context()
+        c.set_scene(f32(newton_fixture[0]))
+        c.set_shard(rank, world)
+        _views(c, newton_fixture)
+        g, h, v = c.accumulate(attr, 0, sec)
+        gs, hs, vs = gs + g, hs + h, vs | v
+    assert np.array_equal(vs, vf)
+    # per-(tile, splat) FP32 partials are summed in smem by atomics in run-dependent order
+    assert qerr(gs, gf) < 2e-5 and qerr(hs, hf) < 2e-5
