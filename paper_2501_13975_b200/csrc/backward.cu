@@ -274,19 +274,19 @@ template <int PASS>
 struct PassTraits;
 template <>
 struct PassTraits<kPassPosition> {
-    static constexpr int NC = kPosConsts, NA = 9, BATCH = 64;
+    static constexpr int NC = kPosConsts, NA = 9, BATCH = 32;
 };
 template <>
 struct PassTraits<kPassRotation> {
-    static constexpr int NC = kRotConsts, NA = 2, BATCH = 128;
+    static constexpr int NC = kRotConsts, NA = 2, BATCH = 64;
 };
 template <>
 struct PassTraits<kPassScaling> {
-    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 128;
+    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 64;
 };
 template <>
 struct PassTraits<kPassOpacityColor> {
-    static constexpr int NC = 0, NA = 8, BATCH = 128;
+    static constexpr int NC = 0, NA = 8, BATCH = 64;
 };
 
 // Copies N float4 from shared memory into a register array.
@@ -302,6 +302,15 @@ __device__ __forceinline__ void ld4(float (&dst)[4 * N], const float4* src) {
     }
 }
 
+// One contributing (pixel, splat) record, as phase 1 hands it to phase 2.
+struct Rec {
+    float G, q0, q1;   // Gaussian weight and Q d at the pixel
+    float Ti;          // transmittance before this splat
+    float wa;          // w_alpha = sigma * T_i
+    float ac[3];       // c~ - behind per channel
+    float gl[3], hl[3];
+};
+
 // Position record (newton.hpp:285-340) via derivatives of the quadratic form
 // q = d^T Sigma^-1 d along p (G = exp(-q/2)):
 //   r_c  = J_c - S_c qd,   q_c = qd . (J_c + r_c),
@@ -309,11 +318,10 @@ __device__ __forceinline__ void ld4(float (&dst)[4 * N], const float4* src) {
 //   dG_c = -G q_c / 2,     d2G_cd = G (q_c q_d / 4 - q_cd / 2),
 // with J = dpi/dp, S_c = dSigma/dp_c, Hpi / S_cd the second derivatives. The
 // three-channel Gauss-Newton and curvature sums are regrouped so each output
-// entry costs a handful of FMAs.
-__device__ __forceinline__ void position_record(const float4* K4, const SplatEval& ev, float qa, float qb, float qc,
-                                                float wa, const float (&acol)[3], const float (&gl)[3],
-                                                const float (&hl)[3], float (&v)[9]) {
-    const float G = ev.g, q0 = ev.qd0, q1 = ev.qd1;
+// entry costs a handful of FMAs (DESIGN.md §5 "K8 position").
+__device__ __forceinline__ void position_record(const float4* K4, const Rec& r, float qa, float qb, float qc,
+                                                float (&v)[9]) {
+    const float G = r.G, q0 = r.q0, q1 = r.q1, wa = r.wa;
     float A[16];
     ld4<4>(A, K4 + kPosJS / 4);
     float r0[3], r1[3], qcv[3], t0[3], t1[3];
@@ -350,11 +358,11 @@ __device__ __forceinline__ void position_record(const float4* K4, const SplatEva
     float sgl = 0.f, A2 = 0.f, vgl[3] = {0.f, 0.f, 0.f}, vh[3] = {0.f, 0.f, 0.f}, ga[3], ha[3];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-        ga[ch] = gl[ch] * wa;
-        ha[ch] = hl[ch] * wa * wa;
-        sgl += ga[ch] * acol[ch];
-        const float hac = ha[ch] * acol[ch];
-        A2 += hac * acol[ch];
+        ga[ch] = r.gl[ch] * wa;
+        ha[ch] = r.hl[ch] * wa * wa;
+        sgl += ga[ch] * r.ac[ch];
+        const float hac = ha[ch] * r.ac[ch];
+        A2 += hac * r.ac[ch];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             vgl[i] += ga[ch] * Jc[4 * ch + i];
@@ -381,16 +389,103 @@ __device__ __forceinline__ void position_record(const float4* K4, const SplatEva
                        G * (dG[c] * vh[d] + vh[c] * dG[d]) + GG * JJ[p];
 }
 
+// Rotation (newton.hpp:366-401): directional derivatives along
+// dSigma/dtheta = S1, d2Sigma/dtheta2 = S2: w = S1 qd, dq = -qd.w,
+// d2q = 2 w^T Q w - qd^T S2 qd.
+__device__ __forceinline__ void rotation_record(const float4* K4, const Rec& r, float qa, float qb, float qc,
+                                                float (&v)[2]) {
+    const float4 k0 = K4[0], k1 = K4[1];
+    const float q0 = r.q0, q1 = r.q1, G = r.G;
+    const float w0 = k0.x * q0 + k0.y * q1, w1 = k0.y * q0 + k0.z * q1;
+    const float dq = -(q0 * w0 + q1 * w1);
+    const float d2q = 2.f * (w0 * (qa * w0 + qb * w1) + w1 * (qb * w0 + qc * w1)) -
+                      (q0 * (k0.w * q0 + k1.x * q1) + q1 * (k1.x * q0 + k1.y * q1));
+    const float dg = -0.5f * G * dq;
+    const float d2g = G * (0.25f * dq * dq - 0.5f * d2q);
+    float sg = 0.f, sh = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float s = r.wa * r.ac[ch];
+        sg += r.gl[ch] * s;
+        sh += r.hl[ch] * s * s;
+    }
+    v[0] = sg * dg;
+    v[1] = sh * dg * dg + sg * d2g;
+}
+
+// Scaling (newton.hpp:426-465): z_i = v_i . qd, dG_i = G z_i^2 / 2,
+// d2G_ij = G (z_i^2 z_j^2 / 4 - z_i z_j v_i^T Q v_j).
+__device__ __forceinline__ void scaling_record(const float4* K4, const Rec& r, float (&v)[5]) {
+    const float4 k0 = K4[0], k1 = K4[1];
+    const float G = r.G;
+    const float z0 = k0.x * r.q0 + k0.y * r.q1;
+    const float z1 = k0.z * r.q0 + k0.w * r.q1;
+    const float zz0 = z0 * z0, zz1 = z1 * z1;
+    const float dg0 = 0.5f * G * zz0, dg1 = 0.5f * G * zz1;
+    const float h00 = G * (0.25f * zz0 * zz0 - zz0 * k1.x);
+    const float h01 = G * (0.25f * zz0 * zz1 - z0 * z1 * k1.y);
+    const float h11 = G * (0.25f * zz1 * zz1 - zz1 * k1.z);
+    float sg = 0.f, sh = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float s = r.wa * r.ac[ch];
+        sg += r.gl[ch] * s;
+        sh += r.hl[ch] * s * s;
+    }
+    v[0] = sg * dg0;
+    v[1] = sg * dg1;
+    v[2] = sh * dg0 * dg0 + sg * h00;
+    v[3] = sh * dg0 * dg1 + sg * h01;
+    v[4] = sh * dg1 * dg1 + sg * h11;
+}
+
+// Opacity data terms + colour accumulators (newton.hpp:516-567):
+// dc/dsigma = G T a, colour weight w = alpha T = G wa.
+__device__ __forceinline__ void opacity_color_record(const Rec& r, float sigma, float (&v)[8]) {
+    const float GT = r.G * r.Ti;
+    const float w = blend_weight(r.Ti, __fmul_rn(r.G, sigma));  // alpha T, as composited
+    v[0] = 0.f;
+    v[1] = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float dc = GT * r.ac[ch];
+        v[0] += r.gl[ch] * dc;
+        v[1] += r.hl[ch] * dc * dc;
+        v[2 + ch] = r.gl[ch] * w;
+        v[5 + ch] = r.hl[ch] * w * w;
+    }
+}
+
+// Per-warp record queue (ring of 64 entries) between the two phases.
+constexpr int kQ = 64;
+struct WarpQueue {
+    float G[kQ], q0[kQ], q1[kQ], Ti[kQ], wa[kQ], a0[kQ], a1[kQ], a2[kQ];
+    unsigned char j[kQ], pix[kQ];
+};
+
+// Backward over one tile (16x16 pixels, 8 warps of 2 rows).
+//  Phase 1 (per pixel, front to back over the depth-ordered splats): recompute
+//    alpha and T bit-identically to the forward, derive behind, and append each
+//    contributing record to the warp's queue (records end up sorted by splat).
+//  Phase 2 (whenever >= 32 records are queued, and at batch end): every lane
+//    evaluates one record's terms, then a segmented warp scan keyed by splat
+//    reduces them and each segment tail adds into the block's per-splat sums.
+//  Batch end: per-splat block sums -> FP64 global accumulators (one atomic per
+//    (tile, splat, component)).
 template <int PASS>
 __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
     constexpr int B = TR::BATCH, NC = TR::NC, NA = TR::NA, NC4 = NC / 4;
+    constexpr int CST = (NC4 % 8 == 0 && NC4 > 0) ? NC4 + 1 : NC4;  // float4 stride, avoids bank conflicts
     __shared__ float4 s_g0[B], s_g1[B];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
     __shared__ float2 s_g2[B];           // (c1, c2)
-    __shared__ float4 s_const[(NC4 > 0 ? NC4 : 1) * B];
+    __shared__ float2 s_yext[B];         // splat y-extent of the cutoff ellipse (tile coordinates)
+    __shared__ float4 s_const[(CST > 0 ? CST : 1) * B];
     __shared__ float s_acc[NA][B];
     __shared__ int s_kid[B];
     __shared__ int s_cnt[B];
+    __shared__ float s_gl[256][3], s_hl[256][3];
+    __shared__ WarpQueue s_q[8];
     __shared__ int s_maxlast;
     unsigned long long block_pairs = 0;
 
@@ -404,17 +499,25 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     const int2 range = a.ranges[tile];
     const size_t plane = static_cast<size_t>(a.W) * a.H;
     const size_t pidx = static_cast<size_t>(y) * a.W + x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float wy0 = 2.f * warp + 0.5f, wy1 = 2.f * warp + 1.5f;  // the warp's pixel-centre rows
+    WarpQueue& Q = s_q[warp];
 
     int last = -1;
     double Cf[3] = {0, 0, 0};
-    float gl[3] = {0, 0, 0}, hl[3] = {0, 0, 0};
     if (inside) {
         last = a.last[pidx];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             Cf[c] = a.image[c * plane + pidx];
-            gl[c] = a.loss_grad[c * plane + pidx];
-            hl[c] = a.loss_hess[c * plane + pidx];
+            s_gl[threadIdx.x][c] = a.loss_grad[c * plane + pidx];
+            s_hl[threadIdx.x][c] = a.loss_hess[c * plane + pidx];
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            s_gl[threadIdx.x][c] = 0.f;
+            s_hl[threadIdx.x][c] = 0.f;
         }
     }
     if (threadIdx.x == 0) s_maxlast = -1;
@@ -424,7 +527,69 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     const int end = min(range.y, s_maxlast + 1);
 
     float T = 1.0f, P[3] = {0.f, 0.f, 0.f};
-    const int lane = threadIdx.x & 31;
+    int qhead = 0, qcount = 0;  // warp-uniform ring state
+
+    // Phase 2 over queue entries [qhead, qhead + n), n <= 32.
+    auto drain = [&](int n) {
+        const bool valid = lane < n;
+        const int e = (qhead + lane) & (kQ - 1);
+        const int jj = valid ? static_cast<int>(Q.j[e]) : -1;
+        float v[NA];
+#pragma unroll
+        for (int c = 0; c < NA; ++c) v[c] = 0.f;
+        if (valid) {
+            Rec r;
+            r.G = Q.G[e];
+            r.q0 = Q.q0[e];
+            r.q1 = Q.q1[e];
+            r.Ti = Q.Ti[e];
+            r.wa = Q.wa[e];
+            r.ac[0] = Q.a0[e];
+            r.ac[1] = Q.a1[e];
+            r.ac[2] = Q.a2[e];
+            const int px = warp * 32 + Q.pix[e];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                r.gl[c] = s_gl[px][c];
+                r.hl[c] = s_hl[px][c];
+            }
+            if constexpr (PASS == kPassPosition) {
+                const float4 g0 = s_g0[jj], g1 = s_g1[jj];
+                position_record(s_const + jj * CST, r, g0.z, g0.w, g1.x, v);
+            } else if constexpr (PASS == kPassRotation) {
+                const float4 g0 = s_g0[jj], g1 = s_g1[jj];
+                rotation_record(s_const + jj * CST, r, g0.z, g0.w, g1.x, v);
+            } else if constexpr (PASS == kPassScaling) {
+                scaling_record(s_const + jj * CST, r, v);
+            } else {
+                opacity_color_record(r, s_g1[jj].y, v);
+            }
+        }
+        // Segmented inclusive scan keyed by splat (entries are sorted by splat).
+        int cnt = valid ? 1 : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int kj = __shfl_up_sync(0xffffffffu, jj, d);
+            const bool take = lane >= d && kj == jj;
+#pragma unroll
+            for (int c = 0; c < NA; ++c) {
+                const float t = __shfl_up_sync(0xffffffffu, v[c], d);
+                if (take) v[c] += t;
+            }
+            const int tc = __shfl_up_sync(0xffffffffu, cnt, d);
+            if (take) cnt += tc;
+        }
+        const int next = __shfl_down_sync(0xffffffffu, jj, 1);
+        const bool tail = valid && (lane == 31 || next != jj);
+        if (tail) {
+#pragma unroll
+            for (int c = 0; c < NA; ++c) atomicAdd(&s_acc[c][jj], v[c]);
+            atomicAdd(&s_cnt[jj], cnt);
+        }
+        if (lane == 0) block_pairs += n;
+        qhead = (qhead + n) & (kQ - 1);
+        qcount -= n;
+    };
 
     for (int base = range.x; base < end; base += B) {
         const int cnt = min(B, end - base);
@@ -435,9 +600,15 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
                 s_kid[i] = k;
                 const double2 p = a.pix[k];
                 const float4 ra = a.ra[k], rb = a.rb[k], rc = a.rc[k];
-                s_g0[i] = make_float4(static_cast<float>(p.x - ox), static_cast<float>(p.y - oy), ra.z, ra.w);
-                s_g1[i] = make_float4(rb.x, rb.y, reject_bound(rb.y, a.cutoff), rb.z);
+                const float qmax = reject_bound(rb.y, a.cutoff);
+                const float py = static_cast<float>(p.y - oy);
+                // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level
+                // skip never drops a record the per-lane test would keep.
+                const float ey = sqrtf(fmaxf(qmax, 0.f) * rc.w) * 1.0001f + 1e-3f;
+                s_g0[i] = make_float4(static_cast<float>(p.x - ox), py, ra.z, ra.w);
+                s_g1[i] = make_float4(rb.x, rb.y, qmax, rb.z);
                 s_g2[i] = make_float2(rb.w, rc.x);
+                s_yext[i] = make_float2(py - ey, py + ey);
             }
 #pragma unroll
             for (int c = 0; c < NA; ++c) s_acc[c][i] = 0.f;
@@ -447,20 +618,20 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
             const float4* src = reinterpret_cast<const float4*>(a.consts);
             for (int i = threadIdx.x; i < cnt * NC4; i += blockDim.x) {
                 const int j = i / NC4, c = i - j * NC4;
-                s_const[i] = src[static_cast<size_t>(a.vals[base + j]) * NC4 + c];
+                s_const[j * CST + c] = src[static_cast<size_t>(a.vals[base + j]) * NC4 + c];
             }
         }
         __syncthreads();
+        // Phase 1
         for (int j = 0; j < cnt; ++j) {
-            float v[NA];
-#pragma unroll
-            for (int c = 0; c < NA; ++c) v[c] = 0.f;
+            const float2 ye = s_yext[j];
+            if (ye.y < wy0 || ye.x > wy1) continue;  // warp-uniform: no pixel of this warp can pass
             bool contrib = false;
+            float G = 0.f, q0 = 0.f, q1 = 0.f, Tr = 0.f, wa = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f;
             if (base + j <= last) {
                 const float4 g0 = s_g0[j], g1 = s_g1[j];
-                const float qa = g0.z, qb = g0.w, qc = g1.x, sig = g1.y;
                 SplatEval ev;
-                if (eval_splat(g0.x, g0.y, qa, qb, qc, sig, fx, fy, g1.z, ev) && !(ev.alpha < a.cutoff)) {
+                if (eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, ev) && !(ev.alpha < a.cutoff)) {
                     contrib = true;
                     const float2 g2 = s_g2[j];
                     const float col[3] = {g1.w, g2.x, g2.y};
@@ -469,86 +640,53 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
                     const float Tn = next_transmittance(Ti, ev.alpha);
                     const bool is_last = (base + j == last);
                     const float inv_tn = __frcp_rn(Tn);
-                    float acol[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
+                    float ac[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const float Pn = __fmaf_rn(w, col[c], P[c]);
                         const float behind =
                             is_last ? a.bg[c] : static_cast<float>(Cf[c] - static_cast<double>(Pn)) * inv_tn;
-                        acol[c] = col[c] - behind;
+                        ac[c] = col[c] - behind;
                         P[c] = Pn;
                     }
                     T = Tn;
-                    const float wa = sig * Ti;  // w_alpha = sigma * T
-                    if constexpr (PASS == kPassPosition) {
-                        position_record(s_const + j * NC4, ev, qa, qb, qc, wa, acol, gl, hl, v);
-                    } else if constexpr (PASS == kPassRotation) {
-                        // Directional derivatives along dSigma/dtheta = S1, d2Sigma/dtheta2 = S2
-                        // (newton.hpp:366-401): w = S1 qd, dq = -qd.w, d2q = 2 w^T Q w - qd^T S2 qd.
-                        const float4 k0 = s_const[j * NC4], k1 = s_const[j * NC4 + 1];
-                        const float q0 = ev.qd0, q1 = ev.qd1, G = ev.g;
-                        const float w0 = k0.x * q0 + k0.y * q1, w1 = k0.y * q0 + k0.z * q1;
-                        const float dq = -(q0 * w0 + q1 * w1);
-                        const float d2q = 2.f * (w0 * (qa * w0 + qb * w1) + w1 * (qb * w0 + qc * w1)) -
-                                          (q0 * (k0.w * q0 + k1.x * q1) + q1 * (k1.x * q0 + k1.y * q1));
-                        const float dg = -0.5f * G * dq;
-                        const float d2g = G * (0.25f * dq * dq - 0.5f * d2q);
-                        float sg = 0.f, sh = 0.f;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const float s = wa * acol[ch];
-                            sg += gl[ch] * s;
-                            sh += hl[ch] * s * s;
-                        }
-                        v[0] = sg * dg;
-                        v[1] = sh * dg * dg + sg * d2g;
-                    } else if constexpr (PASS == kPassScaling) {
-                        // Per-view eigen directions (newton.hpp:426-465): z_i = v_i . qd,
-                        // dG_i = G z_i^2 / 2, d2G_ij = G (z_i^2 z_j^2 / 4 - z_i z_j v_i^T Q v_j).
-                        const float4 k0 = s_const[j * NC4], k1 = s_const[j * NC4 + 1];
-                        const float G = ev.g;
-                        const float z0 = k0.x * ev.qd0 + k0.y * ev.qd1;
-                        const float z1 = k0.z * ev.qd0 + k0.w * ev.qd1;
-                        const float zz0 = z0 * z0, zz1 = z1 * z1;
-                        const float dg0 = 0.5f * G * zz0, dg1 = 0.5f * G * zz1;
-                        const float h00 = G * (0.25f * zz0 * zz0 - zz0 * k1.x);
-                        const float h01 = G * (0.25f * zz0 * zz1 - z0 * z1 * k1.y);
-                        const float h11 = G * (0.25f * zz1 * zz1 - zz1 * k1.z);
-                        float sg = 0.f, sh = 0.f;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const float s = wa * acol[ch];
-                            sg += gl[ch] * s;
-                            sh += hl[ch] * s * s;
-                        }
-                        v[0] = sg * dg0;
-                        v[1] = sg * dg1;
-                        v[2] = sh * dg0 * dg0 + sg * h00;
-                        v[3] = sh * dg0 * dg1 + sg * h01;
-                        v[4] = sh * dg1 * dg1 + sg * h11;
-                    } else {  // opacity data terms + colour accumulators (newton.hpp:516-567)
-                        const float GT = ev.g * Ti;
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            const float dc = GT * acol[ch];
-                            v[0] += gl[ch] * dc;
-                            v[1] += hl[ch] * dc * dc;
-                            v[2 + ch] = gl[ch] * w;
-                            v[5 + ch] = hl[ch] * w * w;
-                        }
-                    }
+                    G = ev.g;
+                    q0 = ev.qd0;
+                    q1 = ev.qd1;
+                    Tr = Ti;
+                    wa = g1.y * Ti;
+                    ac0 = ac[0];
+                    ac1 = ac[1];
+                    ac2 = ac[2];
                 }
             }
             const unsigned ballot = __ballot_sync(0xffffffffu, contrib);
             if (ballot) {
-                const float sum = warp_reduce_scatter<NA>(v, lane);
-                const int idx = reduce_index<NA>(lane);
-                if (reduce_representative<NA>(lane) && idx < NA) atomicAdd(&s_acc[idx][j], sum);
-                if (lane == 0) {
-                    atomicAdd(&s_cnt[j], __popc(ballot));
-                    block_pairs += __popc(ballot);
+                if (contrib) {
+                    const int slot = (qhead + qcount + __popc(ballot & ((1u << lane) - 1u))) & (kQ - 1);
+                    Q.G[slot] = G;
+                    Q.q0[slot] = q0;
+                    Q.q1[slot] = q1;
+                    Q.Ti[slot] = Tr;
+                    Q.wa[slot] = wa;
+                    Q.a0[slot] = ac0;
+                    Q.a1[slot] = ac1;
+                    Q.a2[slot] = ac2;
+                    Q.j[slot] = static_cast<unsigned char>(j);
+                    Q.pix[slot] = static_cast<unsigned char>(lane);
+                }
+                qcount += __popc(ballot);
+                __syncwarp();
+                if (qcount >= 32) {
+                    drain(32);
+                    __syncwarp();
                 }
             }
+        }
+        if (qcount > 0) {
+            __syncwarp();
+            drain(qcount);
+            __syncwarp();
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {

@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
                                                         float* __restrict__ t_final, int* __restrict__ last_out) {
     __shared__ float4 s_g0[kRasterBatch], s_g1[kRasterBatch];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
     __shared__ float2 s_g2[kRasterBatch];                      // (c1, c2)
+    __shared__ float2 s_yext[kRasterBatch];                    // cutoff-ellipse y-extent (tile coordinates)
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
@@ -263,14 +264,23 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
             const int k = vals[i];
             const double2 p = pix[k];
             const float4 a = ra[k], b = rb[k], c = rc[k];
-            s_g0[threadIdx.x] = make_float4(static_cast<float>(p.x - ox), static_cast<float>(p.y - oy), a.z, a.w);
-            s_g1[threadIdx.x] = make_float4(b.x, b.y, reject_bound(b.y, cutoff), b.z);
+            const float qmax = reject_bound(b.y, cutoff);
+            const float py = static_cast<float>(p.y - oy);
+            // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level skip
+            // never drops a splat the per-pixel test would keep.
+            const float ey = sqrtf(fmaxf(qmax, 0.f) * c.w) * 1.0001f + 1e-3f;
+            s_g0[threadIdx.x] = make_float4(static_cast<float>(p.x - ox), py, a.z, a.w);
+            s_g1[threadIdx.x] = make_float4(b.x, b.y, qmax, b.z);
             s_g2[threadIdx.x] = make_float2(b.w, c.x);
+            s_yext[threadIdx.x] = make_float2(py - ey, py + ey);
         }
         __syncthreads();
         const int cnt = min(kRasterBatch, range.y - base);
         if (!done) {
+            const float wy0 = 2.f * (threadIdx.x >> 5) + 0.5f, wy1 = wy0 + 1.f;  // this warp's pixel rows
             for (int j = 0; j < cnt; ++j) {
+                const float2 ye = s_yext[j];
+                if (ye.y < wy0 || ye.x > wy1) continue;
                 const float4 g0 = s_g0[j], g1 = s_g1[j];
                 SplatEval e;
                 if (!eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, e)) continue;
