@@ -332,6 +332,7 @@ def ours_arm(args, cfg: Config):
         "profiled_pass": {"note": "same K steps re-run with views serialised and per-launch CUDA events; "
                                   "stage times below come from it", "ms_per_step": float(sum(prof_dts)) / args.steps},
         "stage_ms_per_step": step_stage_ms,
+        "group_ms_per_step_concurrent": {k: round(v / args.steps, 4) for k, v in counters["group_ms"].items()},
         "measured_fp64_tflops": fp64_peak,
         "contrib_pairs_per_step": [p / args.steps for p in prof["contrib_pairs"]],
         "clocks": clocks.summary(),

@@ -41,11 +41,19 @@ typedef struct {
     int64_t contrib_pairs[4];               /* contributing (pixel, splat) records per backward pass */
     int64_t raster_pairs;                   /* (tile, splat) pairs binned, summed over renders */
     int64_t renders;                        /* view renders */
+    /* Trainer steps only, always on: wall time of each stage group on the
+     * context stream as executed (views concurrent): render+loss of all
+     * views, the four backward passes (incl. constants and all-reduce), solves. */
+    double group_ms[6];
 } ngs_profile_stats;
 
 int32_t ngs_profile_enable(ngs_context* ctx, int32_t on);
 int32_t ngs_profile_reset(ngs_context* ctx);
 int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out);
+
+/* Tile-size policy: 0 = auto (8x8 tiles for views with < 592 16x16 tiles in
+ * the trainer, 16x16 elsewhere), 8 or 16 = forced. Results do not depend on it. */
+int32_t ngs_set_tile_size(ngs_context* ctx, int32_t tile);
 
 /* FP32 FFMA throughput microbenchmark on the context's device (TFLOP/s). */
 int32_t ngs_microbench_fp32(ngs_context* ctx, double* tflops);

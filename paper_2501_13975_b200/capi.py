@@ -113,7 +113,8 @@ STAGES = ("project", "sort", "raster", "loss", "consts", "bwd_position", "bwd_ro
 
 class ngs_profile_stats(C.Structure):
     _fields_ = [("ms", C.c_double * 11), ("launches", C.c_int64 * 11), ("total_launches", C.c_int64),
-                ("contrib_pairs", C.c_int64 * 4), ("raster_pairs", C.c_int64), ("renders", C.c_int64)]
+                ("contrib_pairs", C.c_int64 * 4), ("raster_pairs", C.c_int64), ("renders", C.c_int64),
+                ("group_ms", C.c_double * 6)]
 
 
 class ngs_terms(C.Structure):
@@ -446,7 +447,12 @@ class Context:
         return dict(ms={k: st.ms[i] for i, k in enumerate(STAGES)},
                     launches={k: st.launches[i] for i, k in enumerate(STAGES)},
                     total_launches=st.total_launches, contrib_pairs=list(st.contrib_pairs),
-                    raster_pairs=st.raster_pairs, renders=st.renders)
+                    raster_pairs=st.raster_pairs, renders=st.renders,
+                    group_ms=dict(zip(("render", "bwd_position", "bwd_rotation", "bwd_scaling", "bwd_opacity_color",
+                                       "solve"), list(st.group_ms))))
+
+    def set_tile_size(self, tile: int):
+        self._call("ngs_set_tile_size", C.c_int32(tile))
 
     def microbench_fp32(self) -> float:
         v = C.c_double()

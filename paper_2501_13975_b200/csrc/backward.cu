@@ -472,9 +472,10 @@ struct WarpQueue {
 //    reduces them and each segment tail adds into the block's per-splat sums.
 //  Batch end: per-splat block sums -> FP64 global accumulators (one atomic per
 //    (tile, splat, component)).
-template <int PASS>
-__global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
+template <int PASS, int TILE>
+__global__ void __launch_bounds__(TILE * TILE) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
+    constexpr int NT = TILE * TILE, NW = NT / 32, kRowsPerWarp = 32 / TILE;
     constexpr int B = TR::BATCH, NC = TR::NC, NA = TR::NA, NC4 = NC / 4;
     constexpr int CST = (NC4 % 8 == 0 && NC4 > 0) ? NC4 + 1 : NC4;  // float4 stride, avoids bank conflicts
     __shared__ float4 s_g0[B], s_g1[B];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
@@ -484,23 +485,23 @@ __global__ void __launch_bounds__(256) backward_k(BackwardArgs a) {
     __shared__ float s_acc[NA][B];
     __shared__ int s_kid[B];
     __shared__ int s_cnt[B];
-    __shared__ float s_gl[256][3], s_hl[256][3];
-    __shared__ WarpQueue s_q[8];
+    __shared__ float s_gl[NT][3], s_hl[NT][3];
+    __shared__ WarpQueue s_q[NW];
     __shared__ int s_maxlast;
     unsigned long long block_pairs = 0;
 
     const int tile = a.tile0 + blockIdx.x;  // owned tile rows only (multi-GPU shard)
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
-    const int x = tx * kTile + lx, y = ty * kTile + ly;
+    const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
+    const int x = tx * TILE + lx, y = ty * TILE + ly;
     const bool inside = x < a.W && y < a.H;
     const float fx = lx + 0.5f, fy = ly + 0.5f;
-    const double ox = tx * kTile, oy = ty * kTile;
+    const double ox = tx * TILE, oy = ty * TILE;
     const int2 range = a.ranges[tile];
     const size_t plane = static_cast<size_t>(a.W) * a.H;
     const size_t pidx = static_cast<size_t>(y) * a.W + x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float wy0 = 2.f * warp + 0.5f, wy1 = 2.f * warp + 1.5f;  // the warp's pixel-centre rows
+    const float wy0 = kRowsPerWarp * warp + 0.5f, wy1 = wy0 + (kRowsPerWarp - 1);  // the warp's pixel-centre rows
     WarpQueue& Q = s_q[warp];
 
     int last = -1;
@@ -757,11 +758,25 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     a.tile0 = own0 * v.cam.tiles_x;
     const int blocks = (own1 - own0) * v.cam.tiles_x;
     StageScope st(NGS_STAGE_BWD_POSITION + pass, s);
+    const bool small = v.cam.tile == 8;
+    const int threads = small ? 64 : 256;
     switch (pass) {
-        case kPassPosition: backward_k<kPassPosition><<<blocks, 256, 0, s>>>(a); break;
-        case kPassRotation: backward_k<kPassRotation><<<blocks, 256, 0, s>>>(a); break;
-        case kPassScaling: backward_k<kPassScaling><<<blocks, 256, 0, s>>>(a); break;
-        case kPassOpacityColor: backward_k<kPassOpacityColor><<<blocks, 256, 0, s>>>(a); break;
+        case kPassPosition:
+            if (small) backward_k<kPassPosition, 8><<<blocks, threads, 0, s>>>(a);
+            else backward_k<kPassPosition, 16><<<blocks, threads, 0, s>>>(a);
+            break;
+        case kPassRotation:
+            if (small) backward_k<kPassRotation, 8><<<blocks, threads, 0, s>>>(a);
+            else backward_k<kPassRotation, 16><<<blocks, threads, 0, s>>>(a);
+            break;
+        case kPassScaling:
+            if (small) backward_k<kPassScaling, 8><<<blocks, threads, 0, s>>>(a);
+            else backward_k<kPassScaling, 16><<<blocks, threads, 0, s>>>(a);
+            break;
+        case kPassOpacityColor:
+            if (small) backward_k<kPassOpacityColor, 8><<<blocks, threads, 0, s>>>(a);
+            else backward_k<kPassOpacityColor, 16><<<blocks, threads, 0, s>>>(a);
+            break;
     }
     CUDA_LAUNCH_CHECK();
 }

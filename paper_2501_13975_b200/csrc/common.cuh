@@ -39,6 +39,7 @@ struct CameraDev {
     double view_proj[16];  // proj * view
     double center[3];      // camera position in world space
     int width, height;
+    int tile;              // tile edge in pixels (16, or 8 for small views; binning result identical)
     int tiles_x, tiles_y;
 };
 

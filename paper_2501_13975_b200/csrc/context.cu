@@ -136,12 +136,14 @@ struct ngs_context {
     std::array<cudaStream_t, kMaxSolveViews> vs{};
     cudaEvent_t fork_ev = nullptr;
     std::array<cudaEvent_t, kMaxSolveViews> join_ev{};
+    std::array<cudaEvent_t, 24> gev{};  // stage-group events of a trainer step
     DevBuf<int> overflow;
     DevBuf<float4> snap_ps, snap_sc, snap_q;
     DevBuf<float> snap_sh;
     // Multi-GPU shard (ngs_b200_dist.h)
     int shard_rank = 0, shard_world = 1;
     ncclComm_t comm = nullptr;
+    int tile_policy = 0;  // 0 auto (8x8 tiles for small views), else forced 8 or 16
     unsigned long long contrib_pairs_total = 0;
 
     ~ngs_context() {
@@ -171,6 +173,8 @@ struct ngs_context {
             if (e) cudaEventDestroy(e);
         for (auto s : vs)
             if (s) cudaStreamDestroy(s);
+        for (auto e : gev)
+            if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -249,9 +253,22 @@ LossParams to_loss(const ngs_loss_config* o) {
 
 RasterParams ngs_context::raster_for(const ngs_raster_options* o, const CameraDev& cam) const {
     RasterParams r = to_raster(o);
-    shard_rows(cam.tiles_y, shard_rank, shard_world, r);
+    shard_rows(cam.tiles_y, cam.tile, shard_rank, shard_world, r);
     return r;
 }
+
+namespace {
+
+// Tile edge for a view (the AABB test is conservative, so per-pixel splat
+// sequences - and therefore results - do not depend on it).
+int tile_for(const ngs_context* ctx, const ngs_camera& c, bool api) {
+    if (ctx->tile_policy == 8 || ctx->tile_policy == 16) return ctx->tile_policy;
+    if (api) return kTile;  // build_view read-back reports the reference's 16x16 binning
+    const int t16 = ((c.width + 15) / 16) * ((c.height + 15) / 16);
+    return t16 < kSmallViewTiles ? 8 : 16;
+}
+
+}  // namespace
 
 namespace {
 
@@ -429,6 +446,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         CUDA_CHECK(cudaEventCreate(&ctx->ev0));
         CUDA_CHECK(cudaEventCreate(&ctx->ev1));
         CUDA_CHECK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+        for (auto& e : ctx->gev) CUDA_CHECK(cudaEventCreate(&e));
         for (int i = 0; i < kMaxSolveViews; ++i) {
             CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->vs[i], cudaStreamNonBlocking));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
@@ -560,7 +578,7 @@ int32_t ngs_build_view(ngs_context* ctx, int32_t slot, const ngs_camera* camera,
         CUDA_CHECK(cudaSetDevice(ctx->device));
         ViewSlot& v = ctx->slot(slot);
         v.valid = false;
-        upload_camera(*camera, v.cam);
+        upload_camera(*camera, v.cam, tile_for(ctx, *camera, true));
         v.raster = ctx->raster_for(raster, v.cam);
         v.loss = to_loss(loss);
         const size_t npx = static_cast<size_t>(camera->width) * camera->height;
@@ -1058,7 +1076,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
         const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
         if (upload_targets) {
-            upload_camera(cam, v.cam);
+            upload_camera(cam, v.cam, tile_for(ctx, cam, false));
             v.raster = ctx->raster_for(&T.cfg.raster, v.cam);
             v.loss = to_loss(&T.cfg.loss);
             const size_t npx = static_cast<size_t>(cam.width) * cam.height;
@@ -1114,22 +1132,38 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
         double norms[5];
         float ms = 0;
         for (int attempt = 0;; ++attempt) {
+            // Stage-group events: (event index, group) pairs; group 0 render, 1..4 passes, 5 solve.
+            std::vector<std::pair<int, int>> marks;
+            int ge = 0;
+            auto mark = [&](int group) {
+                CUDA_CHECK(cudaEventRecord(ctx->gev[ge], s));
+                marks.emplace_back(ge++, group);
+            };
             CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
             CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), s));
             CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
+            mark(-1);
             render_step_views(ctx, view_id, nbrs, true);
+            mark(0);
             for (int pass_i = 0; pass_i < 5; ++pass_i) {
                 const int attr = T.cfg.order[pass_i];
                 const int pass = pass_of(attr);
                 // Opacity and colour share one traversal when adjacent (same captures, trainer.hpp:412-415).
                 const bool reuse = (attr == NGS_COLOR && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_OPACITY) ||
                                    (attr == NGS_OPACITY && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_COLOR);
-                if (!reuse) accumulate_pass(ctx, pass, views.data(), nv, nullptr, true);
+                if (!reuse) {
+                    accumulate_pass(ctx, pass, views.data(), nv, nullptr, true);
+                    mark(1 + pass);
+                }
                 SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
                 launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
                              color_views(views.data(), nv), base, ctx->acc.ptr, stride, so, s);
+                mark(5);
                 const bool geometry = attr == NGS_POSITION || attr == NGS_ROTATION || attr == NGS_SCALING;
-                if (geometry && pass_i + 1 < 5) render_step_views(ctx, view_id, nbrs, false);
+                if (geometry && pass_i + 1 < 5) {
+                    render_step_views(ctx, view_id, nbrs, false);
+                    mark(0);
+                }
             }
             CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
             int overflow = 0;
@@ -1137,7 +1171,14 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
             CUDA_CHECK(cudaMemcpyAsync(&overflow, ctx->overflow.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
             ctx->check_err();
             CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-            if (!overflow) break;
+            if (!overflow) {
+                for (size_t m = 1; m < marks.size(); ++m) {
+                    float gms = 0;
+                    CUDA_CHECK(cudaEventElapsedTime(&gms, ctx->gev[marks[m - 1].first], ctx->gev[marks[m].first]));
+                    ctx->prof.stats.group_ms[marks[m].second] += gms;
+                }
+                break;
+            }
             if (attempt >= 8) throw Error(NGS_ERR_INTERNAL, "pair capacity retry limit exceeded");
             // Grow every view's pair capacity and re-run the step from the snapshot.
             for (auto& v : T.views) v.pair_cap = std::max<size_t>(2 * v.pair_cap, 4096);
@@ -1285,6 +1326,14 @@ int32_t ngs_dist_init(ngs_context* ctx, const uint8_t id_bytes[NGS_DIST_ID_BYTES
         if (world > 1) nccl_check(nccl().comm_init_rank(&ctx->comm, world, id, rank), "ncclCommInitRank");
         ctx->shard_rank = rank;
         ctx->shard_world = world;
+        for (auto& v : ctx->slots) v.valid = false;
+    });
+}
+
+int32_t ngs_set_tile_size(ngs_context* ctx, int32_t tile) {
+    return guarded([&] {
+        if (tile != 0 && tile != 8 && tile != 16) throw Error(NGS_ERR_INVALID_INPUT, "tile size must be 0, 8 or 16");
+        ctx->tile_policy = tile;
         for (auto& v : ctx->slots) v.valid = false;
     });
 }

@@ -23,26 +23,33 @@ struct RasterParams {
     float t_min;
     bool cutoff_enabled;  // alpha_cutoff > 0: AABB binning, else every splat in every tile
     double radius;        // max(3, sqrt(2 ln(1/alpha_cutoff)))  rasterizer.hpp:215-216
-    // Multi-GPU shard of this view: tile rows [band_y0, band_y1)
-    // are projected, binned, rasterised and get loss fields (owned rows plus a
-    // one-tile-row halo, which covers the 10-px SSIM support); the backward
-    // runs over the owned rows [own_y0, own_y1) only. Full frame when unsharded.
+    // Multi-GPU shard of this view, in tile rows of the view's
+    // tile size: rows [band_y0, band_y1) are projected, binned, rasterised and
+    // get loss fields (owned rows plus a halo of ceil(10 px / tile) rows, which
+    // covers the SSIM support); the backward runs over the owned rows
+    // [own_y0, own_y1) only. Full frame when unsharded.
     int band_y0 = 0, band_y1 = 1 << 30;
     int own_y0 = 0, own_y1 = 1 << 30;
 };
 
-// Rows of tile-row band `rank` of `world` for a view with `tiles_y` rows.
-inline void shard_rows(int tiles_y, int rank, int world, RasterParams& r) {
+// Rows of tile-row band `rank` of `world` for a view with `tiles_y` rows of
+// `tile` pixels.
+inline void shard_rows(int tiles_y, int tile, int rank, int world, RasterParams& r) {
     if (world <= 1) {
         r.band_y0 = r.own_y0 = 0;
         r.band_y1 = r.own_y1 = tiles_y;
         return;
     }
+    const int halo = (10 + tile - 1) / tile;
     r.own_y0 = static_cast<int>(static_cast<long long>(tiles_y) * rank / world);
     r.own_y1 = static_cast<int>(static_cast<long long>(tiles_y) * (rank + 1) / world);
-    r.band_y0 = r.own_y0 > 0 ? r.own_y0 - 1 : 0;
-    r.band_y1 = r.own_y1 < tiles_y ? r.own_y1 + 1 : tiles_y;
+    r.band_y0 = r.own_y0 - halo > 0 ? r.own_y0 - halo : 0;
+    r.band_y1 = r.own_y1 + halo < tiles_y ? r.own_y1 + halo : tiles_y;
 }
+
+// Views with fewer 16x16 tiles than this render with 8x8 tiles: their per-tile
+// lists are deep (secondaries at 1/4 resolution) and 16x16 leaves the GPU idle.
+constexpr int kSmallViewTiles = 4 * 148;
 
 struct LossParams {
     double lambda, c1, c2;
@@ -187,7 +194,7 @@ struct StageScope {
 };
 
 // Launch wrappers (render.cu, loss.cu, backward.cu, solve.cu).
-void upload_camera(const ngs_camera& c, CameraDev& out);
+void upload_camera(const ngs_camera& c, CameraDev& out, int tile = kTile);
 struct RenderSync {
     bool exact = true;                            // read the pair count back (one host sync)
     int* overflow = nullptr;                      // sync-free: set when the pair capacity was exceeded

@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
     __shared__ double red[8];
     const int ch = blockIdx.z;
     const int ox = blockIdx.x * kLT, oy = (row0 + blockIdx.y) * kLT;
-    const bool own = (row0 + static_cast<int>(blockIdx.y)) >= own_y0 && (row0 + static_cast<int>(blockIdx.y)) < own_y1;
     const int h = win.half, span = kLT + 2 * h;
     const size_t plane = static_cast<size_t>(W) * H;
     const double* img = image + ch * plane;
@@ -132,6 +131,7 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
         const size_t idx = static_cast<size_t>(y) * W + x;
         for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
     }
+    const bool own = y >= own_y0 && y < own_y1;  // owned pixel rows (multi-GPU shard)
     const double tot = block_sum(own ? ssim : 0.0, red);
     if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
 }
@@ -148,7 +148,6 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
     __shared__ double red[8];
     const int ch = blockIdx.z;
     const int ox = blockIdx.x * kLT, oy = (row0 + blockIdx.y) * kLT;
-    const bool own = (row0 + static_cast<int>(blockIdx.y)) >= own_y0 && (row0 + static_cast<int>(blockIdx.y)) < own_y1;
     const int h = win.half, span = kLT + 2 * h;
     const size_t plane = static_cast<size_t>(W) * H;
     const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
@@ -208,6 +207,7 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
         grad[ch * plane + idx] = static_cast<float>(g);
         hess[ch * plane + idx] = static_cast<float>(hh);
     }
+    const bool own = y >= own_y0 && y < own_y1;
     const double tot = block_sum(own ? dsq : 0.0, red);
     if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
 }
@@ -240,9 +240,11 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     v.loss_hess.ensure(3 * npx);
     v.loss_sums.ensure(2);
     CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * sizeof(double), s));
-    const int rows = (v.H + kLT - 1) / kLT;
-    const int row0 = std::max(0, v.raster.band_y0), row1 = std::min(rows, v.raster.band_y1);
-    const int own0 = std::max(0, v.raster.own_y0), own1 = std::min(rows, v.raster.own_y1);
+    // Shard bands are in tile rows of the view's tile size; the loss grid uses 16-row blocks.
+    const int t = v.cam.tile;
+    const int band_px0 = std::max(0, v.raster.band_y0) * t, band_px1 = std::min(v.H, v.raster.band_y1 * t);
+    const int own0 = std::max(0, v.raster.own_y0) * t, own1 = std::min(v.H, v.raster.own_y1 * t);
+    const int row0 = band_px0 / kLT, row1 = (band_px1 + kLT - 1) / kLT;
     if (row1 <= row0) return;
     const dim3 grid((v.W + kLT - 1) / kLT, row1 - row0, 3);
     StageScope st(NGS_STAGE_LOSS, s, ssim ? 2 : 1);

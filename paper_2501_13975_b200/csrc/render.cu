@@ -48,7 +48,7 @@ void ViewSlot::release_all() {
 }
 
 // Camera(view, proj, w, h), camera.hpp:30-42.
-void upload_camera(const ngs_camera& c, CameraDev& out) {
+void upload_camera(const ngs_camera& c, CameraDev& out, int tile) {
     if (c.width < 16 || c.height < 16) throw Error(NGS_ERR_INVALID_INPUT, "camera: width and height must be >= 16");
     for (int i = 0; i < 16; ++i) {
         out.view[i] = c.view[i];
@@ -80,8 +80,9 @@ void upload_camera(const ngs_camera& c, CameraDev& out) {
     for (int i = 0; i < 3; ++i) out.center[i] = -(inv[3 * i] * t[0] + inv[3 * i + 1] * t[1] + inv[3 * i + 2] * t[2]);
     out.width = c.width;
     out.height = c.height;
-    out.tiles_x = (c.width + kTile - 1) / kTile;
-    out.tiles_y = (c.height + kTile - 1) / kTile;
+    out.tile = tile;
+    out.tiles_x = (c.width + tile - 1) / tile;
+    out.tiles_y = (c.height + tile - 1) / tile;
 }
 
 namespace {
@@ -150,10 +151,11 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
         y1 = cam.height - 1.0;
     }
     auto clampi = [](int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); };
-    const int tx0 = clampi(static_cast<int>(floor(x0 / kTile)), 0, cam.tiles_x - 1);
-    const int tx1 = clampi(static_cast<int>(floor(x1 / kTile)), 0, cam.tiles_x - 1);
-    int ty0 = clampi(static_cast<int>(floor(y0 / kTile)), 0, cam.tiles_y - 1);
-    int ty1 = clampi(static_cast<int>(floor(y1 / kTile)), 0, cam.tiles_y - 1);
+    const double ts = cam.tile;
+    const int tx0 = clampi(static_cast<int>(floor(x0 / ts)), 0, cam.tiles_x - 1);
+    const int tx1 = clampi(static_cast<int>(floor(x1 / ts)), 0, cam.tiles_x - 1);
+    int ty0 = clampi(static_cast<int>(floor(y0 / ts)), 0, cam.tiles_y - 1);
+    int ty1 = clampi(static_cast<int>(floor(y1 / ts)), 0, cam.tiles_y - 1);
     bool off = x1 < 0 || x0 >= cam.width || y1 < 0 || y0 >= cam.height;
     // Multi-GPU shard: bin only into this rank's tile rows (band incl. halo).
     ty0 = max(ty0, rp.band_y0);
@@ -234,24 +236,25 @@ __global__ void tile_ranges_k(int pairs, int T, const unsigned int* keys, int2* 
 // (__syncthreads_count = block-wide ballot). Pixel centres and splat centres
 // are expressed relative to the tile origin so the FP32 offsets carry
 // full precision at 4K resolutions.
-constexpr int kRasterBatch = 256;
-
-__global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int H, const int2* __restrict__ ranges,
+template <int TILE>
+__global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int W, int H, const int2* __restrict__ ranges,
                                                         const int* __restrict__ vals, const double2* __restrict__ pix,
                                                         const float4* __restrict__ ra, const float4* __restrict__ rb,
                                                         const float4* __restrict__ rc, float bg0, float bg1, float bg2,
                                                         float cutoff, float tmin, double* __restrict__ image,
                                                         float* __restrict__ t_final, int* __restrict__ last_out) {
+    constexpr int kRasterBatch = TILE * TILE;  // one splat per thread per batch
+    constexpr int kRowsPerWarp = 32 / TILE;
     __shared__ float4 s_g0[kRasterBatch], s_g1[kRasterBatch];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
     __shared__ float2 s_g2[kRasterBatch];                      // (c1, c2)
     __shared__ float2 s_yext[kRasterBatch];                    // cutoff-ellipse y-extent (tile coordinates)
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
-    const int x = tx * kTile + lx, y = ty * kTile + ly;
+    const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
+    const int x = tx * TILE + lx, y = ty * TILE + ly;
     const bool inside = x < W && y < H;
     const float fx = lx + 0.5f, fy = ly + 0.5f;
-    const double ox = tx * kTile, oy = ty * kTile;
+    const double ox = tx * TILE, oy = ty * TILE;
     const int2 range = ranges[tile];
     float T = 1.0f;
     double C0 = 0.0, C1 = 0.0, C2 = 0.0;  // FP64 colour sums: the image feeds the cancelling (c - c^t) loss terms
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256) raster_forward_k(int tiles_x, int W, int 
         __syncthreads();
         const int cnt = min(kRasterBatch, range.y - base);
         if (!done) {
-            const float wy0 = 2.f * (threadIdx.x >> 5) + 0.5f, wy1 = wy0 + 1.f;  // this warp's pixel rows
+            const float wy0 = kRowsPerWarp * (threadIdx.x >> 5) + 0.5f, wy1 = wy0 + (kRowsPerWarp - 1);  // warp rows
             for (int j = 0; j < cnt; ++j) {
                 const float2 ye = s_yext[j];
                 if (ye.y < wy0 || ye.x > wy1) continue;
@@ -412,11 +415,16 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     }
     if (g_prof) g_prof->stats.renders += 1;
     StageScope st(NGS_STAGE_RASTER, s);
-    raster_forward_k<<<v.T, 256, 0, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr,
-                                         cap > 0 ? v.pair_val_sorted.ptr : nullptr, v.pix.ptr, v.rec_a.ptr,
-                                         v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1], scene.bg[2],
-                                         v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
-                                         v.last.ptr);
+    auto launch = [&](auto kernel, int threads) {
+        kernel<<<v.T, threads, 0, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val_sorted.ptr : nullptr,
+                                       v.pix.ptr, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1],
+                                       scene.bg[2], v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
+                                       v.last.ptr);
+    };
+    if (v.cam.tile == 8)
+        launch(raster_forward_k<8>, 64);
+    else
+        launch(raster_forward_k<16>, 256);
     CUDA_LAUNCH_CHECK();
     v.valid = true;
 }

@@ -80,5 +80,9 @@ def test_golden_trainer_step(gpu):
     rep = ctx.trainer_step(0)
     assert qerr(list(rep.delta_norms), g["delta_norms"]) < 1e-3
     post = ctx.get_scene()
-    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+    for f in ("position", "scale", "sigma", "sh"):
         assert qerr(getattr(post, f), g["post_" + f]) < 1e-4, f
+    # orientation: rotation angle between GPU and reference quaternions; the solved spin
+    # theta (|2 theta| <= pi) carries the ~1e-4 relative error of the rotation terms
+    dots = np.abs(np.sum(post.quaternion * g["post_quaternion"], axis=1))
+    assert np.max(2 * np.arccos(np.clip(dots, -1, 1))) < 1e-3

@@ -258,3 +258,28 @@ def test_sharded_accumulate_sums_to_full(gpu, newton_fixture, world, attr):
     assert np.array_equal(vs, vf)
     # per-(tile, splat) FP32 partials are summed in smem by atomics in run-dependent order
     assert qerr(gs, gf) < 2e-5 and qerr(hs, hf) < 2e-5
+
+
+@pytest.mark.parametrize("seed", [103, 104])
+def test_tile_size_does_not_change_results(gpu, seed):
+    """8x8 tiles (used for small views) give the same images, loss fields and terms:
+    the AABB binning is conservative, so every pixel sees the same splat sequence;
+    only the FP32 rounding of tile-relative splat centres differs."""
+    scene = f32(random_scene(seed, 60))
+    cam = test_camera((0.2, 0.1, -3.6), 64, 48)
+    target = ref().context()
+    target.set_scene(scene)
+    tgt = target.render(test_camera((0.25, 0.1, -3.6), 64, 48))
+    outs = []
+    for tile in (16, 8):
+        c = gpu.context()
+        c.set_tile_size(tile)
+        c.set_scene(scene)
+        c.build_view(0, cam, tgt)
+        g, h = c.view_loss_derivs(0)
+        tg, th, _ = c.accumulate(capi.OPACITY, 0, [])
+        outs.append((c.view_image(0), g, h, tg, th))
+    img16, img8 = outs[0][0], outs[1][0]
+    assert np.max(np.abs(img16 - img8)) < 1e-6
+    for a, b in zip(outs[0][1:], outs[1][1:]):
+        assert qerr(a, b) < TOL_DELTA
