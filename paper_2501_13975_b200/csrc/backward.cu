@@ -737,7 +737,7 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     a.W = v.W;
     a.H = v.H;
     a.ranges = v.ranges.ptr;
-    a.vals = v.pair_val_sorted.ptr;
+    a.vals = v.pair_val.ptr;
     a.pix = v.pix.ptr;
     a.ra = v.rec_a.ptr;
     a.rb = v.rec_b.ptr;

@@ -635,7 +635,7 @@ int32_t ngs_view_splats(ngs_context* ctx, int32_t slot, ngs_splat_list* out) {
         }
         CUDA_CHECK(cudaMemcpyAsync(ranges.data(), v.ranges.ptr, sizeof(int2) * v.T, cudaMemcpyDeviceToHost, s));
         if (v.pairs > 0)
-            CUDA_CHECK(cudaMemcpyAsync(vals.data(), v.pair_val_sorted.ptr, sizeof(int) * v.pairs, cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(vals.data(), v.pair_val.ptr, sizeof(int) * v.pairs, cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
         std::vector<int> entry_of(n, -1);
         int e = 0;

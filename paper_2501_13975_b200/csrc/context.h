@@ -100,14 +100,16 @@ struct ViewSlot {
     DevBuf<int> tiles_touched;
     DevBuf<uint8_t> flags;
     DevBuf<double> entry64;  // parity read-back: px, py, s00, s01, s11, bbox x0,y0,x1,y1, colour (kEntry64 per kernel)
-    // K2-K5 binning
-    DevBuf<unsigned long long> depth_key, depth_key_sorted;
-    DevBuf<int> ids, order;
+    // K2-K5 binning (hand-written radix sort, sort.cu)
+    DevBuf<unsigned int> depth_key, depth_key_alt;
+    DevBuf<int> order, order_alt;
     DevBuf<int> counts_sorted, offsets;
-    DevBuf<unsigned int> pair_key, pair_key_sorted;
-    DevBuf<int> pair_val, pair_val_sorted;
+    DevBuf<unsigned int> pair_key, pair_key_alt;
+    DevBuf<int> pair_val, pair_val_alt;
     DevBuf<int2> ranges;
-    DevBuf<unsigned char> cub_temp;
+    DevBuf<int> counters;    // [0] entries n, [1] pairs P, [2] min(P, capacity)
+    int n_host = 0;          // pinned-lifetime source of the counters[0] upload
+    void* sort_scratch = nullptr;
     // K6 forward raster outputs (planar [3][H][W])
     DevBuf<double> image;   // FP64 (see raster_forward_k)
     DevBuf<float> t_final;

@@ -2,13 +2,11 @@
 //
 // Reference semantics: build_splat_list (rasterizer.hpp:182-265) and
 // composite_forward / composite_pixel (rasterizer.hpp:274-442).
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include <cmath>
 
 #include "context.h"
 #include "geometry.cuh"
+#include "sort.h"
 #include "splat.cuh"
 
 namespace ngsb {
@@ -24,17 +22,23 @@ void ViewSlot::release_all() {
     flags.release();
     entry64.release();
     depth_key.release();
-    depth_key_sorted.release();
-    ids.release();
+    depth_key_alt.release();
     order.release();
+    order_alt.release();
     counts_sorted.release();
     offsets.release();
     pair_key.release();
-    pair_key_sorted.release();
+    pair_key_alt.release();
     pair_val.release();
-    pair_val_sorted.release();
+    pair_val_alt.release();
     ranges.release();
-    cub_temp.release();
+    counters.release();
+    if (sort_scratch) {
+        auto* sc = static_cast<SortScratch*>(sort_scratch);
+        sc->release();
+        delete sc;
+        sort_scratch = nullptr;
+    }
     image.release();
     t_final.release();
     last.release();
@@ -87,9 +91,12 @@ void upload_camera(const ngs_camera& c, CameraDev& out, int tile) {
 
 namespace {
 
-__device__ __forceinline__ unsigned long long depth_sort_key(double d) {
-    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
-    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+// Order-preserving 32-bit key of the FP32-rounded depth; equal-key runs are
+// re-ordered by the FP64 depth afterwards (depth_tie_fixup), so the final
+// order is exactly (FP64 depth, kernel id).
+__device__ __forceinline__ unsigned int depth_sort_key(double d) {
+    const unsigned int b = __float_as_uint(static_cast<float>(d));
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
 // K1: per-kernel projection, SH colour and tile extent (FP64 math, coalesced
@@ -97,7 +104,7 @@ __device__ __forceinline__ unsigned long long depth_sort_key(double d) {
 __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev cam, RasterParams rp,
                                                         float4* ra, float4* rb, float4* rc, double2* pix,
                                                         double* depth, int4* rect, int* tiles_touched,
-                                                        uint8_t* flags, unsigned long long* depth_key, int* ids,
+                                                        uint8_t* flags, unsigned int* depth_key, int* ids,
                                                         double* entry64, int* err) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= s.n) return;
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
         tiles_touched[k] = 0;
         flags[k] = 0;
         rect[k] = make_int4(1, 1, 0, 0);
-        depth_key[k] = ~0ull;
+        depth_key[k] = 0xFFFFFFFFu;
         depth[k] = 0;
         return;
     }
@@ -197,12 +204,13 @@ __global__ void gather_counts_k(int n, const int* order, const int* tiles_touche
 // tile key alone keeps depth order (ties by kernel id) inside every tile.
 __global__ void emit_pairs_k(int n, int tiles_x, int cap, const int* order, const int* offsets, const int4* rect,
                              const int* tiles_touched, unsigned int* keys, int* vals, int* overflow,
-                             unsigned long long* pair_counter) {
+                             unsigned long long* pair_counter, int* counters) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r == 0) {
-        const int total = offsets[n];
+        const int total = counters[1];
         if (total > cap && overflow) atomicOr(overflow, 1);
         if (pair_counter) atomicAdd(pair_counter, static_cast<unsigned long long>(total));
+        counters[2] = total < cap ? total : cap;
     }
     if (r >= n) return;
     const int k = order[r];
@@ -219,9 +227,9 @@ __global__ void emit_pairs_k(int n, int tiles_x, int cap, const int* order, cons
         }
 }
 
-// K5: per-tile [start, end) ranges from the tile-sorted key array (padding
-// keys >= T sort after every real key and are ignored).
-__global__ void tile_ranges_k(int pairs, int T, const unsigned int* keys, int2* ranges) {
+// K5: per-tile [start, end) ranges from the tile-sorted key array.
+__global__ void tile_ranges_k(const int* d_pairs, int T, const unsigned int* keys, int2* ranges) {
+    const int pairs = *d_pairs;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= pairs) return;
     const unsigned int t = keys[i];
@@ -333,8 +341,6 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     v.tiles_touched.ensure(n);
     v.flags.ensure(n);
     v.depth_key.ensure(n);
-    v.depth_key_sorted.ensure(n);
-    v.ids.ensure(n);
     v.order.ensure(n);
     v.counts_sorted.ensure(n + 1);
     v.offsets.ensure(n + 1);
@@ -345,32 +351,35 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     v.last.ensure(npx);
     if (want_debug) v.entry64.ensure(kEntry64 * static_cast<size_t>(n));
     int bits = 1;
-    while ((1 << bits) < v.T + 1) ++bits;  // tile keys < T, padding key (all ones) sorts last
+    while ((1 << bits) < v.T) ++bits;
+    if (!v.sort_scratch) v.sort_scratch = new SortScratch();
+    SortScratch& sc = *static_cast<SortScratch*>(v.sort_scratch);
+    v.depth_key_alt.ensure(n);
+    v.order_alt.ensure(n);
+    v.counters.ensure(3);
 
     if (n > 0) {
         StageScope st(NGS_STAGE_PROJECT, s);
         project_kernel_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr,
                                                        v.pix.ptr, v.depth.ptr, v.rect.ptr, v.tiles_touched.ptr,
-                                                       v.flags.ptr, v.depth_key.ptr, v.ids.ptr,
+                                                       v.flags.ptr, v.depth_key.ptr, v.order.ptr,
                                                        want_debug ? v.entry64.ptr : nullptr, d_err);
         CUDA_LAUNCH_CHECK();
     }
     if (n > 0) {
-        StageScope st(NGS_STAGE_SORT, s, 13);
-        // K2: global stable depth order (ties by kernel id: keys are emitted in id order).
-        size_t temp1 = 0, temp2 = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, temp1, v.depth_key.ptr, v.depth_key_sorted.ptr, v.ids.ptr,
-                                        v.order.ptr, n, 0, 64, s);
-        cub::DeviceScan::ExclusiveSum(nullptr, temp2, v.counts_sorted.ptr, v.offsets.ptr, n + 1, s);
-        v.cub_temp.ensure(std::max(temp1, temp2));
-        temp1 = v.cub_temp.cap;
-        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(v.cub_temp.ptr, temp1, v.depth_key.ptr, v.depth_key_sorted.ptr,
-                                                   v.ids.ptr, v.order.ptr, n, 0, 64, s));
+        StageScope st(NGS_STAGE_SORT, s, 18);
+        // K2: global depth order, exactly (FP64 depth, kernel id): 4-pass radix sort of the
+        // FP32 depth key (stable over the id-ordered input) + fix-up of equal-key runs.
+        v.n_host = n;
+        CUDA_CHECK(cudaMemcpyAsync(v.counters.ptr, &v.n_host, sizeof(int), cudaMemcpyHostToDevice, s));
+        radix_sort_pairs(v.depth_key.ptr, v.order.ptr, v.depth_key_alt.ptr, v.order_alt.ptr, v.counters.ptr, n, 32, sc,
+                         s);
+        depth_tie_fixup(v.depth_key.ptr, v.order.ptr, v.depth.ptr, n, s);
         gather_counts_k<<<blocks_for(n), 256, 0, s>>>(n, v.order.ptr, v.tiles_touched.ptr, v.counts_sorted.ptr);
         CUDA_LAUNCH_CHECK();
-        CUDA_CHECK(cudaMemsetAsync(v.counts_sorted.ptr + n, 0, sizeof(int), s));
-        temp2 = v.cub_temp.cap;
-        CUDA_CHECK(cub::DeviceScan::ExclusiveSum(v.cub_temp.ptr, temp2, v.counts_sorted.ptr, v.offsets.ptr, n + 1, s));
+        exclusive_scan(v.counts_sorted.ptr, v.offsets.ptr, n, v.counters.ptr + 1, sc, s);
+    } else {
+        CUDA_CHECK(cudaMemsetAsync(v.counters.ptr, 0, 3 * sizeof(int), s));
     }
     // Pair capacity: exact (one host sync) or the slot's running capacity with a
     // device-side overflow flag (sync-free; the caller re-runs on overflow).
@@ -378,7 +387,7 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     if (sync.exact) {
         int pairs = 0;
         if (n > 0) {
-            CUDA_CHECK(cudaMemcpyAsync(&pairs, v.offsets.ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(&pairs, v.counters.ptr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
             CUDA_CHECK(cudaStreamSynchronize(s));
         }
         v.pairs = pairs;
@@ -391,32 +400,26 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     }
     CUDA_CHECK(cudaMemsetAsync(v.ranges.ptr, 0, sizeof(int2) * v.T, s));
     if (cap > 0 && n > 0) {
-        StageScope st(NGS_STAGE_SORT, s, 5);
+        StageScope st(NGS_STAGE_SORT, s, 2 + 3 * ((bits + 7) / 8));
         v.pair_key.ensure(cap);
-        v.pair_key_sorted.ensure(cap);
+        v.pair_key_alt.ensure(cap);
         v.pair_val.ensure(cap);
-        v.pair_val_sorted.ensure(cap);
-        CUDA_CHECK(cudaMemsetAsync(v.pair_key.ptr, 0xFF, sizeof(unsigned int) * cap, s));
+        v.pair_val_alt.ensure(cap);
         emit_pairs_k<<<blocks_for(n), 256, 0, s>>>(n, v.cam.tiles_x, static_cast<int>(cap), v.order.ptr,
                                                    v.offsets.ptr, v.rect.ptr, v.tiles_touched.ptr, v.pair_key.ptr,
-                                                   v.pair_val.ptr, sync.overflow, sync.pair_counter);
+                                                   v.pair_val.ptr, sync.overflow, sync.pair_counter, v.counters.ptr);
         CUDA_LAUNCH_CHECK();
-        size_t temp = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, temp, v.pair_key.ptr, v.pair_key_sorted.ptr, v.pair_val.ptr,
-                                        v.pair_val_sorted.ptr, static_cast<int>(cap), 0, bits, s);
-        v.cub_temp.ensure(temp);
-        temp = v.cub_temp.cap;
-        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(v.cub_temp.ptr, temp, v.pair_key.ptr, v.pair_key_sorted.ptr,
-                                                   v.pair_val.ptr, v.pair_val_sorted.ptr, static_cast<int>(cap), 0,
-                                                   bits, s));
-        tile_ranges_k<<<blocks_for(static_cast<int>(cap)), 256, 0, s>>>(static_cast<int>(cap), v.T,
-                                                                         v.pair_key_sorted.ptr, v.ranges.ptr);
+        // K4: stable sort of the depth-ordered pairs by tile key -> per-tile depth order.
+        radix_sort_pairs(v.pair_key.ptr, v.pair_val.ptr, v.pair_key_alt.ptr, v.pair_val_alt.ptr, v.counters.ptr + 2,
+                         static_cast<int>(cap), bits, sc, s);
+        tile_ranges_k<<<blocks_for(static_cast<int>(cap)), 256, 0, s>>>(v.counters.ptr + 2, v.T, v.pair_key.ptr,
+                                                                         v.ranges.ptr);
         CUDA_LAUNCH_CHECK();
     }
     if (g_prof) g_prof->stats.renders += 1;
     StageScope st(NGS_STAGE_RASTER, s);
     auto launch = [&](auto kernel, int threads) {
-        kernel<<<v.T, threads, 0, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val_sorted.ptr : nullptr,
+        kernel<<<v.T, threads, 0, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val.ptr : nullptr,
                                        v.pix.ptr, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1],
                                        scene.bg[2], v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
                                        v.last.ptr);
