@@ -54,49 +54,76 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
         const double w[3] = {mrow(VP, 3, 0), mrow(VP, 3, 1), mrow(VP, 3, 2)};
         const double i1 = 1.0 / hw, i2 = i1 * i1, i3 = i2 * i1;
         const double sx = 0.5 * cam.width, sy = 0.5 * cam.height;
+        #pragma unroll
         for (int j = 0; j < 3; ++j) {
             M[0][j] = sx * (a[j] * i1 - hx * i2 * w[j]);
             M[1][j] = sy * (b[j] * i1 - hy * i2 * w[j]);
         }
+        #pragma unroll
         for (int i = 0; i < 3; ++i)
+            #pragma unroll
             for (int j = i; j < 3; ++j) {
                 Hu[0][sym3(i, j)] = sx * (-(a[i] * w[j] + w[i] * a[j]) * i2 + 2.0 * hx * w[i] * w[j] * i3);
                 Hu[1][sym3(i, j)] = sy * (-(b[i] * w[j] + w[i] * b[j]) * i2 + 2.0 * hy * w[i] * w[j] * i3);
             }
     }
-    // Sigma(p) through the EWA Jacobian.
+    // Sigma(p) through the EWA Jacobian (cov2d_derivatives_wrt_position,
+    // camera.hpp:241-284). With t = W p + t_w, the chain of dJ/dt_e and
+    // d2J/dt_e dt_f (camera.hpp:185-206) through W contracts to the 3-vectors
+    // a~ = W^T a, w~ = W^T w (a, b, w = rows 0, 1, 3 of proj):
+    //   dJ/dp_c   row0 = sx (-(w~_c a + a~_c w) / hw^2 + 2 hx w~_c w / hw^3)
+    //   d2J/dp_cd row0 = sx (2 ((w~_c a + a~_c w) w~_d + a~_d w~_c w) / hw^3 - 6 hx w~_c w~_d w / hw^4)
+    // (row1 with b, hy, sy), which avoids materialising the 3x3x2x3 tensors.
     {
         const D3 t = to_camera_space(cam, p);
-        CamProj cp;
-        project_camera_space<true, true>(cam, t, cp);
+        const double* P = cam.proj;
+        const double a[3] = {mrow(P, 0, 0), mrow(P, 0, 1), mrow(P, 0, 2)};
+        const double bb[3] = {mrow(P, 1, 0), mrow(P, 1, 1), mrow(P, 1, 2)};
+        const double w[3] = {mrow(P, 3, 0), mrow(P, 3, 1), mrow(P, 3, 2)};
+        const double hx = a[0] * t.x + a[1] * t.y + a[2] * t.z + mrow(P, 0, 3);
+        const double hy = bb[0] * t.x + bb[1] * t.y + bb[2] * t.z + mrow(P, 1, 3);
+        const double hw = w[0] * t.x + w[1] * t.y + w[2] * t.z + mrow(P, 3, 3);
+        const double i1 = 1.0 / hw, i2 = i1 * i1, i3 = i2 * i1, i4 = i2 * i2;
+        const double sx = 0.5 * cam.width, sy = 0.5 * cam.height;
+        double J[6];
+        #pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            J[j] = sx * (a[j] * i1 - hx * i2 * w[j]);
+            J[3 + j] = sy * (bb[j] * i1 - hy * i2 * w[j]);
+        }
+        double at[3], bt[3], wt[3];
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            at[c] = a[0] * mrow(cam.view, 0, c) + a[1] * mrow(cam.view, 1, c) + a[2] * mrow(cam.view, 2, c);
+            bt[c] = bb[0] * mrow(cam.view, 0, c) + bb[1] * mrow(cam.view, 1, c) + bb[2] * mrow(cam.view, 2, c);
+            wt[c] = w[0] * mrow(cam.view, 0, c) + w[1] * mrow(cam.view, 1, c) + w[2] * mrow(cam.view, 2, c);
+        }
         double A[9], m[9];
         covariance_3d(s.quat[k], s.scale[k], A);
         rotate_cov(cam, A, m);
-        double dj[3][6], d2j[3][3][6];
-        for (int c = 0; c < 3; ++c)
-            for (int q = 0; q < 6; ++q) {
-                double v = 0;
-                for (int e = 0; e < 3; ++e) v += cp.dJ[e][q] * mrow(cam.view, e, c);
-                dj[c][q] = v;
-            }
-        for (int c = 0; c < 3; ++c)
-            for (int d = 0; d < 3; ++d)
-                for (int q = 0; q < 6; ++q) {
-                    double v = 0;
-                    for (int e = 0; e < 3; ++e)
-                        for (int f = 0; f < 3; ++f) v += cp.d2J[e][f][q] * (mrow(cam.view, e, c) * mrow(cam.view, f, d));
-                    d2j[c][d][q] = v;
-                }
         // mjt = m J^T (3x2)
         double mjt[6];
+        #pragma unroll
         for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 2; ++j)
-                mjt[2 * i + j] = m[3 * i] * cp.J[3 * j] + m[3 * i + 1] * cp.J[3 * j + 1] + m[3 * i + 2] * cp.J[3 * j + 2];
+            #pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+                mjt[2 * i + jj] = m[3 * i] * J[3 * jj] + m[3 * i + 1] * J[3 * jj + 1] + m[3 * i + 2] * J[3 * jj + 2];
+        double dj[3][6];
+        #pragma unroll
+        for (int c = 0; c < 3; ++c)
+            #pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                dj[c][j] = sx * (-(wt[c] * a[j] + at[c] * w[j]) * i2 + 2.0 * hx * wt[c] * i3 * w[j]);
+                dj[c][3 + j] = sy * (-(wt[c] * bb[j] + bt[c] * w[j]) * i2 + 2.0 * hy * wt[c] * i3 * w[j]);
+            }
         auto mul23_32 = [](const double* a23, const double* b32, double out[4]) {
+            #pragma unroll
             for (int i = 0; i < 2; ++i)
+                #pragma unroll
                 for (int j = 0; j < 2; ++j)
                     out[2 * i + j] = a23[3 * i] * b32[j] + a23[3 * i + 1] * b32[2 + j] + a23[3 * i + 2] * b32[4 + j];
         };
+        #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double tm[4];
             mul23_32(dj[c], mjt, tm);
@@ -104,29 +131,44 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
             M[3][c] = tm[1] + tm[2];
             M[4][c] = 2.0 * tm[3];
         }
+#pragma unroll
         for (int c = 0; c < 3; ++c)
+#pragma unroll
             for (int d = c; d < 3; ++d) {
+                double d2j[6];
+                #pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    d2j[j] = sx * (2.0 * ((wt[c] * a[j] + at[c] * w[j]) * wt[d] + at[d] * wt[c] * w[j]) * i3 -
+                                   6.0 * hx * wt[c] * wt[d] * i4 * w[j]);
+                    d2j[3 + j] = sy * (2.0 * ((wt[c] * bb[j] + bt[c] * w[j]) * wt[d] + bt[d] * wt[c] * w[j]) * i3 -
+                                       6.0 * hy * wt[c] * wt[d] * i4 * w[j]);
+                }
                 double t1[4], t2[4], md[6];
-                mul23_32(d2j[c][d], mjt, t1);
-                // dj_c m dj_d^T
+                mul23_32(d2j, mjt, t1);
+                #pragma unroll
                 for (int i = 0; i < 3; ++i)
-                    for (int j = 0; j < 2; ++j)
-                        md[2 * i + j] = m[3 * i] * dj[d][3 * j] + m[3 * i + 1] * dj[d][3 * j + 1] + m[3 * i + 2] * dj[d][3 * j + 2];
+                    #pragma unroll
+                    for (int jj = 0; jj < 2; ++jj)
+                        md[2 * i + jj] = m[3 * i] * dj[d][3 * jj] + m[3 * i + 1] * dj[d][3 * jj + 1] + m[3 * i + 2] * dj[d][3 * jj + 2];
                 mul23_32(dj[c], md, t2);
                 Hu[2][sym3(c, d)] = 2.0 * t1[0] + 2.0 * t2[0];
                 Hu[3][sym3(c, d)] = t1[1] + t1[2] + t2[1] + t2[2];
                 Hu[4][sym3(c, d)] = 2.0 * t1[3] + 2.0 * t2[3];
             }
     }
+    #pragma unroll
     for (int c = 0; c < 3; ++c) {
         o[kPosJS + 2 * c] = static_cast<float>(M[0][c]);
         o[kPosJS + 2 * c + 1] = static_cast<float>(M[1][c]);
+        #pragma unroll
         for (int u = 0; u < 3; ++u) o[kPosJS + 6 + 3 * c + u] = static_cast<float>(M[2 + u][c]);
     }
     o[kPosJS + 15] = 0.f;
+    #pragma unroll
     for (int p = 0; p < 6; ++p) {
         o[kPosHpi + 2 * p] = static_cast<float>(Hu[0][p]);
         o[kPosHpi + 2 * p + 1] = static_cast<float>(Hu[1][p]);
+        #pragma unroll
         for (int u = 0; u < 3; ++u) o[kPosScd + 3 * p + u] = static_cast<float>(Hu[2 + u][p]);
     }
     o[kPosScd + 18] = 0.f;
@@ -138,28 +180,38 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
     if (view_direction(cam, p, r, n)) {
         const double rv[3] = {r.x, r.y, r.z};
         double jac[3][3];
+        #pragma unroll
         for (int i = 0; i < 3; ++i)
+            #pragma unroll
             for (int j = 0; j < 3; ++j) jac[i][j] = ((i == j ? 1.0 : 0.0) - rv[i] * rv[j]) / n;
         const double inv_n2 = 1.0 / (n * n);
         double basis[16];
         sh_basis(r, s.sh_degree, basis);
+        #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            double c[16] = {};
+            double c[16];
             double v = 0;
-            for (int i = 0; i < s.n_coeffs; ++i) {
-                c[i] = s.sh[(16 * ch + i) * s.n + k];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                c[i] = i < s.n_coeffs ? static_cast<double>(s.sh[(16 * ch + i) * s.n + k]) : 0.0;
                 v += basis[i] * c[i];
             }
             v += kColorOffset;
             if (v <= 0.0) continue;  // clamped: zero subgradient (sh.hpp:144-147)
             double gr[3], hr[6];
             sh_contract_derivs(r, s.sh_degree, c, gr, hr);
+            #pragma unroll
             for (int j = 0; j < 3; ++j) Jc[ch][j] = jac[0][j] * gr[0] + jac[1][j] * gr[1] + jac[2][j] * gr[2];
+            #pragma unroll
             for (int a = 0; a < 3; ++a)
+                #pragma unroll
                 for (int b = a; b < 3; ++b) {
                     double acc = 0;
+                    #pragma unroll
                     for (int i = 0; i < 3; ++i)
+                        #pragma unroll
                         for (int j = 0; j < 3; ++j) acc += jac[i][a] * hr[sym3(i, j)] * jac[j][b];
+                    #pragma unroll
                     for (int i = 0; i < 3; ++i) {
                         double hv = 3.0 * rv[i] * rv[a] * rv[b];
                         if (i == a) hv -= rv[b];
@@ -171,11 +223,16 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                 }
         }
     }
+    #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
+        #pragma unroll
         for (int j = 0; j < 3; ++j) o[kPosJc + 4 * ch + j] = static_cast<float>(Jc[ch][j]);
         o[kPosJc + 4 * ch + 3] = 0.f;
+        #pragma unroll
         for (int a = 0; a < 3; ++a)
+            #pragma unroll
             for (int bb = a; bb < 3; ++bb) o[kPosJJ + 6 * ch + sym3(a, bb)] = static_cast<float>(Jc[ch][a] * Jc[ch][bb]);
+        #pragma unroll
         for (int j = 0; j < 6; ++j) o[kPosHc + 6 * ch + j] = static_cast<float>(Hc[ch][j]);
     }
 }
@@ -473,7 +530,7 @@ struct WarpQueue {
 //  Batch end: per-splat block sums -> FP64 global accumulators (one atomic per
 //    (tile, splat, component)).
 template <int PASS, int TILE>
-__global__ void __launch_bounds__(TILE * TILE) backward_k(BackwardArgs a) {
+__global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
     constexpr int NT = TILE * TILE, NW = NT / 32, kRowsPerWarp = 32 / TILE;
     constexpr int B = TR::BATCH, NC = TR::NC, NA = TR::NA, NC4 = NC / 4;
@@ -482,9 +539,9 @@ __global__ void __launch_bounds__(TILE * TILE) backward_k(BackwardArgs a) {
     __shared__ float2 s_g2[B];           // (c1, c2)
     __shared__ float2 s_yext[B];         // splat y-extent of the cutoff ellipse (tile coordinates)
     __shared__ float4 s_const[(CST > 0 ? CST : 1) * B];
-    __shared__ float s_acc[NA][B];
+    __shared__ float s_acc[NW][NA][B];  // per-warp sums: segment tails are unique within a drain
     __shared__ int s_kid[B];
-    __shared__ int s_cnt[B];
+    __shared__ int s_vis[B];
     __shared__ float s_gl[NT][3], s_hl[NT][3];
     __shared__ WarpQueue s_q[NW];
     __shared__ int s_maxlast;
@@ -566,8 +623,8 @@ __global__ void __launch_bounds__(TILE * TILE) backward_k(BackwardArgs a) {
                 opacity_color_record(r, s_g1[jj].y, v);
             }
         }
-        // Segmented inclusive scan keyed by splat (entries are sorted by splat).
-        int cnt = valid ? 1 : 0;
+        // Segmented inclusive scan keyed by splat (entries are sorted by splat, so
+        // each splat is one segment and its tail lane is unique in this drain).
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const int kj = __shfl_up_sync(0xffffffffu, jj, d);
@@ -577,15 +634,13 @@ __global__ void __launch_bounds__(TILE * TILE) backward_k(BackwardArgs a) {
                 const float t = __shfl_up_sync(0xffffffffu, v[c], d);
                 if (take) v[c] += t;
             }
-            const int tc = __shfl_up_sync(0xffffffffu, cnt, d);
-            if (take) cnt += tc;
         }
         const int next = __shfl_down_sync(0xffffffffu, jj, 1);
         const bool tail = valid && (lane == 31 || next != jj);
         if (tail) {
 #pragma unroll
-            for (int c = 0; c < NA; ++c) atomicAdd(&s_acc[c][jj], v[c]);
-            atomicAdd(&s_cnt[jj], cnt);
+            for (int c = 0; c < NA; ++c) s_acc[warp][c][jj] += v[c];
+            s_vis[jj] = 1;
         }
         if (lane == 0) block_pairs += n;
         qhead = (qhead + n) & (kQ - 1);
@@ -611,10 +666,9 @@ __global__ void __launch_bounds__(TILE * TILE) backward_k(BackwardArgs a) {
                 s_g2[i] = make_float2(rb.w, rc.x);
                 s_yext[i] = make_float2(py - ey, py + ey);
             }
-#pragma unroll
-            for (int c = 0; c < NA; ++c) s_acc[c][i] = 0.f;
-            s_cnt[i] = 0;
+            s_vis[i] = 0;
         }
+        for (int i = threadIdx.x; i < NW * NA * B; i += blockDim.x) (&s_acc[0][0][0])[i] = 0.f;
         if constexpr (NC4 > 0) {
             const float4* src = reinterpret_cast<const float4*>(a.consts);
             for (int i = threadIdx.x; i < cnt * NC4; i += blockDim.x) {
@@ -692,10 +746,12 @@ __global__ void __launch_bounds__(TILE * TILE) backward_k(BackwardArgs a) {
         __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
             const int k = s_kid[i];
-            if (a.visible && s_cnt[i] > 0) a.visible[k] = 1;
+            if (a.visible && s_vis[i]) a.visible[k] = 1;
 #pragma unroll
             for (int c = 0; c < NA; ++c) {
-                const float val = s_acc[c][i];
+                float val = 0.f;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) val += s_acc[w][c][i];  // fixed order: deterministic block sum
                 if (val != 0.f) atomicAdd(&a.acc[static_cast<size_t>(c) * a.acc_stride + k], static_cast<double>(val));
             }
         }

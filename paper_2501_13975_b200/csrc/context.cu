@@ -447,8 +447,13 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         CUDA_CHECK(cudaEventCreate(&ctx->ev1));
         CUDA_CHECK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
         for (auto& e : ctx->gev) CUDA_CHECK(cudaEventCreate(&e));
+        // Secondary views (deep per-tile lists, few pixels, latency-bound) run on
+        // high-priority streams so their blocks become resident first; the
+        // primary's many blocks fill the remaining SM resources around them.
+        int prio_lo = 0, prio_hi = 0;
+        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         for (int i = 0; i < kMaxSolveViews; ++i) {
-            CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->vs[i], cudaStreamNonBlocking));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->vs[i], cudaStreamNonBlocking, i == 0 ? prio_lo : prio_hi));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
         }
         ctx->overflow.ensure(1);
@@ -728,7 +733,8 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
     CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
     concurrent = concurrent && nv <= kMaxSolveViews && !ctx->prof.enabled;
     if (concurrent) ctx->fork(nv);
-    for (int i = 0; i < nv; ++i) {
+    for (int ii = 0; ii < nv; ++ii) {
+        const int i = concurrent ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
         ViewSlot& v = *views[i];
         cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
         compute_pass_consts(pass, ctx->scene, v, views[0]->cam, s);
@@ -1070,7 +1076,8 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     // Profiling serialises the views so per-launch event times do not overlap.
     const bool concurrent = !ctx->prof.enabled;
     if (concurrent) ctx->fork(nv);
-    for (int i = 0; i < nv; ++i) {
+    for (int ii = 0; ii < nv; ++ii) {
+        const int i = concurrent ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
         ViewSlot& v = T.views[i];
         cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
         const int cam_id = (i == 0) ? view_id : nbrs[i - 1];

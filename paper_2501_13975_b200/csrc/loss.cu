@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
     if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
 }
 
+
 }  // namespace
 
 void compute_loss(ViewSlot& v, cudaStream_t s) {
@@ -247,7 +248,7 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     const int row0 = band_px0 / kLT, row1 = (band_px1 + kLT - 1) / kLT;
     if (row1 <= row0) return;
     const dim3 grid((v.W + kLT - 1) / kLT, row1 - row0, 3);
-    StageScope st(NGS_STAGE_LOSS, s, ssim ? 2 : 1);
+    StageScope st(NGS_STAGE_LOSS, s, 1);
     if (ssim) {
         v.fields.ensure(27 * npx);
         ssim_fields_k<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
