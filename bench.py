@@ -39,9 +39,10 @@ from paper_2501_13975_b200.workload import CONFIGS, Config, cameras_for, make_sc
 METRIC = "Newton-updated training views/sec"
 PEAKS_PATH = os.path.join(REPO, "MEASURED_PEAKS.json")
 # Algorithmic FP32 work per contributing (pixel, splat) record of the position
-# backward (DESIGN.md §4 "K8 position"): G + derivatives in u-space, the chain
-# to p-space and the three-channel GN + curvature assembly.
-POSITION_FLOPS_PER_PAIR = 420
+# backward (DESIGN.md §4 "K8 position", FMA = 2): phase 1 (G, alpha, T, behind)
+# ~40 flop, phase 2 in the 2-D position subspace ~250 flop (derivatives of q
+# along u_x, u_y, the three-channel Gauss-Newton + curvature assembly).
+POSITION_FLOPS_PER_PAIR = 290
 
 
 def dist_env():

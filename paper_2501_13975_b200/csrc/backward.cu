@@ -35,11 +35,13 @@ inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 // derivatives, Jc (3x3) = dc~/dp per channel, Hc (3 x sym3) = d2c~/dp2.
 // projection_derivatives camera.hpp:124-148; cov2d_derivatives_wrt_position
 // camera.hpp:241-284; sh_color_derivs_wrt_position sh.hpp:134-161.
-__global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev cam, const uint8_t* flags,
-                                                         float* out) {
+template <int ND>
+__global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev cam, CameraDev primary,
+                                                         const uint8_t* flags, float* out) {
+    using L = PosLayout<ND>;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= s.n) return;
-    float* o = out + static_cast<size_t>(k) * kPosConsts;
+    float* o = out + static_cast<size_t>(k) * L::N;
     if (!(flags[k] & kProjected)) return;
     const D3 p = load_pos(s, k);
     double M[5][3], Hu[5][6];
@@ -156,23 +158,6 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                 Hu[4][sym3(c, d)] = 2.0 * t1[3] + 2.0 * t2[3];
             }
     }
-    #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        o[kPosJS + 2 * c] = static_cast<float>(M[0][c]);
-        o[kPosJS + 2 * c + 1] = static_cast<float>(M[1][c]);
-        #pragma unroll
-        for (int u = 0; u < 3; ++u) o[kPosJS + 6 + 3 * c + u] = static_cast<float>(M[2 + u][c]);
-    }
-    o[kPosJS + 15] = 0.f;
-    #pragma unroll
-    for (int p = 0; p < 6; ++p) {
-        o[kPosHpi + 2 * p] = static_cast<float>(Hu[0][p]);
-        o[kPosHpi + 2 * p + 1] = static_cast<float>(Hu[1][p]);
-        #pragma unroll
-        for (int u = 0; u < 3; ++u) o[kPosScd + 3 * p + u] = static_cast<float>(Hu[2 + u][p]);
-    }
-    o[kPosScd + 18] = 0.f;
-    o[kPosScd + 19] = 0.f;
     // SH colour derivatives through r(p) (view_direction_derivatives camera.hpp:79-104).
     D3 r;
     double n;
@@ -223,17 +208,71 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                 }
         }
     }
-    #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        #pragma unroll
-        for (int j = 0; j < 3; ++j) o[kPosJc + 4 * ch + j] = static_cast<float>(Jc[ch][j]);
-        o[kPosJc + 4 * ch + 3] = 0.f;
-        #pragma unroll
+    // Directional derivatives along D[a] (world axes, or the primary view's
+    // position subspace for kPassPositionUV): first order x . D[a], second order
+    // D[a]^T X D[b]. With the identity directions the values pass through exactly.
+    double D[ND][3];
+    if constexpr (ND == 3) {
+#pragma unroll
         for (int a = 0; a < 3; ++a)
-            #pragma unroll
-            for (int bb = a; bb < 3; ++bb) o[kPosJJ + 6 * ch + sym3(a, bb)] = static_cast<float>(Jc[ch][a] * Jc[ch][bb]);
-        #pragma unroll
-        for (int j = 0; j < 6; ++j) o[kPosHc + 6 * ch + j] = static_cast<float>(Hc[ch][j]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) D[a][c] = a == c ? 1.0 : 0.0;
+    } else {
+        D3 rp, ux, uy;
+        double np;
+        if (!view_direction(primary, p, rp, np)) rp = d3(0, 0, 1);  // as solve_position_k (error flagged there)
+        position_subspace(rp, ux, uy);
+        D[0][0] = ux.x, D[0][1] = ux.y, D[0][2] = ux.z;
+        D[1][0] = uy.x, D[1][1] = uy.y, D[1][2] = uy.z;
+    }
+    auto d1 = [&](const double* x, int st, int a) {  // sum_c x[c * st] D[a][c]
+        return x[0] * D[a][0] + x[st] * D[a][1] + x[2 * st] * D[a][2];
+    };
+    auto d2 = [&](const double* h, int st, int a, int b) {  // D[a]^T H D[b], H packed sym3 with stride st
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) acc += h[sym3(c, d) * st] * D[a][c] * D[b][d];
+        return acc;
+    };
+#pragma unroll
+    for (int i = 0; i < L::N; ++i) o[i] = 0.f;
+#pragma unroll
+    for (int a = 0; a < ND; ++a) {
+        o[L::JS + 2 * a] = static_cast<float>(d1(M[0], 1, a));
+        o[L::JS + 2 * a + 1] = static_cast<float>(d1(M[1], 1, a));
+#pragma unroll
+        for (int u = 0; u < 3; ++u) o[L::JS + 2 * ND + 3 * a + u] = static_cast<float>(d1(M[2 + u], 1, a));
+    }
+    {
+        int p = 0;
+#pragma unroll
+        for (int a = 0; a < ND; ++a)
+#pragma unroll
+            for (int b = a; b < ND; ++b, ++p) {
+                o[L::HPI + 2 * p] = static_cast<float>(d2(Hu[0], 1, a, b));
+                o[L::HPI + 2 * p + 1] = static_cast<float>(d2(Hu[1], 1, a, b));
+#pragma unroll
+                for (int u = 0; u < 3; ++u) o[L::SCD + 3 * p + u] = static_cast<float>(d2(Hu[2 + u], 1, a, b));
+            }
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        double jd[ND];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+            jd[a] = d1(Jc[ch], 1, a);
+            o[L::JC + 4 * ch + a] = static_cast<float>(jd[a]);
+        }
+        int p = 0;
+#pragma unroll
+        for (int a = 0; a < ND; ++a)
+#pragma unroll
+            for (int b = a; b < ND; ++b, ++p) {
+                o[L::JJ + L::NP * ch + p] = static_cast<float>(jd[a] * jd[b]);
+                o[L::HC + L::NP * ch + p] = static_cast<float>(d2(Hc[ch], 1, a, b));
+            }
     }
 }
 
@@ -334,6 +373,10 @@ struct PassTraits<kPassPosition> {
     static constexpr int NC = kPosConsts, NA = 9, BATCH = 32;
 };
 template <>
+struct PassTraits<kPassPositionUV> {
+    static constexpr int NC = kPosUVConsts, NA = 5, BATCH = 32;
+};
+template <>
 struct PassTraits<kPassRotation> {
     static constexpr int NC = kRotConsts, NA = 2, BATCH = 64;
 };
@@ -376,43 +419,48 @@ struct Rec {
 // with J = dpi/dp, S_c = dSigma/dp_c, Hpi / S_cd the second derivatives. The
 // three-channel Gauss-Newton and curvature sums are regrouped so each output
 // entry costs a handful of FMAs (DESIGN.md §5 "K8 position").
+template <int ND>
 __device__ __forceinline__ void position_record(const float4* K4, const Rec& r, float qa, float qb, float qc,
-                                                float (&v)[9]) {
+                                                float (&v)[ND + ND * (ND + 1) / 2]) {
+    using L = PosLayout<ND>;
+    constexpr int NP = L::NP;
     const float G = r.G, q0 = r.q0, q1 = r.q1, wa = r.wa;
-    float A[16];
-    ld4<4>(A, K4 + kPosJS / 4);
-    float r0[3], r1[3], qcv[3], t0[3], t1[3];
+    float A[L::a4(5 * ND)];
+    ld4<L::a4(5 * ND) / 4>(A, K4 + L::JS / 4);
+    float r0[ND], r1[ND], qcv[ND], t0[ND], t1[ND];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < ND; ++c) {
         const float Jx = A[2 * c], Jy = A[2 * c + 1];
-        const float Sa = A[6 + 3 * c], Sb = A[7 + 3 * c], Sc = A[8 + 3 * c];
+        const float Sa = A[2 * ND + 3 * c], Sb = A[2 * ND + 3 * c + 1], Sc = A[2 * ND + 3 * c + 2];
         r0[c] = Jx - (Sa * q0 + Sb * q1);
         r1[c] = Jy - (Sb * q0 + Sc * q1);
         qcv[c] = q0 * (Jx + r0[c]) + q1 * (Jy + r1[c]);
         t0[c] = qa * r0[c] + qb * r1[c];
         t1[c] = qb * r0[c] + qc * r1[c];
     }
-    float dG[3], d2G[6];
+    float dG[ND], d2G[NP];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) dG[c] = -0.5f * G * qcv[c];
+    for (int c = 0; c < ND; ++c) dG[c] = -0.5f * G * qcv[c];
     {
-        float Hp[12], Sd[20];
-        ld4<3>(Hp, K4 + kPosHpi / 4);
-        ld4<5>(Sd, K4 + kPosScd / 4);
+        float Hp[L::a4(2 * NP)], Sd[L::a4(3 * NP)];
+        ld4<L::a4(2 * NP) / 4>(Hp, K4 + L::HPI / 4);
+        ld4<L::a4(3 * NP) / 4>(Sd, K4 + L::SCD / 4);
         const float m00 = q0 * q0, m01 = 2.f * q0 * q1, m11 = q1 * q1;
         int p = 0;
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < ND; ++c)
 #pragma unroll
-            for (int d = c; d < 3; ++d, ++p) {
+            for (int d = c; d < ND; ++d, ++p) {
                 const float qcd = 2.f * (r0[c] * t0[d] + r1[c] * t1[d]) + 2.f * (q0 * Hp[2 * p] + q1 * Hp[2 * p + 1]) -
                                   (Sd[3 * p] * m00 + Sd[3 * p + 1] * m01 + Sd[3 * p + 2] * m11);
                 d2G[p] = G * (0.25f * qcv[c] * qcv[d] - 0.5f * qcd);
             }
     }
     float Jc[12];
-    ld4<3>(Jc, K4 + kPosJc / 4);
-    float sgl = 0.f, A2 = 0.f, vgl[3] = {0.f, 0.f, 0.f}, vh[3] = {0.f, 0.f, 0.f}, ga[3], ha[3];
+    ld4<3>(Jc, K4 + L::JC / 4);
+    float sgl = 0.f, A2 = 0.f, vgl[ND], vh[ND], ga[3], ha[3];
+#pragma unroll
+    for (int i = 0; i < ND; ++i) vgl[i] = vh[i] = 0.f;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
         ga[ch] = r.gl[ch] * wa;
@@ -421,29 +469,29 @@ __device__ __forceinline__ void position_record(const float4* K4, const Rec& r, 
         const float hac = ha[ch] * r.ac[ch];
         A2 += hac * r.ac[ch];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < ND; ++i) {
             vgl[i] += ga[ch] * Jc[4 * ch + i];
             vh[i] += hac * Jc[4 * ch + i];
         }
     }
-    float E[36];
-    ld4<9>(E, K4 + kPosJJ / 4);
-    float JJ[6], hc[6];
+    float E[L::a4(6 * NP)];
+    ld4<L::a4(6 * NP) / 4>(E, K4 + L::JJ / 4);
+    float JJ[NP], hc[NP];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-        JJ[q] = ha[0] * E[q] + ha[1] * E[6 + q] + ha[2] * E[12 + q];
-        hc[q] = ga[0] * E[18 + q] + ga[1] * E[24 + q] + ga[2] * E[30 + q];
+    for (int q = 0; q < NP; ++q) {
+        JJ[q] = ha[0] * E[q] + ha[1] * E[NP + q] + ha[2] * E[2 * NP + q];
+        hc[q] = ga[0] * E[3 * NP + q] + ga[1] * E[4 * NP + q] + ga[2] * E[5 * NP + q];
     }
     const float GG = G * G;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) v[c] = sgl * dG[c] + G * vgl[c];
+    for (int c = 0; c < ND; ++c) v[c] = sgl * dG[c] + G * vgl[c];
     int p = 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < ND; ++c)
 #pragma unroll
-        for (int d = c; d < 3; ++d, ++p)
-            v[3 + p] = sgl * d2G[p] + G * hc[p] + dG[c] * vgl[d] + vgl[c] * dG[d] + A2 * dG[c] * dG[d] +
-                       G * (dG[c] * vh[d] + vh[c] * dG[d]) + GG * JJ[p];
+        for (int d = c; d < ND; ++d, ++p)
+            v[ND + p] = sgl * d2G[p] + G * hc[p] + dG[c] * vgl[d] + vgl[c] * dG[d] + A2 * dG[c] * dG[d] +
+                        G * (dG[c] * vh[d] + vh[c] * dG[d]) + GG * JJ[p];
 }
 
 // Rotation (newton.hpp:366-401): directional derivatives along
@@ -611,9 +659,9 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 r.gl[c] = s_gl[px][c];
                 r.hl[c] = s_hl[px][c];
             }
-            if constexpr (PASS == kPassPosition) {
+            if constexpr (PASS == kPassPosition || PASS == kPassPositionUV) {
                 const float4 g0 = s_g0[jj], g1 = s_g1[jj];
-                position_record(s_const + jj * CST, r, g0.z, g0.w, g1.x, v);
+                position_record<PASS == kPassPosition ? 3 : 2>(s_const + jj * CST, r, g0.z, g0.w, g1.x, v);
             } else if constexpr (PASS == kPassRotation) {
                 const float4 g0 = s_g0[jj], g1 = s_g1[jj];
                 rotation_record(s_const + jj * CST, r, g0.z, g0.w, g1.x, v);
@@ -768,7 +816,11 @@ void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const Cam
     switch (pass) {
         case kPassPosition:
             v.consts.ensure(static_cast<size_t>(n) * kPosConsts);
-            position_consts_k<<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, v.flags.ptr, v.consts.ptr);
+            position_consts_k<3><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            break;
+        case kPassPositionUV:
+            v.consts.ensure(static_cast<size_t>(n) * kPosUVConsts);
+            position_consts_k<2><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
             break;
         case kPassRotation:
             v.consts.ensure(static_cast<size_t>(n) * kRotConsts);
@@ -813,13 +865,17 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     if (own1 <= own0) return;
     a.tile0 = own0 * v.cam.tiles_x;
     const int blocks = (own1 - own0) * v.cam.tiles_x;
-    StageScope st(NGS_STAGE_BWD_POSITION + pass, s);
+    StageScope st(NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV ? kPassPosition : pass), s);
     const bool small = v.cam.tile == 8;
     const int threads = small ? 64 : 256;
     switch (pass) {
         case kPassPosition:
             if (small) backward_k<kPassPosition, 8><<<blocks, threads, 0, s>>>(a);
             else backward_k<kPassPosition, 16><<<blocks, threads, 0, s>>>(a);
+            break;
+        case kPassPositionUV:
+            if (small) backward_k<kPassPositionUV, 8><<<blocks, threads, 0, s>>>(a);
+            else backward_k<kPassPositionUV, 16><<<blocks, threads, 0, s>>>(a);
             break;
         case kPassRotation:
             if (small) backward_k<kPassRotation, 8><<<blocks, threads, 0, s>>>(a);

@@ -5,23 +5,39 @@
 
 namespace ngsb {
 
-enum PassId { kPassPosition = 0, kPassRotation = 1, kPassScaling = 2, kPassOpacityColor = 3 };
+// kPassPositionUV is the position pass the solvers use: derivatives are taken
+// along the two in-plane directions u_x, u_y of build_position_subspace
+// (newton.hpp:130-139) instead of the world axes. The 2x2 system
+// U^T (sum_v H_v) U = sum_v U^T H_v U is linear in the per-record terms, so the
+// accumulators hold the projected system directly (5 instead of 9 components).
+// kPassPosition (world axes) serves ngs_accumulate, which returns the 3x3 terms.
+enum PassId { kPassPosition = 0, kPassRotation = 1, kPassScaling = 2, kPassOpacityColor = 3, kPassPositionUV = 4 };
 
 // Accumulator components per pass (FP64, component-major [c][N]).
 constexpr int kAccPosition = 9;  // grad 3, hess sym (xx, xy, xz, yy, yz, zz)
+constexpr int kAccPositionUV = 5;  // grad (u_x, u_y), hess (xx, xy, yy) in the subspace
 constexpr int kAccRotation = 2;  // grad, hess
 constexpr int kAccScaling = 5;   // grad 2, hess (00, 01, 11)
 constexpr int kAccOpColor = 8;   // opacity grad, hess; colour g_acc[3], h_acc[3] (per view)
 
 // Per-(Gaussian, view) constant layouts (floats, AoS per Gaussian, float4-aligned
-// groups). Symmetric 3x3 pairs (c, d) are packed (00, 01, 02, 11, 12, 22).
-constexpr int kPosJS = 0;    // J columns (Jx_c, Jy_c) x3, then dSigma/dp_c (a, b, c) x3   [15 + 1 pad]
-constexpr int kPosHpi = 16;  // d2pi/dp_c dp_d: (x, y) per pair                            [12]
-constexpr int kPosScd = 28;  // d2Sigma/dp_c dp_d: (a, b, c) per pair                      [18 + 2 pad]
-constexpr int kPosJc = 48;   // dc~_ch/dp: 3 per channel, padded to 4                       [12]
-constexpr int kPosJJ = 60;   // Jc_ch Jc_ch^T: 6 per channel                                [18]
-constexpr int kPosHc = 78;   // d2c~_ch/dp2: 6 per channel                                  [18]
-constexpr int kPosConsts = 96;
+// groups). ND derivative directions (3 world axes, or the 2 subspace directions);
+// symmetric pairs (c, d), c <= d, packed row by row ((00, 01, 02, 11, 12, 22) for ND = 3).
+template <int ND>
+struct PosLayout {
+    static constexpr int NP = ND * (ND + 1) / 2;
+    __host__ __device__ static constexpr int a4(int x) { return (x + 3) & ~3; }
+    static constexpr int JS = 0;                  // J columns (Jx_c, Jy_c) xND, then dSigma/dp_c (a, b, c) xND
+    static constexpr int HPI = JS + a4(5 * ND);   // d2pi/dp_c dp_d: (x, y) per pair
+    static constexpr int SCD = HPI + a4(2 * NP);  // d2Sigma/dp_c dp_d: (a, b, c) per pair
+    static constexpr int JC = SCD + a4(3 * NP);   // dc~_ch/dp: ND per channel, padded to 4
+    static constexpr int JJ = JC + 12;            // Jc_ch Jc_ch^T: NP per channel
+    static constexpr int HC = JJ + 3 * NP;        // d2c~_ch/dp2: NP per channel
+    static constexpr int N = a4(HC + 3 * NP);
+};
+constexpr int kPosConsts = PosLayout<3>::N;    // 96
+constexpr int kPosUVConsts = PosLayout<2>::N;  // 64
+static_assert(kPosConsts == 96 && kPosUVConsts == 64, "position constant layout");
 constexpr int kRotConsts = 8;    // s1 (00, 01, 11), s2 (00, 01, 11), pad 2
 constexpr int kScaleConsts = 8;  // v0 (2), v1 (2), m00, m01, m11, pad
 

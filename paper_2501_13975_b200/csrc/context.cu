@@ -713,9 +713,13 @@ int pass_of(int attr) {
     }
 }
 
+// The pass whose accumulators the solvers consume (position: the projected 2x2 system).
+int solve_pass_of(int attr) { return attr == NGS_POSITION ? kPassPositionUV : pass_of(attr); }
+
 int acc_components(int pass) {
     switch (pass) {
         case kPassPosition: return kAccPosition;
+        case kPassPositionUV: return kAccPositionUV;
         case kPassRotation: return kAccRotation;
         case kPassScaling: return kAccScaling;
         default: return kAccOpColor;
@@ -900,7 +904,7 @@ int32_t ngs_newton_step(ngs_context* ctx, ngs_attribute attr, int32_t primary_sl
         const int nv = static_cast<int>(views.size());
         const int n = ctx->scene.n;
         const size_t stride = static_cast<size_t>(std::max(n, 1));
-        const int pass = pass_of(attr);
+        const int pass = solve_pass_of(attr);
         accumulate_pass(ctx, pass, views.data(), nv, nullptr);
         const SolveParams sp = to_solve(options, commit);
         const int dsz = (attr == NGS_COLOR) ? 48 : (attr == NGS_POSITION || attr == NGS_SCALING) ? 3 : 1;
@@ -1154,13 +1158,13 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
             mark(0);
             for (int pass_i = 0; pass_i < 5; ++pass_i) {
                 const int attr = T.cfg.order[pass_i];
-                const int pass = pass_of(attr);
+                const int pass = solve_pass_of(attr);
                 // Opacity and colour share one traversal when adjacent (same captures, trainer.hpp:412-415).
                 const bool reuse = (attr == NGS_COLOR && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_OPACITY) ||
                                    (attr == NGS_OPACITY && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_COLOR);
                 if (!reuse) {
                     accumulate_pass(ctx, pass, views.data(), nv, nullptr, true);
-                    mark(1 + pass);
+                    mark(1 + (pass == kPassPositionUV ? kPassPosition : pass));
                 }
                 SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
                 launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,

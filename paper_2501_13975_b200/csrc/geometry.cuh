@@ -375,6 +375,16 @@ __device__ inline bool view_direction(const CameraDev& cam, const D3& p, D3& r, 
     return true;
 }
 
+// build_position_subspace (newton.hpp:130-139): u_y = Gram-Schmidt of the world
+// up axis (z near the poles) against the ray r, u_x = r x u_y.
+__device__ inline void position_subspace(const D3& r, D3& ux, D3& uy) {
+    D3 seed = d3(0, 1, 0);
+    if (fabs(dot3(r, seed)) > 0.99) seed = d3(0, 0, 1);
+    uy = sub3(seed, scale3(r, dot3(r, seed)));
+    uy = scale3(uy, 1.0 / sqrt(dot3(uy, uy)));
+    ux = cross3(r, uy);
+}
+
 __device__ inline D3 load_pos(const SceneDev& s, int k) {
     const float4 v = s.pos_sigma[k];
     return {v.x, v.y, v.z};

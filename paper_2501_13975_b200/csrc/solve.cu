@@ -73,26 +73,15 @@ __global__ void __launch_bounds__(256) solve_position_k(SceneDev s, CameraDev pr
     if (k < s.n) {
         const float4 ps = s.pos_sigma[k];
         const D3 p = {ps.x, ps.y, ps.z};
-        double g[3], H[3][3];
-        for (int i = 0; i < 3; ++i) g[i] = acc[i * stride + k];
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) H[i][j] = acc[(3 + sym3(i, j)) * stride + k];
+        // Accumulators of kPassPositionUV: already U^T g and U^T H U (newton.hpp:604-606).
         D3 r;
         primary_dir(primary, p, r, out.err);
-        // build_position_subspace, newton.hpp:130-139
-        D3 seed = d3(0, 1, 0);
-        if (fabs(dot3(r, seed)) > 0.99) seed = d3(0, 0, 1);
-        D3 uy = sub3(seed, scale3(r, dot3(r, seed)));
-        uy = scale3(uy, 1.0 / sqrt(dot3(uy, uy)));
-        const D3 ux = cross3(r, uy);
+        D3 ux, uy;
+        position_subspace(r, ux, uy);
         const double U[3][2] = {{ux.x, uy.x}, {ux.y, uy.y}, {ux.z, uy.z}};
-        double H2[2][2] = {}, g2[2] = {};
-        for (int a = 0; a < 2; ++a) {
-            for (int i = 0; i < 3; ++i) g2[a] += U[i][a] * g[i];
-            for (int b = 0; b < 2; ++b)
-                for (int i = 0; i < 3; ++i)
-                    for (int j = 0; j < 3; ++j) H2[a][b] += U[i][a] * H[i][j] * U[j][b];
-        }
+        const double g2[2] = {acc[k], acc[stride + k]};
+        const double H2[2][2] = {{acc[2 * stride + k], acc[3 * stride + k]},
+                                 {acc[3 * stride + k], acc[4 * stride + k]}};
         double d0, d1;
         solve2(H2[0][0], 0.5 * (H2[0][1] + H2[1][0]), H2[1][1], g2[0], g2[1], sp, d0, d1);
         double dp[3];
