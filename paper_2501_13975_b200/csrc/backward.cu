@@ -577,22 +577,53 @@ struct WarpQueue {
 //    reduces them and each segment tail adds into the block's per-splat sums.
 //  Batch end: per-splat block sums -> FP64 global accumulators (one atomic per
 //    (tile, splat, component)).
+// cp.async (LDGSTS): 16-byte global -> shared copies without register staging.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Shared memory of one backward block (dynamic: > 48 KB for the position passes).
+template <int PASS, int TILE>
+struct BackwardSmem {
+    using TR = PassTraits<PASS>;
+    static constexpr int NT = TILE * TILE, NW = NT / 32;
+    static constexpr int B = TR::BATCH, NA = TR::NA, NC4 = TR::NC / 4;
+    static constexpr int CST = (NC4 % 8 == 0 && NC4 > 0) ? NC4 + 1 : NC4;  // float4 stride, avoids bank conflicts
+    float4 raw[2][4][B];                   // staged records (pix as double2, ra, rb, rc), double-buffered
+    float4 cst[2][(CST > 0 ? CST : 1) * B];  // staged per-view constants, double-buffered
+    float4 g0[B], g1[B];                   // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
+    float2 g2[B];                          // (c1, c2)
+    float2 yext[B];                        // splat y-extent of the cutoff ellipse (tile coordinates)
+    float acc[NW][NA][B];                  // per-warp sums: segment tails are unique within a drain
+    int kid[2][B];
+    int vis[B];
+    float gl[NT][3], hl[NT][3];
+    WarpQueue q[NW];
+    int maxlast;
+};
+
 template <int PASS, int TILE>
 __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
+    using SM = BackwardSmem<PASS, TILE>;
     constexpr int NT = TILE * TILE, NW = NT / 32, kRowsPerWarp = 32 / TILE;
-    constexpr int B = TR::BATCH, NC = TR::NC, NA = TR::NA, NC4 = NC / 4;
-    constexpr int CST = (NC4 % 8 == 0 && NC4 > 0) ? NC4 + 1 : NC4;  // float4 stride, avoids bank conflicts
-    __shared__ float4 s_g0[B], s_g1[B];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
-    __shared__ float2 s_g2[B];           // (c1, c2)
-    __shared__ float2 s_yext[B];         // splat y-extent of the cutoff ellipse (tile coordinates)
-    __shared__ float4 s_const[(CST > 0 ? CST : 1) * B];
-    __shared__ float s_acc[NW][NA][B];  // per-warp sums: segment tails are unique within a drain
-    __shared__ int s_kid[B];
-    __shared__ int s_vis[B];
-    __shared__ float s_gl[NT][3], s_hl[NT][3];
-    __shared__ WarpQueue s_q[NW];
-    __shared__ int s_maxlast;
+    constexpr int B = TR::BATCH, NA = TR::NA, NC4 = SM::NC4, CST = SM::CST;
+    static_assert(B <= NT, "one loader thread per splat of a batch");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SM& S = *reinterpret_cast<SM*>(smem_raw);
+    auto& s_g0 = S.g0;
+    auto& s_g1 = S.g1;
+    auto& s_g2 = S.g2;
+    auto& s_yext = S.yext;
+    auto& s_acc = S.acc;
+    auto& s_vis = S.vis;
+    auto& s_gl = S.gl;
+    auto& s_hl = S.hl;
+    auto& s_q = S.q;
+    auto& s_maxlast = S.maxlast;
     unsigned long long block_pairs = 0;
 
     const int tile = a.tile0 + blockIdx.x;  // owned tile rows only (multi-GPU shard)
@@ -634,6 +665,8 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
 
     float T = 1.0f, P[3] = {0.f, 0.f, 0.f};
     int qhead = 0, qcount = 0;  // warp-uniform ring state
+
+    const float4* s_const = S.cst[0];  // constants of the batch being traversed
 
     // Phase 2 over queue entries [qhead, qhead + n), n <= 32.
     auto drain = [&](int n) {
@@ -695,36 +728,65 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
         qcount -= n;
     };
 
-    for (int base = range.x; base < end; base += B) {
+    // Software pipeline: while batch `it` is traversed, the records and constants
+    // of batch it+1 are in flight (cp.async) and the list entries of batch it+2
+    // are being loaded into a register.
+    const int tid = threadIdx.x;
+    auto issue = [&](int buf, int b0) {
+        const int n = min(B, end - b0);
+        for (int i = tid; i < 4 * n; i += NT) {
+            const int j = i >> 2, r = i & 3;
+            const int k = S.kid[buf][j];
+            const void* src = r == 0 ? static_cast<const void*>(a.pix + k)
+                                     : static_cast<const void*>((r == 1 ? a.ra : r == 2 ? a.rb : a.rc) + k);
+            cp_async16(&S.raw[buf][r][j], src);
+        }
+        if constexpr (NC4 > 0) {
+            const float4* src = reinterpret_cast<const float4*>(a.consts);
+            for (int i = tid; i < n * NC4; i += NT) {
+                const int j = i / NC4, c = i - j * NC4;
+                cp_async16(&S.cst[buf][j * CST + c], src + static_cast<size_t>(S.kid[buf][j]) * NC4 + c);
+            }
+        }
+    };
+    int kid_next = 0;
+    if (tid < B) {
+        if (range.x + tid < end) S.kid[0][tid] = a.vals[range.x + tid];
+        if (range.x + B + tid < end) kid_next = a.vals[range.x + B + tid];
+    }
+    __syncthreads();
+    if (range.x < end) issue(0, range.x);
+    cp_async_commit();
+    int it = 0;
+    for (int base = range.x; base < end; base += B, ++it) {
+        const int buf = it & 1;
         const int cnt = min(B, end - base);
-        __syncthreads();
-        for (int i = threadIdx.x; i < B; i += blockDim.x) {
-            if (i < cnt) {
-                const int k = a.vals[base + i];
-                s_kid[i] = k;
-                const double2 p = a.pix[k];
-                const float4 ra = a.ra[k], rb = a.rb[k], rc = a.rc[k];
+        s_const = S.cst[buf];
+        cp_async_wait_all();
+        __syncthreads();  // batch `it` staged by every thread; the previous batch's readers are done
+        if (tid < B) {
+            if (tid < cnt) {
+                const double2 p = reinterpret_cast<const double2*>(S.raw[buf][0])[tid];
+                const float4 ra = S.raw[buf][1][tid], rb = S.raw[buf][2][tid], rc = S.raw[buf][3][tid];
                 const float qmax = reject_bound(rb.y, a.cutoff);
                 const float py = static_cast<float>(p.y - oy);
                 // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level
                 // skip never drops a record the per-lane test would keep.
                 const float ey = sqrtf(fmaxf(qmax, 0.f) * rc.w) * 1.0001f + 1e-3f;
-                s_g0[i] = make_float4(static_cast<float>(p.x - ox), py, ra.z, ra.w);
-                s_g1[i] = make_float4(rb.x, rb.y, qmax, rb.z);
-                s_g2[i] = make_float2(rb.w, rc.x);
-                s_yext[i] = make_float2(py - ey, py + ey);
+                s_g0[tid] = make_float4(static_cast<float>(p.x - ox), py, ra.z, ra.w);
+                s_g1[tid] = make_float4(rb.x, rb.y, qmax, rb.z);
+                s_g2[tid] = make_float2(rb.w, rc.x);
+                s_yext[tid] = make_float2(py - ey, py + ey);
             }
-            s_vis[i] = 0;
+            s_vis[tid] = 0;
+            S.kid[buf ^ 1][tid] = kid_next;
+            const int nx = base + 2 * B + tid;
+            kid_next = nx < end ? a.vals[nx] : 0;
         }
-        for (int i = threadIdx.x; i < NW * NA * B; i += blockDim.x) (&s_acc[0][0][0])[i] = 0.f;
-        if constexpr (NC4 > 0) {
-            const float4* src = reinterpret_cast<const float4*>(a.consts);
-            for (int i = threadIdx.x; i < cnt * NC4; i += blockDim.x) {
-                const int j = i / NC4, c = i - j * NC4;
-                s_const[j * CST + c] = src[static_cast<size_t>(a.vals[base + j]) * NC4 + c];
-            }
-        }
+        for (int i = tid; i < NW * NA * B; i += NT) (&s_acc[0][0][0])[i] = 0.f;
         __syncthreads();
+        if (base + B < end) issue(buf ^ 1, base + B);
+        cp_async_commit();
         // Phase 1
         for (int j = 0; j < cnt; ++j) {
             const float2 ye = s_yext[j];
@@ -793,7 +855,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const int k = s_kid[i];
+            const int k = S.kid[buf][i];
             if (a.visible && s_vis[i]) a.visible[k] = 1;
 #pragma unroll
             for (int c = 0; c < NA; ++c) {
@@ -837,6 +899,11 @@ void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const Cam
     CUDA_LAUNCH_CHECK();
 }
 
+template <class T>
+struct SmemTag {
+    using type = T;
+};
+
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
                      unsigned long long* contrib_pairs, cudaStream_t s) {
     if (v.pairs == 0 || v.n == 0) return;
@@ -868,26 +935,35 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     StageScope st(NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV ? kPassPosition : pass), s);
     const bool small = v.cam.tile == 8;
     const int threads = small ? 64 : 256;
+    auto go = [&](auto kernel, auto smem_tag) {
+        using SM = typename decltype(smem_tag)::type;
+        static bool attr_set = false;  // per instantiation
+        if (!attr_set) {
+            CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(SM)));
+            attr_set = true;
+        }
+        kernel<<<blocks, threads, sizeof(SM), s>>>(a);
+    };
     switch (pass) {
         case kPassPosition:
-            if (small) backward_k<kPassPosition, 8><<<blocks, threads, 0, s>>>(a);
-            else backward_k<kPassPosition, 16><<<blocks, threads, 0, s>>>(a);
+            if (small) go(backward_k<kPassPosition, 8>, SmemTag<BackwardSmem<kPassPosition, 8>>{});
+            else go(backward_k<kPassPosition, 16>, SmemTag<BackwardSmem<kPassPosition, 16>>{});
             break;
         case kPassPositionUV:
-            if (small) backward_k<kPassPositionUV, 8><<<blocks, threads, 0, s>>>(a);
-            else backward_k<kPassPositionUV, 16><<<blocks, threads, 0, s>>>(a);
+            if (small) go(backward_k<kPassPositionUV, 8>, SmemTag<BackwardSmem<kPassPositionUV, 8>>{});
+            else go(backward_k<kPassPositionUV, 16>, SmemTag<BackwardSmem<kPassPositionUV, 16>>{});
             break;
         case kPassRotation:
-            if (small) backward_k<kPassRotation, 8><<<blocks, threads, 0, s>>>(a);
-            else backward_k<kPassRotation, 16><<<blocks, threads, 0, s>>>(a);
+            if (small) go(backward_k<kPassRotation, 8>, SmemTag<BackwardSmem<kPassRotation, 8>>{});
+            else go(backward_k<kPassRotation, 16>, SmemTag<BackwardSmem<kPassRotation, 16>>{});
             break;
         case kPassScaling:
-            if (small) backward_k<kPassScaling, 8><<<blocks, threads, 0, s>>>(a);
-            else backward_k<kPassScaling, 16><<<blocks, threads, 0, s>>>(a);
+            if (small) go(backward_k<kPassScaling, 8>, SmemTag<BackwardSmem<kPassScaling, 8>>{});
+            else go(backward_k<kPassScaling, 16>, SmemTag<BackwardSmem<kPassScaling, 16>>{});
             break;
         case kPassOpacityColor:
-            if (small) backward_k<kPassOpacityColor, 8><<<blocks, threads, 0, s>>>(a);
-            else backward_k<kPassOpacityColor, 16><<<blocks, threads, 0, s>>>(a);
+            if (small) go(backward_k<kPassOpacityColor, 8>, SmemTag<BackwardSmem<kPassOpacityColor, 8>>{});
+            else go(backward_k<kPassOpacityColor, 16>, SmemTag<BackwardSmem<kPassOpacityColor, 16>>{});
             break;
     }
     CUDA_LAUNCH_CHECK();
