@@ -577,14 +577,6 @@ struct WarpQueue {
 //    reduces them and each segment tail adds into the block's per-splat sums.
 //  Batch end: per-splat block sums -> FP64 global accumulators (one atomic per
 //    (tile, splat, component)).
-// cp.async (LDGSTS): 16-byte global -> shared copies without register staging.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
 // Shared memory of one backward block (dynamic: > 48 KB for the position passes).
 template <int PASS, int TILE>
 struct BackwardSmem {

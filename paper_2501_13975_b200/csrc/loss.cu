@@ -46,22 +46,64 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return t;
 }
 
+// Separable valid-tap convolutions over a (kLT + 2h)^2 shared-memory halo tile.
+// HT > 0 fixes the window half-width at compile time (the default 11-tap
+// window: fully unrolled, register-blocked two outputs per horizontal task);
+// HT == 0 is the generic path for any window <= 21.
+template <int HT>
+struct SsimGeom {
+    static constexpr int HMAX = HT > 0 ? HT : kMaxHalf;
+    static constexpr int SP = kLT + 2 * HMAX;  // halo tile edge
+};
+
+// Horizontal pass of `nf` planes: out[f][r][c] = sum_k w_f[k] in[f][r][c + k],
+// rows r < span, two adjacent outputs per task (each input loaded once).
+template <int HT, int NF, class In, class Out, class WSel>
+__device__ __forceinline__ void hpass(int h, int span, In in, Out out, WSel wsel) {
+    constexpr int HALF = kLT / 2;
+    for (int task = threadIdx.x; task < NF * span * HALF; task += blockDim.x) {
+        const int f = task / (span * HALF);
+        const int rem = task - f * span * HALF;
+        const int r = rem / HALF, c0 = (rem - r * HALF) * 2;
+        const double* w = wsel(f);
+        double a0 = 0.0, a1 = 0.0;
+        if constexpr (HT > 0) {
+#pragma unroll
+            for (int k = 0; k <= 2 * HT + 1; ++k) {
+                const double v = in(f, r, c0 + k);
+                if (k <= 2 * HT) a0 += w[k] * v;
+                if (k >= 1) a1 += w[k - 1] * v;
+            }
+        } else {
+            for (int k = 0; k <= 2 * h + 1; ++k) {
+                const double v = in(f, r, c0 + k);
+                if (k <= 2 * h) a0 += w[k] * v;
+                if (k >= 1) a1 += w[k - 1] * v;
+            }
+        }
+        out(f, r, c0) = a0;
+        out(f, r, c0 + 1) = a1;
+    }
+}
+
 // Kernel A: window statistics and the 9 window-centre fields for one channel.
+template <int HT>
 __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double* __restrict__ image,
                                                      const double* __restrict__ target, Window win, double c1, double c2,
                                                      double* __restrict__ fields, double* __restrict__ sums, int row0,
                                                      int own_y0, int own_y1) {
-    __shared__ double s_x[kLS][kLS + 1], s_t[kLS][kLS + 1];
-    __shared__ double s_h[5][kLS][kLT + 1];
+    constexpr int SP = SsimGeom<HT>::SP;
+    __shared__ double s_x[SP][SP + 1], s_t[SP][SP + 1];
+    __shared__ double s_h[5][SP][kLT + 1];
     __shared__ double red[8];
     const int ch = blockIdx.z;
     const int ox = blockIdx.x * kLT, oy = (row0 + blockIdx.y) * kLT;
-    const int h = win.half, span = kLT + 2 * h;
+    const int h = HT > 0 ? HT : win.half, span = kLT + 2 * h;
     const size_t plane = static_cast<size_t>(W) * H;
     const double* img = image + ch * plane;
     const double* tgt = target + ch * plane;
     for (int i = threadIdx.x; i < span * span; i += blockDim.x) {
-        const int r = i / span, c = i % span;
+        const int r = i / span, c = i - r * span;
         const int gx = ox - h + c, gy = oy - h + r;
         const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
         const size_t idx = static_cast<size_t>(gy) * W + gx;
@@ -69,58 +111,81 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
         s_t[r][c] = in ? tgt[idx] : 0.0;
     }
     __syncthreads();
-    // Horizontal pass (out-of-image taps are zero == skipped taps).
-    for (int i = threadIdx.x; i < span * kLT; i += blockDim.x) {
-        const int r = i / kLT, c = i % kLT;
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-        for (int k = -h; k <= h; ++k) {
-            const double wk = win.w[k + h];
-            const double xv = s_x[r][c + h + k], tv = s_t[r][c + h + k];
-            a0 += wk * xv;
-            a1 += wk * (xv * xv);
-            a2 += wk * tv;
-            a3 += wk * (tv * tv);
-            a4 += wk * (xv * tv);
+    // Horizontal pass of the 5 statistics (out-of-image taps are zero == skipped taps):
+    // two outputs per task, 5 products per loaded tap.
+    {
+        constexpr int HALF = kLT / 2;
+        for (int task = threadIdx.x; task < span * HALF; task += blockDim.x) {
+            const int r = task / HALF, c0 = (task - r * HALF) * 2;
+            double a[2][5] = {};
+            auto tap = [&](int k) {
+                const double xv = s_x[r][c0 + k], tv = s_t[r][c0 + k];
+                const double p[5] = {xv, xv * xv, tv, tv * tv, xv * tv};
+                const int hh = HT > 0 ? HT : h;
+                if (k <= 2 * hh) {
+                    const double wk = win.w[k];
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) a[0][f] += wk * p[f];
+                }
+                if (k >= 1) {
+                    const double wk = win.w[k - 1];
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) a[1][f] += wk * p[f];
+                }
+            };
+            if constexpr (HT > 0) {
+#pragma unroll
+                for (int k = 0; k <= 2 * HT + 1; ++k) tap(k);
+            } else {
+                for (int k = 0; k <= 2 * h + 1; ++k) tap(k);
+            }
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                s_h[f][r][c0] = a[0][f];
+                s_h[f][r][c0 + 1] = a[1][f];
+            }
         }
-        s_h[0][r][c] = a0;
-        s_h[1][r][c] = a1;
-        s_h[2][r][c] = a2;
-        s_h[3][r][c] = a3;
-        s_h[4][r][c] = a4;
     }
     __syncthreads();
     const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
     const int x = ox + lx, y = oy + ly;
     double ssim = 0.0;
     if (x < W && y < H) {
-        double st[5];
-        for (int f = 0; f < 5; ++f) {
-            double a = 0;
-            for (int k = -h; k <= h; ++k) a += win.w[k + h] * s_h[f][ly + h + k][lx];
-            st[f] = a;
+        double st[5] = {};
+        if constexpr (HT > 0) {
+#pragma unroll
+            for (int k = 0; k <= 2 * HT; ++k)
+#pragma unroll
+                for (int f = 0; f < 5; ++f) st[f] += win.w[k] * s_h[f][ly + k][lx];
+        } else {
+            for (int k = 0; k <= 2 * h; ++k)
+#pragma unroll
+                for (int f = 0; f < 5; ++f) st[f] += win.w[k] * s_h[f][ly + k][lx];
         }
         const double inv_norm = 1.0 / (axis_norm(x, W, win) * axis_norm(y, H, win));
         const double mu = st[0] * inv_norm, mu_t = st[2] * inv_norm;
         const double var = fmax(0.0, st[1] * inv_norm - mu * mu);
         const double var_t = fmax(0.0, st[3] * inv_norm - mu_t * mu_t);
         const double cov = st[4] * inv_norm - mu * mu_t;
-        // loss.hpp:266-303
+        // loss.hpp:266-303 (reciprocals of f2, f3 hoisted: two divisions per pixel)
         const double f0 = 2.0 * mu * mu_t + c1;
         const double f1 = 2.0 * cov + c2;
         const double f2 = mu * mu + mu_t * mu_t + c1;
         const double f3 = var + var_t + c2;
-        const double nn = f0 * f1, dd = f2 * f3;
-        ssim = nn / dd;
-        const double inv_d = 1.0 / dd;
+        const double inv_f2 = 1.0 / f2, inv_f3 = 1.0 / f3;
+        const double nn = f0 * f1;
+        const double inv_d = inv_f2 * inv_f3;
+        ssim = nn * inv_d;
         const double a0 = 2.0 * mu_t, a1 = -2.0 * mu_t, b1 = 2.0;
         const double a2 = 2.0 * mu, a3 = -2.0 * mu, b3 = 2.0;
         const double A = a0 * f1 + f0 * a1, B = f0 * b1, C = a2 * f3 + f2 * a3, E = f2 * b3;
         const double inv_d2 = inv_d * inv_d, inv_d3 = inv_d2 * inv_d, inv_norm2 = inv_norm * inv_norm;
+        const double nnd = nn * inv_d;
         double out[9];
-        out[0] = (2.0 * mu_t * (f1 - f0) * inv_d - 2.0 * mu * nn * inv_d / f2 + 2.0 * mu * nn * inv_d / f3) * inv_norm;
+        out[0] = (2.0 * mu_t * (f1 - f0) * inv_d - 2.0 * mu * nnd * inv_f2 + 2.0 * mu * nnd * inv_f3) * inv_norm;
         out[1] = 2.0 * f0 * inv_d * inv_norm;
-        out[2] = -2.0 * nn * inv_d / f3 * inv_norm;
-        out[3] = -2.0 * nn / (f2 * f3 * f3) * inv_norm;
+        out[2] = -2.0 * nnd * inv_f3 * inv_norm;
+        out[3] = -2.0 * nn * inv_f2 * inv_f3 * inv_f3 * inv_norm;
         out[4] = (2.0 * a0 * a1 * inv_d - 2.0 * A * C * inv_d2 - nn * (2.0 * a2 * a3 + 2.0 * f3 - 2.0 * f2) * inv_d2 +
                   2.0 * nn * C * C * inv_d3) *
                  inv_norm2;
@@ -129,6 +194,7 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
         out[7] = -2.0 * B * E * inv_d2 * inv_norm2;
         out[8] = 2.0 * nn * E * E * inv_d3 * inv_norm2;
         const size_t idx = static_cast<size_t>(y) * W + x;
+#pragma unroll
         for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
     }
     const bool own = y >= own_y0 && y < own_y1;  // owned pixel rows (multi-GPU shard)
@@ -136,19 +202,22 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
     if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
 }
 
-// Kernel B: convolve the 9 centre fields and combine into grad / hess; also the
-// L2 part. lambda == 0 skips the SSIM fields entirely (loss.hpp:345).
+// Kernel B: convolve the 9 centre fields (three per shared-memory round) and
+// combine into grad / hess (loss.hpp:309-329); also the L2 part (loss.hpp:138-156).
+// lambda == 0 skips the SSIM fields entirely (loss.hpp:345).
+template <int HT>
 __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double* __restrict__ image,
                                                      const double* __restrict__ target, Window win, double lambda,
                                                      const double* __restrict__ fields, float* __restrict__ grad,
                                                      float* __restrict__ hess, double* __restrict__ sums, int row0,
                                                      int own_y0, int own_y1) {
-    __shared__ double s_f[kLS][kLS + 1];
-    __shared__ double s_h[kLS][kLT + 1];
+    constexpr int SP = SsimGeom<HT>::SP;
+    __shared__ double s_f[3][SP][SP + 1];
+    __shared__ double s_h[3][SP][kLT + 1];
     __shared__ double red[8];
     const int ch = blockIdx.z;
     const int ox = blockIdx.x * kLT, oy = (row0 + blockIdx.y) * kLT;
-    const int h = win.half, span = kLT + 2 * h;
+    const int h = HT > 0 ? HT : win.half, span = kLT + 2 * h;
     const size_t plane = static_cast<size_t>(W) * H;
     const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
     const int x = ox + lx, y = oy + ly;
@@ -162,36 +231,41 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
     }
     double g_ssim = 0, h_ssim = 0;
     if (lambda != 0.0) {
-        for (int f = 0; f < 9; ++f) {
-            const double* field = fields + (static_cast<size_t>(f) * 3 + ch) * plane;
-            const double* wk = (f <= 3) ? win.w : win.w2;  // fp, fq, fr, fkw use w; the rest w^2
+#pragma unroll 1
+        for (int g = 0; g < 3; ++g) {
             __syncthreads();
-            for (int i = threadIdx.x; i < span * span; i += blockDim.x) {
-                const int r = i / span, cc = i % span;
+            for (int i = threadIdx.x; i < 3 * span * span; i += blockDim.x) {
+                const int f = i / (span * span);
+                const int rem = i - f * span * span;
+                const int r = rem / span, cc = rem - r * span;
                 const int gx = ox - h + cc, gy = oy - h + r;
                 const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
-                s_f[r][cc] = in ? field[static_cast<size_t>(gy) * W + gx] : 0.0;
+                const double* field = fields + (static_cast<size_t>(3 * g + f) * 3 + ch) * plane;
+                s_f[f][r][cc] = in ? field[static_cast<size_t>(gy) * W + gx] : 0.0;
             }
             __syncthreads();
-            for (int i = threadIdx.x; i < span * kLT; i += blockDim.x) {
-                const int r = i / kLT, cc = i % kLT;
-                double a = 0;
-                for (int k = -h; k <= h; ++k) a += wk[k + h] * s_f[r][cc + h + k];
-                s_h[r][cc] = a;
-            }
+            // fp, fq, fr, fkw (fields 0-3) use w; the rest w^2
+            auto wsel = [&](int f) { return (3 * g + f) <= 3 ? win.w : win.w2; };
+            hpass<HT, 3>(h, span, [&](int f, int r, int cc) -> const double& { return s_f[f][r][cc]; },
+                         [&](int f, int r, int cc) -> double& { return s_h[f][r][cc]; }, wsel);
             __syncthreads();
-            double s = 0;
-            for (int k = -h; k <= h; ++k) s += wk[k + h] * s_h[ly + h + k][lx];
-            switch (f) {  // loss.hpp:323-327
-                case 0: g_ssim += s; break;
-                case 1: g_ssim += ct * s; break;
-                case 2: g_ssim += c * s; break;
-                case 3: h_ssim += s; break;
-                case 4: h_ssim += s; break;
-                case 5: h_ssim += c * s; break;
-                case 6: h_ssim += ct * s; break;
-                case 7: h_ssim += c * ct * s; break;
-                case 8: h_ssim += c * c * s; break;
+            double sv[3] = {};
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                const double* wk = wsel(f);
+                if constexpr (HT > 0) {
+#pragma unroll
+                    for (int k = 0; k <= 2 * HT; ++k) sv[f] += wk[k] * s_h[f][ly + k][lx];
+                } else {
+                    for (int k = 0; k <= 2 * h; ++k) sv[f] += wk[k] * s_h[f][ly + k][lx];
+                }
+            }
+            if (g == 0) {  // loss.hpp:323-327
+                g_ssim += sv[0] + ct * sv[1] + c * sv[2];
+            } else if (g == 1) {
+                h_ssim += sv[0] + sv[1] + c * sv[2];
+            } else {
+                h_ssim += ct * sv[0] + c * ct * sv[1] + c * c * sv[2];
             }
         }
     }
@@ -199,19 +273,18 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
     if (valid) {
         const double d = c - ct;
         dsq = d * d;
-        double g = inv3n * d, hh = inv3n;
+        double gg = inv3n * d, hh = inv3n;
         if (lambda != 0.0) {
-            g += lambda * (-inv3n * g_ssim);
+            gg += lambda * (-inv3n * g_ssim);
             hh += lambda * (-inv3n * h_ssim);
         }
-        grad[ch * plane + idx] = static_cast<float>(g);
+        grad[ch * plane + idx] = static_cast<float>(gg);
         hess[ch * plane + idx] = static_cast<float>(hh);
     }
     const bool own = y >= own_y0 && y < own_y1;
     const double tot = block_sum(own ? dsq : 0.0, red);
     if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
 }
-
 
 }  // namespace
 
@@ -249,16 +322,22 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     if (row1 <= row0) return;
     const dim3 grid((v.W + kLT - 1) / kLT, row1 - row0, 3);
     StageScope st(NGS_STAGE_LOSS, s, 1);
-    if (ssim) {
-        v.fields.ensure(27 * npx);
-        ssim_fields_k<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
+    auto run = [&](auto fields_kernel, auto derivs_kernel) {
+        if (ssim) {
+            v.fields.ensure(27 * npx);
+            fields_kernel<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
+                                               v.loss_sums.ptr, row0, own0, own1);
+            CUDA_LAUNCH_CHECK();
+        }
+        derivs_kernel<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.lambda,
+                                           ssim ? v.fields.ptr : nullptr, v.loss_grad.ptr, v.loss_hess.ptr,
                                            v.loss_sums.ptr, row0, own0, own1);
         CUDA_LAUNCH_CHECK();
-    }
-    ssim_derivs_k<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.lambda,
-                                       ssim ? v.fields.ptr : nullptr, v.loss_grad.ptr, v.loss_hess.ptr,
-                                       v.loss_sums.ptr, row0, own0, own1);
-    CUDA_LAUNCH_CHECK();
+    };
+    if (win.half == 5)  // the reference default (window 11)
+        run(ssim_fields_k<5>, ssim_derivs_k<5>);
+    else
+        run(ssim_fields_k<0>, ssim_derivs_k<0>);
 }
 
 }  // namespace ngsb

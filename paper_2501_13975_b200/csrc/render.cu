@@ -268,13 +268,29 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
     double C0 = 0.0, C1 = 0.0, C2 = 0.0;  // FP64 colour sums: the image feeds the cancelling (c - c^t) loss terms
     int last = -1;
     bool done = !inside;
-    for (int base = range.x; base < range.y; base += kRasterBatch) {
+    // Software pipeline: thread t stages splat t of the next batch with cp.async
+    // (into its own slot, so only its own wait is needed) while the current batch
+    // is composited; the list entry of the batch after that is loaded meanwhile.
+    __shared__ float4 s_raw[2][4][kRasterBatch];  // pix (double2), ra, rb, rc
+    const int t = threadIdx.x;
+    auto issue = [&](int buf, int k) {
+        cp_async16(&s_raw[buf][0][t], pix + k);
+        cp_async16(&s_raw[buf][1][t], ra + k);
+        cp_async16(&s_raw[buf][2][t], rb + k);
+        cp_async16(&s_raw[buf][3][t], rc + k);
+    };
+    if (range.x + t < range.y) issue(0, vals[range.x + t]);
+    cp_async_commit();
+    int kn = range.x + kRasterBatch + t < range.y ? vals[range.x + kRasterBatch + t] : 0;
+    int it = 0;
+    for (int base = range.x; base < range.y; base += kRasterBatch, ++it) {
+        const int buf = it & 1;
         if (__syncthreads_count(done) == blockDim.x) break;
-        const int i = base + threadIdx.x;
+        cp_async_wait_all();
+        const int i = base + t;
         if (i < range.y) {
-            const int k = vals[i];
-            const double2 p = pix[k];
-            const float4 a = ra[k], b = rb[k], c = rc[k];
+            const double2 p = reinterpret_cast<const double2*>(s_raw[buf][0])[t];
+            const float4 a = s_raw[buf][1][t], b = s_raw[buf][2][t], c = s_raw[buf][3][t];
             const float qmax = reject_bound(b.y, cutoff);
             const float py = static_cast<float>(p.y - oy);
             // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level skip
@@ -285,6 +301,9 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             s_g2[threadIdx.x] = make_float2(b.w, c.x);
             s_yext[threadIdx.x] = make_float2(py - ey, py + ey);
         }
+        if (i + kRasterBatch < range.y) issue(buf ^ 1, kn);
+        cp_async_commit();
+        kn = i + 2 * kRasterBatch < range.y ? vals[i + 2 * kRasterBatch] : 0;
         __syncthreads();
         const int cnt = min(kRasterBatch, range.y - base);
         if (!done) {
@@ -310,6 +329,7 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             }
         }
     }
+    cp_async_wait_all();
     if (inside) {
         const size_t plane = static_cast<size_t>(W) * H;
         const size_t idx = static_cast<size_t>(y) * W + x;

@@ -23,6 +23,14 @@ struct SplatEval {
 // below the cutoff: q > 2 ln(sigma / cutoff) + margin. The margin absorbs the
 // rounding of logf/expf, so rejecting on it never changes a decision the full
 // evaluation would make (forward and backward stay bit-identical).
+// cp.async (LDGSTS): 16-byte global -> shared copies without register staging.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 __device__ __forceinline__ float reject_bound(float sigma, float cutoff) {
     return cutoff > 0.f ? 2.0f * logf(sigma / cutoff) + 1e-2f : __int_as_float(0x7f800000);
 }

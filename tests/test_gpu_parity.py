@@ -145,6 +145,23 @@ def test_loss_fields(gpu, seed):
     assert e_g < TOL_FIELD and e_h < TOL_FIELD
 
 
+@pytest.mark.parametrize("window,sigma,lam", [(7, 1.0, 0.2), (11, 1.5, 0.0), (11, 1.5, 1.0), (3, 0.8, 0.5)])
+def test_loss_fields_configs(gpu, window, sigma, lam):
+    """Non-default SSIM windows (generic kernel path), pure L2 and pure SSIM weights."""
+    scene, cam, target = check_fixture(1)
+    g, r = pair(gpu, scene)
+    out = []
+    for c in (g, r):
+        lc = c.L.default_loss()
+        lc.window, lc.window_sigma, lc.lambda_ = window, sigma, lam
+        out.append((c.build_view(0, cam, target, loss=lc), *c.view_loss_derivs(0)))
+    (lg, gg, hg), (lr, gr, hr) = out
+    e_g, e_h = qerr(gg, gr), qerr(hg, hr)
+    print(f"loss window {window} lambda {lam}: value {lg:.9g} vs {lr:.9g}; grad {e_g:.2e} hess {e_h:.2e}")
+    assert abs(lg - lr) <= 1e-5 * abs(lr)
+    assert e_g < TOL_FIELD and e_h < TOL_FIELD
+
+
 # ---------------------------------------------------------------------------
 # K8: accumulated terms, K9: solves
 # ---------------------------------------------------------------------------
