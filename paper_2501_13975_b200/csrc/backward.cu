@@ -35,244 +35,262 @@ inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 // derivatives, Jc (3x3) = dc~/dp per channel, Hc (3 x sym3) = d2c~/dp2.
 // projection_derivatives camera.hpp:124-148; cov2d_derivatives_wrt_position
 // camera.hpp:241-284; sh_color_derivs_wrt_position sh.hpp:134-161.
-template <int ND>
+// Two blocks per 128 Gaussians (blockIdx.y): 0 = pixel / Sigma derivatives
+// (JS, HPI, SCD), 1 = SH colour derivatives (JC, JJ, HC); halves the FP64 live
+// state per thread. Rows are staged in shared memory and stored coalesced.
+template <int ND, int PART>
 __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev cam, CameraDev primary,
                                                          const uint8_t* flags, float* out) {
     using L = PosLayout<ND>;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= s.n) return;
-    float* o = out + static_cast<size_t>(k) * L::N;
-    if (!(flags[k] & kProjected)) return;
-    const D3 p = load_pos(s, k);
-    double M[5][3], Hu[5][6];
-    // pi(p) through view_proj.
-    {
-        const double* VP = cam.view_proj;
-        const double hx = mrow(VP, 0, 0) * p.x + mrow(VP, 0, 1) * p.y + mrow(VP, 0, 2) * p.z + mrow(VP, 0, 3);
-        const double hy = mrow(VP, 1, 0) * p.x + mrow(VP, 1, 1) * p.y + mrow(VP, 1, 2) * p.z + mrow(VP, 1, 3);
-        const double hw = mrow(VP, 3, 0) * p.x + mrow(VP, 3, 1) * p.y + mrow(VP, 3, 2) * p.z + mrow(VP, 3, 3);
-        const double a[3] = {mrow(VP, 0, 0), mrow(VP, 0, 1), mrow(VP, 0, 2)};
-        const double b[3] = {mrow(VP, 1, 0), mrow(VP, 1, 1), mrow(VP, 1, 2)};
-        const double w[3] = {mrow(VP, 3, 0), mrow(VP, 3, 1), mrow(VP, 3, 2)};
-        const double i1 = 1.0 / hw, i2 = i1 * i1, i3 = i2 * i1;
-        const double sx = 0.5 * cam.width, sy = 0.5 * cam.height;
-        #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            M[0][j] = sx * (a[j] * i1 - hx * i2 * w[j]);
-            M[1][j] = sy * (b[j] * i1 - hy * i2 * w[j]);
-        }
-        #pragma unroll
-        for (int i = 0; i < 3; ++i)
-            #pragma unroll
-            for (int j = i; j < 3; ++j) {
-                Hu[0][sym3(i, j)] = sx * (-(a[i] * w[j] + w[i] * a[j]) * i2 + 2.0 * hx * w[i] * w[j] * i3);
-                Hu[1][sym3(i, j)] = sy * (-(b[i] * w[j] + w[i] * b[j]) * i2 + 2.0 * hy * w[i] * w[j] * i3);
-            }
-    }
-    // Sigma(p) through the EWA Jacobian (cov2d_derivatives_wrt_position,
-    // camera.hpp:241-284). With t = W p + t_w, the chain of dJ/dt_e and
-    // d2J/dt_e dt_f (camera.hpp:185-206) through W contracts to the 3-vectors
-    // a~ = W^T a, w~ = W^T w (a, b, w = rows 0, 1, 3 of proj):
-    //   dJ/dp_c   row0 = sx (-(w~_c a + a~_c w) / hw^2 + 2 hx w~_c w / hw^3)
-    //   d2J/dp_cd row0 = sx (2 ((w~_c a + a~_c w) w~_d + a~_d w~_c w) / hw^3 - 6 hx w~_c w~_d w / hw^4)
-    // (row1 with b, hy, sy), which avoids materialising the 3x3x2x3 tensors.
-    {
-        const D3 t = to_camera_space(cam, p);
-        const double* P = cam.proj;
-        const double a[3] = {mrow(P, 0, 0), mrow(P, 0, 1), mrow(P, 0, 2)};
-        const double bb[3] = {mrow(P, 1, 0), mrow(P, 1, 1), mrow(P, 1, 2)};
-        const double w[3] = {mrow(P, 3, 0), mrow(P, 3, 1), mrow(P, 3, 2)};
-        const double hx = a[0] * t.x + a[1] * t.y + a[2] * t.z + mrow(P, 0, 3);
-        const double hy = bb[0] * t.x + bb[1] * t.y + bb[2] * t.z + mrow(P, 1, 3);
-        const double hw = w[0] * t.x + w[1] * t.y + w[2] * t.z + mrow(P, 3, 3);
-        const double i1 = 1.0 / hw, i2 = i1 * i1, i3 = i2 * i1, i4 = i2 * i2;
-        const double sx = 0.5 * cam.width, sy = 0.5 * cam.height;
-        double J[6];
-        #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            J[j] = sx * (a[j] * i1 - hx * i2 * w[j]);
-            J[3 + j] = sy * (bb[j] * i1 - hy * i2 * w[j]);
-        }
-        double at[3], bt[3], wt[3];
-        #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            at[c] = a[0] * mrow(cam.view, 0, c) + a[1] * mrow(cam.view, 1, c) + a[2] * mrow(cam.view, 2, c);
-            bt[c] = bb[0] * mrow(cam.view, 0, c) + bb[1] * mrow(cam.view, 1, c) + bb[2] * mrow(cam.view, 2, c);
-            wt[c] = w[0] * mrow(cam.view, 0, c) + w[1] * mrow(cam.view, 1, c) + w[2] * mrow(cam.view, 2, c);
-        }
-        double A[9], m[9];
-        covariance_3d(s.quat[k], s.scale[k], A);
-        rotate_cov(cam, A, m);
-        // mjt = m J^T (3x2)
-        double mjt[6];
-        #pragma unroll
-        for (int i = 0; i < 3; ++i)
-            #pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
-                mjt[2 * i + jj] = m[3 * i] * J[3 * jj] + m[3 * i + 1] * J[3 * jj + 1] + m[3 * i + 2] * J[3 * jj + 2];
-        double dj[3][6];
-        #pragma unroll
-        for (int c = 0; c < 3; ++c)
-            #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                dj[c][j] = sx * (-(wt[c] * a[j] + at[c] * w[j]) * i2 + 2.0 * hx * wt[c] * i3 * w[j]);
-                dj[c][3 + j] = sy * (-(wt[c] * bb[j] + bt[c] * w[j]) * i2 + 2.0 * hy * wt[c] * i3 * w[j]);
-            }
-        auto mul23_32 = [](const double* a23, const double* b32, double out[4]) {
-            #pragma unroll
-            for (int i = 0; i < 2; ++i)
-                #pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    out[2 * i + j] = a23[3 * i] * b32[j] + a23[3 * i + 1] * b32[2 + j] + a23[3 * i + 2] * b32[4 + j];
-        };
-        #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double tm[4];
-            mul23_32(dj[c], mjt, tm);
-            M[2][c] = 2.0 * tm[0];
-            M[3][c] = tm[1] + tm[2];
-            M[4][c] = 2.0 * tm[3];
-        }
+    constexpr int RS = (L::JC > L::N - L::JC ? L::JC : L::N - L::JC) + 1;  // staged row stride (floats)
+    __shared__ float s_o[128 * RS];
+    constexpr int part = PART;
+    const int lo = part == 0 ? 0 : L::JC, hi = part == 0 ? L::JC : L::N;
+    const int k0 = blockIdx.x * 128, k = k0 + threadIdx.x;
+    float* o = s_o + threadIdx.x * RS;  // staged row: entries [lo, hi) at [0, hi - lo)
+    for (int i = 0; i < hi - lo; ++i) o[i] = 0.f;
+    if (k < s.n && (flags[k] & kProjected)) {
+        const D3 p = load_pos(s, k);
+        // Directional derivatives along D[a] (world axes, or the primary view's
+        // position subspace for kPassPositionUV): first order x . D[a], second order
+        // D[a]^T X D[b]. With the identity directions the values pass through exactly.
+        double D[ND][3];
+        if constexpr (ND == 3) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int d = c; d < 3; ++d) {
-                double d2j[6];
-                #pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    d2j[j] = sx * (2.0 * ((wt[c] * a[j] + at[c] * w[j]) * wt[d] + at[d] * wt[c] * w[j]) * i3 -
-                                   6.0 * hx * wt[c] * wt[d] * i4 * w[j]);
-                    d2j[3 + j] = sy * (2.0 * ((wt[c] * bb[j] + bt[c] * w[j]) * wt[d] + bt[d] * wt[c] * w[j]) * i3 -
-                                       6.0 * hy * wt[c] * wt[d] * i4 * w[j]);
-                }
-                double t1[4], t2[4], md[6];
-                mul23_32(d2j, mjt, t1);
-                #pragma unroll
-                for (int i = 0; i < 3; ++i)
-                    #pragma unroll
-                    for (int jj = 0; jj < 2; ++jj)
-                        md[2 * i + jj] = m[3 * i] * dj[d][3 * jj] + m[3 * i + 1] * dj[d][3 * jj + 1] + m[3 * i + 2] * dj[d][3 * jj + 2];
-                mul23_32(dj[c], md, t2);
-                Hu[2][sym3(c, d)] = 2.0 * t1[0] + 2.0 * t2[0];
-                Hu[3][sym3(c, d)] = t1[1] + t1[2] + t2[1] + t2[2];
-                Hu[4][sym3(c, d)] = 2.0 * t1[3] + 2.0 * t2[3];
-            }
-    }
-    // SH colour derivatives through r(p) (view_direction_derivatives camera.hpp:79-104).
-    D3 r;
-    double n;
-    double Jc[3][3] = {}, Hc[3][6] = {};
-    if (view_direction(cam, p, r, n)) {
-        const double rv[3] = {r.x, r.y, r.z};
-        double jac[3][3];
-        #pragma unroll
-        for (int i = 0; i < 3; ++i)
-            #pragma unroll
-            for (int j = 0; j < 3; ++j) jac[i][j] = ((i == j ? 1.0 : 0.0) - rv[i] * rv[j]) / n;
-        const double inv_n2 = 1.0 / (n * n);
-        double basis[16];
-        sh_basis(r, s.sh_degree, basis);
-        #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            double c[16];
-            double v = 0;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                c[i] = i < s.n_coeffs ? static_cast<double>(s.sh[(16 * ch + i) * s.n + k]) : 0.0;
-                v += basis[i] * c[i];
-            }
-            v += kColorOffset;
-            if (v <= 0.0) continue;  // clamped: zero subgradient (sh.hpp:144-147)
-            double gr[3], hr[6];
-            sh_contract_derivs(r, s.sh_degree, c, gr, hr);
-            #pragma unroll
-            for (int j = 0; j < 3; ++j) Jc[ch][j] = jac[0][j] * gr[0] + jac[1][j] * gr[1] + jac[2][j] * gr[2];
-            #pragma unroll
             for (int a = 0; a < 3; ++a)
-                #pragma unroll
-                for (int b = a; b < 3; ++b) {
-                    double acc = 0;
-                    #pragma unroll
-                    for (int i = 0; i < 3; ++i)
-                        #pragma unroll
-                        for (int j = 0; j < 3; ++j) acc += jac[i][a] * hr[sym3(i, j)] * jac[j][b];
-                    #pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        double hv = 3.0 * rv[i] * rv[a] * rv[b];
-                        if (i == a) hv -= rv[b];
-                        if (i == b) hv -= rv[a];
-                        if (a == b) hv -= rv[i];
-                        acc += gr[i] * hv * inv_n2;
-                    }
-                    Hc[ch][sym3(a, b)] = acc;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) D[a][c] = a == c ? 1.0 : 0.0;
+        } else {
+            D3 rp, ux, uy;
+            double np;
+            if (!view_direction(primary, p, rp, np)) rp = d3(0, 0, 1);  // as solve_position_k (error flagged there)
+            position_subspace(rp, ux, uy);
+            D[0][0] = ux.x, D[0][1] = ux.y, D[0][2] = ux.z;
+            D[1][0] = uy.x, D[1][1] = uy.y, D[1][2] = uy.z;
+        }
+        auto d1 = [&](const double* x, int st, int a) {  // sum_c x[c * st] D[a][c]
+            return x[0] * D[a][0] + x[st] * D[a][1] + x[2 * st] * D[a][2];
+        };
+        auto d2 = [&](const double* h, int st, int a, int b) {  // D[a]^T H D[b], H packed sym3 with stride st
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) acc += h[sym3(c, d) * st] * D[a][c] * D[b][d];
+            return acc;
+        };
+
+        if constexpr (PART == 0) {
+            // All derivatives are taken directly along the ND directions D[a]: the
+            // first-order formulas are linear and the second-order ones bilinear in
+            // the per-axis direction vectors, so contracting those vectors first
+            // (x_a = x . D[a]) gives the directional values without the 3-axis tensors.
+            auto dirv = [&](const double (&x)[3], double (&xa)[ND]) {
+#pragma unroll
+                for (int q = 0; q < ND; ++q) xa[q] = x[0] * D[q][0] + x[1] * D[q][1] + x[2] * D[q][2];
+            };
+            // pi(p) through view_proj (projection_derivatives camera.hpp:124-148).
+            {
+                const double* VP = cam.view_proj;
+                const double hx = mrow(VP, 0, 0) * p.x + mrow(VP, 0, 1) * p.y + mrow(VP, 0, 2) * p.z + mrow(VP, 0, 3);
+                const double hy = mrow(VP, 1, 0) * p.x + mrow(VP, 1, 1) * p.y + mrow(VP, 1, 2) * p.z + mrow(VP, 1, 3);
+                const double hw = mrow(VP, 3, 0) * p.x + mrow(VP, 3, 1) * p.y + mrow(VP, 3, 2) * p.z + mrow(VP, 3, 3);
+                double av[ND], bv[ND], wv[ND];
+                dirv({mrow(VP, 0, 0), mrow(VP, 0, 1), mrow(VP, 0, 2)}, av);
+                dirv({mrow(VP, 1, 0), mrow(VP, 1, 1), mrow(VP, 1, 2)}, bv);
+                dirv({mrow(VP, 3, 0), mrow(VP, 3, 1), mrow(VP, 3, 2)}, wv);
+                const double i1 = 1.0 / hw, i2 = i1 * i1, i3 = i2 * i1;
+                const double sx = 0.5 * cam.width, sy = 0.5 * cam.height;
+#pragma unroll
+                for (int q = 0; q < ND; ++q) {
+                    o[L::JS + 2 * q] = static_cast<float>(sx * (av[q] * i1 - hx * i2 * wv[q]));
+                    o[L::JS + 2 * q + 1] = static_cast<float>(sy * (bv[q] * i1 - hy * i2 * wv[q]));
                 }
+                int pp = 0;
+#pragma unroll
+                for (int q = 0; q < ND; ++q)
+#pragma unroll
+                    for (int r = q; r < ND; ++r, ++pp) {
+                        o[L::HPI + 2 * pp] = static_cast<float>(
+                            sx * (-(av[q] * wv[r] + wv[q] * av[r]) * i2 + 2.0 * hx * wv[q] * wv[r] * i3));
+                        o[L::HPI + 2 * pp + 1] = static_cast<float>(
+                            sy * (-(bv[q] * wv[r] + wv[q] * bv[r]) * i2 + 2.0 * hy * wv[q] * wv[r] * i3));
+                    }
+            }
+            // Sigma(p) through the EWA Jacobian (cov2d_derivatives_wrt_position,
+            // camera.hpp:241-284). With t = W p + t_w, the chain of dJ/dt_e and
+            // d2J/dt_e dt_f (camera.hpp:185-206) through W contracts to the 3-vectors
+            // a~ = W^T a, w~ = W^T w (a, b, w = rows 0, 1, 3 of proj), here along D:
+            //   dJ/dp_q   row0 = sx (-(w~_q a + a~_q w) / hw^2 + 2 hx w~_q w / hw^3)
+            //   d2J/dp_qr row0 = sx (2 ((w~_q a + a~_q w) w~_r + a~_r w~_q w) / hw^3 - 6 hx w~_q w~_r w / hw^4)
+            // (row1 with b, hy, sy), which avoids materialising the 3x3x2x3 tensors.
+            {
+                const D3 t = to_camera_space(cam, p);
+                const double* P = cam.proj;
+                const double a[3] = {mrow(P, 0, 0), mrow(P, 0, 1), mrow(P, 0, 2)};
+                const double bb[3] = {mrow(P, 1, 0), mrow(P, 1, 1), mrow(P, 1, 2)};
+                const double w[3] = {mrow(P, 3, 0), mrow(P, 3, 1), mrow(P, 3, 2)};
+                const double hx = a[0] * t.x + a[1] * t.y + a[2] * t.z + mrow(P, 0, 3);
+                const double hy = bb[0] * t.x + bb[1] * t.y + bb[2] * t.z + mrow(P, 1, 3);
+                const double hw = w[0] * t.x + w[1] * t.y + w[2] * t.z + mrow(P, 3, 3);
+                const double i1 = 1.0 / hw, i2 = i1 * i1, i3 = i2 * i1, i4 = i2 * i2;
+                const double sx = 0.5 * cam.width, sy = 0.5 * cam.height;
+                double J[6];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    J[j] = sx * (a[j] * i1 - hx * i2 * w[j]);
+                    J[3 + j] = sy * (bb[j] * i1 - hy * i2 * w[j]);
+                }
+                double at[ND], bt[ND], wt[ND];
+                {
+                    double a3[3], b3[3], w3[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        a3[c] = a[0] * mrow(cam.view, 0, c) + a[1] * mrow(cam.view, 1, c) + a[2] * mrow(cam.view, 2, c);
+                        b3[c] = bb[0] * mrow(cam.view, 0, c) + bb[1] * mrow(cam.view, 1, c) + bb[2] * mrow(cam.view, 2, c);
+                        w3[c] = w[0] * mrow(cam.view, 0, c) + w[1] * mrow(cam.view, 1, c) + w[2] * mrow(cam.view, 2, c);
+                    }
+                    dirv(a3, at);
+                    dirv(b3, bt);
+                    dirv(w3, wt);
+                }
+                double A[9], m[9];
+                covariance_3d(s.quat[k], s.scale[k], A);
+                rotate_cov(cam, A, m);
+                // mjt = m J^T (3x2)
+                double mjt[6];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj)
+                        mjt[2 * i + jj] = m[3 * i] * J[3 * jj] + m[3 * i + 1] * J[3 * jj + 1] + m[3 * i + 2] * J[3 * jj + 2];
+                double dj[ND][6];
+#pragma unroll
+                for (int q = 0; q < ND; ++q)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        dj[q][j] = sx * (-(wt[q] * a[j] + at[q] * w[j]) * i2 + 2.0 * hx * wt[q] * i3 * w[j]);
+                        dj[q][3 + j] = sy * (-(wt[q] * bb[j] + bt[q] * w[j]) * i2 + 2.0 * hy * wt[q] * i3 * w[j]);
+                    }
+                auto mul23_32 = [](const double* a23, const double* b32, double out4[4]) {
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            out4[2 * i + j] = a23[3 * i] * b32[j] + a23[3 * i + 1] * b32[2 + j] + a23[3 * i + 2] * b32[4 + j];
+                };
+#pragma unroll
+                for (int q = 0; q < ND; ++q) {
+                    double tm[4];
+                    mul23_32(dj[q], mjt, tm);
+                    o[L::JS + 2 * ND + 3 * q] = static_cast<float>(2.0 * tm[0]);
+                    o[L::JS + 2 * ND + 3 * q + 1] = static_cast<float>(tm[1] + tm[2]);
+                    o[L::JS + 2 * ND + 3 * q + 2] = static_cast<float>(2.0 * tm[3]);
+                }
+                int pp = 0;
+#pragma unroll
+                for (int q = 0; q < ND; ++q)
+#pragma unroll
+                    for (int r = q; r < ND; ++r, ++pp) {
+                        double d2j[6];
+#pragma unroll
+                        for (int j = 0; j < 3; ++j) {
+                            d2j[j] = sx * (2.0 * ((wt[q] * a[j] + at[q] * w[j]) * wt[r] + at[r] * wt[q] * w[j]) * i3 -
+                                           6.0 * hx * wt[q] * wt[r] * i4 * w[j]);
+                            d2j[3 + j] = sy * (2.0 * ((wt[q] * bb[j] + bt[q] * w[j]) * wt[r] + bt[r] * wt[q] * w[j]) * i3 -
+                                               6.0 * hy * wt[q] * wt[r] * i4 * w[j]);
+                        }
+                        double t1[4], t2[4], md[6];
+                        mul23_32(d2j, mjt, t1);
+#pragma unroll
+                        for (int i = 0; i < 3; ++i)
+#pragma unroll
+                            for (int jj = 0; jj < 2; ++jj)
+                                md[2 * i + jj] = m[3 * i] * dj[r][3 * jj] + m[3 * i + 1] * dj[r][3 * jj + 1] +
+                                                 m[3 * i + 2] * dj[r][3 * jj + 2];
+                        mul23_32(dj[q], md, t2);
+                        o[L::SCD + 3 * pp] = static_cast<float>(2.0 * t1[0] + 2.0 * t2[0]);
+                        o[L::SCD + 3 * pp + 1] = static_cast<float>(t1[1] + t1[2] + t2[1] + t2[2]);
+                        o[L::SCD + 3 * pp + 2] = static_cast<float>(2.0 * t1[3] + 2.0 * t2[3]);
+                    }
+            }
+        } else {
+            // SH colour derivatives through r(p) (view_direction_derivatives camera.hpp:79-104).
+            D3 r;
+            double n;
+            double Jc[3][3] = {}, Hc[3][6] = {};
+            if (view_direction(cam, p, r, n)) {
+                const double rv[3] = {r.x, r.y, r.z};
+                double jac[3][3];
+            #pragma unroll
+                for (int i = 0; i < 3; ++i)
+                #pragma unroll
+                    for (int j = 0; j < 3; ++j) jac[i][j] = ((i == j ? 1.0 : 0.0) - rv[i] * rv[j]) / n;
+                const double inv_n2 = 1.0 / (n * n);
+                double basis[16];
+                sh_basis(r, s.sh_degree, basis);
+            #pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    double c[16];
+                    double v = 0;
+    #pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        c[i] = i < s.n_coeffs ? static_cast<double>(s.sh[(16 * ch + i) * s.n + k]) : 0.0;
+                        v += basis[i] * c[i];
+                    }
+                    v += kColorOffset;
+                    if (v <= 0.0) continue;  // clamped: zero subgradient (sh.hpp:144-147)
+                    double gr[3], hr[6];
+                    sh_contract_derivs(r, s.sh_degree, c, gr, hr);
+                #pragma unroll
+                    for (int j = 0; j < 3; ++j) Jc[ch][j] = jac[0][j] * gr[0] + jac[1][j] * gr[1] + jac[2][j] * gr[2];
+                #pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                    #pragma unroll
+                        for (int b = a; b < 3; ++b) {
+                            double acc = 0;
+                        #pragma unroll
+                            for (int i = 0; i < 3; ++i)
+                            #pragma unroll
+                                for (int j = 0; j < 3; ++j) acc += jac[i][a] * hr[sym3(i, j)] * jac[j][b];
+                        #pragma unroll
+                            for (int i = 0; i < 3; ++i) {
+                                double hv = 3.0 * rv[i] * rv[a] * rv[b];
+                                if (i == a) hv -= rv[b];
+                                if (i == b) hv -= rv[a];
+                                if (a == b) hv -= rv[i];
+                                acc += gr[i] * hv * inv_n2;
+                            }
+                            Hc[ch][sym3(a, b)] = acc;
+                        }
+                }
+            }
+    #pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                double jd[ND];
+    #pragma unroll
+                for (int a = 0; a < ND; ++a) {
+                    jd[a] = d1(Jc[ch], 1, a);
+                    o[4 * ch + a] = static_cast<float>(jd[a]);
+                }
+                int p = 0;
+    #pragma unroll
+                for (int a = 0; a < ND; ++a)
+    #pragma unroll
+                    for (int b = a; b < ND; ++b, ++p) {
+                        o[L::JJ - L::JC + L::NP * ch + p] = static_cast<float>(jd[a] * jd[b]);
+                        o[L::HC - L::JC + L::NP * ch + p] = static_cast<float>(d2(Hc[ch], 1, a, b));
+                    }
+            }
+
         }
     }
-    // Directional derivatives along D[a] (world axes, or the primary view's
-    // position subspace for kPassPositionUV): first order x . D[a], second order
-    // D[a]^T X D[b]. With the identity directions the values pass through exactly.
-    double D[ND][3];
-    if constexpr (ND == 3) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) D[a][c] = a == c ? 1.0 : 0.0;
-    } else {
-        D3 rp, ux, uy;
-        double np;
-        if (!view_direction(primary, p, rp, np)) rp = d3(0, 0, 1);  // as solve_position_k (error flagged there)
-        position_subspace(rp, ux, uy);
-        D[0][0] = ux.x, D[0][1] = ux.y, D[0][2] = ux.z;
-        D[1][0] = uy.x, D[1][1] = uy.y, D[1][2] = uy.z;
-    }
-    auto d1 = [&](const double* x, int st, int a) {  // sum_c x[c * st] D[a][c]
-        return x[0] * D[a][0] + x[st] * D[a][1] + x[2 * st] * D[a][2];
-    };
-    auto d2 = [&](const double* h, int st, int a, int b) {  // D[a]^T H D[b], H packed sym3 with stride st
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) acc += h[sym3(c, d) * st] * D[a][c] * D[b][d];
-        return acc;
-    };
-#pragma unroll
-    for (int i = 0; i < L::N; ++i) o[i] = 0.f;
-#pragma unroll
-    for (int a = 0; a < ND; ++a) {
-        o[L::JS + 2 * a] = static_cast<float>(d1(M[0], 1, a));
-        o[L::JS + 2 * a + 1] = static_cast<float>(d1(M[1], 1, a));
-#pragma unroll
-        for (int u = 0; u < 3; ++u) o[L::JS + 2 * ND + 3 * a + u] = static_cast<float>(d1(M[2 + u], 1, a));
-    }
-    {
-        int p = 0;
-#pragma unroll
-        for (int a = 0; a < ND; ++a)
-#pragma unroll
-            for (int b = a; b < ND; ++b, ++p) {
-                o[L::HPI + 2 * p] = static_cast<float>(d2(Hu[0], 1, a, b));
-                o[L::HPI + 2 * p + 1] = static_cast<float>(d2(Hu[1], 1, a, b));
-#pragma unroll
-                for (int u = 0; u < 3; ++u) o[L::SCD + 3 * p + u] = static_cast<float>(d2(Hu[2 + u], 1, a, b));
-            }
-    }
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        double jd[ND];
-#pragma unroll
-        for (int a = 0; a < ND; ++a) {
-            jd[a] = d1(Jc[ch], 1, a);
-            o[L::JC + 4 * ch + a] = static_cast<float>(jd[a]);
-        }
-        int p = 0;
-#pragma unroll
-        for (int a = 0; a < ND; ++a)
-#pragma unroll
-            for (int b = a; b < ND; ++b, ++p) {
-                o[L::JJ + L::NP * ch + p] = static_cast<float>(jd[a] * jd[b]);
-                o[L::HC + L::NP * ch + p] = static_cast<float>(d2(Hc[ch], 1, a, b));
-            }
+    __syncthreads();
+    const int w = hi - lo;
+    const int rows = min(128, s.n - k0);
+    for (int i = threadIdx.x; i < rows * w; i += 128) {
+        const int r = i / w, c = i - r * w;
+        out[static_cast<size_t>(k0 + r) * L::N + lo + c] = s_o[r * RS + c];
     }
 }
 
@@ -870,11 +888,13 @@ void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const Cam
     switch (pass) {
         case kPassPosition:
             v.consts.ensure(static_cast<size_t>(n) * kPosConsts);
-            position_consts_k<3><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            position_consts_k<3, 0><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            position_consts_k<3, 1><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
             break;
         case kPassPositionUV:
             v.consts.ensure(static_cast<size_t>(n) * kPosUVConsts);
-            position_consts_k<2><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            position_consts_k<2, 0><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            position_consts_k<2, 1><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
             break;
         case kPassRotation:
             v.consts.ensure(static_cast<size_t>(n) * kRotConsts);

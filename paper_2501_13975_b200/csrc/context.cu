@@ -743,7 +743,8 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
         cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
         compute_pass_consts(pass, ctx->scene, v, views[0]->cam, s);
         double* acc = ctx->acc.ptr + (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0);
-        launch_backward(pass, ctx->scene, v, acc, stride, visible, ctx->pairs.ptr + pass, s);
+        unsigned long long* contrib = ctx->pairs.ptr + (pass == kPassPositionUV ? kPassPosition : pass);
+        launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s);
     }
     if (concurrent) ctx->join(nv);
     if (ctx->comm) {
