@@ -222,18 +222,18 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
             if (view_direction(cam, p, r, n)) {
                 const double rv[3] = {r.x, r.y, r.z};
                 double jac[3][3];
-            #pragma unroll
+        #pragma unroll
                 for (int i = 0; i < 3; ++i)
-                #pragma unroll
+            #pragma unroll
                     for (int j = 0; j < 3; ++j) jac[i][j] = ((i == j ? 1.0 : 0.0) - rv[i] * rv[j]) / n;
                 const double inv_n2 = 1.0 / (n * n);
                 double basis[16];
                 sh_basis(r, s.sh_degree, basis);
-            #pragma unroll
+        #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
                     double c[16];
                     double v = 0;
-    #pragma unroll
+#pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         c[i] = i < s.n_coeffs ? static_cast<double>(s.sh[(16 * ch + i) * s.n + k]) : 0.0;
                         v += basis[i] * c[i];
@@ -242,18 +242,18 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                     if (v <= 0.0) continue;  // clamped: zero subgradient (sh.hpp:144-147)
                     double gr[3], hr[6];
                     sh_contract_derivs(r, s.sh_degree, c, gr, hr);
-                #pragma unroll
+            #pragma unroll
                     for (int j = 0; j < 3; ++j) Jc[ch][j] = jac[0][j] * gr[0] + jac[1][j] * gr[1] + jac[2][j] * gr[2];
-                #pragma unroll
+            #pragma unroll
                     for (int a = 0; a < 3; ++a)
-                    #pragma unroll
+                #pragma unroll
                         for (int b = a; b < 3; ++b) {
                             double acc = 0;
-                        #pragma unroll
+                    #pragma unroll
                             for (int i = 0; i < 3; ++i)
-                            #pragma unroll
-                                for (int j = 0; j < 3; ++j) acc += jac[i][a] * hr[sym3(i, j)] * jac[j][b];
                         #pragma unroll
+                                for (int j = 0; j < 3; ++j) acc += jac[i][a] * hr[sym3(i, j)] * jac[j][b];
+                    #pragma unroll
                             for (int i = 0; i < 3; ++i) {
                                 double hv = 3.0 * rv[i] * rv[a] * rv[b];
                                 if (i == a) hv -= rv[b];
@@ -265,18 +265,18 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                         }
                 }
             }
-    #pragma unroll
+#pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
                 double jd[ND];
-    #pragma unroll
+#pragma unroll
                 for (int a = 0; a < ND; ++a) {
                     jd[a] = d1(Jc[ch], 1, a);
                     o[4 * ch + a] = static_cast<float>(jd[a]);
                 }
                 int p = 0;
-    #pragma unroll
+#pragma unroll
                 for (int a = 0; a < ND; ++a)
-    #pragma unroll
+#pragma unroll
                     for (int b = a; b < ND; ++b, ++p) {
                         o[L::JJ - L::JC + L::NP * ch + p] = static_cast<float>(jd[a] * jd[b]);
                         o[L::HC - L::JC + L::NP * ch + p] = static_cast<float>(d2(Hc[ch], 1, a, b));
@@ -396,11 +396,11 @@ struct PassTraits<kPassPositionUV> {
 };
 template <>
 struct PassTraits<kPassRotation> {
-    static constexpr int NC = kRotConsts, NA = 2, BATCH = 64;
+    static constexpr int NC = kRotConsts, NA = 2, BATCH = 128;
 };
 template <>
 struct PassTraits<kPassScaling> {
-    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 64;
+    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 128;
 };
 template <>
 struct PassTraits<kPassOpacityColor> {
@@ -600,13 +600,13 @@ template <int PASS, int TILE>
 struct BackwardSmem {
     using TR = PassTraits<PASS>;
     static constexpr int NT = TILE * TILE, NW = NT / 32;
-    static constexpr int B = TR::BATCH, NA = TR::NA, NC4 = TR::NC / 4;
+    static constexpr int B = TR::BATCH < NT ? TR::BATCH : NT, NA = TR::NA, NC4 = TR::NC / 4;
     static constexpr int CST = (NC4 % 8 == 0 && NC4 > 0) ? NC4 + 1 : NC4;  // float4 stride, avoids bank conflicts
     float4 raw[2][4][B];                   // staged records (pix as double2, ra, rb, rc), double-buffered
     float4 cst[2][(CST > 0 ? CST : 1) * B];  // staged per-view constants, double-buffered
     float4 g0[B], g1[B];                   // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
     float2 g2[B];                          // (c1, c2)
-    float2 yext[B];                        // splat y-extent of the cutoff ellipse (tile coordinates)
+    unsigned char wmask[B];                // bit w: the splat's cutoff ellipse reaches warp w's pixel rows
     float acc[NW][NA][B];                  // per-warp sums: segment tails are unique within a drain
     int kid[2][B];
     int vis[B];
@@ -620,14 +620,13 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
     using TR = PassTraits<PASS>;
     using SM = BackwardSmem<PASS, TILE>;
     constexpr int NT = TILE * TILE, NW = NT / 32, kRowsPerWarp = 32 / TILE;
-    constexpr int B = TR::BATCH, NA = TR::NA, NC4 = SM::NC4, CST = SM::CST;
-    static_assert(B <= NT, "one loader thread per splat of a batch");
+    constexpr int B = SM::B, NA = TR::NA, NC4 = SM::NC4, CST = SM::CST;
+    static_assert(B <= NT && B % 32 == 0, "one loader thread per splat of a batch");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& S = *reinterpret_cast<SM*>(smem_raw);
     auto& s_g0 = S.g0;
     auto& s_g1 = S.g1;
     auto& s_g2 = S.g2;
-    auto& s_yext = S.yext;
     auto& s_acc = S.acc;
     auto& s_vis = S.vis;
     auto& s_gl = S.gl;
@@ -647,16 +646,17 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
     const size_t plane = static_cast<size_t>(a.W) * a.H;
     const size_t pidx = static_cast<size_t>(y) * a.W + x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float wy0 = kRowsPerWarp * warp + 0.5f, wy1 = wy0 + (kRowsPerWarp - 1);  // the warp's pixel-centre rows
     WarpQueue& Q = s_q[warp];
 
     int last = -1;
-    double Cf[3] = {0, 0, 0};
+    float Cf_hi[3] = {0.f, 0.f, 0.f}, Cf_lo[3] = {0.f, 0.f, 0.f};  // final colour as an unevaluated float pair
     if (inside) {
         last = a.last[pidx];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            Cf[c] = a.image[c * plane + pidx];
+            const double cf = a.image[c * plane + pidx];
+            Cf_hi[c] = static_cast<float>(cf);
+            Cf_lo[c] = static_cast<float>(cf - static_cast<double>(Cf_hi[c]));
             s_gl[threadIdx.x][c] = a.loss_grad[c * plane + pidx];
             s_hl[threadIdx.x][c] = a.loss_hess[c * plane + pidx];
         }
@@ -672,6 +672,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
     if (last >= 0) atomicMax(&s_maxlast, last);
     __syncthreads();
     const int end = min(range.y, s_maxlast + 1);
+    const int wlast = __reduce_max_sync(0xffffffffu, last);  // the warp's last contributing list entry
 
     float T = 1.0f, P[3] = {0.f, 0.f, 0.f};
     int qhead = 0, qcount = 0;  // warp-uniform ring state
@@ -786,7 +787,15 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 s_g0[tid] = make_float4(static_cast<float>(p.x - ox), py, ra.z, ra.w);
                 s_g1[tid] = make_float4(rb.x, rb.y, qmax, rb.z);
                 s_g2[tid] = make_float2(rb.w, rc.x);
-                s_yext[tid] = make_float2(py - ey, py + ey);
+                unsigned m = 0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {  // warp w owns pixel-centre rows [kRowsPerWarp w + 0.5, + kRowsPerWarp - 1]
+                    const float r0 = kRowsPerWarp * w + 0.5f, r1 = r0 + (kRowsPerWarp - 1);
+                    if (!(py + ey < r0 || py - ey > r1)) m |= 1u << w;
+                }
+                S.wmask[tid] = static_cast<unsigned char>(m);
+            } else {
+                S.wmask[tid] = 0;
             }
             s_vis[tid] = 0;
             S.kid[buf ^ 1][tid] = kid_next;
@@ -797,64 +806,70 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
         __syncthreads();
         if (base + B < end) issue(buf ^ 1, base + B);
         cp_async_commit();
-        // Phase 1
-        for (int j = 0; j < cnt; ++j) {
-            const float2 ye = s_yext[j];
-            if (ye.y < wy0 || ye.x > wy1) continue;  // warp-uniform: no pixel of this warp can pass
-            bool contrib = false;
-            float G = 0.f, q0 = 0.f, q1 = 0.f, Tr = 0.f, wa = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f;
-            if (base + j <= last) {
-                const float4 g0 = s_g0[j], g1 = s_g1[j];
-                SplatEval ev;
-                if (eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, ev) && !(ev.alpha < a.cutoff)) {
-                    contrib = true;
-                    const float2 g2 = s_g2[j];
-                    const float col[3] = {g1.w, g2.x, g2.y};
-                    const float Ti = T;
-                    const float w = blend_weight(Ti, ev.alpha);
-                    const float Tn = next_transmittance(Ti, ev.alpha);
-                    const bool is_last = (base + j == last);
-                    const float inv_tn = __frcp_rn(Tn);
-                    float ac[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
+        // Phase 1: only the splats whose cutoff ellipse reaches this warp's rows
+        // (per-warp bit masks, increasing j), up to the warp's last contributor.
+#pragma unroll 1
+        for (int c32 = 0; c32 < cnt; c32 += 32) {
+            unsigned m = __ballot_sync(0xffffffffu, ((S.wmask[c32 + lane] >> warp) & 1u) && base + c32 + lane <= wlast);
+            while (m) {
+                const int j = c32 + __ffs(m) - 1;
+                m &= m - 1;
+                bool contrib = false;
+                float G = 0.f, q0 = 0.f, q1 = 0.f, Tr = 0.f, wa = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f;
+                if (base + j <= last) {
+                    const float4 g0 = s_g0[j], g1 = s_g1[j];
+                    SplatEval ev;
+                    if (eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, ev) && !(ev.alpha < a.cutoff)) {
+                        contrib = true;
+                        const float2 g2 = s_g2[j];
+                        const float col[3] = {g1.w, g2.x, g2.y};
+                        const float Ti = T;
+                        const float w = blend_weight(Ti, ev.alpha);
+                        const float Tn = next_transmittance(Ti, ev.alpha);
+                        const bool is_last = (base + j == last);
+                        float inv_tn;  // behind is a derived quantity (not re-composited): approximate 1/T is enough
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_tn) : "f"(Tn));
+                        float ac[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float Pn = __fmaf_rn(w, col[c], P[c]);
-                        const float behind =
-                            is_last ? a.bg[c] : static_cast<float>(Cf[c] - static_cast<double>(Pn)) * inv_tn;
-                        ac[c] = col[c] - behind;
-                        P[c] = Pn;
+                        for (int c = 0; c < 3; ++c) {
+                            const float Pn = __fmaf_rn(w, col[c], P[c]);
+                            const float behind =
+                                is_last ? a.bg[c] : ((Cf_hi[c] - Pn) + Cf_lo[c]) * inv_tn;
+                            ac[c] = col[c] - behind;
+                            P[c] = Pn;
+                        }
+                        T = Tn;
+                        G = ev.g;
+                        q0 = ev.qd0;
+                        q1 = ev.qd1;
+                        Tr = Ti;
+                        wa = g1.y * Ti;
+                        ac0 = ac[0];
+                        ac1 = ac[1];
+                        ac2 = ac[2];
                     }
-                    T = Tn;
-                    G = ev.g;
-                    q0 = ev.qd0;
-                    q1 = ev.qd1;
-                    Tr = Ti;
-                    wa = g1.y * Ti;
-                    ac0 = ac[0];
-                    ac1 = ac[1];
-                    ac2 = ac[2];
                 }
-            }
-            const unsigned ballot = __ballot_sync(0xffffffffu, contrib);
-            if (ballot) {
-                if (contrib) {
-                    const int slot = (qhead + qcount + __popc(ballot & ((1u << lane) - 1u))) & (kQ - 1);
-                    Q.G[slot] = G;
-                    Q.q0[slot] = q0;
-                    Q.q1[slot] = q1;
-                    Q.Ti[slot] = Tr;
-                    Q.wa[slot] = wa;
-                    Q.a0[slot] = ac0;
-                    Q.a1[slot] = ac1;
-                    Q.a2[slot] = ac2;
-                    Q.j[slot] = static_cast<unsigned char>(j);
-                    Q.pix[slot] = static_cast<unsigned char>(lane);
-                }
-                qcount += __popc(ballot);
-                __syncwarp();
-                if (qcount >= 32) {
-                    drain(32);
+                const unsigned ballot = __ballot_sync(0xffffffffu, contrib);
+                if (ballot) {
+                    if (contrib) {
+                        const int slot = (qhead + qcount + __popc(ballot & ((1u << lane) - 1u))) & (kQ - 1);
+                        Q.G[slot] = G;
+                        Q.q0[slot] = q0;
+                        Q.q1[slot] = q1;
+                        Q.Ti[slot] = Tr;
+                        Q.wa[slot] = wa;
+                        Q.a0[slot] = ac0;
+                        Q.a1[slot] = ac1;
+                        Q.a2[slot] = ac2;
+                        Q.j[slot] = static_cast<unsigned char>(j);
+                        Q.pix[slot] = static_cast<unsigned char>(lane);
+                    }
+                    qcount += __popc(ballot);
                     __syncwarp();
+                    if (qcount >= 32) {
+                        drain(32);
+                        __syncwarp();
+                    }
                 }
             }
         }
