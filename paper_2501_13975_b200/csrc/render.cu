@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
     constexpr int kRowsPerWarp = 32 / TILE;
     __shared__ float4 s_g0[kRasterBatch], s_g1[kRasterBatch];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
     __shared__ float2 s_g2[kRasterBatch];                      // (c1, c2)
-    __shared__ float2 s_yext[kRasterBatch];                    // cutoff-ellipse y-extent (tile coordinates)
+    __shared__ unsigned char s_wmask[kRasterBatch];            // bit w: the cutoff ellipse reaches warp w's rows
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
@@ -299,18 +299,30 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             s_g0[threadIdx.x] = make_float4(static_cast<float>(p.x - ox), py, a.z, a.w);
             s_g1[threadIdx.x] = make_float4(b.x, b.y, qmax, b.z);
             s_g2[threadIdx.x] = make_float2(b.w, c.x);
-            s_yext[threadIdx.x] = make_float2(py - ey, py + ey);
+            unsigned m = 0;
+#pragma unroll
+            for (int w = 0; w < kRasterBatch / 32; ++w) {  // warp w owns rows [kRowsPerWarp w + 0.5, + kRowsPerWarp - 1]
+                const float r0 = kRowsPerWarp * w + 0.5f, r1 = r0 + (kRowsPerWarp - 1);
+                if (!(py + ey < r0 || py - ey > r1)) m |= 1u << w;
+            }
+            s_wmask[threadIdx.x] = static_cast<unsigned char>(m);
+        } else {
+            s_wmask[threadIdx.x] = 0;
         }
         if (i + kRasterBatch < range.y) issue(buf ^ 1, kn);
         cp_async_commit();
         kn = i + 2 * kRasterBatch < range.y ? vals[i + 2 * kRasterBatch] : 0;
         __syncthreads();
         const int cnt = min(kRasterBatch, range.y - base);
-        if (!done) {
-            const float wy0 = kRowsPerWarp * (threadIdx.x >> 5) + 0.5f, wy1 = wy0 + (kRowsPerWarp - 1);  // warp rows
-            for (int j = 0; j < cnt; ++j) {
-                const float2 ye = s_yext[j];
-                if (ye.y < wy0 || ye.x > wy1) continue;
+        // Only the splats whose cutoff ellipse reaches this warp's rows (per-warp bit
+        // masks, increasing j); lanes that terminated skip the body.
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int c32 = 0; c32 < cnt && !__all_sync(0xffffffffu, done); c32 += 32) {
+            unsigned m = __ballot_sync(0xffffffffu, (s_wmask[c32 + lane] >> warp) & 1u);
+            while (m) {
+                const int j = c32 + __ffs(m) - 1;
+                m &= m - 1;
+                if (done) continue;
                 const float4 g0 = s_g0[j], g1 = s_g1[j];
                 SplatEval e;
                 if (!eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, e)) continue;
@@ -322,10 +334,7 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
                 C2 = __fma_rn(w, g2.y, C2);
                 T = next_transmittance(T, e.alpha);
                 last = base + j;
-                if (tmin > 0.f && T < tmin) {
-                    done = true;
-                    break;
-                }
+                if (tmin > 0.f && T < tmin) done = true;
             }
         }
     }

@@ -4,9 +4,9 @@
 // build_splat_list (rasterizer.hpp:228-263). Item counts are read from device
 // memory, so the binning never synchronises with the host.
 //
-// Each 8-bit pass is three kernels: per-block digit histograms, a per-digit
-// scan over blocks, and a stable scatter (items ranked in index order inside a
-// block with warp match_any + cross-warp prefix counts). 2048 items per block.
+// One global histogram kernel for all passes, then one onesweep kernel per
+// 8-bit pass (stable in-tile ranks + decoupled look-back across tiles).
+// 2048 items per block.
 #include "sort.h"
 
 namespace ngsb {
@@ -18,109 +18,168 @@ constexpr int kItems = 8;
 constexpr int kTileItems = kThreads * kItems;  // 2048
 constexpr int kDigits = 256;
 
-__global__ void __launch_bounds__(kThreads) radix_hist_k(const uint32_t* __restrict__ keys, const int* __restrict__ d_n,
-                                                         int shift, int nblocks, int* __restrict__ counts) {
-    __shared__ int s_hist[kDigits];
+// ---------------------------------------------------------------------------
+// Onesweep-style LSD radix sort: one global histogram kernel for all passes,
+// then ONE kernel per 8-bit pass. Each block takes a 2048-item tile in ticket
+// order, ranks its items stably (warp-contiguous ranges, match_any per round),
+// obtains the exclusive prefix of every digit over earlier tiles by decoupled
+// look-back on per-(tile, digit) status words, and writes through shared memory
+// so that runs of equal digits are stored contiguously.
+// ---------------------------------------------------------------------------
+
+constexpr int kMaxPasses = 4;
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1;
+
+__global__ void __launch_bounds__(kThreads) radix_global_hist_k(const uint32_t* __restrict__ keys,
+                                                                const int* __restrict__ d_n, int passes,
+                                                                unsigned* __restrict__ hist) {
+    __shared__ unsigned s_hist[kMaxPasses][kDigits];
     const int n = *d_n;
-    s_hist[threadIdx.x] = 0;
+    for (int p = 0; p < passes; ++p) s_hist[p][threadIdx.x] = 0;
     __syncthreads();
     const int base = blockIdx.x * kTileItems;
+    if (base < n) {
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int i = base + r * kThreads + threadIdx.x;
-        if (i < n) atomicAdd(&s_hist[(keys[i] >> shift) & 0xFF], 1);
-    }
-    __syncthreads();
-    counts[threadIdx.x * nblocks + blockIdx.x] = s_hist[threadIdx.x];
-}
-
-// One block per digit: exclusive scan of counts[digit][0..nblocks) in place;
-// the digit total goes to totals[digit].
-__global__ void __launch_bounds__(kThreads) radix_scan_digit_k(int* __restrict__ counts, int nblocks,
-                                                               int* __restrict__ totals) {
-    __shared__ int s_warp[kThreads / 32];
-    __shared__ int s_carry;
-    int* row = counts + blockIdx.x * nblocks;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int start = 0; start < nblocks; start += kThreads) {
-        const int i = start + threadIdx.x;
-        const int v = i < nblocks ? row[i] : 0;
-        int x = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += t;
+        for (int r = 0; r < kItems; ++r) {
+            const int i = base + r * kThreads + threadIdx.x;
+            if (i < n) {
+                const uint32_t k = keys[i];
+                for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xFF], 1u);
+            }
         }
-        if (lane == 31) s_warp[warp] = x;
-        __syncthreads();
-        int wbase = 0;
-        for (int w = 0; w < warp; ++w) wbase += s_warp[w];
-        const int carry = s_carry;
-        if (i < nblocks) row[i] = carry + wbase + x - v;
-        __syncthreads();
-        if (threadIdx.x == kThreads - 1) s_carry = carry + wbase + x;
-        __syncthreads();
     }
-    if (threadIdx.x == 0) totals[blockIdx.x] = s_carry;
+    __syncthreads();
+    for (int p = 0; p < passes; ++p) {
+        const unsigned v = s_hist[p][threadIdx.x];
+        if (v) atomicAdd(&hist[p * kDigits + threadIdx.x], v);
+    }
 }
 
-__global__ void __launch_bounds__(kThreads) radix_scatter_k(const uint32_t* __restrict__ keys_in,
-                                                            const int* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-                                                            int* __restrict__ vals_out, const int* __restrict__ d_n,
-                                                            int shift, int nblocks, const int* __restrict__ counts,
-                                                            const int* __restrict__ totals) {
-    __shared__ int s_base[kDigits];               // running output position per digit
-    __shared__ int s_wcount[kThreads / 32][kDigits];
+// Block-wide exclusive scan of one value per thread (256 threads); returns the total in *total.
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* s_warp, unsigned* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += t;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    unsigned wbase = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        const unsigned sw = s_warp[w];
+        if (w < warp) wbase += sw;
+        tot += sw;
+    }
+    if (total) *total = tot;
+    __syncthreads();
+    return wbase + x - v;
+}
+
+// Exclusive digit starts per pass: dstart[p][d] = sum of hist[p][d' < d].
+__global__ void __launch_bounds__(kThreads) radix_digit_starts_k(const unsigned* __restrict__ hist, int passes,
+                                                                 unsigned* __restrict__ dstart) {
+    __shared__ unsigned s_warp[kThreads / 32];
+    for (int p = 0; p < passes; ++p)
+        dstart[p * kDigits + threadIdx.x] = block_exclusive_scan(hist[p * kDigits + threadIdx.x], s_warp, nullptr);
+}
+
+__global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __restrict__ keys_in,
+                                                             const int* __restrict__ vals_in,
+                                                             uint32_t* __restrict__ keys_out, int* __restrict__ vals_out,
+                                                             const int* __restrict__ d_n, int shift,
+                                                             const unsigned* __restrict__ dstart,
+                                                             unsigned* __restrict__ status, unsigned* __restrict__ ticket) {
+    __shared__ unsigned s_wc[kThreads / 32][kDigits];  // per-warp digit counts -> per-warp exclusive prefix
+    __shared__ unsigned s_bstart[kDigits];             // block-local digit starts
+    __shared__ unsigned s_gbase[kDigits];              // global position of the block's first item of each digit
+    __shared__ uint32_t s_k[kTileItems];
+    __shared__ int s_v[kTileItems];
+    __shared__ unsigned s_warp[kThreads / 32];
+    __shared__ int s_tile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(ticket, 1u));  // in-order tile ids for the look-back
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) s_wc[w][threadIdx.x] = 0;
+    __syncthreads();
+    const int tile = s_tile;
     const int n = *d_n;
-    const int base = blockIdx.x * kTileItems;
+    const int base = tile * kTileItems;
     if (base >= n) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    {
-        // digit start = sum of totals of smaller digits + this block's scanned offset
-        __shared__ int s_tot[kDigits];
-        s_tot[threadIdx.x] = totals[threadIdx.x];
-        __syncthreads();
-        int acc = 0;
-        for (int d = 0; d < static_cast<int>(threadIdx.x); ++d) acc += s_tot[d];
-        s_base[threadIdx.x] = acc + counts[threadIdx.x * nblocks + blockIdx.x];
-    }
-    for (int w = 0; w < kThreads / 32; ++w) s_wcount[w][threadIdx.x] = 0;
-    __syncthreads();
-#pragma unroll 1
-    for (int r = 0; r < kItems; ++r) {
-        const int i = base + r * kThreads + threadIdx.x;
-        const bool valid = i < n;
-        uint32_t key = 0;
-        int val = 0, digit = -1;
-        if (valid) {
-            key = keys_in[i];
-            val = vals_in[i];
-            digit = static_cast<int>((key >> shift) & 0xFF);
-        }
-        const unsigned active = __ballot_sync(0xffffffffu, valid);
-        const unsigned peers = __match_any_sync(0xffffffffu, digit) & active;
-        const int wrank = __popc(peers & ((1u << lane) - 1u));
-        const bool leader = valid && wrank == 0;
-        if (leader) s_wcount[warp][digit] = __popc(peers);
-        __syncthreads();
-        if (valid) {
-            int pos = s_base[digit] + wrank;
-            for (int w = 0; w < warp; ++w) pos += s_wcount[w][digit];
-            keys_out[pos] = key;
-            vals_out[pos] = val;
-        }
-        __syncthreads();
-        // advance the per-digit bases by this round's counts and clear them
-        int add = 0;
+
+    // 1. Stable ranks inside each warp's contiguous 256-item range.
+    uint32_t key[kItems];
+    int val[kItems];
+    unsigned wrank[kItems];
 #pragma unroll
-        for (int w = 0; w < kThreads / 32; ++w) {
-            add += s_wcount[w][threadIdx.x];
-            s_wcount[w][threadIdx.x] = 0;
+    for (int r = 0; r < kItems; ++r) {
+        const int i = base + warp * (kItems * 32) + r * 32 + lane;
+        const bool valid = i < n;
+        key[r] = valid ? keys_in[i] : 0u;
+        val[r] = valid ? vals_in[i] : 0;
+        const int digit = valid ? static_cast<int>((key[r] >> shift) & 0xFF) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        const unsigned before = __popc(peers & ((1u << lane) - 1u));
+        unsigned old = 0;
+        if (valid) old = s_wc[warp][digit];
+        __syncwarp();
+        if (valid && before == 0) s_wc[warp][digit] = old + __popc(peers);
+        __syncwarp();
+        wrank[r] = old + before;
+    }
+    __syncthreads();
+    // 2. Per digit (thread d): exclusive prefix over warps, block count, block-local start.
+    const int d = threadIdx.x;
+    unsigned bc = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        const unsigned c = s_wc[w][d];
+        s_wc[w][d] = bc;
+        bc += c;
+    }
+    // 3. Decoupled look-back for digit d over earlier tiles.
+    unsigned* st = status + static_cast<size_t>(tile) * kDigits + d;
+    unsigned excl = 0;
+    if (tile == 0) {
+        atomicExch(st, kFlagInc | bc);
+    } else {
+        atomicExch(st, kFlagAgg | bc);
+        for (int t = tile - 1; t >= 0; --t) {
+            const volatile unsigned* sp = status + static_cast<size_t>(t) * kDigits + d;
+            unsigned v;
+            do {
+                v = *sp;
+            } while ((v & ~kCountMask) == 0);
+            excl += v & kCountMask;
+            if ((v & ~kCountMask) == kFlagInc) break;
         }
-        s_base[threadIdx.x] += add;
-        __syncthreads();
+        atomicExch(st, kFlagInc | (excl + bc));
+    }
+    const unsigned bstart = block_exclusive_scan(bc, s_warp, nullptr);
+    s_bstart[d] = bstart;
+    s_gbase[d] = dstart[d] + excl;
+    __syncthreads();
+    // 4. Local placement in digit order, then contiguous global stores.
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int i = base + warp * (kItems * 32) + r * 32 + lane;
+        if (i < n) {
+            const int digit = static_cast<int>((key[r] >> shift) & 0xFF);
+            const unsigned lpos = s_bstart[digit] + s_wc[warp][digit] + wrank[r];
+            s_k[lpos] = key[r];
+            s_v[lpos] = val[r];
+        }
+    }
+    __syncthreads();
+    const int cnt = min(kTileItems, n - base);
+    for (int i = threadIdx.x; i < cnt; i += kThreads) {
+        const uint32_t k = s_k[i];
+        const int digit = static_cast<int>((k >> shift) & 0xFF);
+        const unsigned g = s_gbase[digit] + (static_cast<unsigned>(i) - s_bstart[digit]);
+        keys_out[g] = k;
+        vals_out[g] = s_v[i];
     }
 }
 
@@ -224,8 +283,10 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 void SortScratch::ensure(int n_max) {
     const int nb = cdiv(std::max(n_max, 1), kTileItems);
-    counts.ensure(static_cast<size_t>(kDigits) * nb);
-    totals.ensure(kDigits);
+    // one memset clears: hist [passes][256], tickets [passes], status [passes][nb][256]
+    onesweep.ensure(static_cast<size_t>(kMaxPasses) * kDigits + kMaxPasses +
+                    static_cast<size_t>(kMaxPasses) * nb * kDigits);
+    dstart.ensure(static_cast<size_t>(kMaxPasses) * kDigits);
     sums.ensure(nb + 1);
 }
 
@@ -235,15 +296,22 @@ void radix_sort_pairs(uint32_t* keys, int* vals, uint32_t* keys_alt, int* vals_a
     sc.ensure(n_max);
     const int nb = cdiv(n_max, kTileItems);
     const int passes = cdiv(bits, 8);
+    if (passes > kMaxPasses) throw Error(NGS_ERR_INTERNAL, "radix sort: more than 32 key bits");
+    unsigned* hist = sc.onesweep.ptr;
+    unsigned* tickets = hist + kMaxPasses * kDigits;
+    unsigned* status = tickets + kMaxPasses;
+    CUDA_CHECK(cudaMemsetAsync(hist, 0,
+                               sizeof(unsigned) * (kMaxPasses * kDigits + kMaxPasses + static_cast<size_t>(passes) * nb * kDigits),
+                               s));
+    radix_global_hist_k<<<nb, kThreads, 0, s>>>(keys, d_n, passes, hist);
+    radix_digit_starts_k<<<1, kThreads, 0, s>>>(hist, passes, sc.dstart.ptr);
     uint32_t* kin = keys;
     int* vin = vals;
     uint32_t* kout = keys_alt;
     int* vout = vals_alt;
     for (int p = 0; p < passes; ++p) {
-        const int shift = 8 * p;
-        radix_hist_k<<<nb, kThreads, 0, s>>>(kin, d_n, shift, nb, sc.counts.ptr);
-        radix_scan_digit_k<<<kDigits, kThreads, 0, s>>>(sc.counts.ptr, nb, sc.totals.ptr);
-        radix_scatter_k<<<nb, kThreads, 0, s>>>(kin, vin, kout, vout, d_n, shift, nb, sc.counts.ptr, sc.totals.ptr);
+        radix_onesweep_k<<<nb, kThreads, 0, s>>>(kin, vin, kout, vout, d_n, 8 * p, sc.dstart.ptr + p * kDigits,
+                                                 status + static_cast<size_t>(p) * nb * kDigits, tickets + p);
         std::swap(kin, kout);
         std::swap(vin, vout);
     }

@@ -8,11 +8,12 @@
 namespace ngsb {
 
 struct SortScratch {
-    DevBuf<int> counts, totals, sums;
+    DevBuf<unsigned> onesweep, dstart;  // histograms + tickets + look-back status; digit starts
+    DevBuf<int> sums;
     void ensure(int n_max);
     void release() {
-        counts.release();
-        totals.release();
+        onesweep.release();
+        dstart.release();
         sums.release();
     }
 };
