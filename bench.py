@@ -65,7 +65,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -74,7 +74,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc:
@@ -85,10 +85,14 @@ class ClockSampler:
                 self.proc.kill()
             self.thread.join(timeout=2)
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Samples taken inside [t0, t1] (the timed region); the sampler is started
+        before the warm-up so that nvidia-smi is already polling when timing starts."""
         sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in self.lines:
+        for ts, line in self.lines:
+            if t0 is not None and not (t0 <= ts <= t1 + 0.1):
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -228,15 +232,16 @@ def ours_arm(args, cfg: Config):
     def view(i):
         return shard[i % len(shard)]
 
-    for i in range(args.warmup):
-        ctx.trainer_step(view(i))
-    ctx.profile_reset()
     dts = []
     prof_range = os.environ.get("NGS_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with ClockSampler(local) as clocks:
+        for i in range(args.warmup):
+            ctx.trainer_step(view(i))
+        ctx.profile_reset()
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        t_timed0 = time.time()
         for i in range(args.steps):
             l2_flush(flush)
             if prof_range:
@@ -248,6 +253,7 @@ def ours_arm(args, cfg: Config):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
+        t_timed1 = time.time()
     counters = ctx.profile_read()
     total_ms = float(sum(dts))
 
@@ -313,6 +319,17 @@ def ours_arm(args, cfg: Config):
     achieved = POSITION_FLOPS_PER_PAIR * pairs / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else 0.0
     step_stage_ms = {k: round(v / args.steps, 4) for k, v in prof["ms"].items()}
 
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # (ncu numbers are never bench values; this only sizes traffic vs algorithmic bytes).
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(REPO, "profiles", "r1_roofline_traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+        traffic_src = f"{tj['kernel']}: {tj['source']}"
+    except (OSError, KeyError, ValueError):
+        pass
+
     cpu = None
     if not args.no_cpu_baseline:
         cpu = run_reference_sample(cfg, 2, 0, args.ref_shrink, target_ctx=lib.context(local))
@@ -329,7 +346,8 @@ def ours_arm(args, cfg: Config):
         "gpu_launches": int(counters["total_launches"]),
         "roofline": {"bound": "fp32", "kernel": "backward_k<position>", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
-                     "traffic": None, "peak_source": "measured FFMA microbenchmark (ngs_microbench_fp32)",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": "measured FFMA microbenchmark (ngs_microbench_fp32)",
                      "algorithmic": f"{POSITION_FLOPS_PER_PAIR} flop x {pairs} contributing records / "
                                     f"{bwd_launches} launches"},
         "profiled_pass": {"note": "same K steps re-run with views serialised and per-launch CUDA events; "
@@ -338,7 +356,7 @@ def ours_arm(args, cfg: Config):
         "group_ms_per_step_concurrent": {k: round(v / args.steps, 4) for k, v in counters["group_ms"].items()},
         "measured_fp64_tflops": fp64_peak,
         "contrib_pairs_per_step": [p / args.steps for p in prof["contrib_pairs"]],
-        "clocks": clocks.summary(),
+        "clocks": clocks.summary(t_timed0, t_timed1),
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
@@ -347,7 +365,7 @@ def ours_arm(args, cfg: Config):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2", choices=sorted(CONFIGS))

@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
 void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s) {
     const int n = scene.n;
     if (n == 0 || pass == kPassOpacityColor) return;
-    StageScope st(NGS_STAGE_CONSTS, s);
+    StageScope st(NGS_STAGE_CONSTS, s, pass == kPassPosition || pass == kPassPositionUV ? 2 : 1);
     switch (pass) {
         case kPassPosition:
             v.consts.ensure(static_cast<size_t>(n) * kPosConsts);

@@ -321,7 +321,7 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     const int row0 = band_px0 / kLT, row1 = (band_px1 + kLT - 1) / kLT;
     if (row1 <= row0) return;
     const dim3 grid((v.W + kLT - 1) / kLT, row1 - row0, 3);
-    StageScope st(NGS_STAGE_LOSS, s, 1);
+    StageScope st(NGS_STAGE_LOSS, s, ssim ? 2 : 1);
     auto run = [&](auto fields_kernel, auto derivs_kernel) {
         if (ssim) {
             v.fields.ensure(27 * npx);

@@ -396,7 +396,7 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
         CUDA_LAUNCH_CHECK();
     }
     if (n > 0) {
-        StageScope st(NGS_STAGE_SORT, s, 18);
+        StageScope st(NGS_STAGE_SORT, s, 11);  // sort 2 + 4 passes, fix-up, gather, scan 3
         // K2: global depth order, exactly (FP64 depth, kernel id): 4-pass radix sort of the
         // FP32 depth key (stable over the id-ordered input) + fix-up of equal-key runs.
         v.n_host = n;
@@ -429,7 +429,7 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     }
     CUDA_CHECK(cudaMemsetAsync(v.ranges.ptr, 0, sizeof(int2) * v.T, s));
     if (cap > 0 && n > 0) {
-        StageScope st(NGS_STAGE_SORT, s, 2 + 3 * ((bits + 7) / 8));
+        StageScope st(NGS_STAGE_SORT, s, 4 + (bits + 7) / 8);  // emit, sort 2 + passes, ranges
         v.pair_key.ensure(cap);
         v.pair_key_alt.ensure(cap);
         v.pair_val.ensure(cap);
