@@ -36,7 +36,7 @@ inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 // projection_derivatives camera.hpp:124-148; cov2d_derivatives_wrt_position
 // camera.hpp:241-284; sh_color_derivs_wrt_position sh.hpp:134-161.
 // Two blocks per 128 Gaussians (blockIdx.y): 0 = pixel / Sigma derivatives
-// (JS, HPI, SCD), 1 = SH colour derivatives (JC, JJ, HC); halves the FP64 live
+// (JS, HPI, SCD), 1 = SH colour derivatives (JC, HC); halves the FP64 live
 // state per thread. Rows are staged in shared memory and stored coalesced.
 template <int ND, int PART>
 __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev cam, CameraDev primary,
@@ -271,14 +271,13 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
 #pragma unroll
                 for (int a = 0; a < ND; ++a) {
                     jd[a] = d1(Jc[ch], 1, a);
-                    o[4 * ch + a] = static_cast<float>(jd[a]);
+                    o[ND * ch + a] = static_cast<float>(jd[a]);
                 }
                 int p = 0;
 #pragma unroll
                 for (int a = 0; a < ND; ++a)
 #pragma unroll
                     for (int b = a; b < ND; ++b, ++p) {
-                        o[L::JJ - L::JC + L::NP * ch + p] = static_cast<float>(jd[a] * jd[b]);
                         o[L::HC - L::JC + L::NP * ch + p] = static_cast<float>(d2(Hc[ch], 1, a, b));
                     }
             }
@@ -388,23 +387,23 @@ template <int PASS>
 struct PassTraits;
 template <>
 struct PassTraits<kPassPosition> {
-    static constexpr int NC = kPosConsts, NA = 9, BATCH = 32;
+    static constexpr int NC = kPosConsts, NA = 9, BATCH = 32, BATCH8 = 32;
 };
 template <>
 struct PassTraits<kPassPositionUV> {
-    static constexpr int NC = kPosUVConsts, NA = 5, BATCH = 32;
+    static constexpr int NC = kPosUVConsts, NA = 5, BATCH = 64, BATCH8 = 32;
 };
 template <>
 struct PassTraits<kPassRotation> {
-    static constexpr int NC = kRotConsts, NA = 2, BATCH = 128;
+    static constexpr int NC = kRotConsts, NA = 2, BATCH = 128, BATCH8 = 64;
 };
 template <>
 struct PassTraits<kPassScaling> {
-    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 128;
+    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 128, BATCH8 = 64;
 };
 template <>
 struct PassTraits<kPassOpacityColor> {
-    static constexpr int NC = 0, NA = 8, BATCH = 64;
+    static constexpr int NC = 0, NA = 8, BATCH = 64, BATCH8 = 64;
 };
 
 // Copies N float4 from shared memory into a register array.
@@ -474,8 +473,8 @@ __device__ __forceinline__ void position_record(const float4* K4, const Rec& r, 
                 d2G[p] = G * (0.25f * qcv[c] * qcv[d] - 0.5f * qcd);
             }
     }
-    float Jc[12];
-    ld4<3>(Jc, K4 + L::JC / 4);
+    float Jc[L::a4(3 * ND)];
+    ld4<L::a4(3 * ND) / 4>(Jc, K4 + L::JC / 4);
     float sgl = 0.f, A2 = 0.f, vgl[ND], vh[ND], ga[3], ha[3];
 #pragma unroll
     for (int i = 0; i < ND; ++i) vgl[i] = vh[i] = 0.f;
@@ -488,17 +487,23 @@ __device__ __forceinline__ void position_record(const float4* K4, const Rec& r, 
         A2 += hac * r.ac[ch];
 #pragma unroll
         for (int i = 0; i < ND; ++i) {
-            vgl[i] += ga[ch] * Jc[4 * ch + i];
-            vh[i] += hac * Jc[4 * ch + i];
+            vgl[i] += ga[ch] * Jc[ND * ch + i];
+            vh[i] += hac * Jc[ND * ch + i];
         }
     }
-    float E[L::a4(6 * NP)];
-    ld4<L::a4(6 * NP) / 4>(E, K4 + L::JJ / 4);
+    // Gauss-Newton block sum_ch hl wa^2 Jc Jc^T from the loaded Jc (not stored).
+    float Hc[L::a4(3 * NP)];
+    ld4<L::a4(3 * NP) / 4>(Hc, K4 + L::HC / 4);
     float JJ[NP], hc[NP];
+    {
+        int q = 0;
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
-        JJ[q] = ha[0] * E[q] + ha[1] * E[NP + q] + ha[2] * E[2 * NP + q];
-        hc[q] = ga[0] * E[3 * NP + q] + ga[1] * E[4 * NP + q] + ga[2] * E[5 * NP + q];
+        for (int c = 0; c < ND; ++c)
+#pragma unroll
+            for (int d = c; d < ND; ++d, ++q) {
+                JJ[q] = ha[0] * Jc[c] * Jc[d] + ha[1] * Jc[ND + c] * Jc[ND + d] + ha[2] * Jc[2 * ND + c] * Jc[2 * ND + d];
+                hc[q] = ga[0] * Hc[q] + ga[1] * Hc[NP + q] + ga[2] * Hc[2 * NP + q];
+            }
     }
     const float GG = G * G;
 #pragma unroll
@@ -600,7 +605,7 @@ template <int PASS, int TILE>
 struct BackwardSmem {
     using TR = PassTraits<PASS>;
     static constexpr int NT = TILE * TILE, NW = NT / 32;
-    static constexpr int B = TR::BATCH < NT ? TR::BATCH : NT, NA = TR::NA, NC4 = TR::NC / 4;
+    static constexpr int B = TILE == 16 ? TR::BATCH : TR::BATCH8, NA = TR::NA, NC4 = TR::NC / 4;
     static constexpr int CST = (NC4 % 8 == 0 && NC4 > 0) ? NC4 + 1 : NC4;  // float4 stride, avoids bank conflicts
     float4 raw[2][4][B];                   // staged records (pix as double2, ra, rb, rc), double-buffered
     float4 cst[2][(CST > 0 ? CST : 1) * B];  // staged per-view constants, double-buffered
@@ -609,7 +614,7 @@ struct BackwardSmem {
     unsigned char wmask[B];                // bit w: the splat's cutoff ellipse reaches warp w's pixel rows
     float acc[NW][NA][B];                  // per-warp sums: segment tails are unique within a drain
     int kid[2][B];
-    int vis[B];
+    unsigned char vis[NW][B];              // per warp: the splat had >= 1 record in this warp
     float gl[NT][3], hl[NT][3];
     WarpQueue q[NW];
     int maxlast;
@@ -668,6 +673,8 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
         }
     }
     if (threadIdx.x == 0) s_maxlast = -1;
+    for (int i = threadIdx.x; i < NW * NA * B; i += NT) (&s_acc[0][0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < NW * B; i += NT) (&s_vis[0][0])[i] = 0;
     __syncthreads();
     if (last >= 0) atomicMax(&s_maxlast, last);
     __syncthreads();
@@ -732,7 +739,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
         if (tail) {
 #pragma unroll
             for (int c = 0; c < NA; ++c) s_acc[warp][c][jj] += v[c];
-            s_vis[jj] = 1;
+            s_vis[warp][jj] = 1;
         }
         if (lane == 0) block_pairs += n;
         qhead = (qhead + n) & (kQ - 1);
@@ -797,12 +804,10 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
             } else {
                 S.wmask[tid] = 0;
             }
-            s_vis[tid] = 0;
             S.kid[buf ^ 1][tid] = kid_next;
             const int nx = base + 2 * B + tid;
             kid_next = nx < end ? a.vals[nx] : 0;
         }
-        for (int i = tid; i < NW * NA * B; i += NT) (&s_acc[0][0][0])[i] = 0.f;
         __syncthreads();
         if (base + B < end) issue(buf ^ 1, base + B);
         cp_async_commit();
@@ -876,17 +881,19 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
         if (qcount > 0) {
             __syncwarp();
             drain(qcount);
-            __syncwarp();
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        __syncwarp();
+        // Each warp flushes its own per-splat sums (FP64 global atomics, zeros
+        // skipped) and clears them: no block-wide barrier at the batch end.
+        for (int i = lane; i < cnt; i += 32) {
+            if (!s_vis[warp][i]) continue;
+            s_vis[warp][i] = 0;
             const int k = S.kid[buf][i];
-            if (a.visible && s_vis[i]) a.visible[k] = 1;
+            if (a.visible) a.visible[k] = 1;
 #pragma unroll
             for (int c = 0; c < NA; ++c) {
-                float val = 0.f;
-#pragma unroll
-                for (int w = 0; w < NW; ++w) val += s_acc[w][c][i];  // fixed order: deterministic block sum
+                const float val = s_acc[warp][c][i];
+                s_acc[warp][c][i] = 0.f;
                 if (val != 0.f) atomicAdd(&a.acc[static_cast<size_t>(c) * a.acc_stride + k], static_cast<double>(val));
             }
         }

@@ -30,14 +30,13 @@ struct PosLayout {
     static constexpr int JS = 0;                  // J columns (Jx_c, Jy_c) xND, then dSigma/dp_c (a, b, c) xND
     static constexpr int HPI = JS + a4(5 * ND);   // d2pi/dp_c dp_d: (x, y) per pair
     static constexpr int SCD = HPI + a4(2 * NP);  // d2Sigma/dp_c dp_d: (a, b, c) per pair
-    static constexpr int JC = SCD + a4(3 * NP);   // dc~_ch/dp: ND per channel, padded to 4
-    static constexpr int JJ = JC + 12;            // Jc_ch Jc_ch^T: NP per channel
-    static constexpr int HC = JJ + 3 * NP;        // d2c~_ch/dp2: NP per channel
-    static constexpr int N = a4(HC + 3 * NP);
+    static constexpr int JC = SCD + a4(3 * NP);   // dc~_ch/dp: ND per channel (channel-major)
+    static constexpr int HC = JC + a4(3 * ND);    // d2c~_ch/dp2: NP per channel
+    static constexpr int N = HC + a4(3 * NP);
 };
-constexpr int kPosConsts = PosLayout<3>::N;    // 96
-constexpr int kPosUVConsts = PosLayout<2>::N;  // 64
-static_assert(kPosConsts == 96 && kPosUVConsts == 64, "position constant layout");
+constexpr int kPosConsts = PosLayout<3>::N;    // 80
+constexpr int kPosUVConsts = PosLayout<2>::N;  // 52
+static_assert(kPosConsts == 80 && kPosUVConsts == 52, "position constant layout");
 constexpr int kRotConsts = 8;    // s1 (00, 01, 11), s2 (00, 01, 11), pad 2
 constexpr int kScaleConsts = 8;  // v0 (2), v1 (2), m00, m01, m11, pad
 
