@@ -133,7 +133,8 @@ struct ngs_context {
     Profiler prof;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // Per-view streams: the 1+K views of a step render and back-propagate concurrently.
-    std::array<cudaStream_t, kMaxSolveViews> vs{};
+    std::array<cudaStream_t, kMaxSolveViews> vs{};  // backward streams (secondaries at high priority)
+    std::array<cudaStream_t, kMaxSolveViews> vr{};  // render streams (equal priority)
     cudaEvent_t fork_ev = nullptr;
     std::array<cudaEvent_t, kMaxSolveViews> join_ev{};
     std::array<cudaEvent_t, 24> gev{};  // stage-group events of a trainer step
@@ -143,6 +144,7 @@ struct ngs_context {
     // Multi-GPU shard (ngs_b200_dist.h)
     int shard_rank = 0, shard_world = 1;
     ncclComm_t comm = nullptr;
+    int stream_policy = 0;  // 0: secondaries first, high priority; 1: primary first+high; 2: none, sec first; 3: none, primary first
     int tile_policy = 0;  // 0 auto (8x8 tiles for small views), else forced 8 or 16
     unsigned long long contrib_pairs_total = 0;
 
@@ -173,6 +175,8 @@ struct ngs_context {
             if (e) cudaEventDestroy(e);
         for (auto s : vs)
             if (s) cudaStreamDestroy(s);
+        for (auto s : vr)
+            if (s) cudaStreamDestroy(s);
         for (auto e : gev)
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
@@ -192,13 +196,13 @@ struct ngs_context {
     }
 
     // Fork the per-view streams off the main stream / join them back.
-    void fork(int nv) {
+    void fork(int nv, const cudaStream_t* ss) {
         CUDA_CHECK(cudaEventRecord(fork_ev, stream));
-        for (int i = 0; i < nv; ++i) CUDA_CHECK(cudaStreamWaitEvent(vs[i], fork_ev, 0));
+        for (int i = 0; i < nv; ++i) CUDA_CHECK(cudaStreamWaitEvent(ss[i], fork_ev, 0));
     }
-    void join(int nv) {
+    void join(int nv, const cudaStream_t* ss) {
         for (int i = 0; i < nv; ++i) {
-            CUDA_CHECK(cudaEventRecord(join_ev[i], vs[i]));
+            CUDA_CHECK(cudaEventRecord(join_ev[i], ss[i]));
             CUDA_CHECK(cudaStreamWaitEvent(stream, join_ev[i], 0));
         }
     }
@@ -452,8 +456,14 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         // primary's many blocks fill the remaining SM resources around them.
         int prio_lo = 0, prio_hi = 0;
         CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        if (const char* e = getenv("NGS_STREAM_POLICY")) ctx->stream_policy = atoi(e);  // experiments only
         for (int i = 0; i < kMaxSolveViews; ++i) {
-            CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->vs[i], cudaStreamNonBlocking, i == 0 ? prio_lo : prio_hi));
+            int prio = i == 0 ? prio_lo : prio_hi;
+            if (ctx->stream_policy == 1) prio = i == 0 ? prio_hi : prio_lo;
+            if (ctx->stream_policy >= 2) prio = prio_lo;
+            CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->vs[i], cudaStreamNonBlocking, prio));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->vr[i], cudaStreamNonBlocking,
+                                                    ctx->stream_policy == 0 ? prio_lo : prio));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
         }
         ctx->overflow.ensure(1);
@@ -736,9 +746,10 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
     ctx->acc.ensure(stride * comps);
     CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
     concurrent = concurrent && nv <= kMaxSolveViews && !ctx->prof.enabled;
-    if (concurrent) ctx->fork(nv);
+    if (concurrent) ctx->fork(nv, ctx->vs.data());
     for (int ii = 0; ii < nv; ++ii) {
-        const int i = concurrent ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
+        const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
+        const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
         ViewSlot& v = *views[i];
         cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
         compute_pass_consts(pass, ctx->scene, v, views[0]->cam, s);
@@ -746,7 +757,7 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
         unsigned long long* contrib = ctx->pairs.ptr + (pass == kPassPositionUV ? kPassPosition : pass);
         launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s);
     }
-    if (concurrent) ctx->join(nv);
+    if (concurrent) ctx->join(nv, ctx->vs.data());
     if (ctx->comm) {
         // Exchange step: per-Gaussian FP64 accumulators summed over ranks (NVLink / NVSwitch).
         StageScope st(NGS_STAGE_OTHER, ctx->stream, 0);
@@ -1080,11 +1091,12 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     const int nv = 1 + static_cast<int>(nbrs.size());
     // Profiling serialises the views so per-launch event times do not overlap.
     const bool concurrent = !ctx->prof.enabled;
-    if (concurrent) ctx->fork(nv);
+    if (concurrent) ctx->fork(nv, ctx->vr.data());
     for (int ii = 0; ii < nv; ++ii) {
-        const int i = concurrent ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
+        const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
+        const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
         ViewSlot& v = T.views[i];
-        cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
+        cudaStream_t s = concurrent ? ctx->vr[i] : ctx->stream;
         const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
         const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
         if (upload_targets) {
@@ -1108,7 +1120,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
         compute_loss(v, s);
     }
-    if (concurrent) ctx->join(nv);
+    if (concurrent) ctx->join(nv, ctx->vr.data());
 }
 
 }  // namespace

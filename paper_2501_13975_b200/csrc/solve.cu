@@ -331,7 +331,7 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
 // the null space of Phi^T carries no gradient. Nothing n-dimensional is
 // stored: phi_v is re-evaluated when beta is committed.
 template <int MV>
-__global__ void __launch_bounds__(128) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
+__global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
                                                      const double* __restrict__ acc, size_t stride,
                                                      SolveOutputs out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
