@@ -609,8 +609,7 @@ struct BackwardSmem {
     static constexpr int CST = (NC4 % 8 == 0 && NC4 > 0) ? NC4 + 1 : NC4;  // float4 stride, avoids bank conflicts
     float4 raw[2][4][B];                   // staged records (pix as double2, ra, rb, rc), double-buffered
     float4 cst[2][(CST > 0 ? CST : 1) * B];  // staged per-view constants, double-buffered
-    float4 g0[B], g1[B];                   // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
-    float2 g2[B];                          // (c1, c2)
+    SplatSh sp[B];                         // staged splats of the batch
     unsigned char wmask[B];                // bit w: the splat's cutoff ellipse reaches warp w's pixel rows
     float acc[NW][NA][B];                  // per-warp sums: segment tails are unique within a drain
     int kid[2][B];
@@ -629,9 +628,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
     static_assert(B <= NT && B % 32 == 0, "one loader thread per splat of a batch");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& S = *reinterpret_cast<SM*>(smem_raw);
-    auto& s_g0 = S.g0;
-    auto& s_g1 = S.g1;
-    auto& s_g2 = S.g2;
+    auto& s_sp = S.sp;
     auto& s_acc = S.acc;
     auto& s_vis = S.vis;
     auto& s_gl = S.gl;
@@ -711,15 +708,15 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 r.hl[c] = s_hl[px][c];
             }
             if constexpr (PASS == kPassPosition || PASS == kPassPositionUV) {
-                const float4 g0 = s_g0[jj], g1 = s_g1[jj];
-                position_record<PASS == kPassPosition ? 3 : 2>(s_const + jj * CST, r, g0.z, g0.w, g1.x, v);
+                const float4 g0 = s_sp[jj].g0;
+                position_record<PASS == kPassPosition ? 3 : 2>(s_const + jj * CST, r, g0.z, g0.w, s_sp[jj].g1.x, v);
             } else if constexpr (PASS == kPassRotation) {
-                const float4 g0 = s_g0[jj], g1 = s_g1[jj];
-                rotation_record(s_const + jj * CST, r, g0.z, g0.w, g1.x, v);
+                const float4 g0 = s_sp[jj].g0;
+                rotation_record(s_const + jj * CST, r, g0.z, g0.w, s_sp[jj].g1.x, v);
             } else if constexpr (PASS == kPassScaling) {
                 scaling_record(s_const + jj * CST, r, v);
             } else {
-                opacity_color_record(r, s_g1[jj].y, v);
+                opacity_color_record(r, s_sp[jj].g1.y, v);
             }
         }
         // Segmented inclusive scan keyed by splat (entries are sorted by splat, so
@@ -791,9 +788,12 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level
                 // skip never drops a record the per-lane test would keep.
                 const float ey = sqrtf(fmaxf(qmax, 0.f) * rc.w) * 1.0001f + 1e-3f;
-                s_g0[tid] = make_float4(static_cast<float>(p.x - ox), py, ra.z, ra.w);
-                s_g1[tid] = make_float4(rb.x, rb.y, qmax, rb.z);
-                s_g2[tid] = make_float2(rb.w, rc.x);
+                SplatSh sp;
+                sp.g0 = make_float4(static_cast<float>(p.x - ox), py, ra.z, ra.w);
+                sp.g1 = make_float4(rb.x, rb.y, qmax, rb.z);
+                sp.g2 = make_float2(rb.w, rc.x);
+                sp.pad = make_float2(0.f, 0.f);
+                s_sp[tid] = sp;
                 unsigned m = 0;
 #pragma unroll
                 for (int w = 0; w < NW; ++w) {  // warp w owns pixel-centre rows [kRowsPerWarp w + 0.5, + kRowsPerWarp - 1]
@@ -821,13 +821,13 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 m &= m - 1;
                 bool contrib = false;
                 float G = 0.f, q0 = 0.f, q1 = 0.f, Tr = 0.f, wa = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f;
-                if (base + j <= last) {
-                    const float4 g0 = s_g0[j], g1 = s_g1[j];
-                    SplatEval ev;
-                    if (eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, ev) && !(ev.alpha < a.cutoff)) {
+                const SplatSh sp = s_sp[j];
+                SplatEval ev;
+                const bool cand = eval_splat_bf(sp, fx, fy, a.cutoff, ev);
+                {
+                    if (cand && base + j <= last) {
                         contrib = true;
-                        const float2 g2 = s_g2[j];
-                        const float col[3] = {g1.w, g2.x, g2.y};
+                        const float col[3] = {sp.g1.w, sp.g2.x, sp.g2.y};
                         const float Ti = T;
                         const float w = blend_weight(Ti, ev.alpha);
                         const float Tn = next_transmittance(Ti, ev.alpha);
@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                         q0 = ev.qd0;
                         q1 = ev.qd1;
                         Tr = Ti;
-                        wa = g1.y * Ti;
+                        wa = sp.g1.y * Ti;
                         ac0 = ac[0];
                         ac1 = ac[1];
                         ac2 = ac[2];

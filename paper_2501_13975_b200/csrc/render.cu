@@ -253,8 +253,7 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
                                                         float* __restrict__ t_final, int* __restrict__ last_out) {
     constexpr int kRasterBatch = TILE * TILE;  // one splat per thread per batch
     constexpr int kRowsPerWarp = 32 / TILE;
-    __shared__ float4 s_g0[kRasterBatch], s_g1[kRasterBatch];  // (px, py, Q00, Q01), (Q11, sigma, qmax, c0)
-    __shared__ float2 s_g2[kRasterBatch];                      // (c1, c2)
+    __shared__ SplatSh s_sp[kRasterBatch];
     __shared__ unsigned char s_wmask[kRasterBatch];            // bit w: the cutoff ellipse reaches warp w's rows
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -296,9 +295,12 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level skip
             // never drops a splat the per-pixel test would keep.
             const float ey = sqrtf(fmaxf(qmax, 0.f) * c.w) * 1.0001f + 1e-3f;
-            s_g0[threadIdx.x] = make_float4(static_cast<float>(p.x - ox), py, a.z, a.w);
-            s_g1[threadIdx.x] = make_float4(b.x, b.y, qmax, b.z);
-            s_g2[threadIdx.x] = make_float2(b.w, c.x);
+            SplatSh sp;
+            sp.g0 = make_float4(static_cast<float>(p.x - ox), py, a.z, a.w);
+            sp.g1 = make_float4(b.x, b.y, qmax, b.z);
+            sp.g2 = make_float2(b.w, c.x);
+            sp.pad = make_float2(0.f, 0.f);
+            s_sp[threadIdx.x] = sp;
             unsigned m = 0;
 #pragma unroll
             for (int w = 0; w < kRasterBatch / 32; ++w) {  // warp w owns rows [kRowsPerWarp w + 0.5, + kRowsPerWarp - 1]
@@ -322,19 +324,17 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             while (m) {
                 const int j = c32 + __ffs(m) - 1;
                 m &= m - 1;
-                if (done) continue;
-                const float4 g0 = s_g0[j], g1 = s_g1[j];
+                const SplatSh sp = s_sp[j];
                 SplatEval e;
-                if (!eval_splat(g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, fx, fy, g1.z, e)) continue;
-                if (e.alpha < cutoff) continue;
-                const float2 g2 = s_g2[j];
-                const double w = blend_weight(T, e.alpha);
-                C0 = __fma_rn(w, g1.w, C0);
-                C1 = __fma_rn(w, g2.x, C1);
-                C2 = __fma_rn(w, g2.y, C2);
-                T = next_transmittance(T, e.alpha);
-                last = base + j;
-                if (tmin > 0.f && T < tmin) done = true;
+                if (eval_splat_bf(sp, fx, fy, cutoff, e) && !done) {
+                    const double w = blend_weight(T, e.alpha);
+                    C0 = __fma_rn(w, sp.g1.w, C0);
+                    C1 = __fma_rn(w, sp.g2.x, C1);
+                    C2 = __fma_rn(w, sp.g2.y, C2);
+                    T = next_transmittance(T, e.alpha);
+                    last = base + j;
+                    if (tmin > 0.f && T < tmin) done = true;
+                }
             }
         }
     }

@@ -35,6 +35,36 @@ __device__ __forceinline__ float reject_bound(float sigma, float cutoff) {
     return cutoff > 0.f ? 2.0f * logf(sigma / cutoff) + 1e-2f : __int_as_float(0x7f800000);
 }
 
+// A splat as staged in shared memory for a tile batch: one 48-byte record so
+// every visit is a single broadcast base address.
+struct SplatSh {
+    float4 g0;  // (px, py, Q00, Q01) in tile coordinates
+    float4 g1;  // (Q11, sigma, qmax, c0)
+    float2 g2;  // (c1, c2)
+    float2 pad;
+};
+
+// exp(-q/2) = 2^(-q log2(e) / 2) on the SFU (MUFU.EX2, ~2 ulp). Forward and
+// backward call the same instruction sequence, so alpha stays bit-identical.
+__device__ __forceinline__ float exp_neg_half(float q) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fmul_rn(q, -0.72134752044448170368f)));
+    return r;
+}
+
+// Branch-free evaluation: every lane computes G and alpha; returns whether the
+// (pixel, splat) pair composites (q within the reject bound and alpha >= cutoff).
+__device__ __forceinline__ bool eval_splat_bf(const SplatSh& sp, float x, float y, float cutoff, SplatEval& e) {
+    e.dx = __fsub_rn(sp.g0.x, x);
+    e.dy = __fsub_rn(sp.g0.y, y);
+    e.qd0 = __fmaf_rn(sp.g0.z, e.dx, __fmul_rn(sp.g0.w, e.dy));
+    e.qd1 = __fmaf_rn(sp.g0.w, e.dx, __fmul_rn(sp.g1.x, e.dy));
+    const float q = __fmaf_rn(e.dx, e.qd0, __fmul_rn(e.dy, e.qd1));
+    e.g = exp_neg_half(q);
+    e.alpha = __fmul_rn(e.g, sp.g1.y);
+    return q <= sp.g1.z && !(e.alpha < cutoff);
+}
+
 // Returns false (and leaves e.g / e.alpha unset) when q exceeds `qmax`.
 __device__ __forceinline__ bool eval_splat(float px, float py, float qa, float qb, float qc, float sigma, float x,
                                            float y, float qmax, SplatEval& e) {
