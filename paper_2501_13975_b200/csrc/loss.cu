@@ -19,7 +19,6 @@ namespace {
 
 constexpr int kLT = 16;       // output tile edge
 constexpr int kMaxHalf = 10;  // window <= 21
-constexpr int kLS = kLT + 2 * kMaxHalf;
 
 struct Window {
     double w[2 * kMaxHalf + 1];
@@ -44,6 +43,42 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     if (threadIdx.x == 0)
         for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
     return t;
+}
+
+// SSIM and its 9 window-centre derivative fields from the 5 filtered window
+// statistics (loss.hpp:262-305); reciprocals of f2, f3 hoisted (two divisions).
+__device__ __forceinline__ double ssim_centre_fields(const double (&st)[5], double inv_norm, double c1, double c2,
+                                                     double (&out)[9]) {
+    const double mu = st[0] * inv_norm, mu_t = st[2] * inv_norm;
+    const double var = fmax(0.0, st[1] * inv_norm - mu * mu);
+    const double var_t = fmax(0.0, st[3] * inv_norm - mu_t * mu_t);
+    const double cov = st[4] * inv_norm - mu * mu_t;
+    // loss.hpp:266-303 (reciprocals of f2, f3 hoisted: two divisions per pixel)
+    const double f0 = 2.0 * mu * mu_t + c1;
+    const double f1 = 2.0 * cov + c2;
+    const double f2 = mu * mu + mu_t * mu_t + c1;
+    const double f3 = var + var_t + c2;
+    const double inv_f2 = 1.0 / f2, inv_f3 = 1.0 / f3;
+    const double nn = f0 * f1;
+    const double inv_d = inv_f2 * inv_f3;
+    const double ssim = nn * inv_d;
+    const double a0 = 2.0 * mu_t, a1 = -2.0 * mu_t, b1 = 2.0;
+    const double a2 = 2.0 * mu, a3 = -2.0 * mu, b3 = 2.0;
+    const double A = a0 * f1 + f0 * a1, B = f0 * b1, C = a2 * f3 + f2 * a3, E = f2 * b3;
+    const double inv_d2 = inv_d * inv_d, inv_d3 = inv_d2 * inv_d, inv_norm2 = inv_norm * inv_norm;
+    const double nnd = nn * inv_d;
+    out[0] = (2.0 * mu_t * (f1 - f0) * inv_d - 2.0 * mu * nnd * inv_f2 + 2.0 * mu * nnd * inv_f3) * inv_norm;
+    out[1] = 2.0 * f0 * inv_d * inv_norm;
+    out[2] = -2.0 * nnd * inv_f3 * inv_norm;
+    out[3] = -2.0 * nn * inv_f2 * inv_f3 * inv_f3 * inv_norm;
+    out[4] = (2.0 * a0 * a1 * inv_d - 2.0 * A * C * inv_d2 - nn * (2.0 * a2 * a3 + 2.0 * f3 - 2.0 * f2) * inv_d2 +
+              2.0 * nn * C * C * inv_d3) *
+             inv_norm2;
+    out[5] = (-2.0 * A * E * inv_d2 - 2.0 * nn * a2 * b3 * inv_d2 + 4.0 * nn * C * E * inv_d3) * inv_norm2;
+    out[6] = (2.0 * a0 * b1 * inv_d - 2.0 * B * C * inv_d2) * inv_norm2;
+    out[7] = -2.0 * B * E * inv_d2 * inv_norm2;
+    out[8] = 2.0 * nn * E * E * inv_d3 * inv_norm2;
+    return ssim;
 }
 
 // Separable valid-tap convolutions over a (kLT + 2h)^2 shared-memory halo tile.
@@ -163,36 +198,8 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
                 for (int f = 0; f < 5; ++f) st[f] += win.w[k] * s_h[f][ly + k][lx];
         }
         const double inv_norm = 1.0 / (axis_norm(x, W, win) * axis_norm(y, H, win));
-        const double mu = st[0] * inv_norm, mu_t = st[2] * inv_norm;
-        const double var = fmax(0.0, st[1] * inv_norm - mu * mu);
-        const double var_t = fmax(0.0, st[3] * inv_norm - mu_t * mu_t);
-        const double cov = st[4] * inv_norm - mu * mu_t;
-        // loss.hpp:266-303 (reciprocals of f2, f3 hoisted: two divisions per pixel)
-        const double f0 = 2.0 * mu * mu_t + c1;
-        const double f1 = 2.0 * cov + c2;
-        const double f2 = mu * mu + mu_t * mu_t + c1;
-        const double f3 = var + var_t + c2;
-        const double inv_f2 = 1.0 / f2, inv_f3 = 1.0 / f3;
-        const double nn = f0 * f1;
-        const double inv_d = inv_f2 * inv_f3;
-        ssim = nn * inv_d;
-        const double a0 = 2.0 * mu_t, a1 = -2.0 * mu_t, b1 = 2.0;
-        const double a2 = 2.0 * mu, a3 = -2.0 * mu, b3 = 2.0;
-        const double A = a0 * f1 + f0 * a1, B = f0 * b1, C = a2 * f3 + f2 * a3, E = f2 * b3;
-        const double inv_d2 = inv_d * inv_d, inv_d3 = inv_d2 * inv_d, inv_norm2 = inv_norm * inv_norm;
-        const double nnd = nn * inv_d;
         double out[9];
-        out[0] = (2.0 * mu_t * (f1 - f0) * inv_d - 2.0 * mu * nnd * inv_f2 + 2.0 * mu * nnd * inv_f3) * inv_norm;
-        out[1] = 2.0 * f0 * inv_d * inv_norm;
-        out[2] = -2.0 * nnd * inv_f3 * inv_norm;
-        out[3] = -2.0 * nn * inv_f2 * inv_f3 * inv_f3 * inv_norm;
-        out[4] = (2.0 * a0 * a1 * inv_d - 2.0 * A * C * inv_d2 - nn * (2.0 * a2 * a3 + 2.0 * f3 - 2.0 * f2) * inv_d2 +
-                  2.0 * nn * C * C * inv_d3) *
-                 inv_norm2;
-        out[5] = (-2.0 * A * E * inv_d2 - 2.0 * nn * a2 * b3 * inv_d2 + 4.0 * nn * C * E * inv_d3) * inv_norm2;
-        out[6] = (2.0 * a0 * b1 * inv_d - 2.0 * B * C * inv_d2) * inv_norm2;
-        out[7] = -2.0 * B * E * inv_d2 * inv_norm2;
-        out[8] = 2.0 * nn * E * E * inv_d3 * inv_norm2;
+        ssim = ssim_centre_fields(st, inv_norm, c1, c2, out);
         const size_t idx = static_cast<size_t>(y) * W + x;
 #pragma unroll
         for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
@@ -286,6 +293,199 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
     if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
 }
 
+// ---------------------------------------------------------------------------
+// 11-tap fast path: 32x32 output tiles, 256 threads. The horizontal pass reads
+// its 14-column input windows straight from global memory (L1-resident tile)
+// and writes 4 outputs per task to shared memory; the vertical pass gives each
+// thread one column x 4 rows and slides the 11 taps over 14 loaded rows, so
+// every shared-memory load feeds ~3 FMAs. Thread t owns pixels
+// (ox + t % 32, oy + 4 (t / 32) + i), i < 4.
+// ---------------------------------------------------------------------------
+constexpr int kFT = 32;              // output tile edge
+constexpr int kFH = 5;               // window half-width (11 taps)
+constexpr int kFS = kFT + 2 * kFH;   // 42 rows / columns incl. halo
+constexpr int kFR = 4;               // outputs per task (both passes)
+
+template <int NF, class Load>
+__device__ __forceinline__ void hpass32(const Window& win, unsigned w2mask, Load load, double (*s_h)[kFS][kFT + 1]) {
+    // task = (f, r, column group of kFR); inputs c0 .. c0 + kFR + 9
+    for (int task = threadIdx.x; task < NF * kFS * (kFT / kFR); task += blockDim.x) {
+        const int f = task / (kFS * (kFT / kFR));
+        const int rem = task - f * kFS * (kFT / kFR);
+        const int r = rem / (kFT / kFR), c0 = (rem - r * (kFT / kFR)) * kFR;
+        const bool w2 = (w2mask >> f) & 1u;  // weights selected by value (no parameter-space pointers)
+        double acc[kFR] = {};
+#pragma unroll
+        for (int k = 0; k < kFR + 2 * kFH; ++k) {
+            const double v = load(f, r, c0 + k);
+#pragma unroll
+            for (int o = 0; o < kFR; ++o)
+                if (k - o >= 0 && k - o <= 2 * kFH) acc[o] += (w2 ? win.w2[k - o] : win.w[k - o]) * v;
+        }
+#pragma unroll
+        for (int o = 0; o < kFR; ++o) s_h[f][r][c0 + o] = acc[o];
+    }
+}
+
+// Vertical pass for the calling thread's column and 4 rows: out[o] = sum_k w[k] s_h[r0 + o + k][c].
+__device__ __forceinline__ void vpass32(const Window& win, bool w2, const double (*s_hf)[kFT + 1], int c, int r0,
+                                        double (&out)[kFR]) {
+#pragma unroll
+    for (int o = 0; o < kFR; ++o) out[o] = 0.0;
+#pragma unroll
+    for (int k = 0; k < kFR + 2 * kFH; ++k) {
+        const double v = s_hf[r0 + k][c];
+#pragma unroll
+        for (int o = 0; o < kFR; ++o)
+            if (k - o >= 0 && k - o <= 2 * kFH) out[o] += (w2 ? win.w2[k - o] : win.w[k - o]) * v;
+    }
+}
+
+__global__ void __launch_bounds__(256) ssim_fields32_k(int W, int H, const double* __restrict__ image,
+                                                       const double* __restrict__ target, Window win, double c1,
+                                                       double c2, double* __restrict__ fields,
+                                                       double* __restrict__ sums, int row0, int own_y0, int own_y1) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [5][kFS][kFT + 1]
+    __shared__ double red[8];
+    const int ch = blockIdx.z;
+    const int ox = blockIdx.x * kFT, oy = (row0 + blockIdx.y) * kFT;
+    const size_t plane = static_cast<size_t>(W) * H;
+    const double* img = image + ch * plane;
+    const double* tgt = target + ch * plane;
+    // Horizontal pass of the 5 statistics (out-of-image taps are zero == skipped taps).
+    for (int task = threadIdx.x; task < kFS * (kFT / kFR); task += blockDim.x) {
+        const int r = task / (kFT / kFR), c0 = (task - r * (kFT / kFR)) * kFR;
+        const int gy = oy - kFH + r;
+        const bool row_in = gy >= 0 && gy < H;
+        double acc[kFR][5] = {};
+#pragma unroll
+        for (int k = 0; k < kFR + 2 * kFH; ++k) {
+            const int gx = ox - kFH + c0 + k;
+            double xv = 0.0, tv = 0.0;
+            if (row_in && gx >= 0 && gx < W) {
+                const size_t idx = static_cast<size_t>(gy) * W + gx;
+                xv = __ldg(img + idx);
+                tv = __ldg(tgt + idx);
+            }
+            const double p[5] = {xv, xv * xv, tv, tv * tv, xv * tv};
+#pragma unroll
+            for (int o = 0; o < kFR; ++o)
+                if (k - o >= 0 && k - o <= 2 * kFH) {
+                    const double wk = win.w[k - o];
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) acc[o][f] += wk * p[f];
+                }
+        }
+#pragma unroll
+        for (int o = 0; o < kFR; ++o)
+#pragma unroll
+            for (int f = 0; f < 5; ++f) s_h[f][r][c0 + o] = acc[o][f];
+    }
+    __syncthreads();
+    const int c = threadIdx.x % kFT, r0 = (threadIdx.x / kFT) * kFR;
+    const int x = ox + c;
+    double st[kFR][5];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+        double o4[kFR];
+        vpass32(win, false, s_h[f], c, r0, o4);
+#pragma unroll
+        for (int o = 0; o < kFR; ++o) st[o][f] = o4[o];
+    }
+    double ssim_own = 0.0;
+    if (x < W) {
+        const double nx = axis_norm(x, W, win);
+#pragma unroll
+        for (int o = 0; o < kFR; ++o) {
+            const int y = oy + r0 + o;
+            if (y >= H) break;
+            double out[9];
+            const double ss = ssim_centre_fields(st[o], 1.0 / (nx * axis_norm(y, H, win)), c1, c2, out);
+            if (y >= own_y0 && y < own_y1) ssim_own += ss;  // owned pixel rows (multi-GPU shard)
+            const size_t idx = static_cast<size_t>(y) * W + x;
+#pragma unroll
+            for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
+        }
+    }
+    const double tot = block_sum(ssim_own, red);
+    if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
+}
+
+__global__ void __launch_bounds__(256) ssim_derivs32_k(int W, int H, const double* __restrict__ image,
+                                                       const double* __restrict__ target, Window win, double lambda,
+                                                       const double* __restrict__ fields, float* __restrict__ grad,
+                                                       float* __restrict__ hess, double* __restrict__ sums, int row0,
+                                                       int own_y0, int own_y1) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [3][kFS][kFT + 1]
+    __shared__ double red[8];
+    const int ch = blockIdx.z;
+    const int ox = blockIdx.x * kFT, oy = (row0 + blockIdx.y) * kFT;
+    const size_t plane = static_cast<size_t>(W) * H;
+    const int c = threadIdx.x % kFT, r0 = (threadIdx.x / kFT) * kFR;
+    const int x = ox + c;
+    const double inv3n = 1.0 / (3.0 * static_cast<double>(plane));
+    double cv[kFR], ctv[kFR];
+#pragma unroll
+    for (int o = 0; o < kFR; ++o) {
+        const int y = oy + r0 + o;
+        cv[o] = ctv[o] = 0.0;
+        if (x < W && y < H) {
+            cv[o] = image[ch * plane + static_cast<size_t>(y) * W + x];
+            ctv[o] = target[ch * plane + static_cast<size_t>(y) * W + x];
+        }
+    }
+    double g_ssim[kFR] = {}, h_ssim[kFR] = {};
+    if (lambda != 0.0) {
+#pragma unroll 1
+        for (int g = 0; g < 3; ++g) {  // fields 3g .. 3g + 2; fp, fq, fr, fkw (0-3) use w, the rest w^2
+            const unsigned w2mask = g == 0 ? 0u : g == 1 ? 6u : 7u;  // field 3g + f uses w^2 iff 3g + f >= 4
+            if (g > 0) __syncthreads();
+            hpass32<3>(win, w2mask,
+                       [&](int f, int r, int cc) -> double {
+                           const int gx = ox - kFH + cc, gy = oy - kFH + r;
+                           if (gx < 0 || gx >= W || gy < 0 || gy >= H) return 0.0;
+                           return __ldg(fields + (static_cast<size_t>(3 * g + f) * 3 + ch) * plane +
+                                        static_cast<size_t>(gy) * W + gx);
+                       },
+                       s_h);
+            __syncthreads();
+            double sv[3][kFR];
+#pragma unroll
+            for (int f = 0; f < 3; ++f) vpass32(win, (w2mask >> f) & 1u, s_h[f], c, r0, sv[f]);
+#pragma unroll
+            for (int o = 0; o < kFR; ++o) {  // loss.hpp:323-327
+                if (g == 0) {
+                    g_ssim[o] += sv[0][o] + ctv[o] * sv[1][o] + cv[o] * sv[2][o];
+                } else if (g == 1) {
+                    h_ssim[o] += sv[0][o] + sv[1][o] + cv[o] * sv[2][o];
+                } else {
+                    h_ssim[o] += ctv[o] * sv[0][o] + cv[o] * ctv[o] * sv[1][o] + cv[o] * cv[o] * sv[2][o];
+                }
+            }
+        }
+    }
+    double dsq_own = 0.0;
+#pragma unroll
+    for (int o = 0; o < kFR; ++o) {
+        const int y = oy + r0 + o;
+        if (x >= W || y >= H) continue;
+        const double d = cv[o] - ctv[o];
+        if (y >= own_y0 && y < own_y1) dsq_own += d * d;
+        double gg = inv3n * d, hh = inv3n;
+        if (lambda != 0.0) {
+            gg += lambda * (-inv3n * g_ssim[o]);
+            hh += lambda * (-inv3n * h_ssim[o]);
+        }
+        const size_t idx = ch * plane + static_cast<size_t>(y) * W + x;
+        grad[idx] = static_cast<float>(gg);
+        hess[idx] = static_cast<float>(hh);
+    }
+    const double tot = block_sum(dsq_own, red);
+    if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
+}
+
 }  // namespace
 
 void compute_loss(ViewSlot& v, cudaStream_t s) {
@@ -334,10 +534,29 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
                                            v.loss_sums.ptr, row0, own0, own1);
         CUDA_LAUNCH_CHECK();
     };
-    if (win.half == 5)  // the reference default (window 11)
-        run(ssim_fields_k<5>, ssim_derivs_k<5>);
-    else
+    if (win.half == kFH) {  // the reference default (window 11): 32x32 register-blocked tiles
+        const int r32a = band_px0 / kFT, r32b = (band_px1 + kFT - 1) / kFT;
+        const dim3 g32((v.W + kFT - 1) / kFT, r32b - r32a, 3);
+        const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1), sm_d = sizeof(double) * 3 * kFS * (kFT + 1);
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(ssim_fields32_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_f));
+            CUDA_CHECK(cudaFuncSetAttribute(ssim_derivs32_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
+            attr = true;
+        }
+        if (ssim) {
+            v.fields.ensure(27 * npx);
+            ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
+                                                   v.loss_sums.ptr, r32a, own0, own1);
+            CUDA_LAUNCH_CHECK();
+        }
+        ssim_derivs32_k<<<g32, 256, ssim ? sm_d : 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.lambda,
+                                                           ssim ? v.fields.ptr : nullptr, v.loss_grad.ptr,
+                                                           v.loss_hess.ptr, v.loss_sums.ptr, r32a, own0, own1);
+        CUDA_LAUNCH_CHECK();
+    } else {
         run(ssim_fields_k<0>, ssim_derivs_k<0>);
+    }
 }
 
 }  // namespace ngsb
