@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(256) ssim_fields32_k(int W, int H, const doubl
     const size_t plane = static_cast<size_t>(W) * H;
     const double* img = image + ch * plane;
     const double* tgt = target + ch * plane;
+    const bool interior = ox >= kFH && oy >= kFH && ox + kFT + kFH <= W && oy + kFT + kFH <= H;
     // Horizontal pass of the 5 statistics (out-of-image taps are zero == skipped taps).
     for (int task = threadIdx.x; task < kFS * (kFT / kFR); task += blockDim.x) {
         const int r = task / (kFT / kFR), c0 = (task - r * (kFT / kFR)) * kFR;
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(256) ssim_fields32_k(int W, int H, const doubl
         for (int k = 0; k < kFR + 2 * kFH; ++k) {
             const int gx = ox - kFH + c0 + k;
             double xv = 0.0, tv = 0.0;
-            if (row_in && gx >= 0 && gx < W) {
+            if (interior || (row_in && gx >= 0 && gx < W)) {
                 const size_t idx = static_cast<size_t>(gy) * W + gx;
                 xv = __ldg(img + idx);
                 tv = __ldg(tgt + idx);
@@ -437,19 +438,30 @@ __global__ void __launch_bounds__(256) ssim_derivs32_k(int W, int H, const doubl
         }
     }
     double g_ssim[kFR] = {}, h_ssim[kFR] = {};
+    const bool interior = ox >= kFH && oy >= kFH && ox + kFT + kFH <= W && oy + kFT + kFH <= H;
     if (lambda != 0.0) {
 #pragma unroll 1
         for (int g = 0; g < 3; ++g) {  // fields 3g .. 3g + 2; fp, fq, fr, fkw (0-3) use w, the rest w^2
             const unsigned w2mask = g == 0 ? 0u : g == 1 ? 6u : 7u;  // field 3g + f uses w^2 iff 3g + f >= 4
             if (g > 0) __syncthreads();
-            hpass32<3>(win, w2mask,
-                       [&](int f, int r, int cc) -> double {
-                           const int gx = ox - kFH + cc, gy = oy - kFH + r;
-                           if (gx < 0 || gx >= W || gy < 0 || gy >= H) return 0.0;
-                           return __ldg(fields + (static_cast<size_t>(3 * g + f) * 3 + ch) * plane +
-                                        static_cast<size_t>(gy) * W + gx);
-                       },
-                       s_h);
+            const double* fbase = fields + (static_cast<size_t>(3 * g) * 3 + ch) * plane +
+                                  static_cast<ptrdiff_t>(oy - kFH) * W + (ox - kFH);
+            if (interior) {  // block-uniform: the whole halo tile is inside the image
+                hpass32<3>(win, w2mask,
+                           [&](int f, int r, int cc) -> double {
+                               return __ldg(fbase + static_cast<size_t>(f) * 3 * plane + static_cast<size_t>(r) * W + cc);
+                           },
+                           s_h);
+            } else {
+                hpass32<3>(win, w2mask,
+                           [&](int f, int r, int cc) -> double {
+                               const int gx = ox - kFH + cc, gy = oy - kFH + r;
+                               if (gx < 0 || gx >= W || gy < 0 || gy >= H) return 0.0;
+                               return __ldg(fields + (static_cast<size_t>(3 * g + f) * 3 + ch) * plane +
+                                            static_cast<size_t>(gy) * W + gx);
+                           },
+                           s_h);
+            }
             __syncthreads();
             double sv[3][kFR];
 #pragma unroll
