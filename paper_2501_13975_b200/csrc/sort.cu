@@ -15,7 +15,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kItems = 8;
-constexpr int kTileItems = kThreads * kItems;  // 2048
+constexpr int kTileItems = kThreads * kItems;  // 2048 (scan tiles)
+constexpr int kSItems = 16;                      // onesweep items per thread
+constexpr int kSTile = kThreads * kSItems;       // 4096 keys per onesweep tile
 constexpr int kDigits = 256;
 
 // ---------------------------------------------------------------------------
@@ -37,10 +39,10 @@ __global__ void __launch_bounds__(kThreads) radix_global_hist_k(const uint32_t* 
     const int n = *d_n;
     for (int p = 0; p < passes; ++p) s_hist[p][threadIdx.x] = 0;
     __syncthreads();
-    const int base = blockIdx.x * kTileItems;
+    const int base = blockIdx.x * kSTile;
     if (base < n) {
 #pragma unroll
-        for (int r = 0; r < kItems; ++r) {
+        for (int r = 0; r < kSItems; ++r) {
             const int i = base + r * kThreads + threadIdx.x;
             if (i < n) {
                 const uint32_t k = keys[i];
@@ -95,8 +97,8 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __r
     __shared__ unsigned s_wc[kThreads / 32][kDigits];  // per-warp digit counts -> per-warp exclusive prefix
     __shared__ unsigned s_bstart[kDigits];             // block-local digit starts
     __shared__ unsigned s_gbase[kDigits];              // global position of the block's first item of each digit
-    __shared__ uint32_t s_k[kTileItems];
-    __shared__ int s_v[kTileItems];
+    __shared__ uint32_t s_k[kSTile];
+    __shared__ int s_v[kSTile];
     __shared__ unsigned s_warp[kThreads / 32];
     __shared__ int s_tile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -106,16 +108,16 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __r
     __syncthreads();
     const int tile = s_tile;
     const int n = *d_n;
-    const int base = tile * kTileItems;
+    const int base = tile * kSTile;
     if (base >= n) return;
 
     // 1. Stable ranks inside each warp's contiguous 256-item range.
-    uint32_t key[kItems];
-    int val[kItems];
-    unsigned wrank[kItems];
+    uint32_t key[kSItems];
+    int val[kSItems];
+    unsigned wrank[kSItems];
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int i = base + warp * (kItems * 32) + r * 32 + lane;
+    for (int r = 0; r < kSItems; ++r) {
+        const int i = base + warp * (kSItems * 32) + r * 32 + lane;
         const bool valid = i < n;
         key[r] = valid ? keys_in[i] : 0u;
         val[r] = valid ? vals_in[i] : 0;
@@ -163,8 +165,8 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __r
     __syncthreads();
     // 4. Local placement in digit order, then contiguous global stores.
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int i = base + warp * (kItems * 32) + r * 32 + lane;
+    for (int r = 0; r < kSItems; ++r) {
+        const int i = base + warp * (kSItems * 32) + r * 32 + lane;
         if (i < n) {
             const int digit = static_cast<int>((key[r] >> shift) & 0xFF);
             const unsigned lpos = s_bstart[digit] + s_wc[warp][digit] + wrank[r];
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __r
         }
     }
     __syncthreads();
-    const int cnt = min(kTileItems, n - base);
+    const int cnt = min(kSTile, n - base);
     for (int i = threadIdx.x; i < cnt; i += kThreads) {
         const uint32_t k = s_k[i];
         const int digit = static_cast<int>((k >> shift) & 0xFF);
@@ -282,19 +284,20 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 }  // namespace
 
 void SortScratch::ensure(int n_max) {
-    const int nb = cdiv(std::max(n_max, 1), kTileItems);
+    const int nb = cdiv(std::max(n_max, 1), kSTile);
+    const int nbs = cdiv(std::max(n_max, 1), kTileItems);
     // one memset clears: hist [passes][256], tickets [passes], status [passes][nb][256]
     onesweep.ensure(static_cast<size_t>(kMaxPasses) * kDigits + kMaxPasses +
                     static_cast<size_t>(kMaxPasses) * nb * kDigits);
     dstart.ensure(static_cast<size_t>(kMaxPasses) * kDigits);
-    sums.ensure(nb + 1);
+    sums.ensure(nbs + 1);
 }
 
 void radix_sort_pairs(uint32_t* keys, int* vals, uint32_t* keys_alt, int* vals_alt, const int* d_n, int n_max,
                       int bits, SortScratch& sc, cudaStream_t s) {
     if (n_max <= 0) return;
     sc.ensure(n_max);
-    const int nb = cdiv(n_max, kTileItems);
+    const int nb = cdiv(n_max, kSTile);
     const int passes = cdiv(bits, 8);
     if (passes > kMaxPasses) throw Error(NGS_ERR_INTERNAL, "radix sort: more than 32 key bits");
     unsigned* hist = sc.onesweep.ptr;
