@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define NGS_ABI_VERSION 1
+#define NGS_ABI_VERSION 2
 #define NGS_SH_COEFFS 16        /* scene.hpp:11 kShCoeffsPerChannel */
 #define NGS_MAX_VIEW_SLOTS 16   /* primary + up to 15 secondary view contexts */
 
@@ -120,7 +120,16 @@ typedef struct {
     ngs_loss_config loss;
     int32_t host_targets;    /* CUDA: keep targets in pinned host memory and
                                 upload the step's 1+K images inside each step */
+    int32_t probe_cadence;   /* TrainConfig::probe_cadence: probe every N steps in run() */
 } ngs_train_config;
+
+/* Trainer::ProbeMetrics (trainer.hpp:209-213); also one view's
+ * total_loss_value / psnr / ssim_metric (loss.hpp:359-375, metrics.hpp:14-30). */
+typedef struct {
+    double loss;
+    double psnr;
+    double ssim;
+} ngs_metrics;
 
 /* trainer.hpp:90-98 IterationReport */
 typedef struct {
@@ -253,6 +262,23 @@ int32_t ngs_trainer_neighbors(ngs_context* ctx, int32_t view_id, int32_t* out, i
 /* Trainer::step(view_id) — one Newton step on one training view. */
 int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_iteration_report* report);
 int32_t ngs_trainer_barrier_weight(ngs_context* ctx, double* out);
+/* Trainer::probe_metrics (trainer.hpp:215-233): render every probe view (the
+ * training views when there are none), mean total_loss_value / psnr (inf
+ * counted as 99) / ssim_metric. */
+int32_t ngs_trainer_probe(ngs_context* ctx, ngs_metrics* out);
+/* Trainer::run (trainer.hpp:238-277) without the CSV / checkpoint I/O: rows[0]
+ * is the initial probe row (step 0), then one row per step over `epochs`
+ * epochs of the train ids shuffled by the config-seeded Rng (core.hpp:52-81),
+ * re-probing every probe_cadence steps and decaying the barrier weight per
+ * epoch. *n_rows = 1 + epochs * n_train (capacity must be at least that). */
+int32_t ngs_trainer_run(ngs_context* ctx, ngs_iteration_report* rows, int32_t capacity, int32_t* n_rows);
+
+/* ---- evaluation (metrics.hpp, loss.hpp:359-375) ------------------------ */
+/* render(scene, camera, raster) against target_rgb (3*w*h doubles,
+ * interleaved): total_loss_value, psnr (+inf for identical images) and
+ * ssim_metric (mean SSIM over channels with the loss config's window). */
+int32_t ngs_view_metrics(ngs_context* ctx, const ngs_camera* camera, const double* target_rgb,
+                         const ngs_raster_options* raster, const ngs_loss_config* loss, ngs_metrics* out);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@
 
 #include <array>
 #include <memory>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -115,6 +116,7 @@ inline ngs_newton_options newton_defaults() { ngs_newton_options o; ngs_newton_o
 inline ngs_train_config train_defaults() { ngs_train_config o; ngs_train_config_default(&o); return o; }
 
 using IterationReport = ngs_iteration_report;  // trainer.hpp:90-98
+using ProbeMetrics = ngs_metrics;             // trainer.hpp:209-213 (loss, psnr, ssim)
 
 // Per-field host arrays for the C-ABI scene (scene.hpp layout -> ngs_scene).
 struct SceneArrays {
@@ -193,6 +195,16 @@ public:
         return img;
     }
 
+    // total_loss_value / psnr / ssim_metric of render(scene, cam) against target
+    // (loss.hpp:359-375, metrics.hpp:14-30).
+    ProbeMetrics view_metrics(const Camera& cam, const Image& target, const ngs_raster_options& ro = raster_defaults(),
+                              const ngs_loss_config& lc = loss_defaults()) const {
+        ProbeMetrics m{};
+        const ngs_camera c = cam.c();
+        check(ngs_view_metrics(get(), &c, target.data.data(), &ro, &lc, &m));
+        return m;
+    }
+
     // build_view_context — newton.hpp:101-118; returns the loss value.
     double build_view(int slot, const Camera& cam, const Image& target,
                       const ngs_raster_options& r = raster_defaults(), const ngs_loss_config& l = loss_defaults()) {
@@ -258,7 +270,7 @@ struct Dataset {
 class Trainer {
 public:
     Trainer(const Scene& scene, const Dataset& ds, const ngs_train_config& cfg = train_defaults(), int device = 0)
-        : ctx_(device) {
+        : ctx_(device), epochs_(cfg.epochs), n_train_(static_cast<int>(ds.train_ids.size())) {
         ctx_.set_scene(scene);
         std::vector<ngs_camera> cams;
         std::vector<const double*> tg, st;
@@ -287,11 +299,37 @@ public:
         check(ngs_trainer_barrier_weight(ctx_.get(), &w));
         return w;
     }
+    // Trainer::probe_metrics — trainer.hpp:215-233.
+    ProbeMetrics probe_metrics() {
+        ProbeMetrics m{};
+        check(ngs_trainer_probe(ctx_.get(), &m));
+        return m;
+    }
+    // Trainer::run — trainer.hpp:238-277 (CSV rows as the reference writes them;
+    // checkpoints are not part of this library).
+    std::vector<IterationReport> run(std::ostream* csv = nullptr) {
+        std::vector<IterationReport> rows(1 + static_cast<size_t>(epochs_ > 0 ? epochs_ : 0) * n_train_);
+        int32_t n = 0;
+        check(ngs_trainer_run(ctx_.get(), rows.data(), static_cast<int32_t>(rows.size()), &n));
+        rows.resize(n);
+        if (csv) {
+            *csv << "step,image_id,probe_loss,psnr,ssim,dt_ms\n";
+            for (const auto& r : rows) {
+                *csv << r.step << ',' << r.image_id << ',';
+                const auto old = csv->precision(17);
+                *csv << r.probe_loss << ',' << r.probe_psnr << ',' << r.probe_ssim;
+                csv->precision(old);
+                *csv << ',' << r.dt_ms << '\n';
+            }
+        }
+        return rows;
+    }
     Scene scene() const { return ctx_.scene(); }
     Context& context() { return ctx_; }
 
 private:
     Context ctx_;
+    int epochs_ = 1, n_train_ = 0;
 };
 
 }  // namespace ngs::b200

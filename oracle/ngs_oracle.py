@@ -564,6 +564,85 @@ def total_loss_derivs(img, tgt, cfg):
     return value, grad + lam * gs, hess + lam * hs
 
 
+def ssim_mean_value(img, tgt, cfg):
+    """ssim_mean_value (loss.hpp:378-382): mean SSIM map over channels and pixels."""
+    H, W, _ = img.shape
+    if W < cfg["window"] or H < cfg["window"]:
+        raise InvalidInput("ssim stats: image smaller than the filter window")
+    w = gaussian_window(cfg["window"], cfg["window_sigma"])
+    inv_norm = 1.0 / np.outer(axis_norms(H, w), axis_norms(W, w))
+    c1, c2 = cfg["c1"], cfg["c2"]
+    total = 0.0
+    for ch in range(3):
+        c, t = img[:, :, ch], tgt[:, :, ch]
+        mu = sep_conv(c, w) * inv_norm
+        mu_t = sep_conv(t, w) * inv_norm
+        var = np.maximum(0.0, sep_conv(c * c, w) * inv_norm - mu * mu)
+        var_t = np.maximum(0.0, sep_conv(t * t, w) * inv_norm - mu_t * mu_t)
+        cov = sep_conv(c * t, w) * inv_norm - mu * mu_t
+        total += float(((2 * mu * mu_t + c1) * (2 * cov + c2) / ((mu * mu + mu_t * mu_t + c1) * (var + var_t + c2))).sum())
+    return total / (3.0 * H * W)
+
+
+def total_loss_value(img, tgt, cfg):
+    """total_loss_value (loss.hpp:359-375): value-only L2 + lambda (1 - mean SSIM)."""
+    d = img - tgt
+    value = 0.5 * float((d * d).sum()) / (3.0 * img.shape[0] * img.shape[1])
+    if cfg["lambda"] != 0.0:
+        value += cfg["lambda"] * (1.0 - ssim_mean_value(img, tgt, cfg))
+    return value
+
+
+def psnr(img, tgt):
+    """psnr (metrics.hpp:14-24): dB over all pixels and channels, +inf if identical."""
+    d = img - tgt
+    mse = float((d * d).sum()) / d.size
+    return math.inf if mse == 0.0 else -10.0 * math.log10(mse)
+
+
+class Rng:
+    """ngs::Rng (core.hpp:52-81): std::mt19937_64 (restated: MT19937-64 of the
+    C++ standard, [rand.eng.mers]) with the reference's uniform/index/shuffle."""
+
+    N, M = 312, 156
+    MASK = (1 << 64) - 1
+
+    def __init__(self, seed=5489):
+        self.mt = [0] * self.N
+        self.mt[0] = seed & self.MASK
+        for i in range(1, self.N):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & self.MASK
+        self.i = self.N
+
+    def _twist(self):
+        up, lo = 0xFFFFFFFF80000000, 0x7FFFFFFF
+        for k in range(self.N):
+            x = (self.mt[k] & up) | (self.mt[(k + 1) % self.N] & lo)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            self.mt[k] = self.mt[(k + self.M) % self.N] ^ xa
+        self.i = 0
+
+    def next(self):
+        if self.i >= self.N:
+            self._twist()
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self.MASK
+
+    def shuffle(self, v):
+        """core.hpp:76-81: for i = n..2: swap(v[i-1], v[engine() % i])."""
+        for i in range(len(v), 1, -1):
+            j = self.next() % i
+            v[i - 1], v[j] = v[j], v[i - 1]
+        return v
+
+
 # ---------------------------------------------------------------------------
 # newton.hpp
 # ---------------------------------------------------------------------------
@@ -1063,6 +1142,7 @@ class OracleTrainer:
                  secondary_downsample=0, knn=3, downsample=4, order=(0, 1, 2, 3, 4), raster=None, loss=None,
                  newton=None):
         self.ctx = ctx
+        self.train_ids = list(train_ids)
         self.cams = [Cam.of(c) for c in cameras]
         self.targets = [np.asarray(t, np.float64) for t in targets]
         self.raster = _opts(raster, DEFAULT_RASTER)
@@ -1086,6 +1166,36 @@ class OracleTrainer:
                 self.down_targets.append(st)
             else:
                 self.down_targets.append(downsample_box(self.targets[i], f))
+
+    def probe_metrics(self, probe_ids=()):
+        """Trainer::probe_metrics (trainer.hpp:215-233)."""
+        ids = list(probe_ids) if len(probe_ids) else list(self.train_ids)
+        loss = ps = ss = 0.0
+        for i in ids:
+            img = self.ctx.render(self.cams[i], self.raster)
+            loss += total_loss_value(img, self.targets[i], self.loss)
+            p = psnr(img, self.targets[i])
+            ps += 99.0 if math.isinf(p) else p
+            ss += ssim_mean_value(img, self.targets[i], self.loss)
+        n = float(len(ids))
+        return loss / n, ps / n, ss / n
+
+    def run(self, epochs=1, seed=0, probe_cadence=1, probe_ids=(), barrier_decay=0.5, barrier_floor=1e-6):
+        """Trainer::run (trainer.hpp:238-277): [(step, image_id, probe metrics, delta norms)]."""
+        rng = Rng(seed)
+        last = self.probe_metrics(probe_ids)
+        rows = [(0, -1, last, np.zeros(5))]
+        step = 0
+        for _ in range(epochs):
+            order = rng.shuffle(list(self.train_ids))
+            for vid in order:
+                norms = self.step(vid)
+                step += 1
+                if probe_cadence > 0 and step % probe_cadence == 0:
+                    last = self.probe_metrics(probe_ids)
+                rows.append((step, vid, last, norms))
+            self.barrier = max(barrier_floor, self.barrier * barrier_decay)
+        return rows
 
     def _views(self, view_id):
         snap = self.ctx._snapshot()

@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "ngs/metrics.hpp"
 #include "ngs/newton.hpp"
 #include "ngs/rasterizer.hpp"
 #include "ngs/secondary.hpp"
@@ -172,6 +173,7 @@ void ngs_train_config_default(ngs_train_config* out) {
     ngs_raster_options_default(&out->raster);
     ngs_loss_config_default(&out->loss);
     out->host_targets = 0;
+    out->probe_cadence = t.probe_cadence;
 }
 
 int32_t ngs_context_create(int32_t /*device*/, ngs_context** out) {
@@ -558,6 +560,7 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
         cfg.newton = to_newton(&c->newton);
         cfg.raster = to_raster(&c->raster);
         cfg.loss = to_loss(&c->loss);
+        cfg.probe_cadence = c->probe_cadence;
         ctx->trainer.reset();
         ctx->trainer.emplace(ctx->scene, std::move(ds), std::move(cfg));
     });
@@ -586,6 +589,45 @@ int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_iteration_report
             for (int i = 0; i < 5; ++i) report->delta_norms[i] = r.delta_norms[i];
             report->dt_ms = r.dt_ms;
         }
+    });
+}
+
+static void to_report(const ngs::IterationReport& r, ngs_iteration_report* report) {
+    report->step = r.step;
+    report->image_id = r.image_id;
+    report->probe_loss = r.probe_loss;
+    report->probe_psnr = r.probe_psnr;
+    report->probe_ssim = r.probe_ssim;
+    for (int i = 0; i < 5; ++i) report->delta_norms[i] = r.delta_norms[i];
+    report->dt_ms = r.dt_ms;
+}
+
+int32_t ngs_trainer_probe(ngs_context* ctx, ngs_metrics* out) {
+    return guarded([&] {
+        if (!ctx->trainer) throw ngs::InvalidInput("trainer not configured");
+        const auto m = ctx->trainer->probe_metrics();
+        *out = {m.loss, m.psnr, m.ssim};
+    });
+}
+
+int32_t ngs_trainer_run(ngs_context* ctx, ngs_iteration_report* rows, int32_t capacity, int32_t* n_rows) {
+    return guarded([&] {
+        if (!ctx->trainer) throw ngs::InvalidInput("trainer not configured");
+        const std::vector<ngs::IterationReport> r = ctx->trainer->run(nullptr);
+        if (static_cast<int32_t>(r.size()) > capacity) throw ngs::InvalidInput("trainer run: rows capacity too small");
+        for (size_t i = 0; i < r.size(); ++i) to_report(r[i], rows + i);
+        *n_rows = static_cast<int32_t>(r.size());
+    });
+}
+
+int32_t ngs_view_metrics(ngs_context* ctx, const ngs_camera* camera, const double* target_rgb,
+                         const ngs_raster_options* raster, const ngs_loss_config* loss, ngs_metrics* out) {
+    return guarded([&] {
+        const ngs::Camera cam = to_camera(*camera);
+        const ngs::Image img = ngs::render(ctx->current(), cam, to_raster(raster)).image;
+        const ngs::Image tgt = to_image(target_rgb, cam.width, cam.height);
+        const ngs::LossConfig lc = to_loss(loss);
+        *out = {ngs::total_loss_value(img, tgt, lc), ngs::psnr(img, tgt), ngs::ssim_metric(img, tgt, lc)};
     });
 }
 

@@ -85,7 +85,11 @@ class ngs_train_config(C.Structure):
     _fields_ = [("order", C.c_int32 * 5), ("epochs", C.c_int32), ("seed", C.c_uint64), ("knn", C.c_int32),
                 ("secondary_downsample", C.c_int32), ("threads", C.c_int32), ("barrier_decay", C.c_double),
                 ("barrier_floor", C.c_double), ("newton", ngs_newton_options), ("raster", ngs_raster_options),
-                ("loss", ngs_loss_config), ("host_targets", C.c_int32)]
+                ("loss", ngs_loss_config), ("host_targets", C.c_int32), ("probe_cadence", C.c_int32)]
+
+
+class ngs_metrics(C.Structure):
+    _fields_ = [("loss", C.c_double), ("psnr", C.c_double), ("ssim", C.c_double)]
 
 
 class ngs_iteration_report(C.Structure):
@@ -135,6 +139,7 @@ EXPORTED_SYMBOLS = (
     "ngs_get_scene_info", "ngs_get_scene", "ngs_render", "ngs_build_view", "ngs_get_view_info",
     "ngs_view_splats", "ngs_view_image", "ngs_view_loss_derivs", "ngs_accumulate", "ngs_newton_step",
     "ngs_trainer_configure", "ngs_trainer_neighbors", "ngs_trainer_step", "ngs_trainer_barrier_weight",
+    "ngs_trainer_probe", "ngs_trainer_run", "ngs_view_metrics",
 )
 
 
@@ -433,6 +438,30 @@ class Context:
         rep = ngs_iteration_report()
         self._call("ngs_trainer_step", C.c_int32(view_id), C.byref(rep))
         return rep
+
+    def trainer_probe(self) -> ngs_metrics:
+        """Trainer::probe_metrics (trainer.hpp:215-233)."""
+        m = ngs_metrics()
+        self._call("ngs_trainer_probe", C.byref(m))
+        return m
+
+    def trainer_run(self, epochs: int, n_train: int) -> list:
+        """Trainer::run (trainer.hpp:238-277) without CSV/checkpoints; returns the rows."""
+        cap = 1 + max(epochs, 0) * n_train
+        rows = (ngs_iteration_report * cap)()
+        n = C.c_int32()
+        self._call("ngs_trainer_run", rows, C.c_int32(cap), C.byref(n))
+        return [rows[i] for i in range(n.value)]
+
+    def view_metrics(self, camera: Camera, target: np.ndarray, raster=None, loss=None) -> ngs_metrics:
+        """total_loss_value / psnr / ssim_metric of render(scene, camera) vs target (metrics.hpp)."""
+        t = np.ascontiguousarray(target, dtype=np.float64)
+        assert t.shape == (camera.height, camera.width, 3)
+        r = raster if raster is not None else self.L.default_raster()
+        l = loss if loss is not None else self.L.default_loss()
+        m = ngs_metrics()
+        self._call("ngs_view_metrics", C.byref(camera.to_c()), _dptr(t), C.byref(r), C.byref(l), C.byref(m))
+        return m
 
     # measurement hooks (include/ngs_b200_profile.h; CUDA library only)
     def profile_enable(self, on: bool = True):

@@ -12,9 +12,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <numeric>
 #include <string>
+#include <random>
 #include <vector>
 
 #include "backward.h"
@@ -99,6 +101,8 @@ struct TrainerState {
     std::vector<double*> host_targets, host_down_targets;
     double barrier_weight = 1e-4;
     int step_count = 0;
+    double probe_loss_cache = 0.0;  // trainer.hpp:186-188, 231
+    std::mt19937_64 rng;            // Rng(config.seed), core.hpp:52-81
     std::vector<ViewSlot> views;  // primary + secondaries of the current step
     void release() {
         for (auto& t : targets) t.release();
@@ -436,6 +440,7 @@ void ngs_train_config_default(ngs_train_config* out) {
     ngs_raster_options_default(&out->raster);
     ngs_loss_config_default(&out->loss);
     out->host_targets = 0;
+    out->probe_cadence = 1;
 }
 
 int32_t ngs_context_create(int32_t device, ngs_context** out) {
@@ -975,6 +980,8 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
         T.probe_ids.assign(probe_ids, probe_ids + std::max(n_probe, 0));
         T.barrier_weight = c->newton.barrier_weight;
         T.step_count = 0;
+        T.probe_loss_cache = 0.0;
+        T.rng.seed(c->seed);
         // fit_bounding_sphere (secondary.hpp:24-36) over the current kernel centres.
         const int n = ctx->scene.n;
         std::vector<float4> ps(n);
@@ -1133,6 +1140,8 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
         if (!T.active) throw Error(NGS_ERR_INVALID_INPUT, "trainer not configured");
         if (view_id < 0 || view_id >= static_cast<int>(T.cameras.size()))
             throw Error(NGS_ERR_INVALID_INPUT, "trainer: view id out of range");
+        if (!std::isfinite(T.probe_loss_cache))
+            throw Error(NGS_ERR_NUMERICAL, "trainer: non-finite probe loss, aborting");
         const std::vector<int>& nbrs = T.neighbors[view_id];
         const int nv = 1 + static_cast<int>(nbrs.size());
         std::vector<ViewSlot*> views(nv);
@@ -1217,12 +1226,132 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
         if (report) {
             report->step = T.step_count;
             report->image_id = view_id;
-            report->probe_loss = 0;
+            report->probe_loss = 0;  // IterationReport defaults (trainer.hpp:90-98)
             report->probe_psnr = 0;
-            report->probe_ssim = 0;
+            report->probe_ssim = 1;
             for (int i = 0; i < 5; ++i) report->delta_norms[i] = std::sqrt(norms[i]);
             report->dt_ms = ms;
         }
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Evaluation: metrics.hpp, total_loss_value (loss.hpp:359-375), probe_metrics
+// and run (trainer.hpp:215-277)
+// ---------------------------------------------------------------------------
+
+namespace {
+
+// Renders `cam` into the scratch slot (full image, never sharded) and returns
+// (sum (c - c^t)^2, sum SSIM) against the planar FP64 target already in the slot.
+void metrics_of_slot(ngs_context* ctx, ViewSlot& v, const ngs_loss_config& lc, ngs_metrics* out) {
+    v.loss = to_loss(&lc);
+    compute_loss_value(v, ctx->stream);
+    double sums[2];
+    CUDA_CHECK(cudaMemcpyAsync(sums, v.loss_sums.ptr, sizeof(sums), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->check_err();
+    const double n3 = 3.0 * static_cast<double>(v.W) * v.H;
+    const double mse = sums[0] / n3;
+    out->loss = 0.5 * mse + (lc.lambda != 0.0 ? lc.lambda * (1.0 - sums[1] / n3) : 0.0);
+    out->psnr = mse == 0.0 ? std::numeric_limits<double>::infinity() : -10.0 * std::log10(mse);
+    out->ssim = sums[1] / n3;
+}
+
+void render_scratch(ngs_context* ctx, const ngs_camera& cam, const ngs_raster_options* ro) {
+    ViewSlot& v = ctx->slots[kScratchSlot];
+    upload_camera(cam, v.cam);
+    v.raster = to_raster(ro);
+    render_view(ctx->scene, v, false, ctx->err.ptr, ctx->stream);
+}
+
+ngs_metrics trainer_probe(ngs_context* ctx) {
+    TrainerState& T = ctx->trainer;
+    const std::vector<int>& ids = T.probe_ids.empty() ? T.train_ids : T.probe_ids;
+    ngs_metrics acc{0.0, 0.0, 0.0};
+    ViewSlot& v = ctx->slots[kScratchSlot];
+    for (int id : ids) {
+        render_scratch(ctx, T.cameras[id], &T.cfg.raster);
+        const size_t npx = static_cast<size_t>(v.W) * v.H;
+        v.target.ensure(3 * npx);
+        const double* src = T.cfg.host_targets ? T.host_targets[id] : T.targets[id].ptr;
+        CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx, cudaMemcpyDefault, ctx->stream));
+        ngs_metrics m;
+        metrics_of_slot(ctx, v, T.cfg.loss, &m);
+        acc.loss += m.loss;
+        acc.psnr += std::isinf(m.psnr) ? 99.0 : m.psnr;
+        acc.ssim += m.ssim;
+    }
+    const double n = static_cast<double>(ids.size());
+    acc.loss /= n;
+    acc.psnr /= n;
+    acc.ssim /= n;
+    T.probe_loss_cache = acc.loss;
+    return acc;
+}
+
+}  // namespace
+
+extern "C" int32_t ngs_view_metrics(ngs_context* ctx, const ngs_camera* camera, const double* target_rgb,
+                                    const ngs_raster_options* raster, const ngs_loss_config* loss, ngs_metrics* out) {
+    return guarded([&] {
+        ProfInstall pi(ctx);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        render_scratch(ctx, *camera, raster);
+        ViewSlot& v = ctx->slots[kScratchSlot];
+        const size_t npx = static_cast<size_t>(v.W) * v.H;
+        std::vector<double> tgt;
+        interleaved_to_planar(target_rgb, camera->width, camera->height, tgt);
+        v.target.ensure(3 * npx);
+        CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, tgt.data(), sizeof(double) * 3 * npx, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+        ngs_loss_config lc;
+        if (loss) lc = *loss;
+        else ngs_loss_config_default(&lc);
+        metrics_of_slot(ctx, v, lc, out);  // synchronises (tgt stays alive until then)
+    });
+}
+
+extern "C" int32_t ngs_trainer_probe(ngs_context* ctx, ngs_metrics* out) {
+    return guarded([&] {
+        ProfInstall pi(ctx);
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (!ctx->trainer.active) throw Error(NGS_ERR_INVALID_INPUT, "trainer not configured");
+        *out = trainer_probe(ctx);
+    });
+}
+
+extern "C" int32_t ngs_trainer_run(ngs_context* ctx, ngs_iteration_report* rows, int32_t capacity, int32_t* n_rows) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        TrainerState& T = ctx->trainer;
+        if (!T.active) throw Error(NGS_ERR_INVALID_INPUT, "trainer not configured");
+        const long need = 1 + static_cast<long>(std::max(T.cfg.epochs, 0)) * static_cast<long>(T.train_ids.size());
+        if (!rows || capacity < need) throw Error(NGS_ERR_INVALID_INPUT, "trainer run: rows capacity too small");
+        int r = 0;
+        ngs_iteration_report initial{};
+        initial.image_id = -1;
+        const ngs_metrics m0 = trainer_probe(ctx);
+        initial.probe_loss = m0.loss;
+        initial.probe_psnr = m0.psnr;
+        initial.probe_ssim = m0.ssim;
+        rows[r++] = initial;
+        ngs_metrics last = m0;
+        for (int epoch = 0; epoch < T.cfg.epochs; ++epoch) {
+            std::vector<int> order = T.train_ids;
+            for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[T.rng() % i]);  // Rng::shuffle
+            for (int view_id : order) {
+                ngs_iteration_report rep{};
+                const int32_t st = ngs_trainer_step(ctx, view_id, &rep);
+                if (st != NGS_OK) throw Error(st, ngs_last_error());
+                if (T.cfg.probe_cadence > 0 && T.step_count % T.cfg.probe_cadence == 0) last = trainer_probe(ctx);
+                rep.probe_loss = last.loss;
+                rep.probe_psnr = last.psnr;
+                rep.probe_ssim = last.ssim;
+                rows[r++] = rep;
+            }
+            T.barrier_weight = std::max(T.cfg.barrier_floor, T.barrier_weight * T.cfg.barrier_decay);
+        }
+        *n_rows = r;
     });
 }
 

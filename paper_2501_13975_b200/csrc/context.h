@@ -205,5 +205,6 @@ struct RenderSync {
 void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
                  const RenderSync& sync = RenderSync{});
 void compute_loss(ViewSlot& v, cudaStream_t s);
+void compute_loss_value(ViewSlot& v, cudaStream_t s);  // sums only (metrics)
 
 }  // namespace ngsb

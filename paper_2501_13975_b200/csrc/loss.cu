@@ -81,6 +81,32 @@ __device__ __forceinline__ double ssim_centre_fields(const double (&st)[5], doub
     return ssim;
 }
 
+// SSIM value alone (ssim_value_and_derivs with want_derivs = false, loss.hpp:262-277).
+__device__ __forceinline__ double ssim_value_only(const double (&st)[5], double inv_norm, double c1, double c2) {
+    const double mu = st[0] * inv_norm, mu_t = st[2] * inv_norm;
+    const double var = fmax(0.0, st[1] * inv_norm - mu * mu);
+    const double var_t = fmax(0.0, st[3] * inv_norm - mu_t * mu_t);
+    const double cov = st[4] * inv_norm - mu * mu_t;
+    const double f0 = 2.0 * mu * mu_t + c1, f1 = 2.0 * cov + c2;
+    const double f2 = mu * mu + mu_t * mu_t + c1, f3 = var + var_t + c2;
+    return (f0 * f1) / (f2 * f3);
+}
+
+// Sum of squared differences of two planar images (the L2 part of
+// total_loss_value and the PSNR numerator, loss.hpp:363-368, metrics.hpp:16-20).
+__global__ void __launch_bounds__(256) l2_sum_k(const double* __restrict__ a, const double* __restrict__ b, size_t n,
+                                                double* __restrict__ sum) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double d = a[i] - b[i];
+        acc += d * d;
+    }
+    const double tot = block_sum(acc, red);
+    if (threadIdx.x == 0) atomicAdd(sum, tot);
+}
+
 // Separable valid-tap convolutions over a (kLT + 2h)^2 shared-memory halo tile.
 // HT > 0 fixes the window half-width at compile time (the default 11-tap
 // window: fully unrolled, register-blocked two outputs per horizontal task);
@@ -198,11 +224,15 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
                 for (int f = 0; f < 5; ++f) st[f] += win.w[k] * s_h[f][ly + k][lx];
         }
         const double inv_norm = 1.0 / (axis_norm(x, W, win) * axis_norm(y, H, win));
-        double out[9];
-        ssim = ssim_centre_fields(st, inv_norm, c1, c2, out);
-        const size_t idx = static_cast<size_t>(y) * W + x;
+        if (fields) {
+            double out[9];
+            ssim = ssim_centre_fields(st, inv_norm, c1, c2, out);
+            const size_t idx = static_cast<size_t>(y) * W + x;
 #pragma unroll
-        for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
+            for (int f = 0; f < 9; ++f) fields[(static_cast<size_t>(f) * 3 + ch) * plane + idx] = out[f];
+        } else {
+            ssim = ssim_value_only(st, inv_norm, c1, c2);  // value-only path (metrics)
+        }
     }
     const bool own = y >= own_y0 && y < own_y1;  // owned pixel rows (multi-GPU shard)
     const double tot = block_sum(own ? ssim : 0.0, red);
@@ -401,8 +431,13 @@ __global__ void __launch_bounds__(256) ssim_fields32_k(int W, int H, const doubl
         for (int o = 0; o < kFR; ++o) {
             const int y = oy + r0 + o;
             if (y >= H) break;
+            const double inv_norm = 1.0 / (nx * axis_norm(y, H, win));
+            if (!fields) {  // value-only path (metrics)
+                if (y >= own_y0 && y < own_y1) ssim_own += ssim_value_only(st[o], inv_norm, c1, c2);
+                continue;
+            }
             double out[9];
-            const double ss = ssim_centre_fields(st[o], 1.0 / (nx * axis_norm(y, H, win)), c1, c2, out);
+            const double ss = ssim_centre_fields(st[o], inv_norm, c1, c2, out);
             if (y >= own_y0 && y < own_y1) ssim_own += ss;  // owned pixel rows (multi-GPU shard)
             const size_t idx = static_cast<size_t>(y) * W + x;
 #pragma unroll
@@ -569,6 +604,47 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     } else {
         run(ssim_fields_k<0>, ssim_derivs_k<0>);
     }
+}
+
+void compute_loss_value(ViewSlot& v, cudaStream_t s) {
+    // Value-only evaluation of the whole image: sums[0] = sum (c - c^t)^2, sums[1] =
+    // sum of the per-pixel SSIM over channels (always, for ssim_metric).
+    const LossParams& L = v.loss;
+    if (L.window < 3 || L.window % 2 == 0) throw Error(NGS_ERR_INVALID_INPUT, "loss: window must be odd and >= 3");
+    if (L.window > 2 * kMaxHalf + 1) throw Error(NGS_ERR_INVALID_INPUT, "loss: window larger than 21 unsupported");
+    if (v.W < L.window || v.H < L.window)
+        throw Error(NGS_ERR_INVALID_INPUT, "ssim stats: image smaller than the filter window");
+    Window win{};
+    win.half = L.window / 2;
+    double sum = 0;
+    for (int i = 0; i < L.window; ++i) {
+        const double d = i - win.half;
+        win.w[i] = std::exp(-d * d / (2.0 * L.window_sigma * L.window_sigma));
+        sum += win.w[i];
+    }
+    for (int i = 0; i < L.window; ++i) {
+        win.w[i] /= sum;
+        win.w2[i] = win.w[i] * win.w[i];
+    }
+    const size_t npx = static_cast<size_t>(v.W) * v.H;
+    v.loss_sums.ensure(2);
+    CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * sizeof(double), s));
+    StageScope st(NGS_STAGE_LOSS, s, 2);
+    l2_sum_k<<<std::min<size_t>((3 * npx + 255) / 256, 4 * 148), 256, 0, s>>>(v.image.ptr, v.target.ptr, 3 * npx,
+                                                                           v.loss_sums.ptr);
+    CUDA_LAUNCH_CHECK();
+    if (win.half == kFH) {
+        const dim3 g32((v.W + kFT - 1) / kFT, (v.H + kFT - 1) / kFT, 3);
+        const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1);
+        CUDA_CHECK(cudaFuncSetAttribute(ssim_fields32_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_f));
+        ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, nullptr,
+                                               v.loss_sums.ptr, 0, 0, v.H);
+    } else {
+        const dim3 grid((v.W + kLT - 1) / kLT, (v.H + kLT - 1) / kLT, 3);
+        ssim_fields_k<0><<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, nullptr,
+                                              v.loss_sums.ptr, 0, 0, v.H);
+    }
+    CUDA_LAUNCH_CHECK();
 }
 
 }  // namespace ngsb

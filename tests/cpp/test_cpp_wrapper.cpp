@@ -3,6 +3,7 @@
 // Built by __graft_entry__.build(); run by tests/test_cpp_host.py on the GPU.
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <cstdlib>
 
 #include "ngs_b200.hpp"
@@ -143,6 +144,18 @@ int main() {
         EXPECT(tr.scene().kernels[7].position[0] != init.kernels[7].position[0]);
         EXPECT(tr.neighbors(3).size() == 2);
         for (double d : r.delta_norms) EXPECT(std::isfinite(d));
+        // Trainer::probe_metrics / Trainer::run with the reference's CSV rows (trainer.hpp:215-277).
+        const ProbeMetrics pm = tr.probe_metrics();
+        EXPECT(std::isfinite(pm.loss) && pm.psnr > 0 && pm.ssim > 0 && pm.ssim <= 1.0);
+        std::ostringstream csv;
+        const std::vector<IterationReport> rows = tr.run(&csv);
+        EXPECT(rows.size() == 1 + ds.train_ids.size());
+        EXPECT(rows[0].step == 0 && rows[0].image_id == -1);
+        EXPECT(rows.back().step == 4 + static_cast<int>(ds.train_ids.size()));
+        EXPECT(csv.str().rfind("step,image_id,probe_loss,psnr,ssim,dt_ms\n", 0) == 0);
+        const ProbeMetrics vm = probe.view_metrics(ds.cameras[0], ds.targets[0]);
+        EXPECT(std::isfinite(vm.loss) && vm.psnr > 0);
+        std::printf("probe: loss %.6g psnr %.3f ssim %.5f; run rows %zu\n", pm.loss, pm.psnr, pm.ssim, rows.size());
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;

@@ -118,10 +118,53 @@ def trainer_golden():
     np.savez_compressed(os.path.join(HERE, "trainer.npz"), **out)
 
 
+EVAL_RUN = dict(epochs=1, seed=7, probe_cadence=2)
+
+
+def eval_golden():
+    """total_loss_value / psnr / ssim_metric, probe_metrics and run (metrics.hpp,
+    loss.hpp:359-375, trainer.hpp:215-277) on a synth dataset with probe views."""
+    L = ref()
+    d = synth(seed=29, kernels=20, views=4, probe_views=2, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    ctx = L.context()
+    ctx.set_scene(d["init"])
+    out = dict(scene_arrays(d["init"], "init_"))
+    n = len(d["cameras"])
+    for i, c in enumerate(d["cameras"]):
+        out.update(cam_arrays(c, f"cam{i}_"))
+        out[f"target{i}"] = d["targets"][i]
+        out[f"sec_target{i}"] = d["secondary"][i]
+    out["train"], out["probe"] = np.array(d["train"]), np.array(d["probe"])
+    m = ctx.view_metrics(d["cameras"][0], d["targets"][0])
+    out["view_metrics"] = np.array([m.loss, m.psnr, m.ssim])
+    lc = L.default_loss()
+    lc.lambda_ = 0.0
+    m = ctx.view_metrics(d["cameras"][1], d["targets"][1], loss=lc)
+    out["view_metrics_l2"] = np.array([m.loss, m.psnr, m.ssim])
+    cfg = L.default_train()
+    cfg.knn = 2
+    cfg.secondary_downsample = 2
+    cfg.epochs, cfg.seed, cfg.probe_cadence = EVAL_RUN["epochs"], EVAL_RUN["seed"], EVAL_RUN["probe_cadence"]
+    ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"], d["probe"], d["secondary"],
+                          d["secondary_downsample"])
+    m = ctx.trainer_probe()
+    out["probe0"] = np.array([m.loss, m.psnr, m.ssim])
+    rows = ctx.trainer_run(cfg.epochs, len(d["train"]))
+    out["run_ids"] = np.array([[r.step, r.image_id] for r in rows])
+    out["run_probe"] = np.array([[r.probe_loss, r.probe_psnr, r.probe_ssim] for r in rows])
+    out["run_norms"] = np.array([list(r.delta_norms) for r in rows])
+    out["barrier_after"] = np.array(ctx.barrier_weight())
+    out["run_cfg"] = np.array([EVAL_RUN["epochs"], EVAL_RUN["seed"], EVAL_RUN["probe_cadence"]])
+    out.update(scene_arrays(ctx.get_scene(), "post_"))
+    np.savez_compressed(os.path.join(HERE, "eval.npz"), **out)
+
+
 if __name__ == "__main__":
     render_golden()
     newton_golden()
     trainer_golden()
+    eval_golden()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

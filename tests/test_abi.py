@@ -31,7 +31,7 @@ def test_product_library_exports_every_declared_symbol(header):
 def test_product_library_reports_backend_without_a_gpu():
     lib = capi.NgsLibrary(capi.PRODUCT_LIB)
     assert lib.backend == "cuda-sm_100a"
-    assert lib.lib.ngs_abi_version() == 1
+    assert lib.lib.ngs_abi_version() == 2
     r = lib.default_raster()
     assert (r.lambda_lp, r.alpha_cutoff, r.t_min, r.tiled) == (0.3, 1e-4, 1e-4, 1)   # rasterizer.hpp:25-31
     n = lib.default_newton()

@@ -86,3 +86,51 @@ def test_golden_trainer_step(gpu):
     # theta (|2 theta| <= pi) carries the ~1e-4 relative error of the rotation terms
     dots = np.abs(np.sum(post.quaternion * g["post_quaternion"], axis=1))
     assert np.max(2 * np.arccos(np.clip(dots, -1, 1))) < 1e-3
+
+
+# ---------------------------------------------------------------------------
+# Evaluation path: metrics, probe_metrics, run
+# ---------------------------------------------------------------------------
+
+def _eval_ctx(gpu, g):
+    ctx = gpu.context()
+    ctx.set_scene(scene_from(g, "init_"))
+    n = len([k for k in g if k.startswith("cam") and k.endswith("_view")])
+    cams = [cam_from(g, f"cam{i}_") for i in range(n)]
+    return ctx, cams, [g[f"target{i}"] for i in range(n)]
+
+
+def test_golden_view_metrics(gpu):
+    """total_loss_value / psnr / ssim_metric of the GPU render (loss.hpp:359-375, metrics.hpp)."""
+    g = load("eval.npz")
+    ctx, cams, targets = _eval_ctx(gpu, g)
+    m = ctx.view_metrics(cams[0], targets[0])
+    assert qerr([m.loss, m.psnr, m.ssim], g["view_metrics"]) < 1e-5
+    lc = gpu.default_loss()
+    lc.lambda_ = 0.0
+    m = ctx.view_metrics(cams[1], targets[1], loss=lc)
+    assert qerr([m.loss, m.psnr, m.ssim], g["view_metrics_l2"]) < 1e-5
+    own = ctx.render(cams[1])
+    m = ctx.view_metrics(cams[1], own)
+    assert m.psnr == float("inf") and abs(m.ssim - 1.0) < 1e-9 and m.loss < 1e-12
+
+
+def test_golden_probe_and_run(gpu):
+    """Trainer::probe_metrics + Trainer::run: same shuffled view order (exact), probe
+    rows and delta norms within the trainer-step tolerances."""
+    g = load("eval.npz")
+    ctx, cams, targets = _eval_ctx(gpu, g)
+    epochs, seed, cadence = (int(x) for x in g["run_cfg"])
+    cfg = gpu.default_train()
+    cfg.knn = 2
+    cfg.secondary_downsample = 2
+    cfg.epochs, cfg.seed, cfg.probe_cadence = epochs, seed, cadence
+    ctx.trainer_configure(cfg, cams, targets, list(g["train"]), list(g["probe"]),
+                          [g[f"sec_target{i}"] for i in range(len(cams))], 2)
+    p0 = ctx.trainer_probe()
+    assert qerr([p0.loss, p0.psnr, p0.ssim], g["probe0"]) < 1e-5
+    rows = ctx.trainer_run(epochs, len(g["train"]))
+    assert [[r.step, r.image_id] for r in rows] == g["run_ids"].tolist()
+    assert qerr([[r.probe_loss, r.probe_psnr, r.probe_ssim] for r in rows], g["run_probe"]) < 1e-4
+    assert qerr([list(r.delta_norms) for r in rows], g["run_norms"]) < 2e-3
+    assert ctx.barrier_weight() == pytest.approx(float(g["barrier_after"]), rel=1e-12)

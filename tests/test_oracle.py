@@ -196,3 +196,65 @@ def test_oracle_trainer_step_matches_reference():
     post = ctx.get_scene_arrays()
     for f in ("position", "scale", "quaternion", "sigma", "sh"):
         assert rel(post[f], g["post_" + f]) < 1e-7, f
+
+
+# ---------------------------------------------------------------------------
+# Evaluation path: metrics, probe_metrics, run
+# ---------------------------------------------------------------------------
+
+def test_rng_is_mt19937_64():
+    """ngs::Rng wraps std::mt19937_64 (core.hpp:52-83): the C++ standard's
+    known answer ([rand.predef]: 10000th output of the default engine)."""
+    r = O.Rng(5489)
+    assert r.next() == 14514284786278117030
+    r = O.Rng(5489)
+    for _ in range(9999):
+        r.next()
+    assert r.next() == 9981545732273789042
+    v = O.Rng(3).shuffle(list(range(10)))
+    assert sorted(v) == list(range(10)) and v != list(range(10))
+
+
+def _eval_fixture():
+    g = load("eval.npz")
+    n = len([k for k in g if k.startswith("cam") and k.endswith("_view")])
+    cams = [cam_from(g, f"cam{i}_") for i in range(n)]
+    targets = [g[f"target{i}"] for i in range(n)]
+    return g, cams, targets
+
+
+def test_oracle_metrics_match_reference():
+    """total_loss_value / psnr / ssim_metric (loss.hpp:359-375, metrics.hpp:14-30)."""
+    g, cams, targets = _eval_fixture()
+    ctx = O.OracleContext()
+    ctx.set_scene(scene_from(g, "init_"))
+    img = ctx.render(cams[0])
+    got = [O.total_loss_value(img, targets[0], O.DEFAULT_LOSS), O.psnr(img, targets[0]),
+           O.ssim_mean_value(img, targets[0], O.DEFAULT_LOSS)]
+    assert rel(got, g["view_metrics"]) < TOL
+    img = ctx.render(cams[1])
+    l2 = dict(O.DEFAULT_LOSS, **{"lambda": 0.0})
+    got = [O.total_loss_value(img, targets[1], l2), O.psnr(img, targets[1]), O.ssim_mean_value(img, targets[1], l2)]
+    assert rel(got, g["view_metrics_l2"]) < TOL
+    assert O.psnr(img, img) == float("inf")
+
+
+def test_oracle_run_matches_reference():
+    """Trainer::run (trainer.hpp:238-277): shuffled order, probe cadence, barrier decay."""
+    g, cams, targets = _eval_fixture()
+    epochs, seed, cadence = (int(x) for x in g["run_cfg"])
+    ctx = O.OracleContext()
+    ctx.set_scene(scene_from(g, "init_"))
+    n = len(cams)
+    tr = O.OracleTrainer(ctx, cams, targets, list(g["train"]), [g[f"sec_target{i}"] for i in range(n)], 2, knn=2,
+                         downsample=2)
+    p0 = tr.probe_metrics(list(g["probe"]))
+    assert rel(p0, g["probe0"]) < TOL
+    rows = tr.run(epochs=epochs, seed=seed, probe_cadence=cadence, probe_ids=list(g["probe"]))
+    assert [[r[0], r[1]] for r in rows] == g["run_ids"].tolist()
+    assert rel([r[2] for r in rows], g["run_probe"]) < TOL
+    assert rel([r[3] for r in rows], g["run_norms"]) < TOL
+    assert tr.barrier == pytest.approx(float(g["barrier_after"]), rel=1e-15)
+    post = ctx.get_scene_arrays()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        assert rel(post[f], g["post_" + f]) < TOL, f
