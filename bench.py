@@ -292,10 +292,29 @@ def ours_arm(args, cfg: Config):
         t0 = time.perf_counter()
         ectx.trainer_step(view(args.warmup + i))
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    ectx.close()
+
+    # First-order baselines on the same workload (first_order_step, trainer.hpp:419-509):
+    # device time per step, for the Newton-vs-GD cost ratio (not the headline).
+    fo = {}
+    if world == 1:
+        for name, opt in (("gd", capi.OPT_GD),):  # Adam's cost follows its (diverging) splat sizes here
+            fctx = lib.context(local)
+            fctx.set_scene(init)
+            tc.optimizer = opt
+            fctx.trainer_configure(tc, cams, targets, list(range(cfg.views)))
+            for i in range(args.warmup):
+                fctx.trainer_step(view(i))
+            fdt = []
+            for i in range(args.steps):
+                l2_flush(flush)
+                fdt.append(fctx.trainer_step(view(args.warmup + i)).dt_ms)
+            fctx.close()
+            fo[f"{name}_ms_per_step"] = float(sum(fdt)) / args.steps
+        tc.optimizer = capi.OPT_NEWTON
     ds = 4
     h2d = 3 * 8 * (cfg.width * cfg.height + 3 * (cfg.width // ds) * (cfg.height // ds))
     d2h = 8 * 5 + 8  # delta norms + error word
-    ectx.close()
 
     if world > 1:
         t = torch.tensor([total_ms, sum(e2e_ms)], dtype=torch.float64, device="cuda")
@@ -355,6 +374,10 @@ def ours_arm(args, cfg: Config):
         "stage_ms_per_step": step_stage_ms,
         "group_ms_per_step_concurrent": {k: round(v / args.steps, 4) for k, v in counters["group_ms"].items()},
         "measured_fp64_tflops": fp64_peak,
+        "first_order_baselines": dict(fo, newton_ms_per_step=total_ms / args.steps,
+                                      newton_over_gd=(total_ms / args.steps) / fo["gd_ms_per_step"],
+                                      note="GD steps (first_order_step: primary view only, one gradient traversal) "
+                                           "on the same workload: the paper's Newton-vs-GD per-step cost") if fo else None,
         "contrib_pairs_per_step": [p / args.steps for p in prof["contrib_pairs"]],
         "clocks": clocks.summary(t_timed0, t_timed1),
         "cpu_baseline": cpu,

@@ -104,8 +104,19 @@ typedef struct {
     double eigengap_rel;
 } ngs_newton_options;
 
-/* trainer.hpp:58-88 TrainConfig (Newton optimizer only; the GD/Adam
- * baselines are out of scope). */
+/* trainer.hpp:24 OptimizerKind */
+typedef enum { NGS_OPT_NEWTON = 0, NGS_OPT_GD = 1, NGS_OPT_ADAM = 2 } ngs_optimizer;
+
+/* trainer.hpp:40-56 LearningRates (first-order baselines) */
+typedef struct {
+    double position;
+    double rotation;
+    double scaling;
+    double opacity;
+    double color;
+} ngs_learning_rates;
+
+/* trainer.hpp:58-88 TrainConfig. */
 typedef struct {
     int32_t order[5];        /* permutation of ngs_attribute */
     int32_t epochs;
@@ -121,6 +132,10 @@ typedef struct {
     int32_t host_targets;    /* CUDA: keep targets in pinned host memory and
                                 upload the step's 1+K images inside each step */
     int32_t probe_cadence;   /* TrainConfig::probe_cadence: probe every N steps in run() */
+    int32_t optimizer;       /* ngs_optimizer: Newton (the hot path) or the GD / Adam baselines
+                                (first_order_step, trainer.hpp:419-509) */
+    ngs_learning_rates gd_lr;
+    ngs_learning_rates adam_lr;
 } ngs_train_config;
 
 /* Trainer::ProbeMetrics (trainer.hpp:209-213); also one view's
@@ -259,7 +274,9 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* config,
                               int32_t secondary_targets_downsample);
 int32_t ngs_trainer_neighbors(ngs_context* ctx, int32_t view_id, int32_t* out, int32_t capacity,
                               int32_t* n_out);
-/* Trainer::step(view_id) — one Newton step on one training view. */
+/* Trainer::step(view_id) — one step on one training view: newton_step
+ * (trainer.hpp:299-417), or first_order_step (GD / Adam, trainer.hpp:419-509)
+ * when config.optimizer selects a baseline. */
 int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_iteration_report* report);
 int32_t ngs_trainer_barrier_weight(ngs_context* ctx, double* out);
 /* Trainer::probe_metrics (trainer.hpp:215-233): render every probe view (the

@@ -834,6 +834,26 @@ def scaling_terms(k, v: View, eigengap_rel):
     return g, Hm, True
 
 
+def scaling_gradient_s(k, v: View):
+    """newton.hpp:472-503: 3-dof scale-space gradient (first-order baselines)."""
+    grad = np.zeros(3)
+    recs = v.records[k]
+    if k not in v.entry_of or not recs:
+        return grad
+    kern = kernel_of(v.scene, k)
+    e = v.sl["entries"][v.entry_of[k]]
+    n = e["proj"]["J"] @ v.cam.rot @ quaternion_to_rotation(kern["q"])
+    dsig = [2.0 * kern["s"][c] * np.outer(n[:, c], n[:, c]) for c in range(3)]
+    for rec in recs:
+        gl = v.grad[rec["py"], rec["px"]]
+        gw = gaussian_weight(e["proj"]["cov"], e["proj"]["pixel"], np.array([rec["px"] + 0.5, rec["py"] + 0.5]))
+        dg = np.array([(gw["d_sigma"] * dsig[c]).sum() for c in range(3)])
+        wa = e["sigma"] * rec["T"]
+        for ch in range(3):
+            grad += gl[ch] * wa * (rec["color"][ch] - rec["behind"][ch]) * dg
+    return grad
+
+
 def opacity_terms(k, v: View):
     """newton.hpp:507-526."""
     recs = v.records[k]
@@ -1196,6 +1216,59 @@ class OracleTrainer:
                 rows.append((step, vid, last, norms))
             self.barrier = max(barrier_floor, self.barrier * barrier_decay)
         return rows
+
+    def first_order_step(self, view_id, adam, lr, state):
+        """first_order_step (trainer.hpp:419-509); lr = (position, rotation, scaling,
+        opacity, color); state = dict(t, m, v) Adam moments (56 per kernel)."""
+        sc = self.ctx.scene
+        n = sc["n"]
+        prim = build_view(self.ctx._snapshot(), self.cams[view_id], self.targets[view_id], self.raster, self.loss)
+        if adam:
+            state["t"] += 1
+        grads = []
+        for k in range(n):
+            kern = kernel_of(sc, k)
+            axis = self.cams[view_id].center
+            r = kern["p"] - axis
+            axis = r / np.linalg.norm(r)
+            grads.append(dict(p=position_terms(k, prim)[0], axis=axis, th=rotation_terms(k, axis, prim)[0],
+                              s=scaling_gradient_s(k, prim), sig=opacity_terms(k, prim)[0],
+                              col=color_terms(k, prim)[0]))
+        b1, b2, eps, t = 0.9, 0.999, 1e-8, state["t"]
+
+        def upd(k, slot, g, rate):
+            if not adam:
+                return -rate * g
+            m = state["m"][k, slot] = b1 * state["m"][k, slot] + (1 - b1) * g
+            v = state["v"][k, slot] = b2 * state["v"][k, slot] + (1 - b2) * g * g
+            return -rate * (m / (1 - b1 ** t)) / (math.sqrt(v / (1 - b2 ** t)) + eps)
+
+        nsq = np.zeros(5)
+        nsh = (sc["deg"] + 1) ** 2
+        lo, hi = np.nextafter(1e-4, 1.0), np.nextafter(1.0 - 1e-4, 0.0)
+        for k in range(n):
+            g = grads[k]
+            dp = np.array([upd(k, c, g["p"][c], lr[0]) for c in range(3)])
+            ds = np.array([upd(k, 4 + c, g["s"][c], lr[2]) for c in range(3)])
+            dth = upd(k, 3, g["th"], lr[1])
+            dsg = upd(k, 7, g["sig"], lr[3])
+            sc["p"][k] = sc["p"][k] + dp
+            nsq[0] += dp @ dp
+            dq = np.array([math.cos(dth), *(math.sin(dth) * g["axis"])])
+            q = quaternion_multiply(dq, sc["q"][k])
+            sc["q"][k] = q / np.linalg.norm(q)
+            nsq[1] += dth * dth
+            sc["s"][k] = np.maximum(1e-8, sc["s"][k] + ds)
+            nsq[2] += ds @ ds
+            before = sc["sigma"][k]
+            sc["sigma"][k] = min(max(before + dsg, lo), hi)
+            nsq[3] += (sc["sigma"][k] - before) ** 2
+            for ch in range(3):
+                for c in range(nsh):
+                    d = upd(k, 8 + 16 * ch + c, g["col"][ch, c], lr[4])
+                    sc["sh"][k][ch, c] += d
+                    nsq[4] += d * d
+        return np.sqrt(nsq)
 
     def _views(self, view_id):
         snap = self.ctx._snapshot()

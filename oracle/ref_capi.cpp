@@ -174,6 +174,9 @@ void ngs_train_config_default(ngs_train_config* out) {
     ngs_loss_config_default(&out->loss);
     out->host_targets = 0;
     out->probe_cadence = t.probe_cadence;
+    out->optimizer = static_cast<int32_t>(t.optimizer);
+    out->gd_lr = {t.gd_lr.position, t.gd_lr.rotation, t.gd_lr.scaling, t.gd_lr.opacity, t.gd_lr.color};
+    out->adam_lr = {t.adam_lr.position, t.adam_lr.rotation, t.adam_lr.scaling, t.adam_lr.opacity, t.adam_lr.color};
 }
 
 int32_t ngs_context_create(int32_t /*device*/, ngs_context** out) {
@@ -561,6 +564,18 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
         cfg.raster = to_raster(&c->raster);
         cfg.loss = to_loss(&c->loss);
         cfg.probe_cadence = c->probe_cadence;
+        cfg.optimizer = static_cast<ngs::OptimizerKind>(c->optimizer);
+        auto lr = [](const ngs_learning_rates& l) {
+            ngs::LearningRates r;
+            r.position = l.position;
+            r.rotation = l.rotation;
+            r.scaling = l.scaling;
+            r.opacity = l.opacity;
+            r.color = l.color;
+            return r;
+        };
+        cfg.gd_lr = lr(c->gd_lr);
+        cfg.adam_lr = lr(c->adam_lr);
         ctx->trainer.reset();
         ctx->trainer.emplace(ctx->scene, std::move(ds), std::move(cfg));
     });

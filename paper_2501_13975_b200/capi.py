@@ -81,11 +81,20 @@ class ngs_newton_options(C.Structure):
                 ("barrier_weight", C.c_double), ("max_backtrack", C.c_int32), ("eigengap_rel", C.c_double)]
 
 
+OPT_NEWTON, OPT_GD, OPT_ADAM = 0, 1, 2  # ngs_optimizer
+
+
+class ngs_learning_rates(C.Structure):
+    _fields_ = [("position", C.c_double), ("rotation", C.c_double), ("scaling", C.c_double),
+                ("opacity", C.c_double), ("color", C.c_double)]
+
+
 class ngs_train_config(C.Structure):
     _fields_ = [("order", C.c_int32 * 5), ("epochs", C.c_int32), ("seed", C.c_uint64), ("knn", C.c_int32),
                 ("secondary_downsample", C.c_int32), ("threads", C.c_int32), ("barrier_decay", C.c_double),
                 ("barrier_floor", C.c_double), ("newton", ngs_newton_options), ("raster", ngs_raster_options),
-                ("loss", ngs_loss_config), ("host_targets", C.c_int32), ("probe_cadence", C.c_int32)]
+                ("loss", ngs_loss_config), ("host_targets", C.c_int32), ("probe_cadence", C.c_int32),
+                ("optimizer", C.c_int32), ("gd_lr", ngs_learning_rates), ("adam_lr", ngs_learning_rates)]
 
 
 class ngs_metrics(C.Structure):

@@ -394,6 +394,10 @@ struct PassTraits<kPassPositionUV> {
     static constexpr int NC = kPosUVConsts, NA = 5, BATCH = 64, BATCH8 = 32;
 };
 template <>
+struct PassTraits<kPassGrad> {
+    static constexpr int NC = 0, NA = kAccGrad, BATCH = 64, BATCH8 = 64;
+};
+template <>
 struct PassTraits<kPassRotation> {
     static constexpr int NC = kRotConsts, NA = 2, BATCH = 128, BATCH8 = 64;
 };
@@ -584,6 +588,29 @@ __device__ __forceinline__ void opacity_color_record(const Rec& r, float sigma, 
     }
 }
 
+// First-order record (image space): with qd = Sigma^-1 d, dG/dpi = -G qd and
+// dG/dSigma = G qd qd^T / 2; sgl = sum_ch gl wa (c~ - behind) (rasterizer.hpp:116-176,
+// newton.hpp:266-343 first-order parts, 472-503, 507-526, 538-574).
+__device__ __forceinline__ void grad_record(const Rec& r, float sigma, float (&v)[kAccGrad]) {
+    float sgl = 0.f, sgo = 0.f;
+    const float w = blend_weight(r.Ti, __fmul_rn(r.G, sigma));  // alpha T, as composited
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        sgl += r.gl[ch] * r.ac[ch];
+        v[5 + ch] = r.gl[ch] * w;
+    }
+    sgo = sgl * r.G * r.Ti;  // dL/dsigma: sum gl G T (c~ - behind)
+    sgl *= r.wa;
+    const float gq = sgl * r.G;
+    v[0] = -gq * r.q0;
+    v[1] = -gq * r.q1;
+    const float h = 0.5f * gq;
+    v[2] = h * r.q0 * r.q0;
+    v[3] = h * r.q0 * r.q1;
+    v[4] = h * r.q1 * r.q1;
+    v[8] = sgo;
+}
+
 // Per-warp record queue (ring of 64 entries) between the two phases.
 constexpr int kQ = 64;
 struct WarpQueue {
@@ -715,6 +742,8 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 rotation_record(s_const + jj * CST, r, g0.z, g0.w, s_sp[jj].g1.x, v);
             } else if constexpr (PASS == kPassScaling) {
                 scaling_record(s_const + jj * CST, r, v);
+            } else if constexpr (PASS == kPassGrad) {
+                grad_record(r, s_sp[jj].g1.y, v);
             } else {
                 opacity_color_record(r, s_sp[jj].g1.y, v);
             }
@@ -903,29 +932,42 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
 
 }  // namespace
 
-void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s) {
+void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s,
+                         float* out) {
     const int n = scene.n;
-    if (n == 0 || pass == kPassOpacityColor) return;
+    if (n == 0 || pass == kPassOpacityColor || pass == kPassGrad) return;
     StageScope st(NGS_STAGE_CONSTS, s, pass == kPassPosition || pass == kPassPositionUV ? 2 : 1);
     switch (pass) {
         case kPassPosition:
-            v.consts.ensure(static_cast<size_t>(n) * kPosConsts);
-            position_consts_k<3, 0><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
-            position_consts_k<3, 1><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            if (!out) {
+                v.consts.ensure(static_cast<size_t>(n) * kPosConsts);
+                out = v.consts.ptr;
+            }
+            position_consts_k<3, 0><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, out);
+            position_consts_k<3, 1><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, out);
             break;
         case kPassPositionUV:
-            v.consts.ensure(static_cast<size_t>(n) * kPosUVConsts);
-            position_consts_k<2, 0><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
-            position_consts_k<2, 1><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            if (!out) {
+                v.consts.ensure(static_cast<size_t>(n) * kPosUVConsts);
+                out = v.consts.ptr;
+            }
+            position_consts_k<2, 0><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, out);
+            position_consts_k<2, 1><<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, out);
             break;
         case kPassRotation:
-            v.consts.ensure(static_cast<size_t>(n) * kRotConsts);
-            rotation_consts_k<<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, v.consts.ptr);
+            if (!out) {
+                v.consts.ensure(static_cast<size_t>(n) * kRotConsts);
+                out = v.consts.ptr;
+            }
+            rotation_consts_k<<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, primary, v.flags.ptr, out);
             break;
         case kPassScaling:
-            v.consts.ensure(static_cast<size_t>(n) * kScaleConsts);
+            if (!out) {
+                v.consts.ensure(static_cast<size_t>(n) * kScaleConsts);
+                out = v.consts.ptr;
+            }
             scaling_consts_k<<<blocks_for(n, 128), 128, 0, s>>>(scene, v.cam, v.raster.lambda_lp, v.flags.ptr,
-                                                                 v.consts.ptr);
+                                                                 out);
             break;
         default:
             return;
@@ -966,7 +1008,7 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     if (own1 <= own0) return;
     a.tile0 = own0 * v.cam.tiles_x;
     const int blocks = (own1 - own0) * v.cam.tiles_x;
-    StageScope st(NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV ? kPassPosition : pass), s);
+    StageScope st(NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV || pass == kPassGrad ? kPassPosition : pass), s);
     const bool small = v.cam.tile == 8;
     const int threads = small ? 64 : 256;
     auto go = [&](auto kernel, auto smem_tag) {
@@ -986,6 +1028,10 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
         case kPassPositionUV:
             if (small) go(backward_k<kPassPositionUV, 8>, SmemTag<BackwardSmem<kPassPositionUV, 8>>{});
             else go(backward_k<kPassPositionUV, 16>, SmemTag<BackwardSmem<kPassPositionUV, 16>>{});
+            break;
+        case kPassGrad:
+            if (small) go(backward_k<kPassGrad, 8>, SmemTag<BackwardSmem<kPassGrad, 8>>{});
+            else go(backward_k<kPassGrad, 16>, SmemTag<BackwardSmem<kPassGrad, 16>>{});
             break;
         case kPassRotation:
             if (small) go(backward_k<kPassRotation, 8>, SmemTag<BackwardSmem<kPassRotation, 8>>{});

@@ -11,7 +11,12 @@ namespace ngsb {
 // U^T (sum_v H_v) U = sum_v U^T H_v U is linear in the per-record terms, so the
 // accumulators hold the projected system directly (5 instead of 9 components).
 // kPassPosition (world axes) serves ngs_accumulate, which returns the 3x3 terms.
-enum PassId { kPassPosition = 0, kPassRotation = 1, kPassScaling = 2, kPassOpacityColor = 3, kPassPositionUV = 4 };
+// kPassGrad: first-order baselines (first_order_step, trainer.hpp:419-509): per
+// record only image-space quantities are accumulated (dL/dpi, dL/dSigma, dL/dc~,
+// dL/dsigma); the per-Gaussian chain to (p, theta, s, sigma, SH) runs once in
+// the update kernel.
+enum PassId { kPassPosition = 0, kPassRotation = 1, kPassScaling = 2, kPassOpacityColor = 3, kPassPositionUV = 4,
+              kPassGrad = 5 };
 
 // Accumulator components per pass (FP64, component-major [c][N]).
 constexpr int kAccPosition = 9;  // grad 3, hess sym (xx, xy, xz, yy, yz, zz)
@@ -19,6 +24,7 @@ constexpr int kAccPositionUV = 5;  // grad (u_x, u_y), hess (xx, xy, yy) in the 
 constexpr int kAccRotation = 2;  // grad, hess
 constexpr int kAccScaling = 5;   // grad 2, hess (00, 01, 11)
 constexpr int kAccOpColor = 8;   // opacity grad, hess; colour g_acc[3], h_acc[3] (per view)
+constexpr int kAccGrad = 9;      // dL/dpi (2), dL/dSigma (00, 01, 11), dL/dc~ (3), dL/dsigma
 
 // Per-(Gaussian, view) constant layouts (floats, AoS per Gaussian, float4-aligned
 // groups). ND derivative directions (3 world axes, or the 2 subspace directions);
@@ -62,7 +68,8 @@ struct BackwardArgs {
     unsigned long long* contrib_pairs;   // optional: count of contributing (pixel, splat) records
 };
 
-void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s);
+void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s,
+                         float* out = nullptr);  // out: destination (default v.consts)
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
                      unsigned long long* contrib_pairs, cudaStream_t s);
 

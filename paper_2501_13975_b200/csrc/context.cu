@@ -103,6 +103,11 @@ struct TrainerState {
     int step_count = 0;
     double probe_loss_cache = 0.0;  // trainer.hpp:186-188, 231
     std::mt19937_64 rng;            // Rng(config.seed), core.hpp:52-81
+    // First-order baselines: Adam moments (56 per Gaussian: p 3, theta, s 3, sigma,
+    // SH 48), step count (AdamState, trainer.hpp:106-122), rotation constants.
+    DevBuf<double> adam_m, adam_v;
+    int adam_t = 0;
+    DevBuf<float> rot_consts;
     std::vector<ViewSlot> views;  // primary + secondaries of the current step
     void release() {
         for (auto& t : targets) t.release();
@@ -115,6 +120,10 @@ struct TrainerState {
         host_down_targets.clear();
         for (auto& v : views) v.release_all();
         views.clear();
+        adam_m.release();
+        adam_v.release();
+        rot_consts.release();
+        adam_t = 0;
         active = false;
     }
 };
@@ -441,6 +450,9 @@ void ngs_train_config_default(ngs_train_config* out) {
     ngs_loss_config_default(&out->loss);
     out->host_targets = 0;
     out->probe_cadence = 1;
+    out->optimizer = NGS_OPT_NEWTON;
+    out->gd_lr = {2.0, 40.0, 1.0, 24.0, 60.0};          // LearningRates{} (trainer.hpp:40-45)
+    out->adam_lr = {1.6e-4, 1.0e-3, 5.0e-3, 2.5e-2, 2.5e-3};  // LearningRates::adam_defaults (trainer.hpp:47-55)
 }
 
 int32_t ngs_context_create(int32_t device, ngs_context** out) {
@@ -735,6 +747,7 @@ int acc_components(int pass) {
     switch (pass) {
         case kPassPosition: return kAccPosition;
         case kPassPositionUV: return kAccPositionUV;
+        case kPassGrad: return kAccGrad;
         case kPassRotation: return kAccRotation;
         case kPassScaling: return kAccScaling;
         default: return kAccOpColor;
@@ -981,6 +994,9 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
         T.barrier_weight = c->newton.barrier_weight;
         T.step_count = 0;
         T.probe_loss_cache = 0.0;
+        T.adam_t = 0;
+        if (c->optimizer < NGS_OPT_NEWTON || c->optimizer > NGS_OPT_ADAM)
+            throw Error(NGS_ERR_INVALID_INPUT, "train config: unknown optimizer");
         T.rng.seed(c->seed);
         // fit_bounding_sphere (secondary.hpp:24-36) over the current kernel centres.
         const int n = ctx->scene.n;
@@ -1130,6 +1146,66 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     if (concurrent) ctx->join(nv, ctx->vr.data());
 }
 
+// first_order_step (trainer.hpp:419-509): one primary render, one image-space
+// gradient traversal, one chain + GD/Adam kernel. Returns the device time.
+float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
+    TrainerState& T = ctx->trainer;
+    const int n = ctx->scene.n;
+    const size_t stride = static_cast<size_t>(std::max(n, 1));
+    cudaStream_t s = ctx->stream;
+    const bool adam = T.cfg.optimizer == NGS_OPT_ADAM;
+    if (adam && !T.adam_m.ptr) {
+        T.adam_m.ensure(56 * stride);
+        T.adam_v.ensure(56 * stride);
+        CUDA_CHECK(cudaMemsetAsync(T.adam_m.ptr, 0, sizeof(double) * 56 * stride, s));
+        CUDA_CHECK(cudaMemsetAsync(T.adam_v.ptr, 0, sizeof(double) * 56 * stride, s));
+    }
+    ctx->norm.ensure(5);
+    ViewSlot& v = T.views[0];
+    const std::vector<int> none;
+    CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
+    for (int attempt = 0;; ++attempt) {  // render only: parameters are untouched until the update kernel
+        CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
+        render_step_views(ctx, view_id, none, true);
+        int overflow = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&overflow, ctx->overflow.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (!overflow) break;
+        if (attempt >= 8) throw Error(NGS_ERR_INTERNAL, "pair capacity retry limit exceeded");
+        v.pair_cap = std::max<size_t>(2 * v.pair_cap, 4096);
+    }
+    CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), s));
+    compute_pass_consts(kPassPosition, ctx->scene, v, v.cam, s);
+    T.rot_consts.ensure(static_cast<size_t>(kRotConsts) * stride);
+    compute_pass_consts(kPassRotation, ctx->scene, v, v.cam, s, T.rot_consts.ptr);
+    ViewSlot* vp = &v;
+    accumulate_pass(ctx, kPassGrad, &vp, 1, nullptr);
+    FirstOrderParams fp{};
+    fp.adam = adam ? 1 : 0;
+    const ngs_learning_rates& lr = adam ? T.cfg.adam_lr : T.cfg.gd_lr;
+    fp.lr[NGS_POSITION] = lr.position;
+    fp.lr[NGS_ROTATION] = lr.rotation;
+    fp.lr[NGS_SCALING] = lr.scaling;
+    fp.lr[NGS_OPACITY] = lr.opacity;
+    fp.lr[NGS_COLOR] = lr.color;
+    if (adam) T.adam_t += 1;  // AdamState::begin_step for all five groups
+    fp.t = T.adam_t;
+    fp.beta1 = 0.9;
+    fp.beta2 = 0.999;
+    fp.eps = 1e-8;
+    const SolveParams sp = to_solve(&T.cfg.newton, 1);
+    fp.sigma_lo = sp.sigma_lo;
+    fp.sigma_hi = sp.sigma_hi;
+    launch_first_order(ctx->scene, v.cam, v.flags.ptr, v.consts.ptr, T.rot_consts.ptr, ctx->acc.ptr, stride, fp,
+                       T.adam_m.ptr, T.adam_v.ptr, ctx->norm.ptr, ctx->err.ptr, s);
+    CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
+    CUDA_CHECK(cudaMemcpyAsync(norms, ctx->norm.ptr, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    ctx->check_err();
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    return ms;
+}
+
 }  // namespace
 
 extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_iteration_report* report) {
@@ -1142,6 +1218,23 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
             throw Error(NGS_ERR_INVALID_INPUT, "trainer: view id out of range");
         if (!std::isfinite(T.probe_loss_cache))
             throw Error(NGS_ERR_NUMERICAL, "trainer: non-finite probe loss, aborting");
+        if (T.cfg.optimizer != NGS_OPT_NEWTON) {
+            double norms[5];
+            const float ms = first_order_step(ctx, view_id, norms);
+            T.step_count += 1;
+            for (double d : norms)
+                if (!std::isfinite(d)) throw Error(NGS_ERR_NUMERICAL, "trainer: non-finite update, aborting");
+            if (report) {
+                report->step = T.step_count;
+                report->image_id = view_id;
+                report->probe_loss = 0;
+                report->probe_psnr = 0;
+                report->probe_ssim = 1;
+                for (int i = 0; i < 5; ++i) report->delta_norms[i] = std::sqrt(norms[i]);
+                report->dt_ms = ms;
+            }
+            return;
+        }
         const std::vector<int>& nbrs = T.neighbors[view_id];
         const int nv = 1 + static_cast<int>(nbrs.size());
         std::vector<ViewSlot*> views(nv);

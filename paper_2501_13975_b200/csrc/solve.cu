@@ -535,7 +535,147 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
     block_add(nsq, out.norm_sq);
 }
 
+// first_order_step (trainer.hpp:419-509) for one Gaussian per thread.
+__global__ void __launch_bounds__(128) first_order_k(SceneDev s, CameraDev cam, const uint8_t* __restrict__ flags,
+                                                     const float* __restrict__ pcst, const float* __restrict__ rcst,
+                                                     const double* __restrict__ acc, size_t stride, FirstOrderParams p,
+                                                     double* __restrict__ am, double* __restrict__ av,
+                                                     double* __restrict__ norms, int* err) {
+    using L = PosLayout<3>;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq[5] = {0, 0, 0, 0, 0};
+    if (k < s.n) {
+        const float4 ps = s.pos_sigma[k];
+        const D3 p3 = {ps.x, ps.y, ps.z};
+        const uint8_t fl = flags[k];
+        // Gradients (zero for kernels without an entry in this view, newton.hpp:271-275 etc.).
+        double gp[3] = {0, 0, 0}, gth = 0, gs[3] = {0, 0, 0}, gsig = 0, gc[3] = {0, 0, 0};
+        D3 axis;
+        double nr;
+        if (!view_direction(cam, p3, axis, nr)) {
+            atomicOr(err, 2);
+            axis = d3(0, 0, 1);
+        }
+        if (fl & kProjected) {
+            double A[kAccGrad];
+#pragma unroll
+            for (int c = 0; c < kAccGrad; ++c) A[c] = acc[c * stride + k];
+            const float* pc = pcst + static_cast<size_t>(k) * L::N;
+            auto sym = [&](double m00, double m01, double m11) { return A[2] * m00 + 2.0 * A[3] * m01 + A[4] * m11; };
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {  // position_terms grad via dG/dpi, dG/dSigma, dc~/dp
+                gp[c] = pc[L::JS + 2 * c] * A[0] + pc[L::JS + 2 * c + 1] * A[1] +
+                        sym(pc[L::JS + 6 + 3 * c], pc[L::JS + 6 + 3 * c + 1], pc[L::JS + 6 + 3 * c + 2]);
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) gp[c] += pc[L::JC + 3 * ch + c] * A[5 + ch];
+            }
+            const float* rc = rcst + static_cast<size_t>(k) * kRotConsts;
+            gth = sym(rc[0], rc[1], rc[2]);  // rotation_terms grad: dG/dSigma : s1
+            // scaling_gradient_s (newton.hpp:472-503): dSigma/ds_c = 2 s_c n_c n_c^T, n = J W R.
+            const D3 t = to_camera_space(cam, p3);
+            CamProj cp;
+            project_camera_space<false, false>(cam, t, cp);
+            double jw[6];
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 3; ++j)
+                    jw[3 * i + j] = cp.J[3 * i] * mrow(cam.view, 0, j) + cp.J[3 * i + 1] * mrow(cam.view, 1, j) +
+                                    cp.J[3 * i + 2] * mrow(cam.view, 2, j);
+            const float4 q = s.quat[k];
+            double R[9];
+            quat_to_rot(q.x, q.y, q.z, q.w, R);
+            const float4 sc = s.scale[k];
+            const double sv[3] = {sc.x, sc.y, sc.z};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double n0 = jw[0] * R[c] + jw[1] * R[3 + c] + jw[2] * R[6 + c];
+                const double n1 = jw[3] * R[c] + jw[4] * R[3 + c] + jw[5] * R[6 + c];
+                gs[c] = 2.0 * sv[c] * sym(n0 * n0, n0 * n1, n1 * n1);
+            }
+            gsig = A[8];  // opacity_data_terms grad
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) gc[ch] = (fl & (kClamp0 << ch)) ? 0.0 : A[5 + ch];  // color_terms g_acc
+        }
+        // Adam moments slot-major ([56][stride]) so a warp's accesses coalesce.
+        const double bc1 = 1.0 - pow(p.beta1, (double)p.t), bc2 = 1.0 - pow(p.beta2, (double)p.t);
+        auto upd = [&](int slot, double g, double lr) {
+            if (!p.adam) return -lr * g;  // gd_update
+            const size_t i = static_cast<size_t>(slot) * stride + k;
+            const double m = p.beta1 * am[i] + (1.0 - p.beta1) * g;
+            const double v = p.beta2 * av[i] + (1.0 - p.beta2) * g * g;
+            am[i] = m;
+            av[i] = v;
+            return -lr * (m / bc1) / (sqrt(v / bc2) + p.eps);
+        };
+        double dp[3], ds[3];
+        for (int c = 0; c < 3; ++c) dp[c] = upd(c, gp[c], p.lr[NGS_POSITION]);
+        for (int c = 0; c < 3; ++c) ds[c] = upd(4 + c, gs[c], p.lr[NGS_SCALING]);
+        const double dth = upd(3, gth, p.lr[NGS_ROTATION]);
+        const double dsg = upd(7, gsig, p.lr[NGS_OPACITY]);
+        // Commit (trainer.hpp:480-505).
+        s.pos_sigma[k] = make_float4((float)(p3.x + dp[0]), (float)(p3.y + dp[1]), (float)(p3.z + dp[2]), ps.w);
+        nsq[NGS_POSITION] = dp[0] * dp[0] + dp[1] * dp[1] + dp[2] * dp[2];
+        {
+            const double c = cos(dth), sn = sin(dth);
+            const double a0 = c, a1 = sn * axis.x, a2 = sn * axis.y, a3 = sn * axis.z;
+            const float4 qq = s.quat[k];
+            const double b0 = qq.x, b1 = qq.y, b2 = qq.z, b3 = qq.w;
+            double w = a0 * b0 - a1 * b1 - a2 * b2 - a3 * b3;
+            double x = a0 * b1 + a1 * b0 + a2 * b3 - a3 * b2;
+            double y = a0 * b2 - a1 * b3 + a2 * b0 + a3 * b1;
+            double z = a0 * b3 + a1 * b2 - a2 * b1 + a3 * b0;
+            const double nq = sqrt(w * w + x * x + y * y + z * z);
+            if (!(nq > 0.0) || !isfinite(nq)) {
+                atomicOr(err, 4);
+            } else {
+                w /= nq;
+                x /= nq;
+                y /= nq;
+                z /= nq;
+            }
+            s.quat[k] = make_float4((float)w, (float)x, (float)y, (float)z);
+        }
+        nsq[NGS_ROTATION] = dth * dth;
+        {
+            const float4 sc = s.scale[k];
+            s.scale[k] = make_float4((float)fmax(1e-8, (double)sc.x + ds[0]), (float)fmax(1e-8, (double)sc.y + ds[1]),
+                                     (float)fmax(1e-8, (double)sc.z + ds[2]), 0.f);
+        }
+        nsq[NGS_SCALING] = ds[0] * ds[0] + ds[1] * ds[1] + ds[2] * ds[2];
+        {
+            float ns = (float)((double)ps.w + dsg);
+            ns = fminf(fmaxf(ns, p.sigma_lo), p.sigma_hi);
+            s.pos_sigma[k].w = ns;
+            const double applied = (double)ns - (double)ps.w;
+            nsq[NGS_OPACITY] = applied * applied;
+        }
+        if (s.n_coeffs > 0) {
+            double basis[16];
+            sh_basis(axis, s.sh_degree, basis);
+            for (int ch = 0; ch < 3; ++ch)
+                for (int i = 0; i < s.n_coeffs; ++i) {
+                    const double d = upd(8 + 16 * ch + i, gc[ch] * basis[i], p.lr[NGS_COLOR]);
+                    float* cc = s.sh + static_cast<size_t>(16 * ch + i) * s.n + k;
+                    *cc = (float)((double)*cc + d);
+                    nsq[NGS_COLOR] += d * d;
+                }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 5; ++a) block_add(nsq[a], norms + a);
+}
+
 }  // namespace
+
+void launch_first_order(const SceneDev& scene, const CameraDev& cam, const uint8_t* flags, const float* pos_consts,
+                        const float* rot_consts, const double* acc, size_t stride, const FirstOrderParams& p,
+                        double* adam_m, double* adam_v, double* norms, int* err, cudaStream_t s) {
+    const int n = scene.n;
+    if (n == 0) return;
+    StageScope st(NGS_STAGE_SOLVE, s);
+    first_order_k<<<blocks_for(n, 128), 128, 0, s>>>(scene, cam, flags, pos_consts, rot_consts, acc, stride, p, adam_m,
+                                                      adam_v, norms, err);
+    CUDA_LAUNCH_CHECK();
+}
 
 void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, double lambda_lp,
                   const uint8_t* primary_flags, const ColorViews& cv, const SolveParams& sp, const double* acc,

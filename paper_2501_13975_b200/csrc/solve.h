@@ -31,6 +31,22 @@ struct ColorViews {
     const uint8_t* flags[kMaxSolveViews];
 };
 
+// First-order baselines (first_order_step, trainer.hpp:419-509).
+struct FirstOrderParams {
+    int adam;               // 0: gd_update (trainer.hpp:104), 1: AdamState::update (trainer.hpp:106-122)
+    double lr[5];           // indexed by ngs_attribute
+    int t;                  // Adam step count after begin_step
+    double beta1, beta2, eps;
+    float sigma_lo, sigma_hi;
+};
+// Chains the image-space accumulators (kPassGrad) of the primary view to
+// (p, theta, s, sigma, SH) gradients and applies GD or Adam to every Gaussian.
+// pos_consts: PosLayout<3> constants of the view; rot_consts: rotation constants
+// with this view's ray as axis; adam_m / adam_v: [56][stride] doubles (slot-major).
+void launch_first_order(const SceneDev& scene, const CameraDev& cam, const uint8_t* flags, const float* pos_consts,
+                        const float* rot_consts, const double* acc, size_t stride, const FirstOrderParams& p,
+                        double* adam_m, double* adam_v, double* norms, int* err, cudaStream_t s);
+
 void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, double lambda_lp,
                   const uint8_t* primary_flags, const ColorViews& cv, const SolveParams& sp, const double* acc,
                   size_t stride, const SolveOutputs& out, cudaStream_t s);

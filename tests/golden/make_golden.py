@@ -160,11 +160,42 @@ def eval_golden():
     np.savez_compressed(os.path.join(HERE, "eval.npz"), **out)
 
 
+FO_STEPS = (1, 3)  # view ids of the two first-order steps
+
+
+def first_order_golden():
+    """first_order_step (trainer.hpp:419-509): two GD and two Adam steps."""
+    L = ref()
+    d = synth(seed=31, kernels=20, views=4, probe_views=0, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    out = dict(scene_arrays(d["init"], "init_"))
+    for i, c in enumerate(d["cameras"]):
+        out.update(cam_arrays(c, f"cam{i}_"))
+        out[f"target{i}"] = d["targets"][i]
+    for name, opt in (("gd", 1), ("adam", 2)):
+        ctx = L.context()
+        ctx.set_scene(d["init"])
+        cfg = L.default_train()
+        cfg.optimizer = opt
+        ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"], [], d["secondary"],
+                              d["secondary_downsample"])
+        norms = [list(ctx.trainer_step(v).delta_norms) for v in FO_STEPS]
+        out[f"{name}_norms"] = np.array(norms)
+        out.update(scene_arrays(ctx.get_scene(), f"{name}_post_"))
+    lr = L.default_train()
+    out["gd_lr"] = np.array([lr.gd_lr.position, lr.gd_lr.rotation, lr.gd_lr.scaling, lr.gd_lr.opacity, lr.gd_lr.color])
+    out["adam_lr"] = np.array([lr.adam_lr.position, lr.adam_lr.rotation, lr.adam_lr.scaling, lr.adam_lr.opacity,
+                               lr.adam_lr.color])
+    out["steps"] = np.array(FO_STEPS)
+    np.savez_compressed(os.path.join(HERE, "first_order.npz"), **out)
+
+
 if __name__ == "__main__":
     render_golden()
     newton_golden()
     trainer_golden()
     eval_golden()
+    first_order_golden()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

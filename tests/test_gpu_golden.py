@@ -134,3 +134,24 @@ def test_golden_probe_and_run(gpu):
     assert qerr([[r.probe_loss, r.probe_psnr, r.probe_ssim] for r in rows], g["run_probe"]) < 1e-4
     assert qerr([list(r.delta_norms) for r in rows], g["run_norms"]) < 2e-3
     assert ctx.barrier_weight() == pytest.approx(float(g["barrier_after"]), rel=1e-12)
+
+
+def test_golden_first_order(gpu):
+    """GD / Adam baselines on the GPU (one image-space gradient traversal + chain kernel)."""
+    g = load("first_order.npz")
+    n = len([k for k in g if k.startswith("cam") and k.endswith("_view")])
+    cams = [cam_from(g, f"cam{i}_") for i in range(n)]
+    for name, opt in (("gd", 1), ("adam", 2)):
+        ctx = gpu.context()
+        ctx.set_scene(scene_from(g, "init_"))
+        cfg = gpu.default_train()
+        cfg.optimizer = opt
+        ctx.trainer_configure(cfg, cams, [g[f"target{i}"] for i in range(n)], list(range(n)))
+        norms = [list(ctx.trainer_step(int(v)).delta_norms) for v in g["steps"]]
+        print(name, np.array(norms), g[f"{name}_norms"])
+        assert qerr(norms, g[f"{name}_norms"]) < 2e-3, name
+        post = ctx.get_scene()
+        for f in ("position", "scale", "sigma", "sh"):
+            assert qerr(getattr(post, f), g[f"{name}_post_" + f]) < 1e-4, (name, f)
+        dots = np.abs(np.sum(post.quaternion * g[f"{name}_post_quaternion"], axis=1))
+        assert np.max(2 * np.arccos(np.clip(dots, -1, 1))) < 1e-3, name

@@ -258,3 +258,21 @@ def test_oracle_run_matches_reference():
     post = ctx.get_scene_arrays()
     for f in ("position", "scale", "quaternion", "sigma", "sh"):
         assert rel(post[f], g["post_" + f]) < TOL, f
+
+
+def test_oracle_first_order_matches_reference():
+    """first_order_step (trainer.hpp:419-509): GD and Adam baselines, two steps each."""
+    g = load("first_order.npz")
+    n = len([k for k in g if k.startswith("cam") and k.endswith("_view")])
+    cams = [cam_from(g, f"cam{i}_") for i in range(n)]
+    targets = [g[f"target{i}"] for i in range(n)]
+    for name, adam in (("gd", False), ("adam", True)):
+        ctx = O.OracleContext()
+        ctx.set_scene(scene_from(g, "init_"))
+        tr = O.OracleTrainer(ctx, cams, targets, list(range(n)), knn=0)
+        state = dict(t=0, m=np.zeros((ctx.scene["n"], 56)), v=np.zeros((ctx.scene["n"], 56)))
+        norms = [tr.first_order_step(int(v), adam, g[f"{name}_lr"], state) for v in g["steps"]]
+        assert rel(norms, g[f"{name}_norms"]) < TOL, name
+        post = ctx.get_scene_arrays()
+        for f in ("position", "scale", "quaternion", "sigma", "sh"):
+            assert rel(post[f], g[f"{name}_post_" + f]) < TOL, (name, f)
