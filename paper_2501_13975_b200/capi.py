@@ -486,8 +486,10 @@ class Context:
                     launches={k: st.launches[i] for i, k in enumerate(STAGES)},
                     total_launches=st.total_launches, contrib_pairs=list(st.contrib_pairs),
                     raster_pairs=st.raster_pairs, renders=st.renders,
-                    group_ms=dict(zip(("render", "bwd_position", "bwd_rotation", "bwd_scaling", "bwd_opacity_color",
-                                       "solve"), list(st.group_ms))))
+                    # Trainer renders are chained per view into the following backward pass, so each
+                    # pass group includes the render before it ("render" stays 0 in trainer steps).
+                    group_ms=dict(zip(("render", "render+bwd_position", "render+bwd_rotation", "render+bwd_scaling",
+                                       "render+bwd_opacity_color", "solve"), list(st.group_ms))))
 
     def set_tile_size(self, tile: int):
         self._call("ngs_set_tile_size", C.c_int32(tile))

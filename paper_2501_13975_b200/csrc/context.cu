@@ -150,6 +150,7 @@ struct ngs_context {
     std::array<cudaStream_t, kMaxSolveViews> vr{};  // render streams (equal priority)
     cudaEvent_t fork_ev = nullptr;
     std::array<cudaEvent_t, kMaxSolveViews> join_ev{};
+    std::array<cudaEvent_t, kMaxSolveViews> rev{};  // per-view 'render + loss done' (chained into the backward)
     std::array<cudaEvent_t, 24> gev{};  // stage-group events of a trainer step
     DevBuf<int> overflow;
     DevBuf<float4> snap_ps, snap_sc, snap_q;
@@ -184,6 +185,8 @@ struct ngs_context {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (fork_ev) cudaEventDestroy(fork_ev);
+        for (auto e : rev)
+            if (e) cudaEventDestroy(e);
         for (auto e : join_ev)
             if (e) cudaEventDestroy(e);
         for (auto s : vs)
@@ -482,6 +485,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
             CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->vr[i], cudaStreamNonBlocking,
                                                     ctx->stream_policy == 0 ? prio_lo : prio));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventCreateWithFlags(&ctx->rev[i], cudaEventDisableTiming));
         }
         ctx->overflow.ensure(1);
         CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), ctx->stream));
@@ -756,15 +760,21 @@ int acc_components(int pass) {
 
 // Zero the accumulators and run one backward pass over views[0..nv).
 // Opacity/colour keep per-view accumulators (colour needs each view's phi).
+// chained: the views were just rendered by render_step_views(join = false); each
+// view's backward waits only for its own render (no step-wide barrier in between).
 void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv, uint8_t* visible,
-                     bool concurrent = false) {
+                     bool concurrent = false, bool chained = false) {
     const int n = ctx->scene.n;
     const size_t stride = static_cast<size_t>(std::max(n, 1));
     const int comps = acc_components(pass) * (pass == kPassOpacityColor ? nv : 1);
     ctx->acc.ensure(stride * comps);
     CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
     concurrent = concurrent && nv <= kMaxSolveViews && !ctx->prof.enabled;
-    if (concurrent) ctx->fork(nv, ctx->vs.data());
+    if (concurrent) {
+        ctx->fork(nv, ctx->vs.data());  // after the accumulator memset
+        if (chained)
+            for (int i = 0; i < nv; ++i) CUDA_CHECK(cudaStreamWaitEvent(ctx->vs[i], ctx->rev[i], 0));
+    }
     for (int ii = 0; ii < nv; ++ii) {
         const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
         const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
@@ -1109,7 +1119,10 @@ namespace {
 // Render + loss for every view of the step (build_view_context x (1+K)); one
 // stream per view, no host synchronisation (pair-capacity overflow is flagged
 // on the device and handled by the caller).
-void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nbrs, bool upload_targets) {
+// join = false leaves the views in flight on their streams (recording rev[i]); the
+// next accumulate_pass(chained = true) picks each view up where its render ends.
+void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nbrs, bool upload_targets,
+                       bool join = true) {
     TrainerState& T = ctx->trainer;
     const int nv = 1 + static_cast<int>(nbrs.size());
     // Profiling serialises the views so per-launch event times do not overlap.
@@ -1142,8 +1155,9 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         rs.pair_counter = ctx->pairs.ptr + 4;
         render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
         compute_loss(v, s);
+        if (concurrent && !join) CUDA_CHECK(cudaEventRecord(ctx->rev[i], s));
     }
-    if (concurrent) ctx->join(nv, ctx->vr.data());
+    if (concurrent && join) ctx->join(nv, ctx->vr.data());
 }
 
 // first_order_step (trainer.hpp:419-509): one primary render, one image-space
@@ -1269,8 +1283,10 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
             CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), s));
             CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
             mark(-1);
-            render_step_views(ctx, view_id, nbrs, true);
-            mark(0);
+            // Renders are chained per view into the next backward pass (no join in between);
+            // a pass's group time therefore includes the render that precedes it.
+            render_step_views(ctx, view_id, nbrs, true, false);
+            bool rendered = true;
             for (int pass_i = 0; pass_i < 5; ++pass_i) {
                 const int attr = T.cfg.order[pass_i];
                 const int pass = solve_pass_of(attr);
@@ -1278,7 +1294,8 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                 const bool reuse = (attr == NGS_COLOR && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_OPACITY) ||
                                    (attr == NGS_OPACITY && pass_i > 0 && T.cfg.order[pass_i - 1] == NGS_COLOR);
                 if (!reuse) {
-                    accumulate_pass(ctx, pass, views.data(), nv, nullptr, true);
+                    accumulate_pass(ctx, pass, views.data(), nv, nullptr, true, rendered);
+                    rendered = false;
                     mark(1 + (pass == kPassPositionUV ? kPassPosition : pass));
                 }
                 SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
@@ -1287,8 +1304,8 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                 mark(5);
                 const bool geometry = attr == NGS_POSITION || attr == NGS_ROTATION || attr == NGS_SCALING;
                 if (geometry && pass_i + 1 < 5) {
-                    render_step_views(ctx, view_id, nbrs, false);
-                    mark(0);
+                    render_step_views(ctx, view_id, nbrs, false, false);
+                    rendered = true;
                 }
             }
             CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
