@@ -323,6 +323,13 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
     if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_l() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all_l() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // 11-tap fast path: 32x32 output tiles, 256 threads. The horizontal pass reads
 // its 14-column input windows straight from global memory (L1-resident tile)
@@ -448,13 +455,13 @@ __global__ void __launch_bounds__(256) ssim_fields32_k(int W, int H, const doubl
     if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
 }
 
-__global__ void __launch_bounds__(256) ssim_derivs32_k(int W, int H, const double* __restrict__ image,
+__global__ void __launch_bounds__(256, 3) ssim_derivs32_k(int W, int H, const double* __restrict__ image,
                                                        const double* __restrict__ target, Window win, double lambda,
                                                        const double* __restrict__ fields, float* __restrict__ grad,
                                                        float* __restrict__ hess, double* __restrict__ sums, int row0,
                                                        int own_y0, int own_y1) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [3][kFS][kFT + 1]
+    auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [1][kFS][kFT + 1], then s_f [2][kFS][kFS + 1]
     __shared__ double red[8];
     const int ch = blockIdx.z;
     const int ox = blockIdx.x * kFT, oy = (row0 + blockIdx.y) * kFT;
@@ -473,43 +480,53 @@ __global__ void __launch_bounds__(256) ssim_derivs32_k(int W, int H, const doubl
         }
     }
     double g_ssim[kFR] = {}, h_ssim[kFR] = {};
-    const bool interior = ox >= kFH && oy >= kFH && ox + kFT + kFH <= W && oy + kFT + kFH <= H;
     if (lambda != 0.0) {
+        // One field per round, double-buffered: the halo tile of field f+1 streams in
+        // (cp.async) while field f is convolved. Horizontal tasks are row-major so a
+        // warp's lanes read different rows (row stride 43 doubles: conflict-free).
+        auto s_f = reinterpret_cast<double (*)[kFS][kFS + 1]>(smem_raw + sizeof(double) * kFS * (kFT + 1));
+        auto issue = [&](int f, int buf) {
+            const double* field = fields + (static_cast<size_t>(f) * 3 + ch) * plane;
+            for (int i = threadIdx.x; i < kFS * kFS; i += blockDim.x) {
+                const int r = i / kFS, cc = i - r * kFS;
+                const int gx = ox - kFH + cc, gy = oy - kFH + r;
+                if (gx >= 0 && gx < W && gy >= 0 && gy < H)
+                    cp_async8(&s_f[buf][r][cc], field + static_cast<size_t>(gy) * W + gx);
+                else
+                    s_f[buf][r][cc] = 0.0;
+            }
+            cp_async_commit_l();
+        };
+        issue(0, 0);
 #pragma unroll 1
-        for (int g = 0; g < 3; ++g) {  // fields 3g .. 3g + 2; fp, fq, fr, fkw (0-3) use w, the rest w^2
-            const unsigned w2mask = g == 0 ? 0u : g == 1 ? 6u : 7u;  // field 3g + f uses w^2 iff 3g + f >= 4
-            if (g > 0) __syncthreads();
-            const double* fbase = fields + (static_cast<size_t>(3 * g) * 3 + ch) * plane +
-                                  static_cast<ptrdiff_t>(oy - kFH) * W + (ox - kFH);
-            if (interior) {  // block-uniform: the whole halo tile is inside the image
-                hpass32<3>(win, w2mask,
-                           [&](int f, int r, int cc) -> double {
-                               return __ldg(fbase + static_cast<size_t>(f) * 3 * plane + static_cast<size_t>(r) * W + cc);
-                           },
-                           s_h);
-            } else {
-                hpass32<3>(win, w2mask,
-                           [&](int f, int r, int cc) -> double {
-                               const int gx = ox - kFH + cc, gy = oy - kFH + r;
-                               if (gx < 0 || gx >= W || gy < 0 || gy >= H) return 0.0;
-                               return __ldg(fields + (static_cast<size_t>(3 * g + f) * 3 + ch) * plane +
-                                            static_cast<size_t>(gy) * W + gx);
-                           },
-                           s_h);
+        for (int f = 0; f < 9; ++f) {
+            const int buf = f & 1;
+            cp_async_wait_all_l();
+            __syncthreads();  // tile f visible; previous round's readers of s_h and s_f[buf ^ 1] done
+            if (f + 1 < 9) issue(f + 1, buf ^ 1);
+            const bool w2 = f >= 4;  // fp, fq, fr, fkw use w; the rest w^2
+            for (int task = threadIdx.x; task < kFS * (kFT / kFR); task += blockDim.x) {
+                const int cg = task / kFS, r = task - cg * kFS, c0 = cg * kFR;
+                double acc[kFR] = {};
+#pragma unroll
+                for (int k = 0; k < kFR + 2 * kFH; ++k) {
+                    const double v = s_f[buf][r][c0 + k];
+#pragma unroll
+                    for (int o = 0; o < kFR; ++o)
+                        if (k - o >= 0 && k - o <= 2 * kFH) acc[o] += (w2 ? win.w2[k - o] : win.w[k - o]) * v;
+                }
+#pragma unroll
+                for (int o = 0; o < kFR; ++o) s_h[0][r][c0 + o] = acc[o];
             }
             __syncthreads();
-            double sv[3][kFR];
-#pragma unroll
-            for (int f = 0; f < 3; ++f) vpass32(win, (w2mask >> f) & 1u, s_h[f], c, r0, sv[f]);
+            double sv[kFR];
+            vpass32(win, w2, s_h[0], c, r0, sv);
 #pragma unroll
             for (int o = 0; o < kFR; ++o) {  // loss.hpp:323-327
-                if (g == 0) {
-                    g_ssim[o] += sv[0][o] + ctv[o] * sv[1][o] + cv[o] * sv[2][o];
-                } else if (g == 1) {
-                    h_ssim[o] += sv[0][o] + sv[1][o] + cv[o] * sv[2][o];
-                } else {
-                    h_ssim[o] += ctv[o] * sv[0][o] + cv[o] * ctv[o] * sv[1][o] + cv[o] * cv[o] * sv[2][o];
-                }
+                const double cf = f == 1 ? ctv[o] : f == 2 ? cv[o] : f == 5 ? cv[o] : f == 6 ? ctv[o]
+                                : f == 7 ? cv[o] * ctv[o] : f == 8 ? cv[o] * cv[o] : 1.0;
+                if (f < 3) g_ssim[o] += cf * sv[o];
+                else h_ssim[o] += cf * sv[o];
             }
         }
     }
@@ -584,7 +601,7 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     if (win.half == kFH) {  // the reference default (window 11): 32x32 register-blocked tiles
         const int r32a = band_px0 / kFT, r32b = (band_px1 + kFT - 1) / kFT;
         const dim3 g32((v.W + kFT - 1) / kFT, r32b - r32a, 3);
-        const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1), sm_d = sizeof(double) * 3 * kFS * (kFT + 1);
+        const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1), sm_d = sizeof(double) * kFS * (kFT + 1 + 2 * (kFS + 1));
         static bool attr = false;
         if (!attr) {
             CUDA_CHECK(cudaFuncSetAttribute(ssim_fields32_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_f));
