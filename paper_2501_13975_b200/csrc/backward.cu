@@ -650,7 +650,7 @@ template <int PASS, int TILE>
 __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
     using SM = BackwardSmem<PASS, TILE>;
-    constexpr int NT = TILE * TILE, NW = NT / 32, kRowsPerWarp = 32 / TILE;
+    constexpr int NT = TILE * TILE, NW = NT / 32;
     constexpr int B = SM::B, NA = TR::NA, NC4 = SM::NC4, CST = SM::CST;
     static_assert(B <= NT && B % 32 == 0, "one loader thread per splat of a batch");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -666,7 +666,8 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
 
     const int tile = a.tile0 + blockIdx.x;  // owned tile rows only (multi-GPU shard)
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
+    int lx, ly;
+    WarpBox<TILE>::pixel(threadIdx.x, lx, ly);
     const int x = tx * TILE + lx, y = ty * TILE + ly;
     const bool inside = x < a.W && y < a.H;
     const float fx = lx + 0.5f, fy = ly + 0.5f;
@@ -814,22 +815,15 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 const float4 ra = S.raw[buf][1][tid], rb = S.raw[buf][2][tid], rc = S.raw[buf][3][tid];
                 const float qmax = reject_bound(rb.y, a.cutoff);
                 const float py = static_cast<float>(p.y - oy);
-                // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level
-                // skip never drops a record the per-lane test would keep.
-                const float ey = sqrtf(fmaxf(qmax, 0.f) * rc.w) * 1.0001f + 1e-3f;
+                const float px = static_cast<float>(p.x - ox);
                 SplatSh sp;
-                sp.g0 = make_float4(static_cast<float>(p.x - ox), py, ra.z, ra.w);
+                sp.g0 = make_float4(px, py, ra.z, ra.w);
                 sp.g1 = make_float4(rb.x, rb.y, qmax, rb.z);
                 sp.g2 = make_float2(rb.w, rc.x);
                 sp.pad = make_float2(0.f, 0.f);
                 s_sp[tid] = sp;
-                unsigned m = 0;
-#pragma unroll
-                for (int w = 0; w < NW; ++w) {  // warp w owns pixel-centre rows [kRowsPerWarp w + 0.5, + kRowsPerWarp - 1]
-                    const float r0 = kRowsPerWarp * w + 0.5f, r1 = r0 + (kRowsPerWarp - 1);
-                    if (!(py + ey < r0 || py - ey > r1)) m |= 1u << w;
-                }
-                S.wmask[tid] = static_cast<unsigned char>(m);
+                S.wmask[tid] = static_cast<unsigned char>(
+                    WarpBox<TILE>::mask(px, py, ellipse_half_extent(qmax, rc.y), ellipse_half_extent(qmax, rc.w)));
             } else {
                 S.wmask[tid] = 0;
             }

@@ -252,12 +252,12 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
                                                         float cutoff, float tmin, double* __restrict__ image,
                                                         float* __restrict__ t_final, int* __restrict__ last_out) {
     constexpr int kRasterBatch = TILE * TILE;  // one splat per thread per batch
-    constexpr int kRowsPerWarp = 32 / TILE;
     __shared__ SplatSh s_sp[kRasterBatch];
     __shared__ unsigned char s_wmask[kRasterBatch];            // bit w: the cutoff ellipse reaches warp w's rows
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
+    int lx, ly;
+    WarpBox<TILE>::pixel(threadIdx.x, lx, ly);
     const int x = tx * TILE + lx, y = ty * TILE + ly;
     const bool inside = x < W && y < H;
     const float fx = lx + 0.5f, fy = ly + 0.5f;
@@ -292,22 +292,15 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             const float4 a = s_raw[buf][1][t], b = s_raw[buf][2][t], c = s_raw[buf][3][t];
             const float qmax = reject_bound(b.y, cutoff);
             const float py = static_cast<float>(p.y - oy);
-            // |dy| <= sqrt(qmax * Sigma11) on {q <= qmax}; widened so the warp-level skip
-            // never drops a splat the per-pixel test would keep.
-            const float ey = sqrtf(fmaxf(qmax, 0.f) * c.w) * 1.0001f + 1e-3f;
+            const float px = static_cast<float>(p.x - ox);
             SplatSh sp;
-            sp.g0 = make_float4(static_cast<float>(p.x - ox), py, a.z, a.w);
+            sp.g0 = make_float4(px, py, a.z, a.w);
             sp.g1 = make_float4(b.x, b.y, qmax, b.z);
             sp.g2 = make_float2(b.w, c.x);
             sp.pad = make_float2(0.f, 0.f);
             s_sp[threadIdx.x] = sp;
-            unsigned m = 0;
-#pragma unroll
-            for (int w = 0; w < kRasterBatch / 32; ++w) {  // warp w owns rows [kRowsPerWarp w + 0.5, + kRowsPerWarp - 1]
-                const float r0 = kRowsPerWarp * w + 0.5f, r1 = r0 + (kRowsPerWarp - 1);
-                if (!(py + ey < r0 || py - ey > r1)) m |= 1u << w;
-            }
-            s_wmask[threadIdx.x] = static_cast<unsigned char>(m);
+            s_wmask[threadIdx.x] = static_cast<unsigned char>(
+                WarpBox<TILE>::mask(px, py, ellipse_half_extent(qmax, c.y), ellipse_half_extent(qmax, c.w)));
         } else {
             s_wmask[threadIdx.x] = 0;
         }

@@ -23,6 +23,37 @@ struct SplatEval {
 // below the cutoff: q > 2 ln(sigma / cutoff) + margin. The margin absorbs the
 // rounding of logf/expf, so rejecting on it never changes a decision the full
 // evaluation would make (forward and backward stay bit-identical).
+// Pixel <-> thread map of a tile block: each warp owns an 8x4 pixel box (two
+// boxes across a 16-wide tile), tighter than a 16x2 strip for the warp-level
+// overlap masks built below.
+template <int TILE>
+struct WarpBox {
+    static constexpr int BW = 8, BH = 4, ACROSS = TILE / BW, NW = TILE * TILE / 32;
+    __device__ static void pixel(int tid, int& lx, int& ly) {
+        const int warp = tid >> 5, lane = tid & 31;
+        lx = (warp % ACROSS) * BW + (lane % BW);
+        ly = (warp / ACROSS) * BH + lane / BW;
+    }
+    // Bit w set when the cutoff ellipse's bounding box [px -+ ex] x [py -+ ey] (tile
+    // coordinates) reaches a pixel centre of warp w's box.
+    __device__ static unsigned mask(float px, float py, float ex, float ey) {
+        unsigned m = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float x0 = (w % ACROSS) * BW + 0.5f, y0 = (w / ACROSS) * BH + 0.5f;
+            if (!(px + ex < x0 || px - ex > x0 + (BW - 1) || py + ey < y0 || py - ey > y0 + (BH - 1))) m |= 1u << w;
+        }
+        return m;
+    }
+};
+
+// Half-extents of the cutoff ellipse {q <= qmax}: |dx| <= sqrt(qmax Sigma00),
+// |dy| <= sqrt(qmax Sigma11); widened so the warp-level skip never drops a
+// splat the per-pixel test would keep.
+__device__ __forceinline__ float ellipse_half_extent(float qmax, float var) {
+    return sqrtf(fmaxf(qmax, 0.f) * var) * 1.0001f + 1e-3f;
+}
+
 // cp.async (LDGSTS): 16-byte global -> shared copies without register staging.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
