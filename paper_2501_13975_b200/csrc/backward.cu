@@ -823,7 +823,8 @@ __global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(Ba
                 sp.pad = make_float2(0.f, 0.f);
                 s_sp[tid] = sp;
                 S.wmask[tid] = static_cast<unsigned char>(
-                    WarpBox<TILE>::mask(px, py, ellipse_half_extent(qmax, rc.y), ellipse_half_extent(qmax, rc.w)));
+                    WarpBox<TILE>::mask_exact(px, py, ellipse_half_extent(qmax, rc.y), ellipse_half_extent(qmax, rc.w),
+                                              ra.z, ra.w, rb.x, qmax));
             } else {
                 S.wmask[tid] = 0;
             }

@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             sp.pad = make_float2(0.f, 0.f);
             s_sp[threadIdx.x] = sp;
             s_wmask[threadIdx.x] = static_cast<unsigned char>(
-                WarpBox<TILE>::mask(px, py, ellipse_half_extent(qmax, c.y), ellipse_half_extent(qmax, c.w)));
+                WarpBox<TILE>::mask_exact(px, py, ellipse_half_extent(qmax, c.y), ellipse_half_extent(qmax, c.w), a.z,
+                                          a.w, b.x, qmax));
         } else {
             s_wmask[threadIdx.x] = 0;
         }

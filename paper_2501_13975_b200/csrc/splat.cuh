@@ -45,6 +45,34 @@ struct WarpBox {
         }
         return m;
     }
+    // As mask(), then refined by the exact minimum of the quadratic form q over the
+    // box: q(d) = qa dx^2 + 2 qb dx dy + qc dy^2 is convex, so unless the centre lies
+    // in the box its minimum is on one of the four edges (1-D minimisation, clamped).
+    // qmax already carries the reject bound's margin (> 1e-3 in q, far above the FP32
+    // rounding here), so a dropped box never holds a pixel with alpha >= cutoff.
+    __device__ static unsigned mask_exact(float px, float py, float ex, float ey, float qa, float qb, float qc,
+                                          float qmax) {
+        const unsigned m0 = mask(px, py, ex, ey);
+        if (!(qmax < 3.0e38f)) return m0;  // no cutoff (reference mode): keep the bounding-box test
+        const float ia = 1.0f / qa, ic = 1.0f / qc;
+        unsigned m = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            if (!((m0 >> w) & 1u)) continue;
+            const float x0 = (w % ACROSS) * BW + 0.5f - px, x1 = x0 + (BW - 1);
+            const float y0 = (w / ACROSS) * BH + 0.5f - py, y1 = y0 + (BH - 1);
+            if (x0 <= 0.f && x1 >= 0.f && y0 <= 0.f && y1 >= 0.f) {
+                m |= 1u << w;
+                continue;
+            }
+            auto qf = [&](float dx, float dy) { return qa * dx * dx + 2.f * qb * dx * dy + qc * dy * dy; };
+            auto ex_ = [&](float dx) { return qf(dx, fminf(fmaxf(-qb * dx * ic, y0), y1)); };
+            auto ey_ = [&](float dy) { return qf(fminf(fmaxf(-qb * dy * ia, x0), x1), dy); };
+            const float qmin = fminf(fminf(ex_(x0), ex_(x1)), fminf(ey_(y0), ey_(y1)));
+            if (qmin <= qmax) m |= 1u << w;
+        }
+        return m;
+    }
 };
 
 // Half-extents of the cutoff ellipse {q <= qmax}: |dx| <= sqrt(qmax Sigma00),
