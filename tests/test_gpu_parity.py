@@ -300,3 +300,29 @@ def test_tile_size_does_not_change_results(gpu, seed):
     assert np.max(np.abs(img16 - img8)) < 1e-6
     for a, b in zip(outs[0][1:], outs[1][1:]):
         assert qerr(a, b) < TOL_DELTA
+
+
+def test_nccl_single_rank_step_matches_local(gpu):
+    """The multi-GPU plumbing on one GPU: NCCL loaded at run time, a 1-rank
+    communicator, per-pass ncclAllReduce of the accumulators; the trainer step must
+    equal the communicator-free step exactly (a 1-rank sum is the identity)."""
+    d = synth(seed=23, kernels=20, views=4, probe_views=0, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    scenes = []
+    for use_nccl in (False, True):
+        ctx = gpu.context()
+        ctx.set_scene(d["init"])
+        if use_nccl:
+            ctx.dist_init(capi.dist_unique_id(gpu), 0, 1)
+        cfg = gpu.default_train()
+        cfg.knn = 2
+        cfg.secondary_downsample = 2
+        ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"], [], d["secondary"],
+                              d["secondary_downsample"])
+        for v in (0, 2):
+            ctx.trainer_step(v)
+        scenes.append(ctx.get_scene())
+        ctx.close()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        a, b = getattr(scenes[0], f), getattr(scenes[1], f)
+        assert np.max(np.abs(a - b)) <= 1e-6 * max(1.0, float(np.max(np.abs(a)))), f
