@@ -477,6 +477,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         int prio_lo = 0, prio_hi = 0;
         CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         if (const char* e = getenv("NGS_STREAM_POLICY")) ctx->stream_policy = atoi(e);  // experiments only
+        if (const char* e = getenv("NGS_TILE_POLICY")) ctx->tile_policy = atoi(e);      // experiments only
         for (int i = 0; i < kMaxSolveViews; ++i) {
             int prio = i == 0 ? prio_lo : prio_hi;
             if (ctx->stream_policy == 1) prio = i == 0 ? prio_hi : prio_lo;

@@ -134,9 +134,12 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
     sh_basis(r, s.sh_degree, basis);
     double col[3];
     uint8_t f = kProjected;
+#pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
         double v = 0;
-        for (int i = 0; i < s.n_coeffs; ++i) v += basis[i] * static_cast<double>(s.sh[(16 * ch + i) * s.n + k]);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)  // fully unrolled (basis in registers, loads issued together)
+            if (i < s.n_coeffs) v += basis[i] * static_cast<double>(s.sh[(16 * ch + i) * s.n + k]);
         v += kColorOffset;
         const bool clamped = v <= 0.0;
         col[ch] = clamped ? 0.0 : v;

@@ -656,8 +656,11 @@ __global__ void __launch_bounds__(128) first_order_k(SceneDev s, CameraDev cam, 
         if (s.n_coeffs > 0) {
             double basis[16];
             sh_basis(axis, s.sh_degree, basis);
+#pragma unroll
             for (int ch = 0; ch < 3; ++ch)
-                for (int i = 0; i < s.n_coeffs; ++i) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    if (i >= s.n_coeffs) continue;
                     const double d = upd(8 + 16 * ch + i, gc[ch] * basis[i], p.lr[NGS_COLOR]);
                     float* cc = s.sh + static_cast<size_t>(16 * ch + i) * s.n + k;
                     *cc = (float)((double)*cc + d);
