@@ -151,6 +151,7 @@ struct ngs_context {
     cudaEvent_t fork_ev = nullptr;
     std::array<cudaEvent_t, kMaxSolveViews> join_ev{};
     std::array<cudaEvent_t, kMaxSolveViews> rev{};  // per-view 'render + loss done' (chained into the backward)
+    std::array<cudaEvent_t, kMaxSolveViews> pev{};  // per-view 'projection done' (flags for the pass constants)
     std::array<cudaEvent_t, 24> gev{};  // stage-group events of a trainer step
     DevBuf<int> overflow;
     DevBuf<float4> snap_ps, snap_sc, snap_q;
@@ -186,6 +187,8 @@ struct ngs_context {
         if (ev1) cudaEventDestroy(ev1);
         if (fork_ev) cudaEventDestroy(fork_ev);
         for (auto e : rev)
+            if (e) cudaEventDestroy(e);
+        for (auto e : pev)
             if (e) cudaEventDestroy(e);
         for (auto e : join_ev)
             if (e) cudaEventDestroy(e);
@@ -487,6 +490,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
                                                     ctx->stream_policy == 0 ? prio_lo : prio));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->rev[i], cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventCreateWithFlags(&ctx->pev[i], cudaEventDisableTiming));
         }
         ctx->overflow.ensure(1);
         CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), ctx->stream));
@@ -771,17 +775,18 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
     ctx->acc.ensure(stride * comps);
     CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
     concurrent = concurrent && nv <= kMaxSolveViews && !ctx->prof.enabled;
-    if (concurrent) {
-        ctx->fork(nv, ctx->vs.data());  // after the accumulator memset
-        if (chained)
-            for (int i = 0; i < nv; ++i) CUDA_CHECK(cudaStreamWaitEvent(ctx->vs[i], ctx->rev[i], 0));
-    }
+    if (concurrent) ctx->fork(nv, ctx->vs.data());  // after the accumulator memset
     for (int ii = 0; ii < nv; ++ii) {
         const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
         const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
         ViewSlot& v = *views[i];
         cudaStream_t s = concurrent ? ctx->vs[i] : ctx->stream;
+        // The per-view constants need only the parameters, the cameras and the
+        // projection flags, so they overlap the rest of the view's render; the
+        // backward then waits for the render + loss.
+        if (concurrent && chained) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->pev[i], 0));
         compute_pass_consts(pass, ctx->scene, v, views[0]->cam, s);
+        if (concurrent && chained) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->rev[i], 0));
         double* acc = ctx->acc.ptr + (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0);
         unsigned long long* contrib = ctx->pairs.ptr + (pass == kPassPositionUV ? kPassPosition : pass);
         launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s);
@@ -1154,6 +1159,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         rs.exact = false;
         rs.overflow = ctx->overflow.ptr;
         rs.pair_counter = ctx->pairs.ptr + 4;
+        if (concurrent && !join) rs.projected = ctx->pev[i];
         render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
         compute_loss(v, s);
         if (concurrent && !join) CUDA_CHECK(cudaEventRecord(ctx->rev[i], s));

@@ -201,6 +201,7 @@ struct RenderSync {
     bool exact = true;                            // read the pair count back (one host sync)
     int* overflow = nullptr;                      // sync-free: set when the pair capacity was exceeded
     unsigned long long* pair_counter = nullptr;   // optional: adds the (tile, splat) pair count
+    cudaEvent_t projected = nullptr;              // optional: recorded after the projection (flags ready)
 };
 void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
                  const RenderSync& sync = RenderSync{});

@@ -392,6 +392,7 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
                                                        want_debug ? v.entry64.ptr : nullptr, d_err);
         CUDA_LAUNCH_CHECK();
     }
+    if (sync.projected) CUDA_CHECK(cudaEventRecord(sync.projected, s));
     if (n > 0) {
         StageScope st(NGS_STAGE_SORT, s, 11);  // sort 2 + 4 passes, fix-up, gather, scan 3
         // K2: global depth order, exactly (FP64 depth, kernel id): 4-pass radix sort of the
