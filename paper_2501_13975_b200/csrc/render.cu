@@ -232,13 +232,13 @@ __global__ void emit_pairs_k(int n, int tiles_x, int cap, const int* order, cons
 
 // K5: per-tile [start, end) ranges from the tile-sorted key array.
 __global__ void tile_ranges_k(const int* d_pairs, int T, const unsigned int* keys, int2* ranges) {
-    const int pairs = *d_pairs;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= pairs) return;
-    const unsigned int t = keys[i];
-    if (t >= static_cast<unsigned int>(T)) return;
-    if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
-    if (i == pairs - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+    const int pairs = *d_pairs;  // grid-stride: the grid is sized for the capacity, the count is on the device
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += gridDim.x * blockDim.x) {
+        const unsigned int t = keys[i];
+        if (t >= static_cast<unsigned int>(T)) continue;
+        if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
+        if (i == pairs - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+    }
 }
 
 // K6: forward alpha-blend rasterizer. One 16x16 tile per 256-thread block;
@@ -439,8 +439,8 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
         // K4: stable sort of the depth-ordered pairs by tile key -> per-tile depth order.
         radix_sort_pairs(v.pair_key.ptr, v.pair_val.ptr, v.pair_key_alt.ptr, v.pair_val_alt.ptr, v.counters.ptr + 2,
                          static_cast<int>(cap), bits, sc, s);
-        tile_ranges_k<<<blocks_for(static_cast<int>(cap)), 256, 0, s>>>(v.counters.ptr + 2, v.T, v.pair_key.ptr,
-                                                                         v.ranges.ptr);
+        tile_ranges_k<<<std::min(blocks_for(static_cast<int>(cap)), 8 * 148), 256, 0, s>>>(
+            v.counters.ptr + 2, v.T, v.pair_key.ptr, v.ranges.ptr);
         CUDA_LAUNCH_CHECK();
     }
     if (g_prof) g_prof->stats.renders += 1;
