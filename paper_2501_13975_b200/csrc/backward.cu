@@ -647,7 +647,7 @@ struct BackwardSmem {
 };
 
 template <int PASS, int TILE>
-__global__ void __launch_bounds__(TILE * TILE, TILE == 16 ? 3 : 8) backward_k(BackwardArgs a) {
+__global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
     using SM = BackwardSmem<PASS, TILE>;
     constexpr int NT = TILE * TILE, NW = NT / 32;
