@@ -349,6 +349,21 @@ def ours_arm(args, cfg: Config):
     except (OSError, KeyError, ValueError):
         pass
 
+    # Newton-solve microbenchmark (BASELINE config 4): 10M Gaussians, random SPD blocks
+    # for every attribute group, colour rank-4 (V = 4 views), HBM-roofline bound.
+    solve_mb = None
+    if world == 1 and not args.no_solve_microbench:
+        mb_n = 10_000_000
+        ms5 = ctx.microbench_solve(mb_n, sh_degree=3, views=4, reps=5)
+        upd_s = mb_n / (sum(ms5) * 1e-3)
+        bytes_per_update = 684  # SH3, V = 4 compact accumulators + params in/out
+        hbm = float(measured_peaks().get("hbm_gbs", 6552.0))
+        solve_mb = {"gaussians": mb_n, "ms_per_attr": dict(zip(("position", "rotation", "scaling", "opacity", "color"),
+                                                                [round(x, 4) for x in ms5])),
+                    "gaussian_updates_per_s": upd_s, "algorithmic_bytes_per_update": bytes_per_update,
+                    "achieved_GBps": upd_s * bytes_per_update / 1e9,
+                    "hbm_frac": upd_s * bytes_per_update / 1e9 / hbm}
+
     cpu = None
     if not args.no_cpu_baseline:
         cpu = run_reference_sample(cfg, 2, 0, args.ref_shrink, target_ctx=lib.context(local))
@@ -374,6 +389,7 @@ def ours_arm(args, cfg: Config):
         "stage_ms_per_step": step_stage_ms,
         "group_ms_per_step_concurrent": {k: round(v / args.steps, 4) for k, v in counters["group_ms"].items()},
         "measured_fp64_tflops": fp64_peak,
+        "solve_microbench": solve_mb,
         "first_order_baselines": dict(fo, newton_ms_per_step=total_ms / args.steps,
                                       newton_over_gd=(total_ms / args.steps) / fo["gd_ms_per_step"],
                                       note="GD steps (first_order_step: primary view only, one gradient traversal) "
@@ -394,6 +410,7 @@ def main():
     p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     p.add_argument("--ref-shrink", type=int, default=64)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-solve-microbench", action="store_true")
     args = p.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -59,6 +59,14 @@ int32_t ngs_set_tile_size(ngs_context* ctx, int32_t tile);
 int32_t ngs_microbench_fp32(ngs_context* ctx, double* tflops);
 /* FP64 DFMA throughput microbenchmark (TFLOP/s). */
 int32_t ngs_microbench_fp64(ngs_context* ctx, double* tflops);
+/* Newton-solve microbenchmark (BASELINE config 4): n synthetic
+ * Gaussians (SH degree sh_degree) with random SPD accumulator blocks for every
+ * attribute group (position/scaling 2x2, rotation/opacity 1x1, colour rank-`views`
+ * per channel), solved without commit `reps` times; ms_out[attr] = mean device
+ * time of solve_<attr> over all n Gaussians. Scratch buffers only (the context's
+ * scene is untouched). */
+int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int32_t views, int32_t reps,
+                             double ms_out[5]);
 
 #ifdef __cplusplus
 }

@@ -504,6 +504,13 @@ class Context:
         self._call("ngs_microbench_fp64", C.byref(v))
         return v.value
 
+    def microbench_solve(self, n: int, sh_degree: int = 3, views: int = 4, reps: int = 5) -> list:
+        """Mean ms of solve_<attr> over n synthetic Gaussians (ngs_microbench_solve)."""
+        out = (C.c_double * 5)()
+        self._call("ngs_microbench_solve", C.c_int32(n), C.c_int32(sh_degree), C.c_int32(views), C.c_int32(reps),
+                   out)
+        return list(out)
+
     # multi-GPU sharding (include/ngs_b200_dist.h; CUDA library only)
     def set_shard(self, rank: int, world: int):
         self._call("ngs_set_shard", C.c_int32(rank), C.c_int32(world))

@@ -1551,6 +1551,159 @@ int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+__device__ __forceinline__ double mb_u01(uint64_t seed, uint64_t k, uint32_t c) {  // splitmix64 -> [0, 1)
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (k * 64 + c + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return static_cast<double>(z >> 11) * 0x1.0p-53;
+}
+
+// Random SPD 2x2 with eigenvalues in [1, 10] * 1e-4 -> (h00, h01, h11).
+__device__ __forceinline__ void mb_spd2(uint64_t seed, uint64_t k, uint32_t c, double* h) {
+    const double l0 = (1.0 + 9.0 * mb_u01(seed, k, c)) * 1e-4, l1 = (1.0 + 9.0 * mb_u01(seed, k, c + 1)) * 1e-4;
+    const double th = 6.283185307179586 * mb_u01(seed, k, c + 2), cs = cos(th), sn = sin(th);
+    h[0] = l0 * cs * cs + l1 * sn * sn;
+    h[1] = (l0 - l1) * cs * sn;
+    h[2] = l0 * sn * sn + l1 * cs * cs;
+}
+
+__global__ void mb_fill_k(SceneDev s, uint8_t* flags, int views, double* apos, double* arot, double* asc, double* aoc,
+                          size_t stride, uint64_t seed) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= s.n) return;
+    auto u = [&](uint32_t c) { return mb_u01(seed, k, c); };
+    s.pos_sigma[k] = make_float4((float)(u(0) - 0.5), (float)(u(1) - 0.5), (float)(u(2) - 0.5), (float)(0.35 + 0.35 * u(3)));
+    s.scale[k] = make_float4((float)(0.005 + 0.007 * u(4)), (float)(0.005 + 0.007 * u(5)), (float)(0.005 + 0.007 * u(6)), 0.f);
+    double q[4] = {u(7) - 0.5, u(8) - 0.5, u(9) - 0.5, u(10) - 0.5};
+    const double qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) + 1e-12;
+    s.quat[k] = make_float4((float)(q[0] / qn), (float)(q[1] / qn), (float)(q[2] / qn), (float)(q[3] / qn));
+    for (int c = 0; c < 48; ++c) {
+        const int i = c % 16;
+        s.sh[static_cast<size_t>(c) * s.n + k] = i == 0 ? (float)(1.8 * u(11 + c) - 0.9) : (float)(0.24 * u(11 + c) - 0.12);
+    }
+    for (int v = 0; v < views; ++v) flags[static_cast<size_t>(v) * s.n + k] = kProjected;
+    double h[3];
+    mb_spd2(seed ^ 1, k, 0, h);
+    apos[k] = 1e-5 * (2 * u(60) - 1);
+    apos[stride + k] = 1e-5 * (2 * u(61) - 1);
+    for (int c = 0; c < 3; ++c) apos[(2 + c) * stride + k] = h[c];
+    arot[k] = 1e-5 * (2 * u(62) - 1);
+    arot[stride + k] = (1.0 + 9.0 * u(63)) * 1e-4;
+    mb_spd2(seed ^ 2, k, 0, h);
+    asc[k] = 1e-5 * (2 * mb_u01(seed ^ 3, k, 0) - 1);
+    asc[stride + k] = 1e-5 * (2 * mb_u01(seed ^ 3, k, 1) - 1);
+    for (int c = 0; c < 3; ++c) asc[(2 + c) * stride + k] = h[c];
+    for (int v = 0; v < views; ++v) {
+        double* a = aoc + static_cast<size_t>(v) * kAccOpColor * stride;
+        a[k] = 1e-5 * (2 * mb_u01(seed ^ 4, k, 8 * v) - 1);
+        a[stride + k] = (1.0 + 9.0 * mb_u01(seed ^ 4, k, 8 * v + 1)) * 1e-4;
+        for (int ch = 0; ch < 3; ++ch) {
+            a[(2 + ch) * stride + k] = 1e-5 * (2 * mb_u01(seed ^ 5, k, 8 * v + ch) - 1);
+            a[(5 + ch) * stride + k] = (1.0 + 9.0 * mb_u01(seed ^ 6, k, 8 * v + ch)) * 1e-4;
+        }
+    }
+}
+
+ngs_camera mb_camera(int i, int views) {  // Fibonacci-sphere camera at radius 2 looking at the origin, 800x800
+    const double ga = 3.141592653589793 * (3.0 - std::sqrt(5.0));
+    const double y = 1.0 - 2.0 * (i + 0.5) / views, r = std::sqrt(std::max(0.0, 1.0 - y * y)), phi = ga * i;
+    const double e[3] = {2.0 * r * std::cos(phi), 2.0 * y, 2.0 * r * std::sin(phi)};
+    double f[3] = {-e[0], -e[1], -e[2]};
+    const double fn = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    for (double& x : f) x /= fn;
+    double up[3] = {0, 1, 0};
+    if (std::fabs(f[1]) > 0.99) up[1] = 0, up[2] = 1;
+    double sx[3] = {f[1] * up[2] - f[2] * up[1], f[2] * up[0] - f[0] * up[2], f[0] * up[1] - f[1] * up[0]};
+    const double sn = std::sqrt(sx[0] * sx[0] + sx[1] * sx[1] + sx[2] * sx[2]);
+    for (double& x : sx) x /= sn;
+    const double uy[3] = {sx[1] * f[2] - sx[2] * f[1], sx[2] * f[0] - sx[0] * f[2], sx[0] * f[1] - sx[1] * f[0]};
+    ngs_camera c{};
+    const double rows[3][3] = {{sx[0], sx[1], sx[2]}, {uy[0], uy[1], uy[2]}, {-f[0], -f[1], -f[2]}};
+    for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) c.view[4 * a + b] = rows[a][b];
+        c.view[4 * a + 3] = -(rows[a][0] * e[0] + rows[a][1] * e[1] + rows[a][2] * e[2]);
+    }
+    c.view[15] = 1.0;
+    const double t = std::tan(0.5 * 60.0 * 3.141592653589793 / 180.0), zn = 0.05, zf = 100.0;
+    c.proj[0] = 1.0 / t;
+    c.proj[5] = 1.0 / t;
+    c.proj[10] = -(zf + zn) / (zf - zn);
+    c.proj[11] = -2.0 * zf * zn / (zf - zn);
+    c.proj[14] = -1.0;
+    c.width = c.height = 800;
+    return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int32_t views, int32_t reps,
+                             double ms_out[5]) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (n <= 0 || views < 1 || views > kMaxSolveViews || sh_degree < 0 || sh_degree > 3 || reps < 1)
+            throw Error(NGS_ERR_INVALID_INPUT, "microbench_solve: bad arguments");
+        const size_t stride = static_cast<size_t>(n);
+        DevBuf<float4> ps, sc, q;
+        DevBuf<float> sh;
+        DevBuf<uint8_t> flags;
+        DevBuf<double> apos, arot, asc, aoc, norm;
+        DevBuf<int> err;
+        ps.ensure(stride);
+        sc.ensure(stride);
+        q.ensure(stride);
+        sh.ensure(48 * stride);
+        flags.ensure(static_cast<size_t>(views) * stride);
+        apos.ensure(kAccPositionUV * stride);
+        arot.ensure(kAccRotation * stride);
+        asc.ensure(kAccScaling * stride);
+        aoc.ensure(static_cast<size_t>(views) * kAccOpColor * stride);
+        norm.ensure(1);
+        err.ensure(1);
+        SceneDev sd{};
+        sd.n = n;
+        sd.sh_degree = sh_degree;
+        sd.n_coeffs = (sh_degree + 1) * (sh_degree + 1);
+        sd.pos_sigma = ps.ptr;
+        sd.scale = sc.ptr;
+        sd.quat = q.ptr;
+        sd.sh = sh.ptr;
+        cudaStream_t s = ctx->stream;
+        mb_fill_k<<<(n + 255) / 256, 256, 0, s>>>(sd, flags.ptr, views, apos.ptr, arot.ptr, asc.ptr, aoc.ptr, stride,
+                                                 0x5EEDull);
+        CUDA_LAUNCH_CHECK();
+        CUDA_CHECK(cudaMemsetAsync(err.ptr, 0, sizeof(int), s));
+        ColorViews cv{};
+        cv.n_views = views;
+        for (int v = 0; v < views; ++v) {
+            upload_camera(mb_camera(v, std::max(views, 2)), cv.cam[v]);
+            cv.flags[v] = flags.ptr + static_cast<size_t>(v) * stride;
+        }
+        const SolveParams sp = to_solve(nullptr, 0);
+        SolveOutputs so{nullptr, nullptr, nullptr, norm.ptr, err.ptr};
+        const double* accs[5] = {apos.ptr, arot.ptr, asc.ptr, aoc.ptr, aoc.ptr};
+        for (int a = 0; a < 5; ++a) {
+            // warm-up, then reps timed launches
+            launch_solve(a, sd, cv.cam[0], 0.3, cv.flags[0], cv, sp, accs[a], stride, so, s);
+            CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
+            for (int r = 0; r < reps; ++r)
+                launch_solve(a, sd, cv.cam[0], 0.3, cv.flags[0], cv, sp, accs[a], stride, so, s);
+            CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
+            CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
+            float ms = 0;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            ms_out[a] = ms / reps;
+        }
+        ctx->check_err();
+    });
+}
+
 int32_t ngs_microbench_fp32(ngs_context* ctx, double* tflops) {
     return guarded([&] {
         CUDA_CHECK(cudaSetDevice(ctx->device));
