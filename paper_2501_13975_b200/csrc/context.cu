@@ -141,6 +141,7 @@ struct ngs_context {
     DevBuf<unsigned long long> pairs;
     DevBuf<uint8_t> visible;
     DevBuf<double> out_delta;
+    DevBuf<double> color_eig;  // colour-solve scratch (ColorViews::eig)
     DevBuf<uint8_t> out_flags;
     TrainerState trainer;
     Profiler prof;
@@ -804,7 +805,7 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
     }
 }
 
-ColorViews color_views(ViewSlot* const* views, int nv) {
+ColorViews color_views(ngs_context* ctx, ViewSlot* const* views, int nv) {
     if (nv > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "at most 8 views per Newton step are supported");
     ColorViews cv{};
     cv.n_views = nv;
@@ -812,6 +813,9 @@ ColorViews color_views(ViewSlot* const* views, int nv) {
         cv.cam[i] = views[i]->cam;
         cv.flags[i] = views[i]->flags.ptr;
     }
+    const int mv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : 8;  // solve_color_k<MV> instantiation
+    ctx->color_eig.ensure(static_cast<size_t>(mv * mv + mv) * std::max(ctx->scene.n, 1));
+    cv.eig = ctx->color_eig.ptr;
     return cv;
 }
 
@@ -960,7 +964,7 @@ int32_t ngs_newton_step(ngs_context* ctx, ngs_attribute attr, int32_t primary_sl
         CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, sizeof(double), ctx->stream));
         CUDA_CHECK(cudaMemsetAsync(ctx->out_flags.ptr, 0, 2 * stride, ctx->stream));
         launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
-                     color_views(views.data(), nv), sp, ctx->acc.ptr, stride, so, ctx->stream);
+                     color_views(ctx, views.data(), nv), sp, ctx->acc.ptr, stride, so, ctx->stream);
         std::vector<double> delta(stride * dsz);
         std::vector<uint8_t> fl(2 * stride);
         double nsq = 0;
@@ -1307,7 +1311,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                 }
                 SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
                 launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
-                             color_views(views.data(), nv), base, ctx->acc.ptr, stride, so, s);
+                             color_views(ctx, views.data(), nv), base, ctx->acc.ptr, stride, so, s);
                 mark(5);
                 const bool geometry = attr == NGS_POSITION || attr == NGS_ROTATION || attr == NGS_SCALING;
                 if (geometry && pass_i + 1 < 5) {
@@ -1681,6 +1685,9 @@ int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int
         CUDA_CHECK(cudaMemsetAsync(err.ptr, 0, sizeof(int), s));
         ColorViews cv{};
         cv.n_views = views;
+        DevBuf<double> eig;
+        eig.ensure(static_cast<size_t>(8 * 8 + 8) * stride);
+        cv.eig = eig.ptr;
         for (int v = 0; v < views; ++v) {
             upload_camera(mb_camera(v, std::max(views, 2)), cv.cam[v]);
             cv.flags[v] = flags.ptr + static_cast<size_t>(v) * stride;

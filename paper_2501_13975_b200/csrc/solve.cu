@@ -332,12 +332,13 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
 // (near-collinear view directions) carry eigenvalue ~0 and are floored to mu;
 // the null space of Phi^T carries no gradient. Nothing n-dimensional is
 // stored: phi_v is re-evaluated when beta is committed.
+// Colour solve, stage 1 (per Gaussian): the Gram matrix G = Phi^T Phi of the
+// views' SH bases and its eigen-decomposition G = E L E^T (stored: E, diag L),
+// shared by the three channels of stage 2.
 template <int MV>
-__global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
-                                                     const double* __restrict__ acc, size_t stride,
-                                                     SolveOutputs out) {
+__global__ void __launch_bounds__(128) solve_color_gram_k(SceneDev s, ColorViews cv, double* __restrict__ eig,
+                                                          size_t stride) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    double nsq = 0.0;
     if (k < s.n) {
         const int n = s.n_coeffs;
         const float4 ps = s.pos_sigma[k];
@@ -378,7 +379,67 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
         for (int a = 0; a < MV; ++a)
 #pragma unroll
             for (int b = 0; b < MV; ++b) L[a][b] = G[a][b];
-        if (n > 1) jacobi_eig<MV>(L, E);
+        jacobi_eig<MV>(L, E);
+#pragma unroll
+        for (int a = 0; a < MV; ++a) {
+            eig[static_cast<size_t>(MV * MV + a) * stride + k] = L[a][a];
+#pragma unroll
+            for (int b = 0; b < MV; ++b) eig[static_cast<size_t>(MV * a + b) * stride + k] = E[a][b];
+        }
+    }
+}
+
+// Colour solve, stage 2 (one thread per Gaussian and channel, blockIdx.y = channel).
+template <int MV>
+__global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
+                                                     const double* __restrict__ acc, size_t stride,
+                                                     const double* __restrict__ eig, SolveOutputs out) {
+    const int ch = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq = 0.0;
+    if (k < s.n) {
+        const int n = s.n_coeffs;
+        const float4 ps = s.pos_sigma[k];
+        const D3 p = {ps.x, ps.y, ps.z};
+        const int nv = cv.n_views;
+        D3 dir[MV];
+        uint8_t fl[MV];
+#pragma unroll
+        for (int v = 0; v < MV; ++v) {
+            fl[v] = 0;
+            dir[v] = d3(0, 0, 1);
+            if (v < nv) {
+                fl[v] = cv.flags[v][k];
+                double nr;
+                if (!view_direction(cv.cam[v], p, dir[v], nr)) dir[v] = d3(0, 0, 1);
+            }
+        }
+        // Gram matrix of the visible views' SH bases (phi_a . phi_b); absent views are zero.
+        double G[MV][MV];
+#pragma unroll
+        for (int a = 0; a < MV; ++a) {
+            double pa[16];
+            sh_basis(dir[a], s.sh_degree, pa);
+#pragma unroll
+            for (int b = 0; b <= a; ++b) {
+                double pb[16];
+                sh_basis(dir[b], s.sh_degree, pb);
+                double t = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) t += pa[i] * pb[i];
+                const bool on = (fl[a] & kProjected) && (fl[b] & kProjected);
+                G[a][b] = on ? t : 0.0;
+                G[b][a] = G[a][b];
+            }
+        }
+        double L[MV][MV], E[MV][MV];  // from stage 1 (diagonal L only is read)
+#pragma unroll
+        for (int a = 0; a < MV; ++a)
+#pragma unroll
+            for (int b = 0; b < MV; ++b) {
+                L[a][b] = (a == b) ? (n > 1 ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : G[a][a]) : 0.0;
+                E[a][b] = n > 1 ? eig[static_cast<size_t>(MV * a + b) * stride + k] : (a == b ? 1.0 : 0.0);
+            }
         double lmax = 0;
 #pragma unroll
         for (int a = 0; a < MV; ++a) lmax = fmax(lmax, L[a][a]);
@@ -391,16 +452,15 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
             isq[a] = kept[a] ? 1.0 / sqrt(L[a][a]) : 0.0;
             r += kept[a] ? 1 : 0;
         }
-        double beta_all[3][MV];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
+        double beta_all[MV];
+        do {
             double gv[MV], hv[MV];
             bool any = false;
 #pragma unroll
             for (int v = 0; v < MV; ++v) {
                 gv[v] = 0.0;
                 hv[v] = 0.0;
-                beta_all[ch][v] = 0.0;
+                beta_all[v] = 0.0;
                 if (v < nv && (fl[v] & kProjected) && !(fl[v] & (kClamp0 << ch))) {
                     const double* a = acc + static_cast<size_t>(v) * kAccOpColor * stride;
                     gv[v] = a[(2 + ch) * stride + k];
@@ -408,7 +468,7 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
                     any = true;
                 }
             }
-            if (!any) continue;
+            if (!any) break;
             double beta[MV];
 #pragma unroll
             for (int a = 0; a < MV; ++a) beta[a] = 0.0;
@@ -504,23 +564,22 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
             if (sp.color_cap > 0.0 && sqrt(nrm2) > sp.color_cap) scale = sp.color_cap / sqrt(nrm2);
             nsq += nrm2 * scale * scale;
 #pragma unroll
-            for (int a = 0; a < MV; ++a) beta_all[ch][a] = beta[a] * scale;
-        }
+            for (int a = 0; a < MV; ++a) beta_all[a] = beta[a] * scale;
+        } while (false);
         // delta_ch = sum_v beta_v phi_v (SH0: delta = beta_0); write / commit.
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
+        {
             double delta[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) delta[i] = 0.0;
             if (n == 1) {
-                delta[0] = beta_all[ch][0];
+                delta[0] = beta_all[0];
             } else {
 #pragma unroll
                 for (int v = 0; v < MV; ++v) {
                     double ph[16];
                     sh_basis(dir[v], s.sh_degree, ph);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) delta[i] += beta_all[ch][v] * ph[i];
+                    for (int i = 0; i < 16; ++i) delta[i] += beta_all[v] * ph[i];
                 }
             }
             if (out.delta)
@@ -535,7 +594,7 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
                     if (i < n) s.sh[(static_cast<size_t>(16 * ch + i)) * s.n + k] = (float)((double)cur[i] + delta[i]);
             }
         }
-        if (out.accepted) out.accepted[k] = 1;
+        if (out.accepted && ch == 0) out.accepted[k] = 1;
     }
     block_add(nsq, out.norm_sq);
 }
@@ -690,7 +749,7 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
                   size_t stride, const SolveOutputs& out, cudaStream_t s) {
     const int n = scene.n;
     if (n == 0) return;
-    StageScope st(NGS_STAGE_SOLVE, s);
+    StageScope st(NGS_STAGE_SOLVE, s, attr == NGS_COLOR && scene.n_coeffs > 1 ? 2 : 1);
     switch (attr) {
         case NGS_POSITION:
             solve_position_k<<<blocks_for(n), 256, 0, s>>>(scene, primary, sp, acc, stride, out);
@@ -705,16 +764,22 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
         case NGS_OPACITY:
             solve_opacity_k<<<blocks_for(n), 256, 0, s>>>(scene, sp, acc, stride, cv.n_views, out);
             break;
-        case NGS_COLOR:
+        case NGS_COLOR: {
+            // stage 1 (Gram eigen-decomposition, only with higher SH bands) + stage 2 per channel
+            auto run = [&](auto gram_kernel, auto ch_kernel, int) {
+                if (scene.n_coeffs > 1) gram_kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, cv.eig, stride);
+                ch_kernel<<<dim3(blocks_for(n, 128), 3), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
+            };
             if (cv.n_views <= 1)
-                solve_color_k<1><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+                run(solve_color_gram_k<1>, solve_color_k<1>, 1);
             else if (cv.n_views <= 2)
-                solve_color_k<2><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+                run(solve_color_gram_k<2>, solve_color_k<2>, 2);
             else if (cv.n_views <= 4)
-                solve_color_k<4><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+                run(solve_color_gram_k<4>, solve_color_k<4>, 4);
             else
-                solve_color_k<8><<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, out);
+                run(solve_color_gram_k<8>, solve_color_k<8>, 8);
             break;
+        }
     }
     CUDA_LAUNCH_CHECK();
 }

@@ -29,6 +29,7 @@ struct ColorViews {
     int n_views;
     CameraDev cam[kMaxSolveViews];
     const uint8_t* flags[kMaxSolveViews];
+    double* eig;  // colour-solve scratch: (MV^2 + MV) doubles per Gaussian (Gram eigen-decomposition)
 };
 
 // First-order baselines (first_order_step, trainer.hpp:419-509).
