@@ -116,11 +116,15 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __r
     int val[kSItems];
     unsigned wrank[kSItems];
 #pragma unroll
+    for (int r = 0; r < kSItems; ++r) {  // all loads first: 2 x kSItems in flight per thread
+        const int i = base + warp * (kSItems * 32) + r * 32 + lane;
+        key[r] = i < n ? keys_in[i] : 0u;
+        val[r] = i < n ? vals_in[i] : 0;
+    }
+#pragma unroll
     for (int r = 0; r < kSItems; ++r) {
         const int i = base + warp * (kSItems * 32) + r * 32 + lane;
         const bool valid = i < n;
-        key[r] = valid ? keys_in[i] : 0u;
-        val[r] = valid ? vals_in[i] : 0;
         const int digit = valid ? static_cast<int>((key[r] >> shift) & 0xFF) : -1;
         const unsigned peers = __match_any_sync(0xffffffffu, digit);
         const unsigned before = __popc(peers & ((1u << lane) - 1u));
@@ -148,14 +152,22 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __r
         atomicExch(st, kFlagInc | bc);
     } else {
         atomicExch(st, kFlagAgg | bc);
-        for (int t = tile - 1; t >= 0; --t) {
-            const volatile unsigned* sp = status + static_cast<size_t>(t) * kDigits + d;
-            unsigned v;
-            do {
-                v = *sp;
-            } while ((v & ~kCountMask) == 0);
-            excl += v & kCountMask;
-            if ((v & ~kCountMask) == kFlagInc) break;
+        // Walk back four predecessors per round (independent loads in flight), in order,
+        // re-polling only a status that is not published yet.
+        bool found = false;
+        for (int t = tile - 1; t >= 0 && !found; t -= 4) {
+            unsigned v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                v[q] = t - q >= 0 ? *(const volatile unsigned*)(status + static_cast<size_t>(t - q) * kDigits + d) : 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (found || t - q < 0) break;
+                const volatile unsigned* sp = status + static_cast<size_t>(t - q) * kDigits + d;
+                while ((v[q] & ~kCountMask) == 0) v[q] = *sp;
+                excl += v[q] & kCountMask;
+                if ((v[q] & ~kCountMask) == kFlagInc) found = true;
+            }
         }
         atomicExch(st, kFlagInc | (excl + bc));
     }
