@@ -182,7 +182,7 @@ def reference_arm(args, cfg: Config):
     r = run_reference_sample(cfg, max(args.steps, 1), args.warmup, args.ref_shrink)
     line = {"metric": METRIC, "value": r["value"], "unit": "views/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 / r["value"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": cfg.name, "desc": cfg.desc, "knn": 3, "secondary_downsample": 4},
             "cpu_baseline": {"value": r["value"], "unit": "views/s", "cores": r["cores"], "kind": "reference",
