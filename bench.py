@@ -218,6 +218,8 @@ def ours_arm(args, cfg: Config):
         tc.knn = int(os.environ["NGS_BENCH_KNN"])
 
     def configure(c, host_targets):
+        if args.deterministic:
+            c.set_deterministic(True)
         c.set_scene(init)
         tc.host_targets = 1 if host_targets else 0
         c.trainer_configure(tc, cams, targets, list(range(cfg.views)))
@@ -373,6 +375,7 @@ def ours_arm(args, cfg: Config):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
         "config": {"workload": cfg.name, "desc": cfg.desc, "knn": int(tc.knn), "secondary_downsample": 4,
+                   "deterministic": bool(args.deterministic),
                    "parallelism": f"tile-row bands x{world} + NCCL all-reduce of accumulators", "l2": "flushed (256 MB write) between steps",
                    "targets": "GPU-rendered from the truth scene"},
         "gaussian_solves_per_s": value * cfg.kernels,
@@ -411,6 +414,7 @@ def main():
     p.add_argument("--ref-shrink", type=int, default=64)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-solve-microbench", action="store_true")
+    p.add_argument("--deterministic", action="store_true", help="exact fixed-point accumulation (bitwise reproducible)")
     args = p.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -225,6 +225,12 @@ typedef struct ngs_context ngs_context;
 
 int32_t ngs_context_create(int32_t device, ngs_context** out);
 int32_t ngs_context_destroy(ngs_context* ctx);
+/* Determinism (SURVEY.md §8(b) threading row; the reference is deterministic for a
+ * fixed seed and thread count): on != 0 makes every per-Gaussian accumulation an
+ * exact integer fixed-point sum (no floating-point atomics), so repeated runs give
+ * bitwise-identical parameters. Off by default (FP64 atomics, same results up to
+ * summation-order rounding). */
+int32_t ngs_set_deterministic(ngs_context* ctx, int32_t on);
 
 /* Scene upload / download (validate_scene, scene.hpp:209-217). */
 int32_t ngs_set_scene(ngs_context* ctx, const ngs_scene* scene);

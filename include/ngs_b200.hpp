@@ -162,6 +162,8 @@ public:
         ctx_.reset(c);
     }
     ngs_context* get() const { return ctx_.get(); }
+    // Bitwise-reproducible accumulation (ngs_set_deterministic).
+    void set_deterministic(bool on) { check(ngs_set_deterministic(get(), on ? 1 : 0)); }
 
     void set_scene(const Scene& s) {
         SceneArrays a(s);

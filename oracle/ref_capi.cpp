@@ -186,6 +186,9 @@ int32_t ngs_context_destroy(ngs_context* ctx) {
     delete ctx;
     return NGS_OK;
 }
+int32_t ngs_set_deterministic(ngs_context*, int32_t) {
+    return NGS_OK;  // the reference is deterministic for a fixed thread count (parallel_for, core.hpp:89-108)
+}
 
 int32_t ngs_set_scene(ngs_context* ctx, const ngs_scene* s) {
     return guarded([&] {

@@ -148,7 +148,7 @@ EXPORTED_SYMBOLS = (
     "ngs_get_scene_info", "ngs_get_scene", "ngs_render", "ngs_build_view", "ngs_get_view_info",
     "ngs_view_splats", "ngs_view_image", "ngs_view_loss_derivs", "ngs_accumulate", "ngs_newton_step",
     "ngs_trainer_configure", "ngs_trainer_neighbors", "ngs_trainer_step", "ngs_trainer_barrier_weight",
-    "ngs_trainer_probe", "ngs_trainer_run", "ngs_view_metrics",
+    "ngs_trainer_probe", "ngs_trainer_run", "ngs_view_metrics", "ngs_set_deterministic",
 )
 
 
@@ -447,6 +447,10 @@ class Context:
         rep = ngs_iteration_report()
         self._call("ngs_trainer_step", C.c_int32(view_id), C.byref(rep))
         return rep
+
+    def set_deterministic(self, on: bool = True):
+        """Exact integer fixed-point accumulation: bitwise-reproducible runs."""
+        self._call("ngs_set_deterministic", C.c_int32(1 if on else 0))
 
     def trainer_probe(self) -> ngs_metrics:
         """Trainer::probe_metrics (trainer.hpp:215-233)."""

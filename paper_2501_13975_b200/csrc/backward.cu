@@ -611,6 +611,35 @@ __device__ __forceinline__ void grad_record(const Rec& r, float sigma, float (&v
     v[8] = sgo;
 }
 
+// Exact, order-independent accumulation of x * 2^kLimbShift (see backward.h).
+__device__ __forceinline__ void add_fixed128(unsigned long long* limbs, float x) {
+    int e;
+    const float m = frexpf(x, &e);                                  // x = m 2^e, 0.5 <= |m| < 1
+    const long long mi = static_cast<long long>(ldexpf(m, 24));      // exact: |mi| < 2^24
+    const int sh = e - 24 + kLimbShift;
+    __int128 v = static_cast<__int128>(mi);
+    v = sh >= 0 ? (v << sh) : (v >> (-sh));                          // deterministic truncation below 2^-88
+    const unsigned __int128 u = static_cast<unsigned __int128>(v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const unsigned long long chunk = static_cast<unsigned long long>((u >> (32 * i)) & 0xffffffffull);
+        if (chunk) atomicAdd(limbs + i, chunk);
+    }
+}
+
+__global__ void limbs_to_double_k(const unsigned long long* __restrict__ limbs, double* __restrict__ acc, size_t count) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        unsigned __int128 u = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u += static_cast<unsigned __int128>(limbs[4 * i + q]) << (32 * q);
+        const __int128 v = static_cast<__int128>(u);
+        const long long hi = static_cast<long long>(v >> 64);
+        const unsigned long long lo = static_cast<unsigned long long>(v);
+        acc[i] = ldexp(static_cast<double>(hi), 64 - kLimbShift) + ldexp(static_cast<double>(lo), -kLimbShift);
+    }
+}
+
 // Per-warp record queue (ring of 64 entries) between the two phases.
 constexpr int kQ = 64;
 struct WarpQueue {
@@ -918,7 +947,12 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
             for (int c = 0; c < NA; ++c) {
                 const float val = s_acc[warp][c][i];
                 s_acc[warp][c][i] = 0.f;
-                if (val != 0.f) atomicAdd(&a.acc[static_cast<size_t>(c) * a.acc_stride + k], static_cast<double>(val));
+                if (val == 0.f) continue;
+                if (a.acc_limbs) {
+                    add_fixed128(a.acc_limbs + (static_cast<size_t>(c) * a.acc_stride + k) * 4, val);
+                } else {
+                    atomicAdd(&a.acc[static_cast<size_t>(c) * a.acc_stride + k], static_cast<double>(val));
+                }
             }
         }
     }
@@ -975,8 +1009,14 @@ struct SmemTag {
     using type = T;
 };
 
+void limbs_to_double(const unsigned long long* limbs, double* acc, size_t count, cudaStream_t s) {
+    if (count == 0) return;
+    limbs_to_double_k<<<static_cast<int>(std::min<size_t>((count + 255) / 256, 8 * 148)), 256, 0, s>>>(limbs, acc, count);
+    CUDA_LAUNCH_CHECK();
+}
+
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
-                     unsigned long long* contrib_pairs, cudaStream_t s) {
+                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs) {
     if (v.pairs == 0 || v.n == 0) return;
     BackwardArgs a;
     a.tiles_x = v.cam.tiles_x;
@@ -997,6 +1037,7 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     for (int c = 0; c < 3; ++c) a.bg[c] = scene.bg[c];
     a.acc = acc;
     a.acc_stride = acc_stride;
+    a.acc_limbs = acc_limbs;
     a.visible = visible;
     a.contrib_pairs = contrib_pairs;
     const int own0 = std::max(0, v.raster.own_y0), own1 = std::min(v.cam.tiles_y, v.raster.own_y1);

@@ -64,13 +64,22 @@ struct BackwardArgs {
     float bg[3];
     double* acc;
     size_t acc_stride;
+    unsigned long long* acc_limbs;  // deterministic mode: exact fixed-point limbs [comp][stride][4] (acc unused)
     uint8_t* visible;                    // optional: set to 1 for kernels with >= 1 record
     unsigned long long* contrib_pairs;   // optional: count of contributing (pixel, splat) records
 };
 
 void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s,
                          float* out = nullptr);  // out: destination (default v.consts)
+// Deterministic accumulation: each FP32 partial is converted exactly to a 128-bit
+// two's-complement fixed-point number (binary point 2^-88) and added as four
+// 32-bit chunks into four 64-bit counters with integer atomics. Integer addition
+// is associative, so the sums do not depend on the order in which blocks finish;
+// limbs_to_double normalises the carries and rounds once to FP64.
+constexpr int kLimbShift = 88;
+void limbs_to_double(const unsigned long long* limbs, double* acc, size_t count, cudaStream_t s);
+
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
-                     unsigned long long* contrib_pairs, cudaStream_t s);
+                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs = nullptr);
 
 }  // namespace ngsb

@@ -142,6 +142,8 @@ struct ngs_context {
     DevBuf<uint8_t> visible;
     DevBuf<double> out_delta;
     DevBuf<double> color_eig;  // colour-solve scratch (ColorViews::eig)
+    bool deterministic = false;             // exact fixed-point accumulation (ngs_set_deterministic)
+    DevBuf<unsigned long long> acc_limbs;   // [comp][stride][4] in deterministic mode
     DevBuf<uint8_t> out_flags;
     TrainerState trainer;
     Profiler prof;
@@ -774,7 +776,14 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
     const size_t stride = static_cast<size_t>(std::max(n, 1));
     const int comps = acc_components(pass) * (pass == kPassOpacityColor ? nv : 1);
     ctx->acc.ensure(stride * comps);
-    CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
+    unsigned long long* limbs = nullptr;
+    if (ctx->deterministic) {
+        ctx->acc_limbs.ensure(4 * stride * comps);
+        limbs = ctx->acc_limbs.ptr;
+        CUDA_CHECK(cudaMemsetAsync(limbs, 0, sizeof(unsigned long long) * 4 * stride * comps, ctx->stream));
+    } else {
+        CUDA_CHECK(cudaMemsetAsync(ctx->acc.ptr, 0, sizeof(double) * stride * comps, ctx->stream));
+    }
     concurrent = concurrent && nv <= kMaxSolveViews && !ctx->prof.enabled;
     if (concurrent) ctx->fork(nv, ctx->vs.data());  // after the accumulator memset
     for (int ii = 0; ii < nv; ++ii) {
@@ -790,19 +799,27 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
         if (concurrent && chained) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->rev[i], 0));
         double* acc = ctx->acc.ptr + (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0);
         unsigned long long* contrib = ctx->pairs.ptr + (pass == kPassPositionUV ? kPassPosition : pass);
-        launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s);
+        unsigned long long* vl =
+            limbs ? limbs + 4 * (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0) : nullptr;
+        launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s, vl);
     }
     if (concurrent) ctx->join(nv, ctx->vs.data());
     if (ctx->comm) {
         // Exchange step: per-Gaussian FP64 accumulators summed over ranks (NVLink / NVSwitch).
         StageScope st(NGS_STAGE_OTHER, ctx->stream, 0);
-        nccl_check(nccl().all_reduce(ctx->acc.ptr, ctx->acc.ptr, stride * comps, ncclFloat64, ncclSum, ctx->comm,
-                                     ctx->stream),
-                   "ncclAllReduce(accumulators)");
+        if (limbs)  // integer limbs: the cross-rank sum is exact as well (32-bit headroom per limb)
+            nccl_check(nccl().all_reduce(limbs, limbs, 4 * stride * comps, ncclUint64, ncclSum, ctx->comm,
+                                         ctx->stream),
+                       "ncclAllReduce(accumulator limbs)");
+        else
+            nccl_check(nccl().all_reduce(ctx->acc.ptr, ctx->acc.ptr, stride * comps, ncclFloat64, ncclSum, ctx->comm,
+                                         ctx->stream),
+                       "ncclAllReduce(accumulators)");
         if (visible)
             nccl_check(nccl().all_reduce(visible, visible, stride, ncclUint8, ncclMax, ctx->comm, ctx->stream),
                        "ncclAllReduce(visible)");
     }
+    if (limbs) limbs_to_double(limbs, ctx->acc.ptr, stride * comps, ctx->stream);
 }
 
 ColorViews color_views(ngs_context* ctx, ViewSlot* const* views, int nv) {
@@ -1646,6 +1663,10 @@ ngs_camera mb_camera(int i, int views) {  // Fibonacci-sphere camera at radius 2
 }  // namespace
 
 extern "C" {
+
+int32_t ngs_set_deterministic(ngs_context* ctx, int32_t on) {
+    return guarded([&] { ctx->deterministic = on != 0; });
+}
 
 int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int32_t views, int32_t reps,
                              double ms_out[5]) {

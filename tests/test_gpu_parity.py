@@ -361,3 +361,47 @@ def test_nccl_single_rank_step_matches_local(gpu):
     for f in ("position", "scale", "quaternion", "sigma", "sh"):
         a, b = getattr(scenes[0], f), getattr(scenes[1], f)
         assert np.max(np.abs(a - b)) <= 1e-6 * max(1.0, float(np.max(np.abs(a)))), f
+
+
+def test_deterministic_mode_is_bitwise_reproducible(gpu):
+    """ngs_set_deterministic: exact integer fixed-point accumulation makes repeated
+    trainer runs bitwise-identical, and stays at reference parity."""
+    from paper_2501_13975_b200.workload import Config, cameras_for, make_scenes
+    cfg = Config("det", 20_000, 6, 160, 128, 3, 0.45)
+    truth, init = make_scenes(cfg, seed=5)
+    cams = cameras_for(cfg)
+    c = gpu.context()
+    c.set_scene(truth)
+    targets = [c.render(x) for x in cams]
+    c.close()
+    outs = []
+    for rep in range(2):
+        ctx = gpu.context()
+        ctx.set_deterministic(True)
+        ctx.set_scene(init)
+        tc = gpu.default_train()
+        tc.knn = 2
+        ctx.trainer_configure(tc, cams, targets, list(range(cfg.views)))
+        for v in (0, 3, 4):
+            ctx.trainer_step(v)
+        outs.append(ctx.get_scene())
+        ctx.close()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        assert np.array_equal(getattr(outs[0], f), getattr(outs[1], f)), f
+    # parity of the deterministic path with the reference (same fixture as test_trainer_step)
+    d = synth(seed=23, kernels=20, views=4, probe_views=0, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    g, r = pair(gpu, d["init"], quantize=False)
+    g.set_deterministic(True)
+    for ctx, lib in ((g, gpu), (r, ref())):
+        cfg2 = lib.default_train()
+        cfg2.knn = 2
+        cfg2.secondary_downsample = 2
+        ctx.trainer_configure(cfg2, d["cameras"], d["targets"], d["train"], d["probe"], d["secondary"],
+                              d["secondary_downsample"])
+    for view in d["train"][:2]:
+        g.trainer_step(view)
+        r.trainer_step(view)
+    sg, sr = g.get_scene(), r.get_scene()
+    for f in ("position", "scale", "sigma", "sh"):
+        assert qerr(getattr(sg, f), getattr(sr, f)) < 1e-4, f
