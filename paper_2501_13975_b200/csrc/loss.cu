@@ -3,12 +3,14 @@
 //
 // FP64 throughout: SSIM variance/covariance are E[x^2]-E[x]^2 differences of
 // O(1) quantities whose result is O(1e-6) in flat regions; FP32 loses them
-// entirely (SURVEY.md §7 hard part 1). Two shared-memory tiled kernels, each
-// a separable valid-tap convolution (loss.hpp:81-115) with an H-halo of
-// window/2 on every side:
+// entirely (SURVEY.md §7 hard part 1). Two kernels, each a separable valid-tap
+// convolution (loss.hpp:81-115) with a halo of window/2 on every side:
 //   A: 5 window statistics -> 9 window-centre fields (loss.hpp:162-214, 262-305)
 //   B: 9 field convolutions (w for grad/kw, w^2 for the rest) -> grad, hess
 //      (loss.hpp:309-329) plus the L2 terms (loss.hpp:138-156).
+// The default 11-tap window runs the 32x32-tile register-blocked kernels
+// (ssim_fields32_k / ssim_derivs32_k); other windows the generic 16x16 ones.
+// compute_loss_value is the value-only variant used by the metrics.
 #include <algorithm>
 
 #include "context.h"

@@ -124,68 +124,6 @@ __device__ __forceinline__ bool eval_splat_bf(const SplatSh& sp, float x, float 
     return q <= sp.g1.z && !(e.alpha < cutoff);
 }
 
-// Returns false (and leaves e.g / e.alpha unset) when q exceeds `qmax`.
-__device__ __forceinline__ bool eval_splat(float px, float py, float qa, float qb, float qc, float sigma, float x,
-                                           float y, float qmax, SplatEval& e) {
-    e.dx = __fsub_rn(px, x);
-    e.dy = __fsub_rn(py, y);
-    e.qd0 = __fmaf_rn(qa, e.dx, __fmul_rn(qb, e.dy));
-    e.qd1 = __fmaf_rn(qb, e.dx, __fmul_rn(qc, e.dy));
-    const float q = __fmaf_rn(e.dx, e.qd0, __fmul_rn(e.dy, e.qd1));
-    if (q > qmax) return false;
-    e.g = expf(__fmul_rn(-0.5f, q));  // full-accuracy exp: the image feeds cancelling (c - c^t) terms
-    e.alpha = __fmul_rn(e.g, sigma);
-    return true;
-}
-
-// Warp reduce-scatter of NA per-lane values: log2(P) halving exchanges
-// (P = next power of two >= NA) followed by a butterfly on the survivor, i.e.
-// ~NA + 5 - log2(P) shuffles instead of 5 NA. Afterwards lane l holds the full
-// warp sum of value index reduce_index<NA>(l) (lanes sharing an index agree).
-template <int NA>
-struct ReducePow2 {
-    static constexpr int P = NA <= 1 ? 1 : NA <= 2 ? 2 : NA <= 4 ? 4 : NA <= 8 ? 8 : 16;
-    static constexpr int L = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : 4;
-};
-
-template <int NA>
-__device__ __forceinline__ float warp_reduce_scatter(const float (&v)[NA], int lane) {
-    constexpr int P = ReducePow2<NA>::P;
-    float x[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) x[i] = i < NA ? v[i] : 0.f;
-    int o = 16;
-#pragma unroll
-    for (int m = P; m > 1; m >>= 1, o >>= 1) {
-        const bool upper = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < m / 2; ++i) {
-            const float send = upper ? x[i] : x[i + m / 2];
-            const float keep = upper ? x[i + m / 2] : x[i];
-            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-    }
-#pragma unroll
-    for (; o > 0; o >>= 1) x[0] += __shfl_xor_sync(0xffffffffu, x[0], o);
-    return x[0];
-}
-
-// Value index held by `lane` after warp_reduce_scatter, and whether the lane
-// is the representative (lowest) lane of that index.
-template <int NA>
-__device__ __forceinline__ int reduce_index(int lane) {
-    constexpr int L = ReducePow2<NA>::L;
-    int idx = 0;
-#pragma unroll
-    for (int b = 0; b < L; ++b) idx |= ((lane >> (4 - b)) & 1) << (L - 1 - b);
-    return idx;
-}
-template <int NA>
-__device__ __forceinline__ bool reduce_representative(int lane) {
-    constexpr int L = ReducePow2<NA>::L;
-    return (lane & ((1 << (5 - L)) - 1)) == 0;
-}
-
 // T <- T * (1 - alpha), C <- C + T * alpha * c (rasterizer.hpp:287-288).
 __device__ __forceinline__ float blend_weight(float t, float alpha) { return __fmul_rn(t, alpha); }
 __device__ __forceinline__ float next_transmittance(float t, float alpha) {
