@@ -248,6 +248,15 @@ __global__ void tile_ranges_k(const int* d_pairs, int T, const unsigned int* key
 // are expressed relative to the tile origin so the FP32 offsets carry
 // full precision at 4K resolutions.
 template <int TILE>
+struct RasterSmem {
+    static constexpr int N = TILE * TILE;
+    float4 raw[2][4][N];  // staged records (pix as double2, ra, rb, rc), double-buffered
+    double col[3][N];
+    SplatSh sp[N];
+    unsigned char wmask[N];
+};
+
+template <int TILE>
 __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int W, int H, const int2* __restrict__ ranges,
                                                         const int* __restrict__ vals, const double2* __restrict__ pix,
                                                         const float4* __restrict__ ra, const float4* __restrict__ rb,
@@ -255,8 +264,13 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
                                                         float cutoff, float tmin, double* __restrict__ image,
                                                         float* __restrict__ t_final, int* __restrict__ last_out) {
     constexpr int kRasterBatch = TILE * TILE;  // one splat per thread per batch
-    __shared__ SplatSh s_sp[kRasterBatch];
-    __shared__ unsigned char s_wmask[kRasterBatch];            // bit w: the cutoff ellipse reaches warp w's rows
+    // Dynamic shared memory (> 48 KB for 16x16 tiles): RasterSmem<TILE>.
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RasterSmem<TILE>& S = *reinterpret_cast<RasterSmem<TILE>*>(smem_raw);
+    auto& s_sp = S.sp;
+    auto& s_col = S.col;    // colours widened once per splat (no per-pixel F2F)
+    auto& s_wmask = S.wmask;  // bit w: the cutoff ellipse reaches warp w's box
+    auto& s_raw = S.raw;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     int lx, ly;
@@ -270,10 +284,10 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
     double C0 = 0.0, C1 = 0.0, C2 = 0.0;  // FP64 colour sums: the image feeds the cancelling (c - c^t) loss terms
     int last = -1;
     bool done = !inside;
+    const float tmin_eff = tmin > 0.f ? tmin : -1.0f;  // T < tmin_eff: early termination (none when tmin = 0)
     // Software pipeline: thread t stages splat t of the next batch with cp.async
     // (into its own slot, so only its own wait is needed) while the current batch
     // is composited; the list entry of the batch after that is loaded meanwhile.
-    __shared__ float4 s_raw[2][4][kRasterBatch];  // pix (double2), ra, rb, rc
     const int t = threadIdx.x;
     auto issue = [&](int buf, int k) {
         cp_async16(&s_raw[buf][0][t], pix + k);
@@ -302,6 +316,9 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             sp.g2 = make_float2(b.w, c.x);
             sp.pad = make_float2(0.f, 0.f);
             s_sp[threadIdx.x] = sp;
+            s_col[0][threadIdx.x] = b.z;
+            s_col[1][threadIdx.x] = b.w;
+            s_col[2][threadIdx.x] = c.x;
             s_wmask[threadIdx.x] = static_cast<unsigned char>(
                 WarpBox<TILE>::mask_exact(px, py, ellipse_half_extent(qmax, c.y), ellipse_half_extent(qmax, c.w), a.z,
                                           a.w, b.x, qmax));
@@ -325,12 +342,12 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
                 SplatEval e;
                 if (eval_splat_bf(sp, fx, fy, cutoff, e) && !done) {
                     const double w = blend_weight(T, e.alpha);
-                    C0 = __fma_rn(w, sp.g1.w, C0);
-                    C1 = __fma_rn(w, sp.g2.x, C1);
-                    C2 = __fma_rn(w, sp.g2.y, C2);
+                    C0 = __fma_rn(w, s_col[0][j], C0);
+                    C1 = __fma_rn(w, s_col[1][j], C1);
+                    C2 = __fma_rn(w, s_col[2][j], C2);
                     T = next_transmittance(T, e.alpha);
                     last = base + j;
-                    if (tmin > 0.f && T < tmin) done = true;
+                    if (T < tmin_eff) done = true;
                 }
             }
         }
@@ -445,16 +462,21 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     }
     if (g_prof) g_prof->stats.renders += 1;
     StageScope st(NGS_STAGE_RASTER, s);
-    auto launch = [&](auto kernel, int threads) {
-        kernel<<<v.T, threads, 0, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val.ptr : nullptr,
+    auto launch = [&](auto kernel, int threads, size_t smem) {
+        static bool attr = false;  // per instantiation
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            attr = true;
+        }
+        kernel<<<v.T, threads, smem, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val.ptr : nullptr,
                                        v.pix.ptr, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1],
                                        scene.bg[2], v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
                                        v.last.ptr);
     };
     if (v.cam.tile == 8)
-        launch(raster_forward_k<8>, 64);
+        launch(raster_forward_k<8>, 64, sizeof(RasterSmem<8>));
     else
-        launch(raster_forward_k<16>, 256);
+        launch(raster_forward_k<16>, 256, sizeof(RasterSmem<16>));
     CUDA_LAUNCH_CHECK();
     v.valid = true;
 }
