@@ -1049,11 +1049,7 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     const int threads = small ? 64 : 256;
     auto go = [&](auto kernel, auto smem_tag) {
         using SM = typename decltype(smem_tag)::type;
-        static bool attr_set = false;  // per instantiation
-        if (!attr_set) {
-            CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(SM)));
-            attr_set = true;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), sizeof(SM));
         kernel<<<blocks, threads, sizeof(SM), s>>>(a);
     };
     switch (pass) {

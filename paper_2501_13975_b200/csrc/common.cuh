@@ -4,8 +4,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <map>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "ngs_b200.h"
 
@@ -31,6 +34,22 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 #define CUDA_CHECK(x) ::ngsb::cuda_check((x), #x, __FILE__, __LINE__)
 #define CUDA_LAUNCH_CHECK() ::ngsb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Opt a kernel into at least `bytes` of dynamic shared memory on the current device. Function
+// attributes are per device, so the high-water mark is kept per (kernel, device).
+inline void ensure_dynamic_smem(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> granted;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice", __FILE__, __LINE__);
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& g = granted[{kernel, dev}];
+    if (bytes > g) {
+        cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
+                   "cudaFuncSetAttribute", __FILE__, __LINE__);
+        g = bytes;
+    }
+}
 
 // Camera constants uploaded per view (camera.hpp:17-45), FP64.
 struct CameraDev {

@@ -604,12 +604,8 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
         const int r32a = band_px0 / kFT, r32b = (band_px1 + kFT - 1) / kFT;
         const dim3 g32((v.W + kFT - 1) / kFT, r32b - r32a, 3);
         const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1), sm_d = sizeof(double) * kFS * (kFT + 1 + 2 * (kFS + 1));
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(ssim_fields32_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_f));
-            CUDA_CHECK(cudaFuncSetAttribute(ssim_derivs32_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
-            attr = true;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(ssim_fields32_k), sm_f);
+        ensure_dynamic_smem(reinterpret_cast<const void*>(ssim_derivs32_k), sm_d);
         if (ssim) {
             v.fields.ensure(27 * npx);
             ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
@@ -655,7 +651,7 @@ void compute_loss_value(ViewSlot& v, cudaStream_t s) {
     if (win.half == kFH) {
         const dim3 g32((v.W + kFT - 1) / kFT, (v.H + kFT - 1) / kFT, 3);
         const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1);
-        CUDA_CHECK(cudaFuncSetAttribute(ssim_fields32_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_f));
+        ensure_dynamic_smem(reinterpret_cast<const void*>(ssim_fields32_k), sm_f);
         ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, nullptr,
                                                v.loss_sums.ptr, 0, 0, v.H);
     } else {

@@ -463,11 +463,7 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     if (g_prof) g_prof->stats.renders += 1;
     StageScope st(NGS_STAGE_RASTER, s);
     auto launch = [&](auto kernel, int threads, size_t smem) {
-        static bool attr = false;  // per instantiation
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            attr = true;
-        }
+        ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
         kernel<<<v.T, threads, smem, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val.ptr : nullptr,
                                        v.pix.ptr, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1],
                                        scene.bg[2], v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,

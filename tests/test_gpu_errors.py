@@ -1,0 +1,85 @@
+"""Error behaviour of the drop-in boundary: invalid inputs raise the same
+exception kind from the CUDA library as from the reference (InvalidInput /
+DegenerateGeometry / NumericalError, core.hpp:30-48), through the C-ABI."""
+import numpy as np
+import pytest
+
+from paper_2501_13975_b200 import capi
+from refimpl import check_fixture, ref, synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    return capi.product()
+
+
+def _scene_cases():
+    base, _, _ = check_fixture(1)
+
+    def mod(f):
+        s = base.copy()
+        for k in ("position", "scale", "quaternion", "sigma", "sh"):
+            setattr(s, k, getattr(s, k).copy())
+        f(s)
+        return s
+
+    return {
+        "non-unit quaternion": mod(lambda s: s.quaternion.__setitem__((0, 0), 2.0)),
+        "zero scale": mod(lambda s: s.scale.__setitem__((1, 2), 0.0)),
+        "opacity at 1": mod(lambda s: s.sigma.__setitem__(2, 1.0)),
+        "opacity at 0": mod(lambda s: s.sigma.__setitem__(3, 0.0)),
+        "background > 1": mod(lambda s: setattr(s, "background", np.array([0.1, 1.5, 0.1]))),
+    }
+
+
+@pytest.mark.parametrize("case", list(_scene_cases()))
+def test_invalid_scene_rejected_like_the_reference(gpu, case):
+    scene = _scene_cases()[case]
+    kinds = []
+    for lib in (gpu, ref()):
+        ctx = lib.context()
+        with pytest.raises(capi.NgsError) as e:
+            ctx.set_scene(scene)
+        kinds.append(type(e.value))
+    assert kinds[0] is kinds[1] is capi.InvalidInput
+
+
+@pytest.mark.parametrize("case", ["duplicate order", "negative knn", "negative epochs", "even window"])
+def test_invalid_train_config_rejected_like_the_reference(gpu, case):
+    d = synth(seed=23, kernels=20, views=4, probe_views=0, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    kinds = []
+    for lib in (gpu, ref()):
+        ctx = lib.context()
+        ctx.set_scene(d["init"])
+        cfg = lib.default_train()
+        if case == "duplicate order":
+            cfg.order[1] = cfg.order[0]
+        elif case == "negative knn":
+            cfg.knn = -1
+        elif case == "negative epochs":
+            cfg.epochs = -1
+        else:
+            cfg.loss.window = 10
+        with pytest.raises(capi.NgsError) as e:
+            ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"], [], d["secondary"], 2)
+            ctx.trainer_step(d["train"][0])
+        kinds.append(type(e.value))
+    assert kinds[0] is kinds[1] is capi.InvalidInput, kinds
+
+
+def test_small_image_and_bad_camera_rejected(gpu):
+    scene, cam, target = check_fixture(1)
+    for lib in (gpu, ref()):
+        ctx = lib.context()
+        ctx.set_scene(scene)
+        small = capi.Camera(cam.view, cam.proj, 8, 8)  # camera.hpp: width and height must be >= 16
+        with pytest.raises(capi.InvalidInput):
+            ctx.render(small)
+        lc = lib.default_loss()  # ssim window larger than the image (loss.hpp:166-168)
+        lc.window = 21
+        tiny = capi.Camera(cam.view, cam.proj, 16, 16)
+        with pytest.raises(capi.InvalidInput):
+            ctx.build_view(0, tiny, np.zeros((16, 16, 3)), loss=lc)
