@@ -103,17 +103,17 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                 const double sx = 0.5 * cam.width, sy = 0.5 * cam.height;
 #pragma unroll
                 for (int q = 0; q < ND; ++q) {
-                    o[L::JS + 2 * q] = static_cast<float>(sx * (av[q] * i1 - hx * i2 * wv[q]));
-                    o[L::JS + 2 * q + 1] = static_cast<float>(sy * (bv[q] * i1 - hy * i2 * wv[q]));
+                    o[L::jx(q)] = static_cast<float>(sx * (av[q] * i1 - hx * i2 * wv[q]));
+                    o[L::jy(q)] = static_cast<float>(sy * (bv[q] * i1 - hy * i2 * wv[q]));
                 }
                 int pp = 0;
 #pragma unroll
                 for (int q = 0; q < ND; ++q)
 #pragma unroll
                     for (int r = q; r < ND; ++r, ++pp) {
-                        o[L::HPI + 2 * pp] = static_cast<float>(
+                        o[L::hpi(pp, 0)] = static_cast<float>(
                             sx * (-(av[q] * wv[r] + wv[q] * av[r]) * i2 + 2.0 * hx * wv[q] * wv[r] * i3));
-                        o[L::HPI + 2 * pp + 1] = static_cast<float>(
+                        o[L::hpi(pp, 1)] = static_cast<float>(
                             sy * (-(bv[q] * wv[r] + wv[q] * bv[r]) * i2 + 2.0 * hy * wv[q] * wv[r] * i3));
                     }
             }
@@ -183,9 +183,9 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                 for (int q = 0; q < ND; ++q) {
                     double tm[4];
                     mul23_32(dj[q], mjt, tm);
-                    o[L::JS + 2 * ND + 3 * q] = static_cast<float>(2.0 * tm[0]);
-                    o[L::JS + 2 * ND + 3 * q + 1] = static_cast<float>(tm[1] + tm[2]);
-                    o[L::JS + 2 * ND + 3 * q + 2] = static_cast<float>(2.0 * tm[3]);
+                    o[L::sg(q, 0)] = static_cast<float>(2.0 * tm[0]);
+                    o[L::sg(q, 1)] = static_cast<float>(tm[1] + tm[2]);
+                    o[L::sg(q, 2)] = static_cast<float>(2.0 * tm[3]);
                 }
                 int pp = 0;
 #pragma unroll
@@ -209,9 +209,9 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                                 md[2 * i + jj] = m[3 * i] * dj[r][3 * jj] + m[3 * i + 1] * dj[r][3 * jj + 1] +
                                                  m[3 * i + 2] * dj[r][3 * jj + 2];
                         mul23_32(dj[q], md, t2);
-                        o[L::SCD + 3 * pp] = static_cast<float>(2.0 * t1[0] + 2.0 * t2[0]);
-                        o[L::SCD + 3 * pp + 1] = static_cast<float>(t1[1] + t1[2] + t2[1] + t2[2]);
-                        o[L::SCD + 3 * pp + 2] = static_cast<float>(2.0 * t1[3] + 2.0 * t2[3]);
+                        o[L::scd(pp, 0)] = static_cast<float>(2.0 * t1[0] + 2.0 * t2[0]);
+                        o[L::scd(pp, 1)] = static_cast<float>(t1[1] + t1[2] + t2[1] + t2[2]);
+                        o[L::scd(pp, 2)] = static_cast<float>(2.0 * t1[3] + 2.0 * t2[3]);
                     }
             }
         } else {
@@ -271,14 +271,14 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
 #pragma unroll
                 for (int a = 0; a < ND; ++a) {
                     jd[a] = d1(Jc[ch], 1, a);
-                    o[ND * ch + a] = static_cast<float>(jd[a]);
+                    o[L::jc(ch, a) - L::JC] = static_cast<float>(jd[a]);
                 }
                 int p = 0;
 #pragma unroll
                 for (int a = 0; a < ND; ++a)
 #pragma unroll
                     for (int b = a; b < ND; ++b, ++p) {
-                        o[L::HC - L::JC + L::NP * ch + p] = static_cast<float>(d2(Hc[ch], 1, a, b));
+                        o[L::hc(ch, p) - L::JC] = static_cast<float>(d2(Hc[ch], 1, a, b));
                     }
             }
 
@@ -519,6 +519,119 @@ __device__ __forceinline__ void position_record(const float4* K4, const Rec& r, 
         for (int d = c; d < ND; ++d, ++p)
             v[ND + p] = sgl * d2G[p] + G * hc[p] + dG[c] * vgl[d] + vgl[c] * dG[d] + A2 * dG[c] * dG[d] +
                         G * (dG[c] * vh[d] + vh[c] * dG[d]) + GG * JJ[p];
+}
+
+// Packed FP32 pairs (f32x2): one FFMA2/FMUL2/FADD2 issue evaluates two lanes of
+// work; a scalar operand is broadcast for free (.F32 operand form).
+struct f2 {
+    unsigned long long u;
+};
+__device__ __forceinline__ f2 pk(float a, float b) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.u) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f2 bc(float a) { return pk(a, a); }
+__device__ __forceinline__ void unpk(f2 v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v.u)); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(a.u), "l"(b.u), "l"(c.u));
+    return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u));
+    return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u));
+    return r;
+}
+__device__ __forceinline__ f2 lo2(float4 v) { return pk(v.x, v.y); }
+__device__ __forceinline__ f2 hi2(float4 v) { return pk(v.z, v.w); }
+
+// position_record<2> on packed pairs: every per-direction quantity (r, t, q_c, dG_c,
+// the gradient) is a (u_x, u_y) pair and every diagonal second-order quantity a
+// (00, 11) pair (PosLayout<2> stores the constants that way); the (01) entries stay
+// scalar. Same formulas as position_record, ~40 % fewer FP32 issues.
+__device__ __forceinline__ void position_record_uv(const float4* K4, const Rec& r, float qa, float qb, float qc,
+                                                   float (&v)[5]) {
+    using L = PosLayout<2>;
+    static_assert(L::JS == 0 && L::HPI == 12 && L::SCD == 20 && L::JC == 32 && L::HC == 40, "PosLayout<2>");
+    const float G = r.G, q0 = r.q0, q1 = r.q1, wa = r.wa;
+    const float4 k0 = K4[0], k1 = K4[1], k2 = K4[2];      // [Jx Jy] [Sa Sb] [Sc -]
+    const f2 Jx = lo2(k0), Jy = hi2(k0), Sa = lo2(k1), Sb = hi2(k1), Sc = lo2(k2);
+    const f2 r0 = fma2(Sb, bc(-q1), fma2(Sa, bc(-q0), Jx));  // J_c - S_c qd (x row)
+    const f2 r1 = fma2(Sc, bc(-q1), fma2(Sb, bc(-q0), Jy));  // (y row)
+    const f2 qcv = fma2(bc(q1), add2(Jy, r1), mul2(bc(q0), add2(Jx, r0)));
+    const f2 t0 = fma2(bc(qb), r1, mul2(bc(qa), r0));       // Q r_c
+    const f2 t1 = fma2(bc(qc), r1, mul2(bc(qb), r0));
+    const f2 dG = mul2(bc(-0.5f * G), qcv);
+    float r00, r01, r10, r11, t00, t01, t10, t11, qc0, qc1, dG0, dG1;
+    unpk(r0, r00, r01);
+    unpk(r1, r10, r11);
+    unpk(t0, t00, t01);
+    unpk(t1, t10, t11);
+    unpk(qcv, qc0, qc1);
+    unpk(dG, dG0, dG1);
+    const float m00 = q0 * q0, m01 = 2.f * q0 * q1, m11 = q1 * q1;
+    const float4 h0 = K4[3], h1 = K4[4];                    // [Hx(00,11) Hy(00,11)] [Hx01 Hy01 - -]
+    const float4 s0 = K4[5], s1 = K4[6], s2 = K4[7];        // [Sa(00,11) Sb(00,11)] [Sc(00,11) Sa01 Sb01] [Sc01 ...]
+    // Diagonal (00, 11) pair of q_cd and d2G.
+    const f2 rt = fma2(r1, t1, mul2(r0, t0));
+    const f2 hq = fma2(bc(q1), hi2(h0), mul2(bc(q0), lo2(h0)));
+    const f2 sdn = fma2(bc(-m11), lo2(s1), fma2(bc(-m01), hi2(s0), mul2(bc(-m00), lo2(s0))));
+    const f2 qcd = fma2(bc(2.f), add2(rt, hq), sdn);
+    const f2 d2G = fma2(bc(0.25f * G), mul2(qcv, qcv), mul2(bc(-0.5f * G), qcd));
+    // Off-diagonal (01) entry.
+    const float qcd01 = 2.f * (r00 * t01 + r10 * t11) + 2.f * (q0 * h1.x + q1 * h1.y) -
+                        (s1.z * m00 + s1.w * m01 + s2.x * m11);
+    const float d2G01 = G * (0.25f * qc0 * qc1 - 0.5f * qcd01);
+    // Colour: Jc per channel is a (u_x, u_y) pair, Hc per channel a (00, 11) pair + (01).
+    const float4 j0 = K4[8], j1 = K4[9];                    // [Jc0 Jc1] [Jc2 -]
+    const float4 c0 = K4[10], c1 = K4[11], c2 = K4[12];     // [Hc0 Hc1] [Hc2 Hc0_01 Hc1_01] [Hc2_01 ...]
+    const f2 Jc[3] = {lo2(j0), hi2(j0), lo2(j1)};
+    const f2 Hd[3] = {lo2(c0), hi2(c0), lo2(c1)};
+    const float Ho[3] = {c1.z, c1.w, c2.x};
+    const float wa2 = wa * wa;
+    float ga[3], ha[3], hac[3], sgl = 0.f, A2 = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        ga[ch] = r.gl[ch] * wa;
+        ha[ch] = r.hl[ch] * wa2;
+        hac[ch] = ha[ch] * r.ac[ch];
+        sgl += ga[ch] * r.ac[ch];
+        A2 += hac[ch] * r.ac[ch];
+    }
+    f2 vgl = mul2(bc(ga[0]), Jc[0]), vh = mul2(bc(hac[0]), Jc[0]), JJ = mul2(bc(ha[0]), mul2(Jc[0], Jc[0]));
+    f2 hcd = mul2(bc(ga[0]), Hd[0]);
+#pragma unroll
+    for (int ch = 1; ch < 3; ++ch) {
+        vgl = fma2(bc(ga[ch]), Jc[ch], vgl);
+        vh = fma2(bc(hac[ch]), Jc[ch], vh);
+        JJ = fma2(bc(ha[ch]), mul2(Jc[ch], Jc[ch]), JJ);
+        hcd = fma2(bc(ga[ch]), Hd[ch], hcd);
+    }
+    float JJ01 = 0.f, hc01 = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        float ja, jb;
+        unpk(Jc[ch], ja, jb);
+        JJ01 += ha[ch] * ja * jb;
+        hc01 += ga[ch] * Ho[ch];
+    }
+    const float GG = G * G;
+    const f2 g = fma2(bc(sgl), dG, mul2(bc(G), vgl));
+    unpk(g, v[0], v[1]);
+    // diag: sgl d2G + G hc + dG (2 vgl + A2 dG + 2 G vh) + GG JJ
+    const f2 w = fma2(bc(2.f * G), vh, fma2(bc(A2), dG, add2(vgl, vgl)));
+    const f2 hd = fma2(dG, w, fma2(bc(GG), JJ, fma2(bc(G), hcd, mul2(bc(sgl), d2G))));
+    unpk(hd, v[2], v[4]);
+    float vgl0, vgl1, vh0, vh1;
+    unpk(vgl, vgl0, vgl1);
+    unpk(vh, vh0, vh1);
+    v[3] = sgl * d2G01 + G * hc01 + dG0 * vgl1 + vgl0 * dG1 + A2 * dG0 * dG1 + G * (dG0 * vh1 + vh0 * dG1) + GG * JJ01;
 }
 
 // Rotation (newton.hpp:366-401): directional derivatives along
@@ -766,7 +879,10 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
             }
             if constexpr (PASS == kPassPosition || PASS == kPassPositionUV) {
                 const float4 g0 = s_sp[jj].g0;
-                position_record<PASS == kPassPosition ? 3 : 2>(s_const + jj * CST, r, g0.z, g0.w, s_sp[jj].g1.x, v);
+                if constexpr (PASS == kPassPosition)
+                    position_record<3>(s_const + jj * CST, r, g0.z, g0.w, s_sp[jj].g1.x, v);
+                else
+                    position_record_uv(s_const + jj * CST, r, g0.z, g0.w, s_sp[jj].g1.x, v);
             } else if constexpr (PASS == kPassRotation) {
                 const float4 g0 = s_sp[jj].g0;
                 rotation_record(s_const + jj * CST, r, g0.z, g0.w, s_sp[jj].g1.x, v);

@@ -39,6 +39,22 @@ struct PosLayout {
     static constexpr int JC = SCD + a4(3 * NP);   // dc~_ch/dp: ND per channel (channel-major)
     static constexpr int HC = JC + a4(3 * ND);    // d2c~_ch/dp2: NP per channel
     static constexpr int N = HC + a4(3 * NP);
+    // Entry indices. ND = 3 keeps the natural order; ND = 2 stores each quantity as
+    // a (direction 0, direction 1) or (00, 11) pair in adjacent floats so the record
+    // evaluation runs on packed f32x2 arithmetic (position_record_uv).
+    __host__ __device__ static constexpr int jx(int q) { return ND == 2 ? JS + q : JS + 2 * q; }
+    __host__ __device__ static constexpr int jy(int q) { return ND == 2 ? JS + 2 + q : JS + 2 * q + 1; }
+    __host__ __device__ static constexpr int sg(int q, int e) { return ND == 2 ? JS + 4 + 2 * e + q : JS + 2 * ND + 3 * q + e; }
+    __host__ __device__ static constexpr int hpi(int pp, int e) {
+        return ND == 2 ? (pp == 1 ? HPI + 4 + e : HPI + 2 * e + (pp == 2)) : HPI + 2 * pp + e;
+    }
+    __host__ __device__ static constexpr int scd(int pp, int e) {
+        return ND == 2 ? (pp == 1 ? SCD + 6 + e : SCD + 2 * e + (pp == 2)) : SCD + 3 * pp + e;
+    }
+    __host__ __device__ static constexpr int jc(int ch, int q) { return JC + ND * ch + q; }
+    __host__ __device__ static constexpr int hc(int ch, int pp) {
+        return ND == 2 ? (pp == 1 ? HC + 6 + ch : HC + 2 * ch + (pp == 2)) : HC + NP * ch + pp;
+    }
 };
 constexpr int kPosConsts = PosLayout<3>::N;    // 80
 constexpr int kPosUVConsts = PosLayout<2>::N;  // 52
