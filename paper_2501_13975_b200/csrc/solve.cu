@@ -271,6 +271,52 @@ __global__ void __launch_bounds__(256) solve_opacity_k(SceneDev s, SolveParams s
     block_add(nsq, out.norm_sq);
 }
 
+// Rotation (c, s, t = s / c) that zeroes a_pq (Numerical Recipes convention); identity
+// when a_pq is zero or negligible against both diagonals.
+__device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, double& c, double& s, double& t) {
+    const double g = 100.0 * fabs(apq);
+    if (fabs(app) + g == fabs(app) && fabs(aqq) + g == fabs(aqq)) {
+        c = 1.0, s = 0.0, t = 0.0;
+        return;
+    }
+    const double theta = (aqq - app) / (2 * apq);
+    t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
+    c = rsqrt(t * t + 1), s = t * c;
+}
+
+// One round of the 4x4 parallel-order Jacobi: the disjoint rotations (P1, Q1) and
+// (P2, Q2) are computed from the same matrix (neither changes the other's 2x2
+// block) and applied together; symmetric updates only (diagonal blocks by the
+// t-formulas, the cross block B' = R1^T B R2), two independent dependency chains.
+template <int P1, int Q1, int P2, int Q2>
+__device__ __forceinline__ void jacobi4_round(double (&a)[4][4], double (&v)[4][4]) {
+    double c1, s1, t1, c2, s2, t2;
+    jacobi_rot(a[P1][P1], a[Q1][Q1], a[P1][Q1], c1, s1, t1);
+    jacobi_rot(a[P2][P2], a[Q2][Q2], a[P2][Q2], c2, s2, t2);
+    const double a1 = a[P1][Q1], a2 = a[P2][Q2];
+    a[P1][P1] -= t1 * a1;
+    a[Q1][Q1] += t1 * a1;
+    a[P1][Q1] = a[Q1][P1] = 0.0;
+    a[P2][P2] -= t2 * a2;
+    a[Q2][Q2] += t2 * a2;
+    a[P2][Q2] = a[Q2][P2] = 0.0;
+    const double x00 = a[P2][P1], x01 = a[P2][Q1], x10 = a[Q2][P1], x11 = a[Q2][Q1];
+    const double y00 = c1 * x00 - s1 * x01, y01 = s1 * x00 + c1 * x01;  // columns (P1, Q1)
+    const double y10 = c1 * x10 - s1 * x11, y11 = s1 * x10 + c1 * x11;
+    a[P2][P1] = a[P1][P2] = c2 * y00 - s2 * y10;                         // rows (P2, Q2)
+    a[Q2][P1] = a[P1][Q2] = s2 * y00 + c2 * y10;
+    a[P2][Q1] = a[Q1][P2] = c2 * y01 - s2 * y11;
+    a[Q2][Q1] = a[Q1][Q2] = s2 * y01 + c2 * y11;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const double vp1 = v[r][P1], vq1 = v[r][Q1], vp2 = v[r][P2], vq2 = v[r][Q2];
+        v[r][P1] = c1 * vp1 - s1 * vq1;
+        v[r][Q1] = s1 * vp1 + c1 * vq1;
+        v[r][P2] = c2 * vp2 - s2 * vq2;
+        v[r][Q2] = s2 * vp2 + c2 * vq2;
+    }
+}
+
 // Cyclic Jacobi for a small symmetric MAXM x MAXM matrix, fully unrolled so
 // the matrices stay in registers (zero rows/columns are inert). Eigenvalues
 // end on the diagonal of `a`, eigenvectors in the columns of `v`.
@@ -291,11 +337,23 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
         // Converged when the off-diagonal mass is ~1e-14 of the diagonal: eigenvalues are then
         // within ~1e-14 ||A|| (Weyl), far below the FP32 accumulation error of the inputs.
         if (off == 0.0 || off <= 1e-28 * diag) break;
+        if constexpr (MAXM == 4) {  // parallel ordering: 3 rounds of 2 disjoint rotations
+            jacobi4_round<0, 1, 2, 3>(a, v);
+            jacobi4_round<0, 2, 1, 3>(a, v);
+            jacobi4_round<0, 3, 1, 2>(a, v);
+            continue;
+        }
 #pragma unroll
         for (int p = 0; p < MAXM; ++p)
 #pragma unroll
             for (int q = p + 1; q < MAXM; ++q) {
-                if (a[p][q] == 0.0) continue;
+                // Negligible off-diagonal (cannot change either diagonal in FP64): zero it
+                // and skip the rotation (the classical cyclic-Jacobi threshold test).
+                const double g = 100.0 * fabs(a[p][q]);
+                if (fabs(a[p][p]) + g == fabs(a[p][p]) && fabs(a[q][q]) + g == fabs(a[q][q])) {
+                    a[p][q] = a[q][p] = 0.0;
+                    continue;
+                }
                 const double theta = (a[q][q] - a[p][p]) / (2 * a[p][q]);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
                 const double c = rsqrt(t * t + 1), sn = t * c;
@@ -340,7 +398,6 @@ __global__ void __launch_bounds__(128) solve_color_gram_k(SceneDev s, ColorViews
                                                           size_t stride) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < s.n) {
-        const int n = s.n_coeffs;
         const float4 ps = s.pos_sigma[k];
         const D3 p = {ps.x, ps.y, ps.z};
         const int nv = cv.n_views;
@@ -399,45 +456,18 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
     double nsq = 0.0;
     if (k < s.n) {
         const int n = s.n_coeffs;
-        const float4 ps = s.pos_sigma[k];
-        const D3 p = {ps.x, ps.y, ps.z};
         const int nv = cv.n_views;
-        D3 dir[MV];
         uint8_t fl[MV];
 #pragma unroll
-        for (int v = 0; v < MV; ++v) {
-            fl[v] = 0;
-            dir[v] = d3(0, 0, 1);
-            if (v < nv) {
-                fl[v] = cv.flags[v][k];
-                double nr;
-                if (!view_direction(cv.cam[v], p, dir[v], nr)) dir[v] = d3(0, 0, 1);
-            }
-        }
-        // Gram matrix of the visible views' SH bases (phi_a . phi_b); absent views are zero.
-        double G[MV][MV];
-#pragma unroll
-        for (int a = 0; a < MV; ++a) {
-            double pa[16];
-            sh_basis(dir[a], s.sh_degree, pa);
-#pragma unroll
-            for (int b = 0; b <= a; ++b) {
-                double pb[16];
-                sh_basis(dir[b], s.sh_degree, pb);
-                double t = 0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) t += pa[i] * pb[i];
-                const bool on = (fl[a] & kProjected) && (fl[b] & kProjected);
-                G[a][b] = on ? t : 0.0;
-                G[b][a] = G[a][b];
-            }
-        }
-        double L[MV][MV], E[MV][MV];  // from stage 1 (diagonal L only is read)
+        for (int v = 0; v < MV; ++v) fl[v] = v < nv ? cv.flags[v][k] : 0;
+        // Stage 1's G = E L E^T (SH0: no stage 1, E = I and L unused). G itself is not
+        // re-formed: G g = E L E^T g and beta^T G beta = sum_j L_j (E^T beta)_j^2.
+        double L[MV][MV], E[MV][MV];
 #pragma unroll
         for (int a = 0; a < MV; ++a)
 #pragma unroll
             for (int b = 0; b < MV; ++b) {
-                L[a][b] = (a == b) ? (n > 1 ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : G[a][a]) : 0.0;
+                L[a][b] = (a == b && n > 1) ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : 0.0;
                 E[a][b] = n > 1 ? eig[static_cast<size_t>(MV * a + b) * stride + k] : (a == b ? 1.0 : 0.0);
             }
         double lmax = 0;
@@ -523,12 +553,19 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
                 if (r < n) lam_min = fmin(lam_min, 0.0);  // zero eigenvalues outside range(Phi)
                 const double mu = fmax(sp.mu_min, sp.eig_floor_rel * lam_abs_max);
                 const bool keep_h = lam_min >= mu;  // newton.hpp:231: PD input solved unmodified
-                double Gg[MV];
+                double Gg[MV], Etg[MV];
+#pragma unroll
+                for (int j = 0; j < MV; ++j) {
+                    double t = 0;
+#pragma unroll
+                    for (int v = 0; v < MV; ++v) t += E[v][j] * gv[v];
+                    Etg[j] = L[j][j] * t;
+                }
 #pragma unroll
                 for (int a = 0; a < MV; ++a) {
                     double t = 0;
 #pragma unroll
-                    for (int b = 0; b < MV; ++b) t += G[a][b] * gv[b];
+                    for (int j = 0; j < MV; ++j) t += E[a][j] * Etg[j];
                     Gg[a] = t;
                 }
 #pragma unroll
@@ -555,9 +592,12 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
                     }
                 }
 #pragma unroll
-                for (int a = 0; a < MV; ++a)
+                for (int j = 0; j < MV; ++j) {
+                    double t = 0;
 #pragma unroll
-                    for (int b = 0; b < MV; ++b) nrm2 += beta[a] * G[a][b] * beta[b];
+                    for (int a = 0; a < MV; ++a) t += E[a][j] * beta[a];
+                    nrm2 += L[j][j] * t * t;
+                }
             }
             // Colour cap (newton.hpp:801-804) on |delta| = sqrt(beta^T G beta).
             double scale = 1.0;
@@ -574,10 +614,15 @@ __global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s
             if (n == 1) {
                 delta[0] = beta_all[0];
             } else {
+                const float4 ps = s.pos_sigma[k];
+                const D3 p = {ps.x, ps.y, ps.z};
 #pragma unroll
                 for (int v = 0; v < MV; ++v) {
+                    D3 dir = d3(0, 0, 1);
+                    double nr;
+                    if (v < nv && !view_direction(cv.cam[v], p, dir, nr)) dir = d3(0, 0, 1);
                     double ph[16];
-                    sh_basis(dir[v], s.sh_degree, ph);
+                    sh_basis(dir, s.sh_degree, ph);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) delta[i] += beta_all[v] * ph[i];
                 }
