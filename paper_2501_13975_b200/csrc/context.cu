@@ -155,6 +155,8 @@ struct ngs_context {
     std::array<cudaEvent_t, kMaxSolveViews> join_ev{};
     std::array<cudaEvent_t, kMaxSolveViews> rev{};  // per-view 'render + loss done' (chained into the backward)
     std::array<cudaEvent_t, kMaxSolveViews> pev{};  // per-view 'projection done' (flags for the pass constants)
+    std::array<cudaEvent_t, kMaxSolveViews> tev{};  // per-view 'target uploaded' (copy stream -> loss)
+    cudaStream_t cs = nullptr;                      // copy stream: target uploads overlap the renders
     std::array<cudaEvent_t, 24> gev{};  // stage-group events of a trainer step
     DevBuf<int> overflow;
     DevBuf<float4> snap_ps, snap_sc, snap_q;
@@ -193,6 +195,9 @@ struct ngs_context {
             if (e) cudaEventDestroy(e);
         for (auto e : pev)
             if (e) cudaEventDestroy(e);
+        for (auto e : tev)
+            if (e) cudaEventDestroy(e);
+        if (cs) cudaStreamDestroy(cs);
         for (auto e : join_ev)
             if (e) cudaEventDestroy(e);
         for (auto s : vs)
@@ -494,7 +499,9 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->rev[i], cudaEventDisableTiming));
             CUDA_CHECK(cudaEventCreateWithFlags(&ctx->pev[i], cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventCreateWithFlags(&ctx->tev[i], cudaEventDisableTiming));
         }
+        CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
         ctx->overflow.ensure(1);
         CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), ctx->stream));
         ctx->err.ensure(1);
@@ -1155,33 +1162,40 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     // Profiling serialises the views so per-launch event times do not overlap.
     const bool concurrent = !ctx->prof.enabled;
     if (concurrent) ctx->fork(nv, ctx->vr.data());
-    for (int ii = 0; ii < nv; ++ii) {
-        const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
-        const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
-        ViewSlot& v = T.views[i];
-        cudaStream_t s = concurrent ? ctx->vr[i] : ctx->stream;
-        const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
-        const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
-        if (upload_targets) {
+    // Target uploads go to the copy stream (primary first, it is the largest), so
+    // the host->device copies overlap projection, sorting and rasterisation; each
+    // view's loss waits for its own target only.
+    if (upload_targets) {
+        if (concurrent) CUDA_CHECK(cudaStreamWaitEvent(ctx->cs, ctx->fork_ev, 0));
+        for (int i = 0; i < nv; ++i) {
+            ViewSlot& v = T.views[i];
+            const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
+            const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
             upload_camera(cam, v.cam, tile_for(ctx, cam, false));
             v.raster = ctx->raster_for(&T.cfg.raster, v.cam);
             v.loss = to_loss(&T.cfg.loss);
             const size_t npx = static_cast<size_t>(cam.width) * cam.height;
             v.target.ensure(3 * npx);
-            if (T.cfg.host_targets) {
-                const double* src = (i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id];
-                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx, cudaMemcpyHostToDevice, s));
-            } else {
-                const double* src = (i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr;
-                CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx, cudaMemcpyDeviceToDevice, s));
-            }
+            cudaStream_t s = concurrent ? ctx->cs : ctx->stream;
+            const double* src = T.cfg.host_targets ? ((i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id])
+                                                   : ((i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr);
+            CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx,
+                                       T.cfg.host_targets ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+            if (concurrent) CUDA_CHECK(cudaEventRecord(ctx->tev[i], s));
         }
+    }
+    for (int ii = 0; ii < nv; ++ii) {
+        const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
+        const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
+        ViewSlot& v = T.views[i];
+        cudaStream_t s = concurrent ? ctx->vr[i] : ctx->stream;
         RenderSync rs;
         rs.exact = false;
         rs.overflow = ctx->overflow.ptr;
         rs.pair_counter = ctx->pairs.ptr + 4;
         if (concurrent && !join) rs.projected = ctx->pev[i];
         render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
+        if (upload_targets && concurrent) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->tev[i], 0));
         compute_loss(v, s);
         if (concurrent && !join) CUDA_CHECK(cudaEventRecord(ctx->rev[i], s));
     }
