@@ -167,6 +167,11 @@ struct ngs_context {
     int stream_policy = 0;  // 0: secondaries first, high priority; 1: primary first+high; 2: none, sec first; 3: none, primary first
     int tile_policy = 0;  // 0 auto (8x8 tiles for small views), else forced 8 or 16
     unsigned long long contrib_pairs_total = 0;
+    // Bumped whenever the positions may change (set_scene, position commits, snapshot
+    // restores, first-order updates, every trainer step start): trainer renders with an
+    // unchanged version and camera keep their slot's depth order (RenderSync::pos_version).
+    unsigned long long pos_version = 1;
+    bool order_reuse = true;  // NGS_ORDER_REUSE=0 disables it (tests compare both)
 
     ~ngs_context() {
         if (comm) nccl().comm_destroy(comm);
@@ -489,6 +494,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         if (const char* e = getenv("NGS_STREAM_POLICY")) ctx->stream_policy = atoi(e);  // experiments only
         if (const char* e = getenv("NGS_TILE_POLICY")) ctx->tile_policy = atoi(e);      // experiments only
+        if (const char* e = getenv("NGS_ORDER_REUSE")) ctx->order_reuse = atoi(e) != 0;  // tests only
         for (int i = 0; i < kMaxSolveViews; ++i) {
             int prio = i == 0 ? prio_lo : prio_hi;
             if (ctx->stream_policy == 1) prio = i == 0 ? prio_hi : prio_lo;
@@ -538,6 +544,7 @@ int32_t ngs_set_scene(ngs_context* ctx, const ngs_scene* s) {
                                s->quaternion[4 * k + 3]);
             for (int c = 0; c < 48; ++c) sh[static_cast<size_t>(c) * n + k] = static_cast<float>(s->sh[48 * k + c]);
         }
+        ++ctx->pos_version;
         ctx->pos_sigma.ensure(std::max(n, 1));
         ctx->scale.ensure(std::max(n, 1));
         ctx->quat.ensure(std::max(n, 1));
@@ -1194,6 +1201,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         rs.overflow = ctx->overflow.ptr;
         rs.pair_counter = ctx->pairs.ptr + 4;
         if (concurrent && !join) rs.projected = ctx->pev[i];
+        rs.pos_version = ctx->order_reuse ? ctx->pos_version : 0;
         render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
         if (upload_targets && concurrent) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->tev[i], 0));
         compute_loss(v, s);
@@ -1209,6 +1217,7 @@ float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
     const int n = ctx->scene.n;
     const size_t stride = static_cast<size_t>(std::max(n, 1));
     cudaStream_t s = ctx->stream;
+    ++ctx->pos_version;  // every first-order step moves the positions
     const bool adam = T.cfg.optimizer == NGS_OPT_ADAM;
     if (adam && !T.adam_m.ptr) {
         T.adam_m.ensure(56 * stride);
@@ -1321,6 +1330,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                 CUDA_CHECK(cudaEventRecord(ctx->gev[ge], s));
                 marks.emplace_back(ge++, group);
             };
+            ++ctx->pos_version;  // step start / snapshot restore
             CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
             CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), s));
             CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
@@ -1341,6 +1351,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                     mark(1 + (pass == kPassPositionUV ? kPassPosition : pass));
                 }
                 SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
+                if (attr == NGS_POSITION) ++ctx->pos_version;  // the next renders re-sort by depth
                 launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
                              color_views(ctx, views.data(), nv), base, ctx->acc.ptr, stride, so, s);
                 mark(5);

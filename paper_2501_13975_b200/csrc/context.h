@@ -82,6 +82,9 @@ struct DevBuf {
 struct ViewSlot {
     bool valid = false;
     CameraDev cam{};
+    unsigned long long order_version = 0;  // RenderSync::pos_version of the last depth sort (0: not reusable)
+    CameraDev order_cam{};
+    int order_n = -1;
     int W = 0, H = 0, T = 0;
     int n = 0;         // kernels projected
     int entries = 0;   // projected (non-culled) kernels
@@ -202,6 +205,10 @@ struct RenderSync {
     int* overflow = nullptr;                      // sync-free: set when the pair capacity was exceeded
     unsigned long long* pair_counter = nullptr;   // optional: adds the (tile, splat) pair count
     cudaEvent_t projected = nullptr;              // optional: recorded after the projection (flags ready)
+    // Position version of the scene (0 = unknown). The depth order (and the culled set) is a
+    // function of the positions and the camera only, so a slot re-rendered with the same
+    // camera and version keeps its sorted order and skips K2.
+    unsigned long long pos_version = 0;
 };
 void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
                  const RenderSync& sync = RenderSync{});

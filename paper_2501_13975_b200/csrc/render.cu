@@ -3,6 +3,7 @@
 // Reference semantics: build_splat_list (rasterizer.hpp:182-265) and
 // composite_forward / composite_pixel (rasterizer.hpp:274-442).
 #include <cmath>
+#include <cstring>
 
 #include "context.h"
 #include "geometry.cuh"
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
                                                         double* entry64, int* err) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= s.n) return;
-    ids[k] = k;
+    if (ids) ids[k] = k;  // null: the slot keeps its sorted depth order (same positions and camera)
     const float4 ps = s.pos_sigma[k];
     const D3 p = {ps.x, ps.y, ps.z};
     Projected pr;
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
         tiles_touched[k] = 0;
         flags[k] = 0;
         rect[k] = make_int4(1, 1, 0, 0);
-        depth_key[k] = 0xFFFFFFFFu;
+        if (depth_key) depth_key[k] = 0xFFFFFFFFu;
         depth[k] = 0;
         return;
     }
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
     tiles_touched[k] = off ? 0 : (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
     flags[k] = f;
     depth[k] = pr.depth;
-    depth_key[k] = depth_sort_key(pr.depth);
+    if (depth_key) depth_key[k] = depth_sort_key(pr.depth);
     pix[k] = make_double2(pr.px, pr.py);
     ra[k] = make_float4(0.f, 0.f, static_cast<float>(qa), static_cast<float>(qb));
     rb[k] = make_float4(static_cast<float>(qc), ps.w, static_cast<float>(col[0]), static_cast<float>(col[1]));
@@ -401,24 +402,34 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     v.order_alt.ensure(n);
     v.counters.ensure(3);
 
+    // The culled set (key 0xFFFFFFFF: behind the near plane) and the depth keys depend on the
+    // positions and the camera only; a non-PD projected covariance is a step error.
+    const bool keep_order = sync.pos_version != 0 && v.order_version == sync.pos_version && v.order_n == n &&
+                            std::memcmp(&v.order_cam, &v.cam, sizeof(CameraDev)) == 0;
+    v.order_version = sync.pos_version;
+    v.order_cam = v.cam;
+    v.order_n = n;
     if (n > 0) {
         StageScope st(NGS_STAGE_PROJECT, s);
         project_kernel_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr,
                                                        v.pix.ptr, v.depth.ptr, v.rect.ptr, v.tiles_touched.ptr,
-                                                       v.flags.ptr, v.depth_key.ptr, v.order.ptr,
+                                                       v.flags.ptr, keep_order ? nullptr : v.depth_key.ptr,
+                                                       keep_order ? nullptr : v.order.ptr,
                                                        want_debug ? v.entry64.ptr : nullptr, d_err);
         CUDA_LAUNCH_CHECK();
     }
     if (sync.projected) CUDA_CHECK(cudaEventRecord(sync.projected, s));
     if (n > 0) {
-        StageScope st(NGS_STAGE_SORT, s, 11);  // sort 2 + 4 passes, fix-up, gather, scan 3
+        StageScope st(NGS_STAGE_SORT, s, keep_order ? 4 : 11);  // sort 2 + 4 passes, fix-up, gather, scan 3
         // K2: global depth order, exactly (FP64 depth, kernel id): 4-pass radix sort of the
         // FP32 depth key (stable over the id-ordered input) + fix-up of equal-key runs.
         v.n_host = n;
         CUDA_CHECK(cudaMemcpyAsync(v.counters.ptr, &v.n_host, sizeof(int), cudaMemcpyHostToDevice, s));
-        radix_sort_pairs(v.depth_key.ptr, v.order.ptr, v.depth_key_alt.ptr, v.order_alt.ptr, v.counters.ptr, n, 32, sc,
-                         s);
-        depth_tie_fixup(v.depth_key.ptr, v.order.ptr, v.depth.ptr, n, s);
+        if (!keep_order) {
+            radix_sort_pairs(v.depth_key.ptr, v.order.ptr, v.depth_key_alt.ptr, v.order_alt.ptr, v.counters.ptr, n, 32,
+                             sc, s);
+            depth_tie_fixup(v.depth_key.ptr, v.order.ptr, v.depth.ptr, n, s);
+        }
         gather_counts_k<<<blocks_for(n), 256, 0, s>>>(n, v.order.ptr, v.tiles_touched.ptr, v.counts_sorted.ptr);
         CUDA_LAUNCH_CHECK();
         exclusive_scan(v.counts_sorted.ptr, v.offsets.ptr, n, v.counters.ptr + 1, sc, s);
