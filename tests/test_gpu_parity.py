@@ -251,6 +251,30 @@ def test_trainer_step(gpu):
         assert e < 1e-4, f
 
 
+def test_trainer_step_with_no_visible_kernels(gpu):
+    """Edge case: every kernel off-screen or behind the near plane in every view (zero
+    (tile, splat) pairs, all-background images). Both libraries must agree on the step
+    (only the barrier and damping terms act) and on the unchanged geometry."""
+    d = synth(seed=23, kernels=20, views=4, probe_views=0, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    scene = d["init"].copy()
+    scene.position = scene.position + np.array([100.0, 0.0, 0.0])
+    g, r = pair(gpu, scene, quantize=False)
+    reports = []
+    for ctx, lib in ((g, gpu), (r, ref())):
+        cfg = lib.default_train()
+        cfg.knn = 2
+        cfg.secondary_downsample = 2
+        ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"], d["probe"], d["secondary"],
+                              d["secondary_downsample"])
+        reports.append(ctx.trainer_step(d["train"][0]))
+    for i in range(5):
+        assert abs(reports[0].delta_norms[i] - reports[1].delta_norms[i]) <= 1e-6 + 1e-4 * abs(reports[1].delta_norms[i])
+    sg, sr = g.get_scene(), r.get_scene()
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        assert qerr(getattr(sg, f), getattr(sr, f)) < 1e-4, f
+
+
 @pytest.mark.parametrize("sh_degree,width,height,knn,order", [
     (0, 48, 48, 2, (0, 1, 2, 3, 4)),
     (1, 50, 37, 1, (0, 1, 2, 3, 4)),
