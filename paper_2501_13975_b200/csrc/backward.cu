@@ -787,7 +787,8 @@ struct BackwardSmem {
     float acc[NW][NA][B];                  // per-warp sums: segment tails are unique within a drain
     int kid[2][B];
     unsigned char vis[NW][B];              // per warp: the splat had >= 1 record in this warp
-    float gl[NT][3], hl[NT][3];
+    float4 lg[NT];                         // per-pixel loss derivatives (gl0, gl1, gl2, hl0)
+    float2 lh[NT];                         // (hl1, hl2): two loads per record instead of six
     WarpQueue q[NW];
     int maxlast;
 };
@@ -804,8 +805,6 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
     auto& s_sp = S.sp;
     auto& s_acc = S.acc;
     auto& s_vis = S.vis;
-    auto& s_gl = S.gl;
-    auto& s_hl = S.hl;
     auto& s_q = S.q;
     auto& s_maxlast = S.maxlast;
     unsigned long long block_pairs = 0;
@@ -826,6 +825,7 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
 
     int last = -1;
     float Cf_hi[3] = {0.f, 0.f, 0.f}, Cf_lo[3] = {0.f, 0.f, 0.f};  // final colour as an unevaluated float pair
+    float gl[3] = {0.f, 0.f, 0.f}, hl[3] = {0.f, 0.f, 0.f};
     if (inside) {
         last = a.last[pidx];
 #pragma unroll
@@ -833,16 +833,12 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
             const double cf = a.image[c * plane + pidx];
             Cf_hi[c] = static_cast<float>(cf);
             Cf_lo[c] = static_cast<float>(cf - static_cast<double>(Cf_hi[c]));
-            s_gl[threadIdx.x][c] = a.loss_grad[c * plane + pidx];
-            s_hl[threadIdx.x][c] = a.loss_hess[c * plane + pidx];
-        }
-    } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            s_gl[threadIdx.x][c] = 0.f;
-            s_hl[threadIdx.x][c] = 0.f;
+            gl[c] = a.loss_grad[c * plane + pidx];
+            hl[c] = a.loss_hess[c * plane + pidx];
         }
     }
+    S.lg[threadIdx.x] = make_float4(gl[0], gl[1], gl[2], hl[0]);
+    S.lh[threadIdx.x] = make_float2(hl[1], hl[2]);
     if (threadIdx.x == 0) s_maxlast = -1;
     for (int i = threadIdx.x; i < NW * NA * B; i += NT) (&s_acc[0][0][0])[i] = 0.f;
     for (int i = threadIdx.x; i < NW * B; i += NT) (&s_vis[0][0])[i] = 0;
@@ -878,11 +874,14 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
             r.ac[1] = r1.z;
             r.ac[2] = r1.w;
             const int px = warp * 32 + static_cast<int>(jp >> 8);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                r.gl[c] = s_gl[px][c];
-                r.hl[c] = s_hl[px][c];
-            }
+            const float4 lg = S.lg[px];
+            const float2 lh = S.lh[px];
+            r.gl[0] = lg.x;
+            r.gl[1] = lg.y;
+            r.gl[2] = lg.z;
+            r.hl[0] = lg.w;
+            r.hl[1] = lh.x;
+            r.hl[2] = lh.y;
             if constexpr (PASS == kPassPosition || PASS == kPassPositionUV) {
                 const float4 g0 = s_sp[jj].g0;
                 if constexpr (PASS == kPassPosition)
