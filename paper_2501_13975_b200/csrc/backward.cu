@@ -784,7 +784,11 @@ struct BackwardSmem {
     float4 cst[2][(CST > 0 ? CST : 1) * B];  // staged per-view constants, double-buffered
     SplatSh sp[B];                         // staged splats of the batch
     unsigned char wmask[B];                // bit w: the splat's cutoff ellipse reaches warp w's pixel rows
-    float acc[NW][NA][B];                  // per-warp sums: segment tails are unique within a drain
+    // Per-warp sums (segment tails are unique within a drain). NA = 2 and 8 store each
+    // splat's components contiguously ([B][NA]: one float2 / two float4 read-modify-writes
+    // per tail); the other passes keep [NA][B] (same size, conflict-free flush reads).
+    static constexpr bool VEC = NA == 2 || NA == 8;
+    alignas(16) float acc[NW][NA * B];
     int kid[2][B];
     unsigned char vis[NW][B];              // per warp: the splat had >= 1 record in this warp
     float4 lg[NT];                         // per-pixel loss derivatives (gl0, gl1, gl2, hl0)
@@ -804,6 +808,8 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
     SM& S = *reinterpret_cast<SM*>(smem_raw);
     auto& s_sp = S.sp;
     auto& s_acc = S.acc;
+    constexpr bool VEC = SM::VEC;
+    auto acc_at = [&](int w, int c, int j) -> float& { return VEC ? s_acc[w][j * NA + c] : s_acc[w][c * B + j]; };
     auto& s_vis = S.vis;
     auto& s_q = S.q;
     auto& s_maxlast = S.maxlast;
@@ -840,7 +846,7 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
     S.lg[threadIdx.x] = make_float4(gl[0], gl[1], gl[2], hl[0]);
     S.lh[threadIdx.x] = make_float2(hl[1], hl[2]);
     if (threadIdx.x == 0) s_maxlast = -1;
-    for (int i = threadIdx.x; i < NW * NA * B; i += NT) (&s_acc[0][0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < NW * NA * B; i += NT) (&s_acc[0][0])[i] = 0.f;
     for (int i = threadIdx.x; i < NW * B; i += NT) (&s_vis[0][0])[i] = 0;
     __syncthreads();
     if (last >= 0) atomicMax(&s_maxlast, last);
@@ -915,7 +921,21 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
         const bool tail = valid && (lane == 31 || next != jj);
         if (tail) {
 #pragma unroll
-            for (int c = 0; c < NA; ++c) s_acc[warp][c][jj] += v[c];
+            for (int c = 0; c < (VEC ? 0 : NA); ++c) acc_at(warp, c, jj) += v[c];
+            if constexpr (NA == 2) {
+                float2& t = *reinterpret_cast<float2*>(&s_acc[warp][jj * 2]);
+                float2 u = t;
+                u.x += v[0];
+                u.y += v[1];
+                t = u;
+            } else if constexpr (NA == 8) {
+                float4* t = reinterpret_cast<float4*>(&s_acc[warp][jj * 8]);
+                float4 u0 = t[0], u1 = t[1];
+                u0.x += v[0], u0.y += v[1], u0.z += v[2], u0.w += v[3];
+                u1.x += v[4], u1.y += v[5], u1.z += v[6], u1.w += v[7];
+                t[0] = u0;
+                t[1] = u1;
+            }
             s_vis[warp][jj] = 1;
         }
         if (lane == 0) block_pairs += n;
@@ -1057,10 +1077,15 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
             s_vis[warp][i] = 0;
             const int k = S.kid[buf][i];
             if (a.visible) a.visible[k] = 1;
+            float vals[NA];
 #pragma unroll
             for (int c = 0; c < NA; ++c) {
-                const float val = s_acc[warp][c][i];
-                s_acc[warp][c][i] = 0.f;
+                vals[c] = acc_at(warp, c, i);
+                acc_at(warp, c, i) = 0.f;
+            }
+#pragma unroll
+            for (int c = 0; c < NA; ++c) {
+                const float val = vals[c];
                 if (val == 0.f) continue;
                 if (a.acc_limbs) {
                     add_fixed128(a.acc_limbs + (static_cast<size_t>(c) * a.acc_stride + k) * 4, val);
