@@ -784,11 +784,14 @@ struct BackwardSmem {
     float4 cst[2][(CST > 0 ? CST : 1) * B];  // staged per-view constants, double-buffered
     SplatSh sp[B];                         // staged splats of the batch
     unsigned char wmask[B];                // bit w: the splat's cutoff ellipse reaches warp w's pixel rows
-    // Per-warp sums (segment tails are unique within a drain). NA = 2 and 8 store each
-    // splat's components contiguously ([B][NA]: one float2 / two float4 read-modify-writes
-    // per tail); the other passes keep [NA][B] (same size, conflict-free flush reads).
-    static constexpr bool VEC = NA == 2 || NA == 8;
-    alignas(16) float acc[NW][NA * B];
+    // Per-warp sums (segment tails are unique within a drain), as NA / 4 float4 planes
+    // plus a float2 and / or a float plane for the remainder: a segment tail adds its NA
+    // components with ceil-ish(NA / 4) vector read-modify-writes; lane-indexed flush
+    // reads stay conflict-free; same size as [NA][B].
+    static constexpr int NQ = NA / 4, R2 = (NA % 4) / 2, R1 = NA % 2;
+    float4 acc4[NW][NQ > 0 ? NQ * B : 1];
+    float2 acc2[NW][R2 > 0 ? B : 1];
+    float acc1[NW][R1 > 0 ? B : 1];
     int kid[2][B];
     unsigned char vis[NW][B];              // per warp: the splat had >= 1 record in this warp
     float4 lg[NT];                         // per-pixel loss derivatives (gl0, gl1, gl2, hl0)
@@ -807,9 +810,13 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& S = *reinterpret_cast<SM*>(smem_raw);
     auto& s_sp = S.sp;
-    auto& s_acc = S.acc;
-    constexpr bool VEC = SM::VEC;
-    auto acc_at = [&](int w, int c, int j) -> float& { return VEC ? s_acc[w][j * NA + c] : s_acc[w][c * B + j]; };
+    constexpr int NQ = SM::NQ, R2 = SM::R2, R1 = SM::R1;
+    // Component c of splat j in warp w's sums.
+    auto acc_at = [&](int w, int c, int j) -> float& {
+        if (c < 4 * NQ) return reinterpret_cast<float*>(&S.acc4[w][(c >> 2) * B + j])[c & 3];
+        if (R2 && c < 4 * NQ + 2) return reinterpret_cast<float*>(&S.acc2[w][j])[c - 4 * NQ];
+        return S.acc1[w][j];
+    };
     auto& s_vis = S.vis;
     auto& s_q = S.q;
     auto& s_maxlast = S.maxlast;
@@ -846,7 +853,9 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
     S.lg[threadIdx.x] = make_float4(gl[0], gl[1], gl[2], hl[0]);
     S.lh[threadIdx.x] = make_float2(hl[1], hl[2]);
     if (threadIdx.x == 0) s_maxlast = -1;
-    for (int i = threadIdx.x; i < NW * NA * B; i += NT) (&s_acc[0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < NW * (NQ > 0 ? NQ * B : 1); i += NT) (&S.acc4[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = threadIdx.x; i < NW * (R2 > 0 ? B : 1); i += NT) (&S.acc2[0][0])[i] = make_float2(0.f, 0.f);
+    for (int i = threadIdx.x; i < NW * (R1 > 0 ? B : 1); i += NT) (&S.acc1[0][0])[i] = 0.f;
     for (int i = threadIdx.x; i < NW * B; i += NT) (&s_vis[0][0])[i] = 0;
     __syncthreads();
     if (last >= 0) atomicMax(&s_maxlast, last);
@@ -921,21 +930,20 @@ __global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
         const bool tail = valid && (lane == 31 || next != jj);
         if (tail) {
 #pragma unroll
-            for (int c = 0; c < (VEC ? 0 : NA); ++c) acc_at(warp, c, jj) += v[c];
-            if constexpr (NA == 2) {
-                float2& t = *reinterpret_cast<float2*>(&s_acc[warp][jj * 2]);
-                float2 u = t;
-                u.x += v[0];
-                u.y += v[1];
+            for (int q = 0; q < NQ; ++q) {
+                float4& t = S.acc4[warp][q * B + jj];
+                float4 u = t;
+                u.x += v[4 * q], u.y += v[4 * q + 1], u.z += v[4 * q + 2], u.w += v[4 * q + 3];
                 t = u;
-            } else if constexpr (NA == 8) {
-                float4* t = reinterpret_cast<float4*>(&s_acc[warp][jj * 8]);
-                float4 u0 = t[0], u1 = t[1];
-                u0.x += v[0], u0.y += v[1], u0.z += v[2], u0.w += v[3];
-                u1.x += v[4], u1.y += v[5], u1.z += v[6], u1.w += v[7];
-                t[0] = u0;
-                t[1] = u1;
             }
+            if constexpr (R2 > 0) {
+                float2& t = S.acc2[warp][jj];
+                float2 u = t;
+                u.x += v[4 * NQ];
+                u.y += v[4 * NQ + 1];
+                t = u;
+            }
+            if constexpr (R1 > 0) S.acc1[warp][jj] += v[NA - 1];
             s_vis[warp][jj] = 1;
         }
         if (lane == 0) block_pairs += n;
