@@ -341,41 +341,41 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
             jacobi4_round<0, 1, 2, 3>(a, v);
             jacobi4_round<0, 2, 1, 3>(a, v);
             jacobi4_round<0, 3, 1, 2>(a, v);
-            continue;
+        } else {
+#pragma unroll
+            for (int p = 0; p < MAXM; ++p)
+#pragma unroll
+                for (int q = p + 1; q < MAXM; ++q) {
+                    // Negligible off-diagonal (cannot change either diagonal in FP64): zero it
+                    // and skip the rotation (the classical cyclic-Jacobi threshold test).
+                    const double g = 100.0 * fabs(a[p][q]);
+                    if (fabs(a[p][p]) + g == fabs(a[p][p]) && fabs(a[q][q]) + g == fabs(a[q][q])) {
+                        a[p][q] = a[q][p] = 0.0;
+                        continue;
+                    }
+                    const double theta = (a[q][q] - a[p][p]) / (2 * a[p][q]);
+                    const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
+                    const double c = rsqrt(t * t + 1), sn = t * c;
+#pragma unroll
+                    for (int kk = 0; kk < MAXM; ++kk) {
+                        const double akp = a[kk][p], akq = a[kk][q];
+                        a[kk][p] = c * akp - sn * akq;
+                        a[kk][q] = sn * akp + c * akq;
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < MAXM; ++kk) {
+                        const double apk = a[p][kk], aqk = a[q][kk];
+                        a[p][kk] = c * apk - sn * aqk;
+                        a[q][kk] = sn * apk + c * aqk;
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < MAXM; ++kk) {
+                        const double vkp = v[kk][p], vkq = v[kk][q];
+                        v[kk][p] = c * vkp - sn * vkq;
+                        v[kk][q] = sn * vkp + c * vkq;
+                    }
+                }
         }
-#pragma unroll
-        for (int p = 0; p < MAXM; ++p)
-#pragma unroll
-            for (int q = p + 1; q < MAXM; ++q) {
-                // Negligible off-diagonal (cannot change either diagonal in FP64): zero it
-                // and skip the rotation (the classical cyclic-Jacobi threshold test).
-                const double g = 100.0 * fabs(a[p][q]);
-                if (fabs(a[p][p]) + g == fabs(a[p][p]) && fabs(a[q][q]) + g == fabs(a[q][q])) {
-                    a[p][q] = a[q][p] = 0.0;
-                    continue;
-                }
-                const double theta = (a[q][q] - a[p][p]) / (2 * a[p][q]);
-                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
-                const double c = rsqrt(t * t + 1), sn = t * c;
-#pragma unroll
-                for (int kk = 0; kk < MAXM; ++kk) {
-                    const double akp = a[kk][p], akq = a[kk][q];
-                    a[kk][p] = c * akp - sn * akq;
-                    a[kk][q] = sn * akp + c * akq;
-                }
-#pragma unroll
-                for (int kk = 0; kk < MAXM; ++kk) {
-                    const double apk = a[p][kk], aqk = a[q][kk];
-                    a[p][kk] = c * apk - sn * aqk;
-                    a[q][kk] = sn * apk + c * aqk;
-                }
-#pragma unroll
-                for (int kk = 0; kk < MAXM; ++kk) {
-                    const double vkp = v[kk][p], vkq = v[kk][q];
-                    v[kk][p] = c * vkp - sn * vkq;
-                    v[kk][q] = sn * vkp + c * vkq;
-                }
-            }
     }
 }
 
