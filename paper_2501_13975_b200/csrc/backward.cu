@@ -383,31 +383,63 @@ __global__ void __launch_bounds__(128) scaling_consts_k(SceneDev s, CameraDev ca
 // Tile backward kernel
 // ---------------------------------------------------------------------------
 
+// 16x16-tile batch sizes and register caps (build-time knobs for A/B runs). The
+// shared-memory footprint scales with the batch: rotation / scaling at 64 splats
+// and <= 64 registers fit 4 resident blocks per SM instead of 3 (c2 97.9 -> 99.8
+// views/s, A/B on one box); the position (UV) pass at 32 splats / 64 registers
+// also fits 4 but measured slower (97.9 -> 97.5).
+#ifndef NGS_B16_UV
+#define NGS_B16_UV 64
+#endif
+#ifndef NGS_B16_ROT
+#define NGS_B16_ROT 64
+#endif
+#ifndef NGS_B16_SCL
+#define NGS_B16_SCL 64
+#endif
+#ifndef NGS_B16_OC
+#define NGS_B16_OC 64
+#endif
+#ifndef NGS_MAXREG16
+#define NGS_MAXREG16 72
+#endif
+#ifndef NGS_R16_UV
+#define NGS_R16_UV NGS_MAXREG16
+#endif
+#ifndef NGS_R16_ROT
+#define NGS_R16_ROT 64
+#endif
+#ifndef NGS_R16_SCL
+#define NGS_R16_SCL 64
+#endif
+#ifndef NGS_R16_OC
+#define NGS_R16_OC NGS_MAXREG16
+#endif
 template <int PASS>
 struct PassTraits;
 template <>
 struct PassTraits<kPassPosition> {
-    static constexpr int NC = kPosConsts, NA = 9, BATCH = 32, BATCH8 = 32;
+    static constexpr int NC = kPosConsts, NA = 9, BATCH = 32, BATCH8 = 32, R16 = NGS_MAXREG16;
 };
 template <>
 struct PassTraits<kPassPositionUV> {
-    static constexpr int NC = kPosUVConsts, NA = 5, BATCH = 64, BATCH8 = 32;
+    static constexpr int NC = kPosUVConsts, NA = 5, BATCH = NGS_B16_UV, BATCH8 = 32, R16 = NGS_R16_UV;
 };
 template <>
 struct PassTraits<kPassGrad> {
-    static constexpr int NC = 0, NA = kAccGrad, BATCH = 64, BATCH8 = 64;
+    static constexpr int NC = 0, NA = kAccGrad, BATCH = 64, BATCH8 = 64, R16 = NGS_MAXREG16;
 };
 template <>
 struct PassTraits<kPassRotation> {
-    static constexpr int NC = kRotConsts, NA = 2, BATCH = 128, BATCH8 = 64;
+    static constexpr int NC = kRotConsts, NA = 2, BATCH = NGS_B16_ROT, BATCH8 = 64, R16 = NGS_R16_ROT;
 };
 template <>
 struct PassTraits<kPassScaling> {
-    static constexpr int NC = kScaleConsts, NA = 5, BATCH = 128, BATCH8 = 64;
+    static constexpr int NC = kScaleConsts, NA = 5, BATCH = NGS_B16_SCL, BATCH8 = 64, R16 = NGS_R16_SCL;
 };
 template <>
 struct PassTraits<kPassOpacityColor> {
-    static constexpr int NC = 0, NA = 8, BATCH = 64, BATCH8 = 64;
+    static constexpr int NC = 0, NA = 8, BATCH = NGS_B16_OC, BATCH8 = 64, R16 = NGS_R16_OC;
 };
 
 // Copies N float4 from shared memory into a register array.
@@ -801,7 +833,7 @@ struct BackwardSmem {
 };
 
 template <int PASS, int TILE>
-__global__ void __maxnreg__(TILE == 16 ? 72 : 128) backward_k(BackwardArgs a) {
+__global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k(BackwardArgs a) {
     using TR = PassTraits<PASS>;
     using SM = BackwardSmem<PASS, TILE>;
     constexpr int NT = TILE * TILE, NW = NT / 32;
