@@ -15,6 +15,14 @@
 
 #include "context.h"
 
+// Minimum resident blocks per SM of the 32-bit SSIM kernels (build-time knobs for A/B runs).
+#ifndef NGS_SSIMD_MINB
+#define NGS_SSIMD_MINB 3
+#endif
+#ifndef NGS_SSIMF_MINB
+#define NGS_SSIMF_MINB 3
+#endif
+
 namespace ngsb {
 
 namespace {
@@ -380,7 +388,7 @@ __device__ __forceinline__ void vpass32(const Window& win, bool w2, const double
     }
 }
 
-__global__ void __launch_bounds__(256) ssim_fields32_k(int W, int H, const double* __restrict__ image,
+__global__ void __launch_bounds__(256, NGS_SSIMF_MINB) ssim_fields32_k(int W, int H, const double* __restrict__ image,
                                                        const double* __restrict__ target, Window win, double c1,
                                                        double c2, double* __restrict__ fields,
                                                        double* __restrict__ sums, int row0, int own_y0, int own_y1) {
@@ -457,7 +465,7 @@ __global__ void __launch_bounds__(256) ssim_fields32_k(int W, int H, const doubl
     if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
 }
 
-__global__ void __launch_bounds__(256, 3) ssim_derivs32_k(int W, int H, const double* __restrict__ image,
+__global__ void __launch_bounds__(256, NGS_SSIMD_MINB) ssim_derivs32_k(int W, int H, const double* __restrict__ image,
                                                        const double* __restrict__ target, Window win, double lambda,
                                                        const double* __restrict__ fields, float* __restrict__ grad,
                                                        float* __restrict__ hess, double* __restrict__ sums, int row0,
