@@ -397,6 +397,12 @@ __global__ void __launch_bounds__(128) scaling_consts_k(SceneDev s, CameraDev ca
 #ifndef NGS_B16_SCL
 #define NGS_B16_SCL 64
 #endif
+#ifndef NGS_B8_ROT
+#define NGS_B8_ROT 64
+#endif
+#ifndef NGS_B8_SCL
+#define NGS_B8_SCL 64
+#endif
 #ifndef NGS_B16_OC
 #define NGS_B16_OC 64
 #endif
@@ -431,11 +437,11 @@ struct PassTraits<kPassGrad> {
 };
 template <>
 struct PassTraits<kPassRotation> {
-    static constexpr int NC = kRotConsts, NA = 2, BATCH = NGS_B16_ROT, BATCH8 = 64, R16 = NGS_R16_ROT;
+    static constexpr int NC = kRotConsts, NA = 2, BATCH = NGS_B16_ROT, BATCH8 = NGS_B8_ROT, R16 = NGS_R16_ROT;
 };
 template <>
 struct PassTraits<kPassScaling> {
-    static constexpr int NC = kScaleConsts, NA = 5, BATCH = NGS_B16_SCL, BATCH8 = 64, R16 = NGS_R16_SCL;
+    static constexpr int NC = kScaleConsts, NA = 5, BATCH = NGS_B16_SCL, BATCH8 = NGS_B8_SCL, R16 = NGS_R16_SCL;
 };
 template <>
 struct PassTraits<kPassOpacityColor> {

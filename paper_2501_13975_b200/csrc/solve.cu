@@ -11,6 +11,11 @@
 #include "geometry.cuh"
 #include "solve.h"
 
+// Minimum resident blocks per SM of the 4-view colour solve (build-time knob for A/B runs).
+#ifndef NGS_COLOR4_MINB
+#define NGS_COLOR4_MINB 4
+#endif
+
 namespace ngsb {
 
 namespace {
@@ -279,8 +284,10 @@ __device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, d
         c = 1.0, s = 0.0, t = 0.0;
         return;
     }
-    const double theta = (aqq - app) / (2 * apq);
-    t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1));
+    // t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)) with theta = d / e, d = aqq - app,
+    // e = 2 apq, multiplied through by |e|: one FP64 division instead of two.
+    const double d = aqq - app, e = 2 * apq;
+    t = (d * e >= 0 ? 1.0 : -1.0) * fabs(e) / (fabs(d) + sqrt(d * d + e * e));
     c = rsqrt(t * t + 1), s = t * c;
 }
 
@@ -448,7 +455,7 @@ __global__ void __launch_bounds__(128) solve_color_gram_k(SceneDev s, ColorViews
 
 // Colour solve, stage 2 (one thread per Gaussian and channel, blockIdx.y = channel).
 template <int MV>
-__global__ void __launch_bounds__(128, MV == 4 ? 4 : 2) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
+__global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
                                                      const double* __restrict__ acc, size_t stride,
                                                      const double* __restrict__ eig, SolveOutputs out) {
     const int ch = blockIdx.y;
