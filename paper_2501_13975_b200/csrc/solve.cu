@@ -286,8 +286,15 @@ __device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, d
     }
     // t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)) with theta = d / e, d = aqq - app,
     // e = 2 apq, multiplied through by |e|: one FP64 division instead of two.
+    // The reciprocal is the MUFU seed refined by two Newton steps (~full FP64
+    // precision; a Jacobi angle only needs to be accurate, not correctly rounded).
     const double d = aqq - app, e = 2 * apq;
-    t = (d * e >= 0 ? 1.0 : -1.0) * fabs(e) / (fabs(d) + sqrt(d * d + e * e));
+    const double den = fabs(d) + sqrt(d * d + e * e);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    r = fma(r, fma(-den, r, 1.0), r);
+    r = fma(r, fma(-den, r, 1.0), r);
+    t = (d * e >= 0 ? 1.0 : -1.0) * fabs(e) * r;
     c = rsqrt(t * t + 1), s = t * c;
 }
 
