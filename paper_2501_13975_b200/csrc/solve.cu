@@ -278,6 +278,17 @@ __global__ void __launch_bounds__(256) solve_opacity_k(SceneDev s, SolveParams s
 
 // Rotation (c, s, t = s / c) that zeroes a_pq (Numerical Recipes convention); identity
 // when a_pq is zero or negligible against both diagonals.
+// 1/sqrt(x) for normal x > 0: the MUFU seed refined by two Newton steps (same
+// role as the reciprocal below: accurate, not correctly rounded).
+__device__ __forceinline__ double rsqrt_pos(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    return y;
+}
+
 __device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, double& c, double& s, double& t) {
     const double g = 100.0 * fabs(apq);
     if (fabs(app) + g == fabs(app) && fabs(aqq) + g == fabs(aqq)) {
@@ -289,13 +300,14 @@ __device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, d
     // The reciprocal is the MUFU seed refined by two Newton steps (~full FP64
     // precision; a Jacobi angle only needs to be accurate, not correctly rounded).
     const double d = aqq - app, e = 2 * apq;
-    const double den = fabs(d) + sqrt(d * d + e * e);
+    const double h2 = d * d + e * e;
+    const double den = fabs(d) + h2 * rsqrt_pos(h2);
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
     r = fma(r, fma(-den, r, 1.0), r);
     r = fma(r, fma(-den, r, 1.0), r);
     t = (d * e >= 0 ? 1.0 : -1.0) * fabs(e) * r;
-    c = rsqrt(t * t + 1), s = t * c;
+    c = rsqrt_pos(t * t + 1), s = t * c;
 }
 
 // One round of the 4x4 parallel-order Jacobi: the disjoint rotations (P1, Q1) and
