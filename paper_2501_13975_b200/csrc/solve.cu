@@ -500,12 +500,13 @@ __global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2) solve_colo
 #pragma unroll
         for (int a = 0; a < MV; ++a) lmax = fmax(lmax, L[a][a]);
         bool kept[MV];
-        double isq[MV];  // L^-1/2 on kept directions
+        double isq[MV], sq[MV];  // L^-1/2 on kept directions
         int r = 0;
 #pragma unroll
         for (int a = 0; a < MV; ++a) {
             kept[a] = L[a][a] > 1e-13 * lmax && L[a][a] > 0.0;
-            isq[a] = kept[a] ? 1.0 / sqrt(L[a][a]) : 0.0;
+            isq[a] = kept[a] ? rsqrt_pos(L[a][a]) : 0.0;
+            sq[a] = L[a][a] * isq[a];  // L^1/2 on kept directions, 0 elsewhere
             r += kept[a] ? 1 : 0;
         }
         double beta_all[MV];
@@ -546,11 +547,11 @@ __global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2) solve_colo
 #pragma unroll
                 for (int i = 0; i < MV; ++i)
 #pragma unroll
-                    for (int j = 0; j < MV; ++j) {
+                    for (int j = i; j < MV; ++j) {
                         double t = 0;
 #pragma unroll
                         for (int v = 0; v < MV; ++v) t += E[v][i] * hv[v] * E[v][j];
-                        K[i][j] = (kept[i] && kept[j]) ? t * sqrt(L[i][i] * L[j][j]) : 0.0;
+                        K[i][j] = K[j][i] = t * sq[i] * sq[j];  // 0 unless both directions are kept
                     }
                 jacobi_eig<MV>(K, W);
                 // Eigenvectors y_e = Phi c_e with c_e = E L^-1/2 W_e; those living in the
