@@ -13,7 +13,7 @@
 
 // Minimum resident blocks per SM of the 4-view colour solve (build-time knob for A/B runs).
 #ifndef NGS_COLOR4_MINB
-#define NGS_COLOR4_MINB 4
+#define NGS_COLOR4_MINB 5
 #endif
 
 namespace ngsb {
