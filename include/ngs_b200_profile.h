@@ -45,6 +45,10 @@ typedef struct {
      * context stream as executed (views concurrent): render+loss of all
      * views, the four backward passes (incl. constants and all-reduce), solves. */
     double group_ms[6];
+    /* Multi-GPU exchange (always counted): NCCL all-reduce calls issued by this rank
+     * and their payload bytes (accumulators, overflow votes). */
+    int64_t allreduce_calls;
+    int64_t allreduce_bytes;
 } ngs_profile_stats;
 
 int32_t ngs_profile_enable(ngs_context* ctx, int32_t on);

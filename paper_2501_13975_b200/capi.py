@@ -127,7 +127,7 @@ STAGES = ("project", "sort", "raster", "loss", "consts", "bwd_position", "bwd_ro
 class ngs_profile_stats(C.Structure):
     _fields_ = [("ms", C.c_double * 11), ("launches", C.c_int64 * 11), ("total_launches", C.c_int64),
                 ("contrib_pairs", C.c_int64 * 4), ("raster_pairs", C.c_int64), ("renders", C.c_int64),
-                ("group_ms", C.c_double * 6)]
+                ("group_ms", C.c_double * 6), ("allreduce_calls", C.c_int64), ("allreduce_bytes", C.c_int64)]
 
 
 class ngs_terms(C.Structure):
@@ -490,6 +490,7 @@ class Context:
                     launches={k: st.launches[i] for i, k in enumerate(STAGES)},
                     total_launches=st.total_launches, contrib_pairs=list(st.contrib_pairs),
                     raster_pairs=st.raster_pairs, renders=st.renders,
+                    allreduce_calls=st.allreduce_calls, allreduce_bytes=st.allreduce_bytes,
                     # Trainer renders are chained per view into the following backward pass, so each
                     # pass group includes the render before it ("render" stays 0 in trainer steps).
                     group_ms=dict(zip(("render", "render+bwd_position", "render+bwd_rotation", "render+bwd_scaling",
@@ -536,13 +537,21 @@ def dist_unique_id(lib: NgsLibrary) -> bytes:
     return bytes(buf)
 
 
-def shard_rows(tiles_y: int, rank: int, world: int):
-    """Mirror of ngsb::shard_rows (csrc/context.h): (band_y0, band_y1, own_y0, own_y1)."""
-    if world <= 1:
-        return 0, tiles_y, 0, tiles_y
-    own0 = tiles_y * rank // world
-    own1 = tiles_y * (rank + 1) // world
-    return (own0 - 1 if own0 > 0 else 0), (own1 + 1 if own1 < tiles_y else tiles_y), own0, own1
+class ngs_shard_rows(C.Structure):
+    _fields_ = [("band_y0", C.c_int32), ("band_y1", C.c_int32), ("own_y0", C.c_int32), ("own_y1", C.c_int32)]
+
+
+def dist_plan(lib: NgsLibrary, world: int, rank: int, sizes, tiles, loss_window: int = 11):
+    """ngs_dist_plan (ngs_b200_dist.h): this rank's (band_y0, band_y1, own_y0, own_y1) tile
+    rows of each view of a step, view 0 the primary. Pure host call (no device)."""
+    n = len(sizes)
+    w = np.asarray([s[0] for s in sizes], np.int32)
+    h = np.asarray([s[1] for s in sizes], np.int32)
+    t = np.asarray(list(tiles), np.int32)
+    out = (ngs_shard_rows * n)()
+    lib.check(lib.lib.ngs_dist_plan(C.c_int32(world), C.c_int32(rank), C.c_int32(n), _iptr(w), _iptr(h), _iptr(t),
+                                    C.c_int32(loss_window), out))
+    return [(r.band_y0, r.band_y1, r.own_y0, r.own_y1) for r in out]
 
 
 _product = None

@@ -763,13 +763,20 @@ __device__ __forceinline__ void grad_record(const Rec& r, float sigma, float (&v
 }
 
 // Exact, order-independent accumulation of x * 2^kLimbShift (see backward.h).
-__device__ __forceinline__ void add_fixed128(unsigned long long* limbs, float x) {
+__device__ __forceinline__ void add_fixed128(unsigned long long* limbs, float x, int* err) {
+    // Non-finite partials (the FP64 path's "non-finite update" abort) and |x| >= 2^38 (the
+    // 128-bit sum, binary point 2^-88, keeps 2^39 of headroom for the accumulation) raise
+    // the device error flag instead of wrapping the fixed-point sum.
+    if (!(fabsf(x) < 0x1p38f)) {
+        atomicOr(err, kErrFixedRange);
+        return;
+    }
     int e;
     const float m = frexpf(x, &e);                                  // x = m 2^e, 0.5 <= |m| < 1
     const long long mi = static_cast<long long>(ldexpf(m, 24));      // exact: |mi| < 2^24
-    const int sh = e - 24 + kLimbShift;
+    const int sh = e - 24 + kLimbShift;                              // <= 102 for |x| < 2^38
     __int128 v = static_cast<__int128>(mi);
-    v = sh >= 0 ? (v << sh) : (v >> (-sh));                          // deterministic truncation below 2^-88
+    v = sh >= 0 ? (v << sh) : (sh > -64 ? (v >> (-sh)) : (mi < 0 ? -1 : 0));  // truncation below 2^-88
     const unsigned __int128 u = static_cast<unsigned __int128>(v);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -778,16 +785,38 @@ __device__ __forceinline__ void add_fixed128(unsigned long long* limbs, float x)
     }
 }
 
+// Sum of the four 32-bit-weighted limbs as a two's-complement 128-bit integer, rounded
+// ONCE to the nearest FP64 (top 64 significant bits with a sticky bit for the rest, then
+// one __ull2double_rn; 64 > 53 + 2 so the sticky bit makes the single rounding exact).
+__device__ __forceinline__ double fixed128_to_double(unsigned __int128 u) {
+    const bool neg = static_cast<__int128>(u) < 0;
+    if (neg) u = ~u + 1;
+    const unsigned long long hi = static_cast<unsigned long long>(u >> 64);
+    const unsigned long long lo = static_cast<unsigned long long>(u);
+    if (hi == 0 && lo == 0) return 0.0;
+    const int lead = hi ? 127 - __clzll(hi) : 63 - __clzll(lo);   // index of the leading 1
+    unsigned long long top;
+    int shift;  // value = top * 2^shift (before the sticky bit)
+    if (lead <= 63) {
+        top = lo;
+        shift = 0;
+    } else {
+        shift = lead - 63;
+        top = static_cast<unsigned long long>(u >> shift);
+        const unsigned __int128 rest = u & ((static_cast<unsigned __int128>(1) << shift) - 1);
+        if (rest) top |= 1ull;
+    }
+    const double d = ldexp(__ull2double_rn(top), shift - kLimbShift);
+    return neg ? -d : d;
+}
+
 __global__ void limbs_to_double_k(const unsigned long long* __restrict__ limbs, double* __restrict__ acc, size_t count) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         unsigned __int128 u = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) u += static_cast<unsigned __int128>(limbs[4 * i + q]) << (32 * q);
-        const __int128 v = static_cast<__int128>(u);
-        const long long hi = static_cast<long long>(v >> 64);
-        const unsigned long long lo = static_cast<unsigned long long>(v);
-        acc[i] = ldexp(static_cast<double>(hi), 64 - kLimbShift) + ldexp(static_cast<double>(lo), -kLimbShift);
+        acc[i] = fixed128_to_double(u);
     }
 }
 
@@ -875,15 +904,17 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
     WarpQueue& Q = s_q[warp];
 
     int last = -1;
-    float Cf_hi[3] = {0.f, 0.f, 0.f}, Cf_lo[3] = {0.f, 0.f, 0.f};  // final colour as an unevaluated float pair
+    // Final colour (the forward's FP64 image) and the FP64 colour prefix, re-accumulated with
+    // exactly the forward's operations (raster_forward_k: C = fma((double)w, (double)c, C)), so
+    // C_final - prefix is the exact FP64 suffix sum: behind = suffix / T_next keeps ~1e-16
+    // relative error even where T_next is ~1e-4 (an FP32 prefix loses ~n*eps/T_next there).
+    double Cf[3] = {0.0, 0.0, 0.0};
     float gl[3] = {0.f, 0.f, 0.f}, hl[3] = {0.f, 0.f, 0.f};
     if (inside) {
         last = a.last[pidx];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double cf = a.image[c * plane + pidx];
-            Cf_hi[c] = static_cast<float>(cf);
-            Cf_lo[c] = static_cast<float>(cf - static_cast<double>(Cf_hi[c]));
+            Cf[c] = a.image[c * plane + pidx];
             gl[c] = a.loss_grad[c * plane + pidx];
             hl[c] = a.loss_hess[c * plane + pidx];
         }
@@ -901,7 +932,8 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
     const int end = min(range.y, s_maxlast + 1);
     const int wlast = __reduce_max_sync(0xffffffffu, last);  // the warp's last contributing list entry
 
-    float T = 1.0f, P[3] = {0.f, 0.f, 0.f};
+    float T = 1.0f;
+    double P[3] = {0.0, 0.0, 0.0};
     int qhead = 0, qcount = 0;  // warp-uniform ring state
 
     const float4* s_const = S.cst[0];  // constants of the batch being traversed
@@ -1077,9 +1109,9 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
                         float ac[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
-                            const float Pn = __fmaf_rn(w, col[c], P[c]);
+                            const double Pn = __fma_rn(static_cast<double>(w), static_cast<double>(col[c]), P[c]);
                             const float behind =
-                                is_last ? a.bg[c] : ((Cf_hi[c] - Pn) + Cf_lo[c]) * inv_tn;
+                                is_last ? a.bg[c] : __double2float_rn(__dsub_rn(Cf[c], Pn)) * inv_tn;
                             ac[c] = col[c] - behind;
                             P[c] = Pn;
                         }
@@ -1134,7 +1166,7 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
                 const float val = vals[c];
                 if (val == 0.f) continue;
                 if (a.acc_limbs) {
-                    add_fixed128(a.acc_limbs + (static_cast<size_t>(c) * a.acc_stride + k) * 4, val);
+                    add_fixed128(a.acc_limbs + (static_cast<size_t>(c) * a.acc_stride + k) * 4, val, a.err);
                 } else {
                     atomicAdd(&a.acc[static_cast<size_t>(c) * a.acc_stride + k], static_cast<double>(val));
                 }
@@ -1194,6 +1226,31 @@ struct SmemTag {
     using type = T;
 };
 
+namespace {
+__global__ void acc_to_f32_k(const double* __restrict__ a, float* __restrict__ f, size_t count) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        f[i] = __double2float_rn(a[i]);
+}
+__global__ void acc_from_f32_k(const float* __restrict__ f, double* __restrict__ a, size_t count) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        a[i] = static_cast<double>(f[i]);
+}
+}  // namespace
+
+void acc_to_f32(const double* acc, float* out, size_t count, cudaStream_t s) {
+    if (count == 0) return;
+    acc_to_f32_k<<<static_cast<int>(std::min<size_t>((count + 255) / 256, 8 * 148)), 256, 0, s>>>(acc, out, count);
+    CUDA_LAUNCH_CHECK();
+}
+
+void acc_from_f32(const float* in, double* acc, size_t count, cudaStream_t s) {
+    if (count == 0) return;
+    acc_from_f32_k<<<static_cast<int>(std::min<size_t>((count + 255) / 256, 8 * 148)), 256, 0, s>>>(in, acc, count);
+    CUDA_LAUNCH_CHECK();
+}
+
 void limbs_to_double(const unsigned long long* limbs, double* acc, size_t count, cudaStream_t s) {
     if (count == 0) return;
     limbs_to_double_k<<<static_cast<int>(std::min<size_t>((count + 255) / 256, 8 * 148)), 256, 0, s>>>(limbs, acc, count);
@@ -1201,7 +1258,8 @@ void limbs_to_double(const unsigned long long* limbs, double* acc, size_t count,
 }
 
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
-                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs) {
+                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs, int* err) {
+    if (acc_limbs && !err) throw Error(NGS_ERR_INTERNAL, "launch_backward: deterministic mode needs the error flag");
     if (v.pairs == 0 || v.n == 0) return;
     BackwardArgs a;
     a.tiles_x = v.cam.tiles_x;
@@ -1225,6 +1283,7 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     a.acc_limbs = acc_limbs;
     a.visible = visible;
     a.contrib_pairs = contrib_pairs;
+    a.err = err;
     const int own0 = std::max(0, v.raster.own_y0), own1 = std::min(v.cam.tiles_y, v.raster.own_y1);
     if (own1 <= own0) return;
     a.tile0 = own0 * v.cam.tiles_x;

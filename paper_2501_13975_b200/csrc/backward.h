@@ -83,6 +83,7 @@ struct BackwardArgs {
     unsigned long long* acc_limbs;  // deterministic mode: exact fixed-point limbs [comp][stride][4] (acc unused)
     uint8_t* visible;                    // optional: set to 1 for kernels with >= 1 record
     unsigned long long* contrib_pairs;   // optional: count of contributing (pixel, splat) records
+    int* err;                            // device error flag (kErrFixedRange in deterministic mode)
 };
 
 void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s,
@@ -91,11 +92,17 @@ void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const Cam
 // two's-complement fixed-point number (binary point 2^-88) and added as four
 // 32-bit chunks into four 64-bit counters with integer atomics. Integer addition
 // is associative, so the sums do not depend on the order in which blocks finish;
-// limbs_to_double normalises the carries and rounds once to FP64.
+// limbs_to_double normalises the carries and rounds once (correctly) to FP64.
+// Non-finite or |x| >= 2^38 partials set kErrFixedRange instead of being added.
 constexpr int kLimbShift = 88;
 void limbs_to_double(const unsigned long long* limbs, double* acc, size_t count, cudaStream_t s);
+// Multi-GPU exchange payload: the FP64 accumulators travel as FP32 (half the bytes; the
+// cross-rank sum of world FP32-rounded partials stays ~1e-7 relative).
+void acc_to_f32(const double* acc, float* out, size_t count, cudaStream_t s);
+void acc_from_f32(const float* in, double* acc, size_t count, cudaStream_t s);
 
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
-                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs = nullptr);
+                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs = nullptr,
+                     int* err = nullptr);
 
 }  // namespace ngsb

@@ -19,6 +19,11 @@ constexpr int kTilePixels = kTile * kTile;
 constexpr double kNearPlaneEps = 1e-6;    // camera.hpp:11
 constexpr double kSigmaMargin = 1e-4;     // scene.hpp:10
 constexpr double kColorOffset = 0.5;      // sh.hpp:21
+// Largest (tile, splat) pair count of one view: the onesweep look-back packs running
+// counts into 30 bits (sort.cu kCountMask) and offsets are int.
+constexpr int kMaxPairs = (1 << 30) - 1;
+// Device error-flag bits (ngs_context::check_err maps them onto status codes).
+constexpr int kErrNonPD = 1, kErrDegenerate = 2, kErrQuat = 4, kErrPairLimit = 8, kErrFixedRange = 16;
 
 // Error carrying an ngs_status; thrown by host code, mapped at the C-ABI edge.
 struct Error : std::runtime_error {

@@ -107,6 +107,7 @@ struct TrainerState {
     // SH 48), step count (AdamState, trainer.hpp:106-122), rotation constants.
     DevBuf<double> adam_m, adam_v;
     int adam_t = 0;
+    int adam_n = -1;  // scene size the moments were made for (-1: none)
     DevBuf<float> rot_consts;
     std::vector<ViewSlot> views;  // primary + secondaries of the current step
     void release() {
@@ -124,6 +125,7 @@ struct TrainerState {
         adam_v.release();
         rot_consts.release();
         adam_t = 0;
+        adam_n = -1;
         active = false;
     }
 };
@@ -159,6 +161,7 @@ struct ngs_context {
     cudaStream_t cs = nullptr;                      // copy stream: target uploads overlap the renders
     std::array<cudaEvent_t, 24> gev{};  // stage-group events of a trainer step
     DevBuf<int> overflow;
+    DevBuf<float> xfer;                    // multi-GPU exchange buffer (FP32 accumulators)
     DevBuf<float4> snap_ps, snap_sc, snap_q;
     DevBuf<float> snap_sh;
     // Multi-GPU shard (ngs_b200_dist.h)
@@ -189,6 +192,7 @@ struct ngs_context {
         out_delta.release();
         out_flags.release();
         overflow.release();
+        xfer.release();
         snap_ps.release();
         snap_sc.release();
         snap_q.release();
@@ -223,8 +227,22 @@ struct ngs_context {
             if (e & 1) throw Error(NGS_ERR_NUMERICAL, "project_kernel: projected covariance is not positive definite");
             if (e & 2) throw Error(NGS_ERR_DEGENERATE, "view_direction: point coincides with camera center");
             if (e & 4) throw Error(NGS_ERR_INVALID_INPUT, "renormalize_quaternion: zero or non-finite quaternion");
+            if (e & kErrPairLimit)
+                throw Error(NGS_ERR_INVALID_INPUT, "render: (tile, splat) pair count exceeds 2^30 - 1 (sort limit)");
+            if (e & kErrFixedRange)
+                throw Error(NGS_ERR_NUMERICAL, "deterministic accumulation: non-finite or out-of-range partial");
             throw Error(NGS_ERR_NUMERICAL, "device error flag " + std::to_string(e));
         }
+    }
+
+    // Multi-GPU: every rank must take the same pair-capacity retry decision (the retried
+    // step re-issues its collectives), so the overflow flag is OR-ed over ranks first.
+    void vote_overflow() {
+        if (!comm) return;
+        nccl_check(nccl().all_reduce(overflow.ptr, overflow.ptr, 1, ncclInt32, ncclMax, comm, stream),
+                   "ncclAllReduce(overflow vote)");
+        prof.stats.allreduce_calls += 1;
+        prof.stats.allreduce_bytes += sizeof(int);
     }
 
     // Fork the per-view streams off the main stream / join them back.
@@ -240,7 +258,7 @@ struct ngs_context {
     }
 
     // Raster parameters of a view with this context's shard applied.
-    RasterParams raster_for(const ngs_raster_options* o, const CameraDev& cam) const;
+    RasterParams raster_for(const ngs_raster_options* o, const CameraDev& cam, int window) const;
 
     ViewSlot& slot(int i) {
         if (i < 0 || i >= NGS_MAX_VIEW_SLOTS) throw Error(NGS_ERR_INVALID_INPUT, "bad view slot");
@@ -287,9 +305,76 @@ LossParams to_loss(const ngs_loss_config* o) {
 
 }  // namespace
 
-RasterParams ngs_context::raster_for(const ngs_raster_options* o, const CameraDev& cam) const {
+namespace ngsb {
+
+void plan_step_shards(int world, int rank, int nv, const int* width, const int* height, const int* tile,
+                      int window, ShardRows* out) {
+    if (nv <= 0) return;
+    std::vector<int> rows(nv);
+    for (int i = 0; i < nv; ++i) rows[i] = (height[i] + tile[i] - 1) / tile[i];
+    if (world <= 1) {
+        for (int i = 0; i < nv; ++i) out[i] = ShardRows{0, rows[i], 0, rows[i]};
+        return;
+    }
+    // Secondaries whole, largest first, to the least-loaded rank (LPT).
+    std::vector<double> load(world, 0.0);
+    std::vector<int> owner(nv, -1);
+    std::vector<int> idx;
+    for (int i = 1; i < nv; ++i) idx.push_back(i);
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+        return static_cast<long long>(width[a]) * height[a] > static_cast<long long>(width[b]) * height[b];
+    });
+    for (int i : idx) {
+        int best = 0;
+        for (int r = 1; r < world; ++r)
+            if (load[r] < load[best]) best = r;
+        owner[i] = best;
+        load[best] += static_cast<double>(width[i]) * height[i];
+    }
+    // Primary rows: water-fill the remaining capacity, contiguous ranges in rank order.
+    const double prim = static_cast<double>(width[0]) * height[0];
+    std::vector<double> sorted(load);
+    std::sort(sorted.begin(), sorted.end());
+    double level = 0.0;
+    {
+        double acc = 0.0;  // sum over the k lowest loads
+        for (int k = 1; k <= world; ++k) {
+            acc += sorted[k - 1];
+            const double l = (prim + acc) / k;  // level if exactly the k lowest ranks take primary rows
+            if (k == world || l <= sorted[k]) {
+                level = l;
+                break;
+            }
+        }
+    }
+    std::vector<double> share(world);
+    double tot = 0.0;
+    for (int r = 0; r < world; ++r) tot += (share[r] = std::max(0.0, level - load[r]));
+    const int halo = [&](int t) { return (std::max(window, 1) - 1 + t - 1) / t; }(tile[0]);
+    double cum = 0.0;
+    for (int r = 0; r <= rank; ++r) {
+        const int y0 = static_cast<int>(std::llround(rows[0] * (tot > 0 ? cum / tot : 0.0)));
+        cum += share[r];
+        const int y1 = r == world - 1 ? rows[0] : static_cast<int>(std::llround(rows[0] * (tot > 0 ? cum / tot : 0.0)));
+        if (r == rank) {
+            if (y1 > y0)
+                out[0] = ShardRows{std::max(0, y0 - halo), std::min(rows[0], y1 + halo), y0, y1};
+            else
+                out[0] = ShardRows{0, 0, 0, 0};
+        }
+    }
+    for (int i = 1; i < nv; ++i) out[i] = owner[i] == rank ? ShardRows{0, rows[i], 0, rows[i]} : ShardRows{0, 0, 0, 0};
+}
+
+}  // namespace ngsb
+
+RasterParams ngs_context::raster_for(const ngs_raster_options* o, const CameraDev& cam, int window) const {
+    // One view on its own (ngs_build_view / ngs_render with a shard set): split evenly.
     RasterParams r = to_raster(o);
-    shard_rows(cam.tiles_y, cam.tile, shard_rank, shard_world, r);
+    ShardRows sr;
+    const int tile = cam.tile;
+    plan_step_shards(shard_world, shard_rank, 1, &cam.width, &cam.height, &tile, window, &sr);
+    apply_shard(sr, r);
     return r;
 }
 
@@ -566,6 +651,7 @@ int32_t ngs_set_scene(ngs_context* ctx, const ngs_scene* s) {
         d.sh = ctx->sh.ptr;
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         for (auto& v : ctx->slots) v.valid = false;
+        ctx->trainer.adam_n = -1;  // first-order moments belong to the previous scene
     });
 }
 
@@ -637,8 +723,8 @@ int32_t ngs_build_view(ngs_context* ctx, int32_t slot, const ngs_camera* camera,
         ViewSlot& v = ctx->slot(slot);
         v.valid = false;
         upload_camera(*camera, v.cam, tile_for(ctx, *camera, true));
-        v.raster = ctx->raster_for(raster, v.cam);
         v.loss = to_loss(loss);
+        v.raster = ctx->raster_for(raster, v.cam, v.loss.window);
         const size_t npx = static_cast<size_t>(camera->width) * camera->height;
         std::vector<double> tgt;
         interleaved_to_planar(target_rgb, camera->width, camera->height, tgt);
@@ -809,29 +895,45 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
         // projection flags, so they overlap the rest of the view's render; the
         // backward then waits for the render + loss.
         if (concurrent && chained) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->pev[i], 0));
+        if (!v.raster.owns_rows()) {  // another rank's view (multi-GPU): nothing to accumulate here
+            if (concurrent && chained) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->rev[i], 0));
+            continue;
+        }
         compute_pass_consts(pass, ctx->scene, v, views[0]->cam, s);
         if (concurrent && chained) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->rev[i], 0));
         double* acc = ctx->acc.ptr + (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0);
         unsigned long long* contrib = ctx->pairs.ptr + (pass == kPassPositionUV ? kPassPosition : pass);
         unsigned long long* vl =
             limbs ? limbs + 4 * (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0) : nullptr;
-        launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s, vl);
+        launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s, vl, ctx->err.ptr);
     }
     if (concurrent) ctx->join(nv, ctx->vs.data());
     if (ctx->comm) {
         // Exchange step: per-Gaussian FP64 accumulators summed over ranks (NVLink / NVSwitch).
         StageScope st(NGS_STAGE_OTHER, ctx->stream, 0);
-        if (limbs)  // integer limbs: the cross-rank sum is exact as well (32-bit headroom per limb)
+        if (limbs) {  // integer limbs: the cross-rank sum is exact as well (32-bit headroom per limb)
             nccl_check(nccl().all_reduce(limbs, limbs, 4 * stride * comps, ncclUint64, ncclSum, ctx->comm,
                                          ctx->stream),
                        "ncclAllReduce(accumulator limbs)");
-        else
-            nccl_check(nccl().all_reduce(ctx->acc.ptr, ctx->acc.ptr, stride * comps, ncclFloat64, ncclSum, ctx->comm,
+            ctx->prof.stats.allreduce_calls += 1;
+            ctx->prof.stats.allreduce_bytes += static_cast<int64_t>(sizeof(unsigned long long) * 4 * stride * comps);
+        } else {  // FP32 payload: half the NVLink bytes of the FP64 accumulators
+            const size_t count = stride * comps;
+            ctx->xfer.ensure(count);
+            acc_to_f32(ctx->acc.ptr, ctx->xfer.ptr, count, ctx->stream);
+            nccl_check(nccl().all_reduce(ctx->xfer.ptr, ctx->xfer.ptr, count, ncclFloat32, ncclSum, ctx->comm,
                                          ctx->stream),
                        "ncclAllReduce(accumulators)");
-        if (visible)
+            acc_from_f32(ctx->xfer.ptr, ctx->acc.ptr, count, ctx->stream);
+            ctx->prof.stats.allreduce_calls += 1;
+            ctx->prof.stats.allreduce_bytes += static_cast<int64_t>(count * sizeof(float));
+        }
+        if (visible) {
             nccl_check(nccl().all_reduce(visible, visible, stride, ncclUint8, ncclMax, ctx->comm, ctx->stream),
                        "ncclAllReduce(visible)");
+            ctx->prof.stats.allreduce_calls += 1;
+            ctx->prof.stats.allreduce_bytes += static_cast<int64_t>(stride);
+        }
     }
     if (limbs) limbs_to_double(limbs, ctx->acc.ptr, stride * comps, ctx->stream);
 }
@@ -1046,6 +1148,7 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
         T.step_count = 0;
         T.probe_loss_cache = 0.0;
         T.adam_t = 0;
+        T.adam_n = -1;
         if (c->optimizer < NGS_OPT_NEWTON || c->optimizer > NGS_OPT_ADAM)
             throw Error(NGS_ERR_INVALID_INPUT, "train config: unknown optimizer");
         T.rng.seed(c->seed);
@@ -1174,13 +1277,25 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     // view's loss waits for its own target only.
     if (upload_targets) {
         if (concurrent) CUDA_CHECK(cudaStreamWaitEvent(ctx->cs, ctx->fork_ev, 0));
+        // The step's views over the ranks (ngs_b200_dist.h): whole secondaries, primary bands.
+        int ws[kMaxSolveViews], hs[kMaxSolveViews], ts[kMaxSolveViews];
+        for (int i = 0; i < nv; ++i) {
+            const ngs_camera& cam = (i == 0) ? T.cameras[view_id] : T.down_cameras[nbrs[i - 1]];
+            ws[i] = cam.width;
+            hs[i] = cam.height;
+            ts[i] = tile_for(ctx, cam, false);
+        }
+        ShardRows plan[kMaxSolveViews];
+        plan_step_shards(ctx->shard_world, ctx->shard_rank, nv, ws, hs, ts, T.cfg.loss.window, plan);
         for (int i = 0; i < nv; ++i) {
             ViewSlot& v = T.views[i];
             const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
             const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
-            upload_camera(cam, v.cam, tile_for(ctx, cam, false));
-            v.raster = ctx->raster_for(&T.cfg.raster, v.cam);
+            upload_camera(cam, v.cam, ts[i]);
+            v.raster = to_raster(&T.cfg.raster);
+            apply_shard(plan[i], v.raster);
             v.loss = to_loss(&T.cfg.loss);
+            if (!v.raster.owns_rows()) continue;  // projection only: no target, no loss
             const size_t npx = static_cast<size_t>(cam.width) * cam.height;
             v.target.ensure(3 * npx);
             cudaStream_t s = concurrent ? ctx->cs : ctx->stream;
@@ -1203,8 +1318,10 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         if (concurrent && !join) rs.projected = ctx->pev[i];
         rs.pos_version = ctx->order_reuse ? ctx->pos_version : 0;
         render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
-        if (upload_targets && concurrent) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->tev[i], 0));
-        compute_loss(v, s);
+        if (v.raster.owns_rows()) {
+            if (upload_targets && concurrent) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->tev[i], 0));
+            compute_loss(v, s);
+        }
         if (concurrent && !join) CUDA_CHECK(cudaEventRecord(ctx->rev[i], s));
     }
     if (concurrent && join) ctx->join(nv, ctx->vr.data());
@@ -1219,11 +1336,15 @@ float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
     cudaStream_t s = ctx->stream;
     ++ctx->pos_version;  // every first-order step moves the positions
     const bool adam = T.cfg.optimizer == NGS_OPT_ADAM;
-    if (adam && !T.adam_m.ptr) {
+    if (adam && T.adam_n != n) {
+        // Moments are sized for (and belong to) one scene: (re)start them whenever the scene
+        // changed since they were made (ngs_set_scene resets adam_n), as AdamState(n) does.
         T.adam_m.ensure(56 * stride);
         T.adam_v.ensure(56 * stride);
         CUDA_CHECK(cudaMemsetAsync(T.adam_m.ptr, 0, sizeof(double) * 56 * stride, s));
         CUDA_CHECK(cudaMemsetAsync(T.adam_v.ptr, 0, sizeof(double) * 56 * stride, s));
+        T.adam_n = n;
+        T.adam_t = 0;
     }
     ctx->norm.ensure(5);
     ViewSlot& v = T.views[0];
@@ -1232,6 +1353,7 @@ float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
     for (int attempt = 0;; ++attempt) {  // render only: parameters are untouched until the update kernel
         CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
         render_step_views(ctx, view_id, none, true);
+        ctx->vote_overflow();
         int overflow = 0;
         CUDA_CHECK(cudaMemcpyAsync(&overflow, ctx->overflow.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
@@ -1362,6 +1484,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                 }
             }
             CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
+            ctx->vote_overflow();
             int overflow = 0;
             CUDA_CHECK(cudaMemcpyAsync(norms, ctx->norm.ptr, sizeof(norms), cudaMemcpyDeviceToHost, s));
             CUDA_CHECK(cudaMemcpyAsync(&overflow, ctx->overflow.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1799,7 +1922,9 @@ int32_t ngs_dist_init(ngs_context* ctx, const uint8_t id_bytes[NGS_DIST_ID_BYTES
             nccl().comm_destroy(ctx->comm);
             ctx->comm = nullptr;
         }
-        if (world > 1) nccl_check(nccl().comm_init_rank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+        // Also at world == 1: the exchange path (FP32 payload, overflow vote) then runs as a
+        // 1-rank all-reduce, which is what the single-GPU NCCL test exercises.
+        nccl_check(nccl().comm_init_rank(&ctx->comm, world, id, rank), "ncclCommInitRank");
         ctx->shard_rank = rank;
         ctx->shard_world = world;
         for (auto& v : ctx->slots) v.valid = false;
@@ -1811,6 +1936,21 @@ int32_t ngs_set_tile_size(ngs_context* ctx, int32_t tile) {
         if (tile != 0 && tile != 8 && tile != 16) throw Error(NGS_ERR_INVALID_INPUT, "tile size must be 0, 8 or 16");
         ctx->tile_policy = tile;
         for (auto& v : ctx->slots) v.valid = false;
+    });
+}
+
+int32_t ngs_dist_plan(int32_t world, int32_t rank, int32_t n_views, const int32_t* width, const int32_t* height,
+                      const int32_t* tile, int32_t loss_window, ngs_shard_rows* out) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) throw Error(NGS_ERR_INVALID_INPUT, "bad rank/world");
+        if (n_views < 1 || n_views > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "bad view count");
+        for (int i = 0; i < n_views; ++i)
+            if (width[i] < 1 || height[i] < 1 || (tile[i] != 8 && tile[i] != 16))
+                throw Error(NGS_ERR_INVALID_INPUT, "bad view size or tile");
+        std::vector<ShardRows> rows(n_views);
+        plan_step_shards(world, rank, n_views, width, height, tile, loss_window, rows.data());
+        for (int i = 0; i < n_views; ++i)
+            out[i] = ngs_shard_rows{rows[i].band_y0, rows[i].band_y1, rows[i].own_y0, rows[i].own_y1};
     });
 }
 

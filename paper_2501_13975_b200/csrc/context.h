@@ -23,28 +23,39 @@ struct RasterParams {
     float t_min;
     bool cutoff_enabled;  // alpha_cutoff > 0: AABB binning, else every splat in every tile
     double radius;        // max(3, sqrt(2 ln(1/alpha_cutoff)))  rasterizer.hpp:215-216
-    // Multi-GPU shard of this view, in tile rows of the view's
-    // tile size: rows [band_y0, band_y1) are projected, binned, rasterised and
-    // get loss fields (owned rows plus a halo of ceil(10 px / tile) rows, which
-    // covers the SSIM support); the backward runs over the owned rows
-    // [own_y0, own_y1) only. Full frame when unsharded.
+    // Multi-GPU shard of this view (plan_step_shards), in tile rows of the
+    // view's tile size: rows [band_y0, band_y1) are projected, binned, rasterised and get
+    // SSIM statistics (owned rows plus a halo of ceil((window - 1) / tile) rows: the loss
+    // derivatives at a pixel read statistics +-window/2 away, which read pixels
+    // +-window/2 further); loss fields and the backward cover the owned rows
+    // [own_y0, own_y1) only. An empty band (band_y0 == band_y1) is a view this rank
+    // does not own: it is only projected (its flags feed the replicated colour solve).
+    // Full frame when unsharded.
     int band_y0 = 0, band_y1 = 1 << 30;
     int own_y0 = 0, own_y1 = 1 << 30;
+    bool owns_rows() const { return own_y0 < own_y1; }
 };
 
-// Rows of tile-row band `rank` of `world` for a view with `tiles_y` rows of
-// `tile` pixels.
-inline void shard_rows(int tiles_y, int tile, int rank, int world, RasterParams& r) {
-    if (world <= 1) {
-        r.band_y0 = r.own_y0 = 0;
-        r.band_y1 = r.own_y1 = tiles_y;
-        return;
-    }
-    const int halo = (10 + tile - 1) / tile;
-    r.own_y0 = static_cast<int>(static_cast<long long>(tiles_y) * rank / world);
-    r.own_y1 = static_cast<int>(static_cast<long long>(tiles_y) * (rank + 1) / world);
-    r.band_y0 = r.own_y0 - halo > 0 ? r.own_y0 - halo : 0;
-    r.band_y1 = r.own_y1 + halo < tiles_y ? r.own_y1 + halo : tiles_y;
+struct ShardRows {
+    int band_y0, band_y1, own_y0, own_y1;
+};
+
+// Partition of the views of one Newton step over `world` ranks (SURVEY.md
+// §8(e) parity mode). View 0 is the primary; views 1..nv-1 are the secondaries.
+//   * Secondaries go whole to ranks, largest first, each to the least-loaded rank
+//     (load = pixels; ties: lowest rank).
+//   * The primary's tile rows are then water-filled: rank r gets a contiguous share
+//     proportional to max(0, L - load_r), L chosen so the shares cover the primary, in
+//     rank order. With nv == 1 the single view is split evenly.
+//   * Halo: ceil((window - 1) / tile) tile rows on each side of an owned range.
+// Identical on every rank (pure function of its arguments). world <= 1: full frames.
+void plan_step_shards(int world, int rank, int nv, const int* width, const int* height, const int* tile,
+                      int window, ShardRows* out);
+inline void apply_shard(const ShardRows& r, RasterParams& rp) {
+    rp.band_y0 = r.band_y0;
+    rp.band_y1 = r.band_y1;
+    rp.own_y0 = r.own_y0;
+    rp.own_y1 = r.own_y1;
 }
 
 // Views with fewer 16x16 tiles than this render with 8x8 tiles: their per-tile

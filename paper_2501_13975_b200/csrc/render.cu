@@ -199,17 +199,33 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
     }
 }
 
-__global__ void gather_counts_k(int n, const int* order, const int* tiles_touched, int* counts_sorted) {
+// Also sums the pair count exactly in 64 bits (`total64`, zeroed by the caller): the int
+// scan below and the onesweep status words (30-bit counts, sort.cu) are only valid up to
+// kMaxPairs, and emit_pairs_k refuses to emit past that instead of corrupting the lists.
+__global__ void gather_counts_k(int n, const int* order, const int* tiles_touched, int* counts_sorted,
+                                unsigned long long* total64) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) counts_sorted[r] = tiles_touched[order[r]];
+    const int c = r < n ? tiles_touched[order[r]] : 0;
+    if (r < n) counts_sorted[r] = c;
+    unsigned long long w = static_cast<unsigned long long>(c);
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(total64, w);
 }
 
 // K3: emit (tile, kernel) pairs in depth order; a later stable sort on the
 // tile key alone keeps depth order (ties by kernel id) inside every tile.
 __global__ void emit_pairs_k(int n, int tiles_x, int cap, const int* order, const int* offsets, const int4* rect,
                              const int* tiles_touched, unsigned int* keys, int* vals, int* overflow,
-                             unsigned long long* pair_counter, int* counters) {
+                             unsigned long long* pair_counter, int* counters, int* d_err) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long total64 = *reinterpret_cast<const unsigned long long*>(counters + 4);
+    if (total64 > static_cast<unsigned long long>(kMaxPairs)) {  // beyond the sort's 30-bit counts: error, no lists
+        if (r == 0) {
+            atomicOr(d_err, kErrPairLimit);
+            counters[2] = 0;
+        }
+        return;
+    }
     if (r == 0) {
         const int total = counters[1];
         if (total > cap && overflow) atomicOr(overflow, 1);
@@ -400,7 +416,7 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     SortScratch& sc = *static_cast<SortScratch*>(v.sort_scratch);
     v.depth_key_alt.ensure(n);
     v.order_alt.ensure(n);
-    v.counters.ensure(3);
+    v.counters.ensure(6);  // [0] n, [1] P (int scan), [2] min(P, cap), [4..5] P as u64
 
     // The culled set (key 0xFFFFFFFF: behind the near plane) and the depth keys depend on the
     // positions and the camera only; a non-PD projected covariance is a step error.
@@ -419,6 +435,14 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
         CUDA_LAUNCH_CHECK();
     }
     if (sync.projected) CUDA_CHECK(cudaEventRecord(sync.projected, s));
+    if (!v.raster.owns_rows()) {
+        // Multi-GPU: another rank owns this view; only its projection (flags for the
+        // replicated colour solve) is needed here. The depth order was not sorted.
+        v.order_version = 0;
+        v.pairs = 0;
+        v.valid = true;
+        return;
+    }
     if (n > 0) {
         StageScope st(NGS_STAGE_SORT, s, keep_order ? 4 : 11);  // sort 2 + 4 passes, fix-up, gather, scan 3
         // K2: global depth order, exactly (FP64 depth, kernel id): 4-pass radix sort of the
@@ -430,22 +454,26 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
                              sc, s);
             depth_tie_fixup(v.depth_key.ptr, v.order.ptr, v.depth.ptr, n, s);
         }
-        gather_counts_k<<<blocks_for(n), 256, 0, s>>>(n, v.order.ptr, v.tiles_touched.ptr, v.counts_sorted.ptr);
+        CUDA_CHECK(cudaMemsetAsync(v.counters.ptr + 4, 0, sizeof(unsigned long long), s));
+        gather_counts_k<<<blocks_for(n), 256, 0, s>>>(n, v.order.ptr, v.tiles_touched.ptr, v.counts_sorted.ptr,
+                                                      reinterpret_cast<unsigned long long*>(v.counters.ptr + 4));
         CUDA_LAUNCH_CHECK();
         exclusive_scan(v.counts_sorted.ptr, v.offsets.ptr, n, v.counters.ptr + 1, sc, s);
     } else {
-        CUDA_CHECK(cudaMemsetAsync(v.counters.ptr, 0, 3 * sizeof(int), s));
+        CUDA_CHECK(cudaMemsetAsync(v.counters.ptr, 0, 6 * sizeof(int), s));
     }
     // Pair capacity: exact (one host sync) or the slot's running capacity with a
     // device-side overflow flag (sync-free; the caller re-runs on overflow).
     size_t cap;
     if (sync.exact) {
-        int pairs = 0;
+        unsigned long long pairs = 0;
         if (n > 0) {
-            CUDA_CHECK(cudaMemcpyAsync(&pairs, v.counters.ptr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaMemcpyAsync(&pairs, v.counters.ptr + 4, sizeof(pairs), cudaMemcpyDeviceToHost, s));
             CUDA_CHECK(cudaStreamSynchronize(s));
         }
-        v.pairs = pairs;
+        if (pairs > static_cast<unsigned long long>(kMaxPairs))
+            throw Error(NGS_ERR_INVALID_INPUT, "render: (tile, splat) pair count exceeds 2^30 - 1 (sort limit)");
+        v.pairs = static_cast<int>(pairs);
         cap = static_cast<size_t>(pairs);
         v.pair_cap = std::max(v.pair_cap, cap + cap / 4 + 4096);
     } else {
@@ -453,6 +481,9 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
         if (v.pair_cap == 0) v.pair_cap = static_cast<size_t>(n) * 4 + 4096;
         cap = v.pair_cap;
     }
+    if (v.pairs > kMaxPairs)
+        throw Error(NGS_ERR_INVALID_INPUT, "render: (tile, splat) pair count exceeds 2^30 - 1 (sort limit)");
+    cap = std::min<size_t>(cap, static_cast<size_t>(kMaxPairs));
     CUDA_CHECK(cudaMemsetAsync(v.ranges.ptr, 0, sizeof(int2) * v.T, s));
     if (cap > 0 && n > 0) {
         StageScope st(NGS_STAGE_SORT, s, 4 + (bits + 7) / 8);  // emit, sort 2 + passes, ranges
@@ -462,7 +493,8 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
         v.pair_val_alt.ensure(cap);
         emit_pairs_k<<<blocks_for(n), 256, 0, s>>>(n, v.cam.tiles_x, static_cast<int>(cap), v.order.ptr,
                                                    v.offsets.ptr, v.rect.ptr, v.tiles_touched.ptr, v.pair_key.ptr,
-                                                   v.pair_val.ptr, sync.overflow, sync.pair_counter, v.counters.ptr);
+                                                   v.pair_val.ptr, sync.overflow, sync.pair_counter, v.counters.ptr,
+                                                   d_err);
         CUDA_LAUNCH_CHECK();
         // K4: stable sort of the depth-ordered pairs by tile key -> per-tile depth order.
         radix_sort_pairs(v.pair_key.ptr, v.pair_val.ptr, v.pair_key_alt.ptr, v.pair_val_alt.ptr, v.counters.ptr + 2,

@@ -166,11 +166,11 @@ def test_loss_fields_configs(gpu, window, sigma, lam):
 # K8: accumulated terms, K9: solves
 # ---------------------------------------------------------------------------
 
-def _views(lib_ctx, scene_fixture):
+def _views(lib_ctx, scene_fixture, loss=None):
     scene, cam, target, secs = scene_fixture
-    lib_ctx.build_view(0, cam, target)
+    lib_ctx.build_view(0, cam, target, loss=loss)
     for i, (c, t) in enumerate(secs):
-        lib_ctx.build_view(1 + i, c, t)
+        lib_ctx.build_view(1 + i, c, t, loss=loss)
     return list(range(1, 1 + len(secs)))
 
 
@@ -316,19 +316,24 @@ def test_trainer_step_variants(gpu, sh_degree, width, height, knn, order):
 # exactly what the NCCL all-reduce of the trainer computes across ranks.
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world,window", [(2, 11), (3, 11), (2, 21), (3, 21)])
 @pytest.mark.parametrize("attr", ATTRS)
-def test_sharded_accumulate_sums_to_full(gpu, newton_fixture, world, attr):
+def test_sharded_accumulate_sums_to_full(gpu, newton_fixture, world, window, attr):
+    """Window 21 needs a 20 px halo (2 tile rows of 16): the band must grow with the loss
+    window (ngs_dist_plan), or the owned rows next to a band edge read stale pixels."""
+    loss = gpu.default_loss()
+    loss.window = window
+    loss.window_sigma = 1.5 * window / 11
     full = gpu.context()
     full.set_scene(f32(newton_fixture[0]))
-    sec = _views(full, newton_fixture)
+    sec = _views(full, newton_fixture, loss)
     gf, hf, vf = full.accumulate(attr, 0, sec)
     gs, hs, vs = 0.0, 0.0, np.zeros_like(vf)
     for rank in range(world):
         c = gpu.context()
         c.set_scene(f32(newton_fixture[0]))
         c.set_shard(rank, world)
-        _views(c, newton_fixture)
+        _views(c, newton_fixture, loss)
         g, h, v = c.accumulate(attr, 0, sec)
         gs, hs, vs = gs + g, hs + h, vs | v
     assert np.array_equal(vs, vf)
@@ -378,8 +383,15 @@ def test_nccl_single_rank_step_matches_local(gpu):
         cfg.secondary_downsample = 2
         ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"], [], d["secondary"],
                               d["secondary_downsample"])
+        ctx.profile_reset()
         for v in (0, 2):
             ctx.trainer_step(v)
+        prof = ctx.profile_read()
+        if use_nccl:  # 4 accumulator all-reduces + 1 overflow vote per step
+            assert prof["allreduce_calls"] == 2 * 5, prof["allreduce_calls"]
+            assert prof["allreduce_bytes"] > 0
+        else:
+            assert prof["allreduce_calls"] == 0
         scenes.append(ctx.get_scene())
         ctx.close()
     for f in ("position", "scale", "quaternion", "sigma", "sh"):
