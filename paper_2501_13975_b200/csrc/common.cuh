@@ -93,6 +93,50 @@ struct ViewRecordsDev {
 
 enum RecordFlag : uint8_t { kProjected = 1, kClamp0 = 2, kClamp1 = 4, kClamp2 = 8 };
 
+// ---- order-independent scalar sums -------------------------------------------
+// Report scalars (loss sums, delta norms) are summed from per-block partials. With
+// FP64 atomics the result depends on block order; instead every partial is added
+// exactly into a 128-bit two's-complement fixed-point number (binary point 2^-88,
+// four 32-bit chunks in 64-bit counters: integer atomics are associative), so the
+// same partials give bitwise the same sum in any order. Word 4 flags a non-finite or
+// out-of-range (|x| >= 2^38) partial: the sum then reads as NaN (the trainer's
+// "non-finite update" abort, trainer.hpp:200-205).
+constexpr int kExactWords = 5;
+constexpr int kExactShift = 88;
+
+__device__ __forceinline__ void exact_add(unsigned long long* w, double x) {
+    if (x == 0.0) return;
+    if (!(fabs(x) < 0x1p38)) {
+        atomicOr(w + 4, 1ull);
+        return;
+    }
+    int e;
+    const double m = frexp(x, &e);                                  // |m| in [0.5, 1)
+    const long long mi = static_cast<long long>(ldexp(m, 53));       // exact
+    const int sh = e - 53 + kExactShift;                            // <= 73
+    __int128 v = static_cast<__int128>(mi);
+    v = sh >= 0 ? (v << sh) : (sh > -127 ? (v >> (-sh)) : (mi < 0 ? -1 : 0));  // truncation below 2^-88
+    const unsigned __int128 u = static_cast<unsigned __int128>(v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const unsigned long long chunk = static_cast<unsigned long long>((u >> (32 * i)) & 0xffffffffull);
+        if (chunk) atomicAdd(w + i, chunk);
+    }
+}
+
+// Host: the exact sum rounded once to FP64 (NaN if flagged).
+inline double exact_value(const unsigned long long* w) {
+    if (w[4]) return __builtin_nan("");
+    unsigned __int128 u = 0;
+    for (int q = 0; q < 4; ++q) u += static_cast<unsigned __int128>(w[q]) << (32 * q);
+    const bool neg = static_cast<__int128>(u) < 0;
+    if (neg) u = ~u + 1;
+    // long double keeps 64 significant bits: one rounding to it, then to double, is exact
+    // enough for a report scalar (the same bits on every run either way).
+    const long double mag = static_cast<long double>(u) * 0x1p-88L;
+    return static_cast<double>(neg ? -mag : mag);
+}
+
 // ---- small device math -----------------------------------------------------
 
 __host__ __device__ inline double mrow(const double* m, int r, int c) { return m[4 * r + c]; }

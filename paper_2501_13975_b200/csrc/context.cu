@@ -139,7 +139,7 @@ struct ngs_context {
     std::array<ViewSlot, NGS_MAX_VIEW_SLOTS + 1> slots;
     DevBuf<double> acc;
     DevBuf<int> err;
-    DevBuf<double> norm;
+    DevBuf<unsigned long long> norm;  // exact report sums, kExactWords per attribute
     DevBuf<unsigned long long> pairs;
     DevBuf<uint8_t> visible;
     DevBuf<double> out_delta;
@@ -596,7 +596,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         ctx->overflow.ensure(1);
         CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), ctx->stream));
         ctx->err.ensure(1);
-        ctx->norm.ensure(1);
+        ctx->norm.ensure(5 * kExactWords);
         ctx->pairs.ensure(5);
         CUDA_CHECK(cudaMemsetAsync(ctx->err.ptr, 0, sizeof(int), ctx->stream));
         CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 5 * sizeof(unsigned long long), ctx->stream));
@@ -707,7 +707,9 @@ int32_t ngs_render(ngs_context* ctx, const ngs_camera* camera, const ngs_raster_
         ProfInstall pi(ctx);
         CUDA_CHECK(cudaSetDevice(ctx->device));
         ViewSlot& v = ctx->slots[kScratchSlot];
-        upload_camera(*camera, v.cam);
+        // The trainer's own render path (same tile choice), so targets rendered here are the
+        // trainer's renders bit for bit (self-consistent fixtures, test_trainer.cpp:29-39).
+        upload_camera(*camera, v.cam, tile_for(ctx, *camera, false));
         v.raster = to_raster(options);  // ngs_render is never sharded (full image out)
         render_view(ctx->scene, v, false, ctx->err.ptr, ctx->stream);
         ctx->check_err();
@@ -733,9 +735,10 @@ int32_t ngs_build_view(ngs_context* ctx, int32_t slot, const ngs_camera* camera,
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         render_view(ctx->scene, v, true, ctx->err.ptr, ctx->stream);
         compute_loss(v, ctx->stream);
-        double sums[2];
-        CUDA_CHECK(cudaMemcpyAsync(sums, v.loss_sums.ptr, sizeof(sums), cudaMemcpyDeviceToHost, ctx->stream));
+        unsigned long long words[2 * kExactWords];
+        CUDA_CHECK(cudaMemcpyAsync(words, v.loss_sums.ptr, sizeof(words), cudaMemcpyDeviceToHost, ctx->stream));
         ctx->check_err();
+        const double sums[2] = {exact_value(words), exact_value(words + kExactWords)};
         const double inv3n = 1.0 / (3.0 * static_cast<double>(npx));
         v.loss_l2 = 0.5 * inv3n * sums[0];
         v.loss_ssim_sum = sums[1];
@@ -1094,17 +1097,18 @@ int32_t ngs_newton_step(ngs_context* ctx, ngs_attribute attr, int32_t primary_sl
         ctx->out_delta.ensure(stride * dsz);
         ctx->out_flags.ensure(2 * stride);
         SolveOutputs so{ctx->out_delta.ptr, ctx->out_flags.ptr, ctx->out_flags.ptr + stride, ctx->norm.ptr, ctx->err.ptr};
-        CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, sizeof(double), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, kExactWords * sizeof(unsigned long long), ctx->stream));
         CUDA_CHECK(cudaMemsetAsync(ctx->out_flags.ptr, 0, 2 * stride, ctx->stream));
         launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
                      color_views(ctx, views.data(), nv), sp, ctx->acc.ptr, stride, so, ctx->stream);
         std::vector<double> delta(stride * dsz);
         std::vector<uint8_t> fl(2 * stride);
-        double nsq = 0;
+        unsigned long long nsq_words[kExactWords];
         CUDA_CHECK(cudaMemcpyAsync(delta.data(), ctx->out_delta.ptr, sizeof(double) * delta.size(), cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_CHECK(cudaMemcpyAsync(fl.data(), ctx->out_flags.ptr, fl.size(), cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(&nsq, ctx->norm.ptr, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(nsq_words, ctx->norm.ptr, sizeof(nsq_words), cudaMemcpyDeviceToHost, ctx->stream));
         ctx->check_err();
+        const double nsq = exact_value(nsq_words);
         if (out) {
             if (out->delta) std::memcpy(out->delta, delta.data(), sizeof(double) * static_cast<size_t>(n) * dsz);
             if (out->accepted) std::memcpy(out->accepted, fl.data(), n);
@@ -1346,7 +1350,7 @@ float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
         T.adam_n = n;
         T.adam_t = 0;
     }
-    ctx->norm.ensure(5);
+    ctx->norm.ensure(5 * kExactWords);
     ViewSlot& v = T.views[0];
     const std::vector<int> none;
     CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
@@ -1361,7 +1365,7 @@ float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
         if (attempt >= 8) throw Error(NGS_ERR_INTERNAL, "pair capacity retry limit exceeded");
         v.pair_cap = std::max<size_t>(2 * v.pair_cap, 4096);
     }
-    CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), s));
+    CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * kExactWords * sizeof(unsigned long long), s));
     compute_pass_consts(kPassPosition, ctx->scene, v, v.cam, s);
     T.rot_consts.ensure(static_cast<size_t>(kRotConsts) * stride);
     compute_pass_consts(kPassRotation, ctx->scene, v, v.cam, s, T.rot_consts.ptr);
@@ -1386,8 +1390,10 @@ float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
     launch_first_order(ctx->scene, v.cam, v.flags.ptr, v.consts.ptr, T.rot_consts.ptr, ctx->acc.ptr, stride, fp,
                        T.adam_m.ptr, T.adam_v.ptr, ctx->norm.ptr, ctx->err.ptr, s);
     CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
-    CUDA_CHECK(cudaMemcpyAsync(norms, ctx->norm.ptr, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    unsigned long long words[5 * kExactWords];
+    CUDA_CHECK(cudaMemcpyAsync(words, ctx->norm.ptr, sizeof(words), cudaMemcpyDeviceToHost, s));
     ctx->check_err();
+    for (int a = 0; a < 5; ++a) norms[a] = exact_value(words + a * kExactWords);
     float ms = 0;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     return ms;
@@ -1431,7 +1437,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
         ngs_newton_options opts = T.cfg.newton;
         opts.barrier_weight = T.barrier_weight;
         const SolveParams base = to_solve(&opts, 1);
-        ctx->norm.ensure(5);
+        ctx->norm.ensure(5 * kExactWords);
         cudaStream_t s = ctx->stream;
         // Parameter snapshot: restored if a sync-free render overflowed its pair capacity.
         ctx->snap_ps.ensure(stride);
@@ -1454,7 +1460,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
             };
             ++ctx->pos_version;  // step start / snapshot restore
             CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
-            CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * sizeof(double), s));
+            CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * kExactWords * sizeof(unsigned long long), s));
             CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
             mark(-1);
             // Renders are chained per view into the next backward pass (no join in between);
@@ -1472,7 +1478,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                     rendered = false;
                     mark(1 + (pass == kPassPositionUV ? kPassPosition : pass));
                 }
-                SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr, ctx->err.ptr};
+                SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr * kExactWords, ctx->err.ptr};
                 if (attr == NGS_POSITION) ++ctx->pos_version;  // the next renders re-sort by depth
                 launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
                              color_views(ctx, views.data(), nv), base, ctx->acc.ptr, stride, so, s);
@@ -1486,10 +1492,12 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
             CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
             ctx->vote_overflow();
             int overflow = 0;
-            CUDA_CHECK(cudaMemcpyAsync(norms, ctx->norm.ptr, sizeof(norms), cudaMemcpyDeviceToHost, s));
+            unsigned long long nwords[5 * kExactWords];
+            CUDA_CHECK(cudaMemcpyAsync(nwords, ctx->norm.ptr, sizeof(nwords), cudaMemcpyDeviceToHost, s));
             CUDA_CHECK(cudaMemcpyAsync(&overflow, ctx->overflow.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
             ctx->check_err();
             CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            for (int a = 0; a < 5; ++a) norms[a] = exact_value(nwords + a * kExactWords);
             if (!overflow) {
                 for (size_t m = 1; m < marks.size(); ++m) {
                     float gms = 0;
@@ -1533,9 +1541,10 @@ namespace {
 void metrics_of_slot(ngs_context* ctx, ViewSlot& v, const ngs_loss_config& lc, ngs_metrics* out) {
     v.loss = to_loss(&lc);
     compute_loss_value(v, ctx->stream);
-    double sums[2];
-    CUDA_CHECK(cudaMemcpyAsync(sums, v.loss_sums.ptr, sizeof(sums), cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long words[2 * kExactWords];
+    CUDA_CHECK(cudaMemcpyAsync(words, v.loss_sums.ptr, sizeof(words), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->check_err();
+    const double sums[2] = {exact_value(words), exact_value(words + kExactWords)};
     const double n3 = 3.0 * static_cast<double>(v.W) * v.H;
     const double mse = sums[0] / n3;
     out->loss = 0.5 * mse + (lc.lambda != 0.0 ? lc.lambda * (1.0 - sums[1] / n3) : 0.0);
@@ -1826,7 +1835,8 @@ int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int
         DevBuf<float4> ps, sc, q;
         DevBuf<float> sh;
         DevBuf<uint8_t> flags;
-        DevBuf<double> apos, arot, asc, aoc, norm;
+        DevBuf<double> apos, arot, asc, aoc;
+        DevBuf<unsigned long long> norm;
         DevBuf<int> err;
         ps.ensure(stride);
         sc.ensure(stride);
@@ -1837,7 +1847,7 @@ int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int
         arot.ensure(kAccRotation * stride);
         asc.ensure(kAccScaling * stride);
         aoc.ensure(static_cast<size_t>(views) * kAccOpColor * stride);
-        norm.ensure(1);
+        norm.ensure(kExactWords);
         err.ensure(1);
         SceneDev sd{};
         sd.n = n;
@@ -1861,21 +1871,45 @@ int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int
             upload_camera(mb_camera(v, std::max(views, 2)), cv.cam[v]);
             cv.flags[v] = flags.ptr + static_cast<size_t>(v) * stride;
         }
-        const SolveParams sp = to_solve(nullptr, 0);
+        // Every timed launch solves AND commits (newton.hpp:817-844) all n Gaussians. The
+        // parameters are restored from a snapshot between launches (outside the events), so
+        // every repetition does identical work on identical inputs.
+        const SolveParams sp = to_solve(nullptr, 1);
         SolveOutputs so{nullptr, nullptr, nullptr, norm.ptr, err.ptr};
         const double* accs[5] = {apos.ptr, arot.ptr, asc.ptr, aoc.ptr, aoc.ptr};
+        DevBuf<float4> ps0, sc0, q0;
+        DevBuf<float> sh0;
+        ps0.ensure(stride);
+        sc0.ensure(stride);
+        q0.ensure(stride);
+        sh0.ensure(48 * stride);
+        CUDA_CHECK(cudaMemcpyAsync(ps0.ptr, ps.ptr, sizeof(float4) * stride, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(sc0.ptr, sc.ptr, sizeof(float4) * stride, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(q0.ptr, q.ptr, sizeof(float4) * stride, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(sh0.ptr, sh.ptr, sizeof(float) * 48 * stride, cudaMemcpyDeviceToDevice, s));
+        auto restore = [&] {
+            CUDA_CHECK(cudaMemcpyAsync(ps.ptr, ps0.ptr, sizeof(float4) * stride, cudaMemcpyDeviceToDevice, s));
+            CUDA_CHECK(cudaMemcpyAsync(sc.ptr, sc0.ptr, sizeof(float4) * stride, cudaMemcpyDeviceToDevice, s));
+            CUDA_CHECK(cudaMemcpyAsync(q.ptr, q0.ptr, sizeof(float4) * stride, cudaMemcpyDeviceToDevice, s));
+            CUDA_CHECK(cudaMemcpyAsync(sh.ptr, sh0.ptr, sizeof(float) * 48 * stride, cudaMemcpyDeviceToDevice, s));
+        };
         for (int a = 0; a < 5; ++a) {
             // warm-up, then reps timed launches
             launch_solve(a, sd, cv.cam[0], 0.3, cv.flags[0], cv, sp, accs[a], stride, so, s);
-            CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
-            for (int r = 0; r < reps; ++r)
+            double total = 0;
+            for (int r = 0; r < reps; ++r) {
+                restore();
+                CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
                 launch_solve(a, sd, cv.cam[0], 0.3, cv.flags[0], cv, sp, accs[a], stride, so, s);
-            CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
-            CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
-            float ms = 0;
-            CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-            ms_out[a] = ms / reps;
+                CUDA_CHECK(cudaEventRecord(ctx->ev1, s));
+                CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
+                float ms = 0;
+                CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+                total += ms;
+            }
+            ms_out[a] = total / reps;
         }
+        restore();
         ctx->check_err();
     });
 }

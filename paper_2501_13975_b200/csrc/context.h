@@ -132,7 +132,7 @@ struct ViewSlot {
     DevBuf<double> target;  // planar [3][H][W], FP64 like the reference Image
     DevBuf<double> fields;  // 9 center fields x 3 channels x H x W
     DevBuf<float> loss_grad, loss_hess;  // planar [3][H][W]
-    DevBuf<double> loss_sums;            // [0] sum d^2, [1] sum ssim
+    DevBuf<unsigned long long> loss_sums;  // exact sums (kExactWords each): [0] sum d^2, [1] sum ssim
     // Per-pass backward constants (per kernel, AoS)
     DevBuf<float> consts;
 

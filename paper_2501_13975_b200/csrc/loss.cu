@@ -105,7 +105,7 @@ __device__ __forceinline__ double ssim_value_only(const double (&st)[5], double 
 // Sum of squared differences of two planar images (the L2 part of
 // total_loss_value and the PSNR numerator, loss.hpp:363-368, metrics.hpp:16-20).
 __global__ void __launch_bounds__(256) l2_sum_k(const double* __restrict__ a, const double* __restrict__ b, size_t n,
-                                                double* __restrict__ sum) {
+                                                unsigned long long* __restrict__ sum) {
     __shared__ double red[8];
     double acc = 0.0;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) l2_sum_k(const double* __restrict__ a, co
         acc += d * d;
     }
     const double tot = block_sum(acc, red);
-    if (threadIdx.x == 0) atomicAdd(sum, tot);
+    if (threadIdx.x == 0) exact_add(sum, tot);
 }
 
 // Separable valid-tap convolutions over a (kLT + 2h)^2 shared-memory halo tile.
@@ -161,7 +161,7 @@ __device__ __forceinline__ void hpass(int h, int span, In in, Out out, WSel wsel
 template <int HT>
 __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double* __restrict__ image,
                                                      const double* __restrict__ target, Window win, double c1, double c2,
-                                                     double* __restrict__ fields, double* __restrict__ sums, int row0,
+                                                     double* __restrict__ fields, unsigned long long* __restrict__ sums, int row0,
                                                      int own_y0, int own_y1) {
     constexpr int SP = SsimGeom<HT>::SP;
     __shared__ double s_x[SP][SP + 1], s_t[SP][SP + 1];
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256) ssim_fields_k(int W, int H, const double*
     }
     const bool own = y >= own_y0 && y < own_y1;  // owned pixel rows (multi-GPU shard)
     const double tot = block_sum(own ? ssim : 0.0, red);
-    if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
+    if (threadIdx.x == 0) exact_add(sums + kExactWords, tot);
 }
 
 // Kernel B: convolve the 9 centre fields (three per shared-memory round) and
@@ -256,7 +256,7 @@ template <int HT>
 __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double* __restrict__ image,
                                                      const double* __restrict__ target, Window win, double lambda,
                                                      const double* __restrict__ fields, float* __restrict__ grad,
-                                                     float* __restrict__ hess, double* __restrict__ sums, int row0,
+                                                     float* __restrict__ hess, unsigned long long* __restrict__ sums, int row0,
                                                      int own_y0, int own_y1) {
     constexpr int SP = SsimGeom<HT>::SP;
     __shared__ double s_f[3][SP][SP + 1];
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) ssim_derivs_k(int W, int H, const double*
     }
     const bool own = y >= own_y0 && y < own_y1;
     const double tot = block_sum(own ? dsq : 0.0, red);
-    if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
+    if (threadIdx.x == 0) exact_add(sums, tot);
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -391,7 +391,7 @@ __device__ __forceinline__ void vpass32(const Window& win, bool w2, const double
 __global__ void __launch_bounds__(256, NGS_SSIMF_MINB) ssim_fields32_k(int W, int H, const double* __restrict__ image,
                                                        const double* __restrict__ target, Window win, double c1,
                                                        double c2, double* __restrict__ fields,
-                                                       double* __restrict__ sums, int row0, int own_y0, int own_y1) {
+                                                       unsigned long long* __restrict__ sums, int row0, int own_y0, int own_y1) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [5][kFS][kFT + 1]
     __shared__ double red[8];
@@ -462,13 +462,13 @@ __global__ void __launch_bounds__(256, NGS_SSIMF_MINB) ssim_fields32_k(int W, in
         }
     }
     const double tot = block_sum(ssim_own, red);
-    if (threadIdx.x == 0) atomicAdd(&sums[1], tot);
+    if (threadIdx.x == 0) exact_add(sums + kExactWords, tot);
 }
 
 __global__ void __launch_bounds__(256, NGS_SSIMD_MINB) ssim_derivs32_k(int W, int H, const double* __restrict__ image,
                                                        const double* __restrict__ target, Window win, double lambda,
                                                        const double* __restrict__ fields, float* __restrict__ grad,
-                                                       float* __restrict__ hess, double* __restrict__ sums, int row0,
+                                                       float* __restrict__ hess, unsigned long long* __restrict__ sums, int row0,
                                                        int own_y0, int own_y1) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [1][kFS][kFT + 1], then s_f [2][kFS][kFS + 1]
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(256, NGS_SSIMD_MINB) ssim_derivs32_k(int W, in
         hess[idx] = static_cast<float>(hh);
     }
     const double tot = block_sum(dsq_own, red);
-    if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
+    if (threadIdx.x == 0) exact_add(sums, tot);
 }
 
 }  // namespace
@@ -586,8 +586,8 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     const size_t npx = static_cast<size_t>(v.W) * v.H;
     v.loss_grad.ensure(3 * npx);
     v.loss_hess.ensure(3 * npx);
-    v.loss_sums.ensure(2);
-    CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * sizeof(double), s));
+    v.loss_sums.ensure(2 * kExactWords);
+    CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * kExactWords * sizeof(unsigned long long), s));
     // Shard bands are in tile rows of the view's tile size; the loss grid uses 16-row blocks.
     const int t = v.cam.tile;
     const int band_px0 = std::max(0, v.raster.band_y0) * t, band_px1 = std::min(v.H, v.raster.band_y1 * t);
@@ -650,8 +650,8 @@ void compute_loss_value(ViewSlot& v, cudaStream_t s) {
         win.w2[i] = win.w[i] * win.w[i];
     }
     const size_t npx = static_cast<size_t>(v.W) * v.H;
-    v.loss_sums.ensure(2);
-    CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * sizeof(double), s));
+    v.loss_sums.ensure(2 * kExactWords);
+    CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * kExactWords * sizeof(unsigned long long), s));
     StageScope st(NGS_STAGE_LOSS, s, 2);
     l2_sum_k<<<std::min<size_t>((3 * npx + 255) / 256, 4 * 148), 256, 0, s>>>(v.image.ptr, v.target.ptr, 3 * npx,
                                                                            v.loss_sums.ptr);

@@ -22,7 +22,7 @@ namespace {
 
 inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 
-__device__ __forceinline__ void block_add(double v, double* target) {
+__device__ __forceinline__ void block_add(double v, unsigned long long* target) {
     __shared__ double red[8];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -31,7 +31,7 @@ __device__ __forceinline__ void block_add(double v, double* target) {
     if (threadIdx.x == 0) {
         double t = 0;
         for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
-        if (t != 0.0) atomicAdd(target, t);
+        exact_add(target, t);  // order-independent: the report's norms are bitwise reproducible
     }
 }
 
@@ -121,7 +121,11 @@ __global__ void __launch_bounds__(256) solve_rotation_k(SceneDev s, CameraDev pr
         if (out.delta) out.delta[k] = theta;
         if (out.accepted) out.accepted[k] = 1;
         nsq = theta * theta;
-        if (sp.commit) {  // commit_rotation newton.hpp:822-826
+        // commit_rotation newton.hpp:822-826: q <- normalize(dq (x) q). A rotation too small to
+        // move the FP32-stored quaternion (dq (x) q rounds back to q, e.g. theta ~ 1e-14 at a fixed
+        // point) leaves it bit for bit: renormalising the FP32-rounded q alone would move it by an
+        // ulp, which the reference's FP64 q (unit to 1e-16) never sees.
+        if (sp.commit) {
             const double c = cos(theta), sn = sin(theta);
             const double a0 = c, a1 = sn * r.x, a2 = sn * r.y, a3 = sn * r.z;
             const float4 q = s.quat[k];
@@ -130,6 +134,7 @@ __global__ void __launch_bounds__(256) solve_rotation_k(SceneDev s, CameraDev pr
             double x = a0 * b1 + a1 * b0 + a2 * b3 - a3 * b2;
             double y = a0 * b2 - a1 * b3 + a2 * b0 + a3 * b1;
             double z = a0 * b3 + a1 * b2 - a2 * b1 + a3 * b0;
+            const bool moved = (float)w != q.x || (float)x != q.y || (float)y != q.z || (float)z != q.w;
             const double nq = sqrt(w * w + x * x + y * y + z * z);
             if (!(nq > 0.0) || !isfinite(nq)) {
                 atomicOr(out.err, 4);
@@ -139,7 +144,8 @@ __global__ void __launch_bounds__(256) solve_rotation_k(SceneDev s, CameraDev pr
                 y /= nq;
                 z /= nq;
             }
-            s.quat[k] = make_float4((float)w, (float)x, (float)y, (float)z);
+            if (moved || !(nq > 0.0) || !isfinite(nq))
+                s.quat[k] = make_float4((float)w, (float)x, (float)y, (float)z);
         }
     }
     block_add(nsq, out.norm_sq);
@@ -676,7 +682,7 @@ __global__ void __launch_bounds__(128) first_order_k(SceneDev s, CameraDev cam, 
                                                      const float* __restrict__ pcst, const float* __restrict__ rcst,
                                                      const double* __restrict__ acc, size_t stride, FirstOrderParams p,
                                                      double* __restrict__ am, double* __restrict__ av,
-                                                     double* __restrict__ norms, int* err) {
+                                                     unsigned long long* __restrict__ norms, int* err) {
     using L = PosLayout<3>;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     double nsq[5] = {0, 0, 0, 0, 0};
@@ -759,6 +765,7 @@ __global__ void __launch_bounds__(128) first_order_k(SceneDev s, CameraDev cam, 
             double x = a0 * b1 + a1 * b0 + a2 * b3 - a3 * b2;
             double y = a0 * b2 - a1 * b3 + a2 * b0 + a3 * b1;
             double z = a0 * b3 + a1 * b2 - a2 * b1 + a3 * b0;
+            const bool moved = (float)w != qq.x || (float)x != qq.y || (float)y != qq.z || (float)z != qq.w;
             const double nq = sqrt(w * w + x * x + y * y + z * z);
             if (!(nq > 0.0) || !isfinite(nq)) {
                 atomicOr(err, 4);
@@ -768,7 +775,8 @@ __global__ void __launch_bounds__(128) first_order_k(SceneDev s, CameraDev cam, 
                 y /= nq;
                 z /= nq;
             }
-            s.quat[k] = make_float4((float)w, (float)x, (float)y, (float)z);
+            if (moved || !(nq > 0.0) || !isfinite(nq))  // see solve_rotation_k
+                s.quat[k] = make_float4((float)w, (float)x, (float)y, (float)z);
         }
         nsq[NGS_ROTATION] = dth * dth;
         {
@@ -800,14 +808,14 @@ __global__ void __launch_bounds__(128) first_order_k(SceneDev s, CameraDev cam, 
         }
     }
 #pragma unroll
-    for (int a = 0; a < 5; ++a) block_add(nsq[a], norms + a);
+    for (int a = 0; a < 5; ++a) block_add(nsq[a], norms + a * kExactWords);
 }
 
 }  // namespace
 
 void launch_first_order(const SceneDev& scene, const CameraDev& cam, const uint8_t* flags, const float* pos_consts,
                         const float* rot_consts, const double* acc, size_t stride, const FirstOrderParams& p,
-                        double* adam_m, double* adam_v, double* norms, int* err, cudaStream_t s) {
+                        double* adam_m, double* adam_v, unsigned long long* norms, int* err, cudaStream_t s) {
     const int n = scene.n;
     if (n == 0) return;
     StageScope st(NGS_STAGE_SOLVE, s);

@@ -20,7 +20,7 @@ struct SolveOutputs {
     double* delta;        // optional, layout of ngs_solve_result::delta
     uint8_t* accepted;    // optional
     uint8_t* degenerate;  // optional
-    double* norm_sq;      // required: device accumulator of the report's delta norm
+    unsigned long long* norm_sq;  // required: exact (kExactWords) accumulator of the report's delta norm
     int* err;             // device error bits
 };
 
@@ -46,7 +46,7 @@ struct FirstOrderParams {
 // with this view's ray as axis; adam_m / adam_v: [56][stride] doubles (slot-major).
 void launch_first_order(const SceneDev& scene, const CameraDev& cam, const uint8_t* flags, const float* pos_consts,
                         const float* rot_consts, const double* acc, size_t stride, const FirstOrderParams& p,
-                        double* adam_m, double* adam_v, double* norms, int* err, cudaStream_t s);
+                        double* adam_m, double* adam_v, unsigned long long* norms, int* err, cudaStream_t s);
 
 void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, double lambda_lp,
                   const uint8_t* primary_flags, const ColorViews& cv, const SolveParams& sp, const double* acc,

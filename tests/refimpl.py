@@ -134,3 +134,14 @@ def rel_error(a, b, floor=1e-9):
     b = np.asarray(b, np.float64)
     scale = np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)
     return np.abs(a - b) / scale
+
+
+def accept_raster_scene(trial: int):
+    """Scene + 64x64 camera of acceptance criterion 2's trial `trial` (acceptance.cpp:67-99)."""
+    L = ref()
+    cnt = C.c_int32()
+    L.check(L.lib.ngsref_accept_raster_scene(C.c_int32(trial), None, None, C.byref(cnt)))
+    s, cs = _scene_struct(cnt.value)
+    cam = ngs_camera()
+    L.check(L.lib.ngsref_accept_raster_scene(C.c_int32(trial), C.byref(cs), C.byref(cam), C.byref(cnt)))
+    return _finish(s, cs), camera_from_c(cam)
