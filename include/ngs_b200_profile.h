@@ -51,6 +51,17 @@ typedef struct {
     int64_t allreduce_bytes;
 } ngs_profile_stats;
 
+/* Timeline of the concurrent schedule (views NOT serialised): one row per stage
+ * bracket (a kernel or a short kernel sequence) with its stream and device times in
+ * ms relative to the first bracket recorded after ngs_profile_timeline(ctx, 1). */
+typedef struct {
+    int32_t stage;
+    int32_t stream;  /* opaque stream id */
+    float start_ms, end_ms;
+} ngs_timeline_row;
+int32_t ngs_profile_timeline(ngs_context* ctx, int32_t on);
+int32_t ngs_profile_read_timeline(ngs_context* ctx, ngs_timeline_row* rows, int32_t capacity, int32_t* n_rows);
+
 int32_t ngs_profile_enable(ngs_context* ctx, int32_t on);
 int32_t ngs_profile_reset(ngs_context* ctx);
 int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out);

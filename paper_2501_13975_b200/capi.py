@@ -496,6 +496,20 @@ class Context:
                     group_ms=dict(zip(("render", "render+bwd_position", "render+bwd_rotation", "render+bwd_scaling",
                                        "render+bwd_opacity_color", "solve"), list(st.group_ms))))
 
+    def profile_timeline(self, on: bool = True):
+        """Per-launch events on the concurrent schedule (views not serialised)."""
+        self._call("ngs_profile_timeline", C.c_int32(1 if on else 0))
+
+    def read_timeline(self) -> list:
+        """[(stage name, stream id, start_ms, end_ms)] since profile_timeline(True)."""
+        class Row(C.Structure):
+            _fields_ = [("stage", C.c_int32), ("stream", C.c_int32), ("start_ms", C.c_float), ("end_ms", C.c_float)]
+        n = C.c_int32()
+        self._call("ngs_profile_read_timeline", None, C.c_int32(0), C.byref(n))
+        rows = (Row * max(n.value, 1))()
+        self._call("ngs_profile_read_timeline", rows, C.c_int32(n.value), C.byref(n))
+        return [(STAGES[r.stage], r.stream, r.start_ms, r.end_ms) for r in rows[: n.value]]
+
     def set_tile_size(self, tile: int):
         self._call("ngs_set_tile_size", C.c_int32(tile))
 

@@ -1554,7 +1554,7 @@ void metrics_of_slot(ngs_context* ctx, ViewSlot& v, const ngs_loss_config& lc, n
 
 void render_scratch(ngs_context* ctx, const ngs_camera& cam, const ngs_raster_options* ro) {
     ViewSlot& v = ctx->slots[kScratchSlot];
-    upload_camera(cam, v.cam);
+    upload_camera(cam, v.cam, tile_for(ctx, cam, false));  // the same render path as ngs_render / the trainer
     v.raster = to_raster(ro);
     render_view(ctx->scene, v, false, ctx->err.ptr, ctx->stream);
 }
@@ -1704,6 +1704,27 @@ extern "C" {
 
 int32_t ngs_profile_enable(ngs_context* ctx, int32_t on) {
     return guarded([&] { ctx->prof.enabled = on != 0; });
+}
+
+int32_t ngs_profile_timeline(ngs_context* ctx, int32_t on) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->prof.reset();
+        ctx->prof.timeline = on != 0;
+        if (on) {
+            CUDA_CHECK(cudaEventCreate(&ctx->prof.origin));
+            CUDA_CHECK(cudaEventRecord(ctx->prof.origin, ctx->stream));
+        }
+    });
+}
+
+int32_t ngs_profile_read_timeline(ngs_context* ctx, ngs_timeline_row* rows, int32_t capacity, int32_t* n_rows) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->prof.resolve();
+        *n_rows = static_cast<int32_t>(ctx->prof.rows.size());
+        for (int i = 0; i < std::min<int>(capacity, *n_rows); ++i) rows[i] = ctx->prof.rows[i];
+    });
 }
 
 int32_t ngs_profile_reset(ngs_context* ctx) {

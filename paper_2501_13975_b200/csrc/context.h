@@ -143,11 +143,18 @@ struct ViewSlot {
 // the calling thread is installed by each C-ABI entry point.
 struct Profiler {
     bool enabled = false;
+    // Timeline mode: per-launch events WITHOUT serialising the views (the concurrent
+    // schedule as executed); resolve() also keeps (stage, stream, start, end) rows,
+    // relative to `origin`, for ngs_profile_timeline.
+    bool timeline = false;
+    cudaEvent_t origin = nullptr;
     struct Rec {
         int stage;
         cudaEvent_t a, b;
+        cudaStream_t s;
     };
     std::vector<Rec> pending;
+    std::vector<ngs_timeline_row> rows;
     std::vector<cudaEvent_t> pool;
     ngs_profile_stats stats{};
 
@@ -167,6 +174,13 @@ struct Profiler {
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
             stats.ms[r.stage] += ms;
+            if (timeline && origin) {
+                float t0 = 0, t1 = 0;
+                CUDA_CHECK(cudaEventElapsedTime(&t0, origin, r.a));
+                CUDA_CHECK(cudaEventElapsedTime(&t1, origin, r.b));
+                rows.push_back(ngs_timeline_row{r.stage, static_cast<int32_t>(reinterpret_cast<uintptr_t>(r.s) & 0x7fffffff),
+                                                t0, t1});
+            }
             pool.push_back(r.a);
             pool.push_back(r.b);
         }
@@ -175,6 +189,9 @@ struct Profiler {
     void reset() {
         resolve();
         stats = ngs_profile_stats{};
+        rows.clear();
+        if (origin) cudaEventDestroy(origin);
+        origin = nullptr;
     }
     ~Profiler() {
         for (auto& r : pending) {
@@ -197,7 +214,7 @@ struct StageScope {
         if (!p) return;
         p->stats.launches[stage] += launches;
         p->stats.total_launches += launches;
-        if (p->enabled) {
+        if (p->enabled || p->timeline) {
             a = p->get();
             CUDA_CHECK(cudaEventRecord(a, s));
         }
@@ -205,7 +222,7 @@ struct StageScope {
     ~StageScope() {
         if (!p || !a) return;
         cudaEvent_t b = p->get();
-        if (cudaEventRecord(b, s) == cudaSuccess) p->pending.push_back({stage, a, b});
+        if (cudaEventRecord(b, s) == cudaSuccess) p->pending.push_back({stage, a, b, s});
     }
 };
 

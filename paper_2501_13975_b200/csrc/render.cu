@@ -207,9 +207,17 @@ __global__ void gather_counts_k(int n, const int* order, const int* tiles_touche
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int c = r < n ? tiles_touched[order[r]] : 0;
     if (r < n) counts_sorted[r] = c;
+    // one atomic per block (a per-warp atomic on one address serialises ~n/32 updates)
+    __shared__ unsigned long long red[8];
     unsigned long long w = static_cast<unsigned long long>(c);
     for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-    if ((threadIdx.x & 31) == 0 && w) atomicAdd(total64, w);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) t += red[i];
+        if (t) atomicAdd(total64, t);
+    }
 }
 
 // K3: emit (tile, kernel) pairs in depth order; a later stable sort on the
