@@ -38,8 +38,14 @@ inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 // Two blocks per 128 Gaussians (blockIdx.y): 0 = pixel / Sigma derivatives
 // (JS, HPI, SCD), 1 = SH colour derivatives (JC, HC); halves the FP64 live
 // state per thread. Rows are staged in shared memory and stored coalesced.
+// Resident blocks per SM of the position constants (the FP64 chain is latency-bound: 6
+// blocks at 80 registers, with a little spill, beat 1 block-bound 124 registers: c3 consts
+// 4.26 -> 3.43 ms per step).
+#ifndef NGS_PCONST_MINB
+#define NGS_PCONST_MINB 6
+#endif
 template <int ND, int PART>
-__global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev cam, CameraDev primary,
+__global__ void __launch_bounds__(128, NGS_PCONST_MINB) position_consts_k(SceneDev s, CameraDev cam, CameraDev primary,
                                                          const uint8_t* flags, float* out) {
     using L = PosLayout<ND>;
     constexpr int RS = (L::JC > L::N - L::JC ? L::JC : L::N - L::JC) + 1;  // staged row stride (floats)
@@ -215,73 +221,74 @@ __global__ void __launch_bounds__(128) position_consts_k(SceneDev s, CameraDev c
                     }
             }
         } else {
-            // SH colour derivatives through r(p) (view_direction_derivatives camera.hpp:79-104).
+            // SH colour derivatives through r(p) (view_direction_derivatives camera.hpp:79-104,
+            // sh_color_derivs_wrt_position sh.hpp:134-161), taken directly along the ND
+            // directions: with u_a = (dr/dp) D[a] = (D[a] - r (r . D[a])) / n,
+            //   dc/dp . D[a]        = g . u_a,
+            //   D[a]^T d2c/dp2 D[b] = u_a^T H u_b + g . v_ab / n^2,
+            //   v_ab = 3 r (r.D[a])(r.D[b]) - D[a] (r.D[b]) - D[b] (r.D[a]) - r (D[a].D[b]),
+            // where (g, H) are the gradient / Hessian of sum_i c_i Phi_i(r) in r. v_ab and u_a
+            // do not depend on the channel; the clamp of each channel is the projection's
+            // (flags: zero subgradient when clamped, sh.hpp:144-147).
             D3 r;
             double n;
-            double Jc[3][3] = {}, Hc[3][6] = {};
+            double jdir[3][ND] = {}, hdir[3][ND * (ND + 1) / 2] = {};
             if (view_direction(cam, p, r, n)) {
                 const double rv[3] = {r.x, r.y, r.z};
-                double jac[3][3];
-        #pragma unroll
-                for (int i = 0; i < 3; ++i)
-            #pragma unroll
-                    for (int j = 0; j < 3; ++j) jac[i][j] = ((i == j ? 1.0 : 0.0) - rv[i] * rv[j]) / n;
-                const double inv_n2 = 1.0 / (n * n);
-                double basis[16];
-                sh_basis(r, s.sh_degree, basis);
-        #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    double c[16];
-                    double v = 0;
+                const double inv_n = 1.0 / n, inv_n2 = inv_n * inv_n;
+                double rd[ND], ua[ND][3];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        c[i] = i < s.n_coeffs ? static_cast<double>(s.sh[(16 * ch + i) * s.n + k]) : 0.0;
-                        v += basis[i] * c[i];
-                    }
-                    v += kColorOffset;
-                    if (v <= 0.0) continue;  // clamped: zero subgradient (sh.hpp:144-147)
+                for (int a = 0; a < ND; ++a) {
+                    rd[a] = rv[0] * D[a][0] + rv[1] * D[a][1] + rv[2] * D[a][2];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) ua[a][i] = (D[a][i] - rv[i] * rd[a]) * inv_n;
+                }
+                double vab[ND * (ND + 1) / 2][3];
+                {
+                    int pp = 0;
+#pragma unroll
+                    for (int a = 0; a < ND; ++a)
+#pragma unroll
+                        for (int b = a; b < ND; ++b, ++pp) {
+                            const double dd = D[a][0] * D[b][0] + D[a][1] * D[b][1] + D[a][2] * D[b][2];
+#pragma unroll
+                            for (int i = 0; i < 3; ++i)
+                                vab[pp][i] = (3.0 * rv[i] * rd[a] * rd[b] - D[a][i] * rd[b] - D[b][i] * rd[a] -
+                                              rv[i] * dd) * inv_n2;
+                        }
+                }
+                const uint8_t fl = flags[k];
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    if (fl & (kClamp0 << ch)) continue;
+                    double c[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) c[i] = i < s.n_coeffs ? static_cast<double>(s.sh[(16 * ch + i) * s.n + k]) : 0.0;
                     double gr[3], hr[6];
                     sh_contract_derivs(r, s.sh_degree, c, gr, hr);
-            #pragma unroll
-                    for (int j = 0; j < 3; ++j) Jc[ch][j] = jac[0][j] * gr[0] + jac[1][j] * gr[1] + jac[2][j] * gr[2];
-            #pragma unroll
-                    for (int a = 0; a < 3; ++a)
-                #pragma unroll
-                        for (int b = a; b < 3; ++b) {
-                            double acc = 0;
-                    #pragma unroll
-                            for (int i = 0; i < 3; ++i)
-                        #pragma unroll
-                                for (int j = 0; j < 3; ++j) acc += jac[i][a] * hr[sym3(i, j)] * jac[j][b];
-                    #pragma unroll
-                            for (int i = 0; i < 3; ++i) {
-                                double hv = 3.0 * rv[i] * rv[a] * rv[b];
-                                if (i == a) hv -= rv[b];
-                                if (i == b) hv -= rv[a];
-                                if (a == b) hv -= rv[i];
-                                acc += gr[i] * hv * inv_n2;
-                            }
-                            Hc[ch][sym3(a, b)] = acc;
-                        }
+#pragma unroll
+                    for (int a = 0; a < ND; ++a) jdir[ch][a] = gr[0] * ua[a][0] + gr[1] * ua[a][1] + gr[2] * ua[a][2];
+                    int pp = 0;
+#pragma unroll
+                    for (int a = 0; a < ND; ++a) {
+                        double hu[3];  // H u_a
+#pragma unroll
+                        for (int i = 0; i < 3; ++i)
+                            hu[i] = hr[sym3(i, 0)] * ua[a][0] + hr[sym3(i, 1)] * ua[a][1] + hr[sym3(i, 2)] * ua[a][2];
+#pragma unroll
+                        for (int b = a; b < ND; ++b, ++pp)
+                            hdir[ch][pp] = hu[0] * ua[b][0] + hu[1] * ua[b][1] + hu[2] * ua[b][2] +
+                                           gr[0] * vab[pp][0] + gr[1] * vab[pp][1] + gr[2] * vab[pp][2];
+                    }
                 }
             }
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-                double jd[ND];
 #pragma unroll
-                for (int a = 0; a < ND; ++a) {
-                    jd[a] = d1(Jc[ch], 1, a);
-                    o[L::jc(ch, a) - L::JC] = static_cast<float>(jd[a]);
-                }
-                int p = 0;
+                for (int a = 0; a < ND; ++a) o[L::jc(ch, a) - L::JC] = static_cast<float>(jdir[ch][a]);
 #pragma unroll
-                for (int a = 0; a < ND; ++a)
-#pragma unroll
-                    for (int b = a; b < ND; ++b, ++p) {
-                        o[L::hc(ch, p) - L::JC] = static_cast<float>(d2(Hc[ch], 1, a, b));
-                    }
+                for (int pp = 0; pp < ND * (ND + 1) / 2; ++pp) o[L::hc(ch, pp) - L::JC] = static_cast<float>(hdir[ch][pp]);
             }
-
         }
     }
     __syncthreads();

@@ -1275,12 +1275,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     const int nv = 1 + static_cast<int>(nbrs.size());
     // Profiling serialises the views so per-launch event times do not overlap.
     const bool concurrent = !ctx->prof.enabled;
-    if (concurrent) ctx->fork(nv, ctx->vr.data());
-    // Target uploads go to the copy stream (primary first, it is the largest), so
-    // the host->device copies overlap projection, sorting and rasterisation; each
-    // view's loss waits for its own target only.
     if (upload_targets) {
-        if (concurrent) CUDA_CHECK(cudaStreamWaitEvent(ctx->cs, ctx->fork_ev, 0));
         // The step's views over the ranks (ngs_b200_dist.h): whole secondaries, primary bands.
         int ws[kMaxSolveViews], hs[kMaxSolveViews], ts[kMaxSolveViews];
         for (int i = 0; i < nv; ++i) {
@@ -1291,6 +1286,13 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         }
         ShardRows plan[kMaxSolveViews];
         plan_step_shards(ctx->shard_world, ctx->shard_rank, nv, ws, hs, ts, T.cfg.loss.window, plan);
+        // Target uploads go to the copy stream (primary first, it is the largest), so the
+        // host->device copies overlap projection, sorting and rasterisation; each view's
+        // loss waits for its own target only.
+        if (concurrent) {
+            CUDA_CHECK(cudaEventRecord(ctx->fork_ev, ctx->stream));
+            CUDA_CHECK(cudaStreamWaitEvent(ctx->cs, ctx->fork_ev, 0));
+        }
         for (int i = 0; i < nv; ++i) {
             ViewSlot& v = T.views[i];
             const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
@@ -1310,6 +1312,10 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
             if (concurrent) CUDA_CHECK(cudaEventRecord(ctx->tev[i], s));
         }
     }
+    // Each view projects, bins, rasterises and evaluates its loss on its own stream. (One
+    // fused projection launch for all views was measured slower: it serialises the views'
+    // chains behind one kernel and re-reads the SH planes per view anyway.)
+    if (concurrent) ctx->fork(nv, ctx->vr.data());
     for (int ii = 0; ii < nv; ++ii) {
         const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
         const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)

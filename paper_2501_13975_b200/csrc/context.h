@@ -94,6 +94,7 @@ struct ViewSlot {
     bool valid = false;
     CameraDev cam{};
     unsigned long long order_version = 0;  // RenderSync::pos_version of the last depth sort (0: not reusable)
+    bool keep_order = false;               // this render reuses the sorted depth order (prepare_view)
     CameraDev order_cam{};
     int order_n = -1;
     int W = 0, H = 0, T = 0;
@@ -240,6 +241,13 @@ struct RenderSync {
 };
 void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
                  const RenderSync& sync = RenderSync{});
+// render_view in three parts, so the 1+K views of a step share ONE projection launch:
+// prepare_view (allocations, order reuse) per view, project_views for all of them, then
+// bin_and_raster per view on its own stream.
+bool prepare_view(const SceneDev& scene, ViewSlot& v, bool want_debug, const RenderSync& sync);
+void project_views(const SceneDev& scene, ViewSlot* const* views, int nv, bool want_debug, int* d_err,
+                   cudaStream_t s);
+void bin_and_raster(const SceneDev& scene, ViewSlot& v, int* d_err, cudaStream_t s, const RenderSync& sync);
 void compute_loss(ViewSlot& v, cudaStream_t s);
 void compute_loss_value(ViewSlot& v, cudaStream_t s);  // sums only (metrics)
 

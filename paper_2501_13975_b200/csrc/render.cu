@@ -6,6 +6,7 @@
 #include <cstring>
 
 #include "context.h"
+#include "solve.h"
 #include "geometry.cuh"
 #include "sort.h"
 #include "splat.cuh"
@@ -100,16 +101,25 @@ __device__ __forceinline__ unsigned int depth_sort_key(double d) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+// Outputs of one view's projection (K1); `depth_key`/`ids` null when the slot keeps its
+// sorted depth order (same positions and camera), `entry64` only for parity read-back.
+struct ProjOut {
+    float4 *ra, *rb, *rc;
+    double2* pix;
+    double* depth;
+    int4* rect;
+    int* tiles_touched;
+    uint8_t* flags;
+    unsigned int* depth_key;
+    int* ids;
+    double* entry64;
+};
+
 // K1: per-kernel projection, SH colour and tile extent (FP64 math, coalesced
 // float4 SoA loads; build_splat_list per-entry block rasterizer.hpp:192-226).
-__global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev cam, RasterParams rp,
-                                                        float4* ra, float4* rb, float4* rc, double2* pix,
-                                                        double* depth, int4* rect, int* tiles_touched,
-                                                        uint8_t* flags, unsigned int* depth_key, int* ids,
-                                                        double* entry64, int* err) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= s.n) return;
-    if (ids) ids[k] = k;  // null: the slot keeps its sorted depth order (same positions and camera)
+__device__ __forceinline__ void project_one(const SceneDev& s, int k, const CameraDev& cam, const RasterParams& rp,
+                                            const ProjOut& o, int* err) {
+    if (o.ids) o.ids[k] = k;  // null: the slot keeps its sorted depth order (same positions and camera)
     const float4 ps = s.pos_sigma[k];
     const D3 p = {ps.x, ps.y, ps.z};
     Projected pr;
@@ -117,18 +127,18 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
     double det = 0;
     if (ok) det = pr.s00 * pr.s11 - pr.s01 * pr.s01;
     if (!ok || !(det > 0.0)) {
-        if (ok) atomicOr(err, 1);  // project_kernel: projected covariance is not positive definite
-        tiles_touched[k] = 0;
-        flags[k] = 0;
-        rect[k] = make_int4(1, 1, 0, 0);
-        if (depth_key) depth_key[k] = 0xFFFFFFFFu;
-        depth[k] = 0;
+        if (ok) atomicOr(err, kErrNonPD);  // project_kernel: projected covariance is not positive definite
+        o.tiles_touched[k] = 0;
+        o.flags[k] = 0;
+        o.rect[k] = make_int4(1, 1, 0, 0);
+        if (o.depth_key) o.depth_key[k] = 0xFFFFFFFFu;
+        o.depth[k] = 0;
         return;
     }
     D3 r;
     double rn;
     if (!view_direction(cam, p, r, rn)) {
-        atomicOr(err, 2);  // DegenerateGeometry
+        atomicOr(err, kErrDegenerate);  // DegenerateGeometry
         r = d3(0, 0, 1);
     }
     double basis[16];
@@ -172,18 +182,18 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
     ty0 = max(ty0, rp.band_y0);
     ty1 = min(ty1, rp.band_y1 - 1);
     off = off || ty0 > ty1;
-    rect[k] = off ? make_int4(1, 1, 0, 0) : make_int4(tx0, ty0, tx1, ty1);
-    tiles_touched[k] = off ? 0 : (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-    flags[k] = f;
-    depth[k] = pr.depth;
-    if (depth_key) depth_key[k] = depth_sort_key(pr.depth);
-    pix[k] = make_double2(pr.px, pr.py);
-    ra[k] = make_float4(0.f, 0.f, static_cast<float>(qa), static_cast<float>(qb));
-    rb[k] = make_float4(static_cast<float>(qc), ps.w, static_cast<float>(col[0]), static_cast<float>(col[1]));
-    rc[k] = make_float4(static_cast<float>(col[2]), static_cast<float>(pr.s00), static_cast<float>(pr.s01),
-                        static_cast<float>(pr.s11));
-    if (entry64) {
-        double* e = entry64 + kEntry64 * static_cast<size_t>(k);
+    o.rect[k] = off ? make_int4(1, 1, 0, 0) : make_int4(tx0, ty0, tx1, ty1);
+    o.tiles_touched[k] = off ? 0 : (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+    o.flags[k] = f;
+    o.depth[k] = pr.depth;
+    if (o.depth_key) o.depth_key[k] = depth_sort_key(pr.depth);
+    o.pix[k] = make_double2(pr.px, pr.py);
+    o.ra[k] = make_float4(0.f, 0.f, static_cast<float>(qa), static_cast<float>(qb));
+    o.rb[k] = make_float4(static_cast<float>(qc), ps.w, static_cast<float>(col[0]), static_cast<float>(col[1]));
+    o.rc[k] = make_float4(static_cast<float>(col[2]), static_cast<float>(pr.s00), static_cast<float>(pr.s01),
+                          static_cast<float>(pr.s11));
+    if (o.entry64) {
+        double* e = o.entry64 + kEntry64 * static_cast<size_t>(k);
         e[0] = pr.px;
         e[1] = pr.py;
         e[2] = pr.s00;
@@ -197,6 +207,12 @@ __global__ void __launch_bounds__(256) project_kernel_k(SceneDev s, CameraDev ca
         e[10] = col[1];
         e[11] = col[2];
     }
+}
+
+// One launch per view (a fused all-views launch measured slower: DESIGN.md §6).
+__global__ void __launch_bounds__(256) project_view_k(SceneDev s, CameraDev cam, RasterParams rp, ProjOut o, int* err) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < s.n) project_one(s, k, cam, rp, o, err);
 }
 
 // Also sums the pair count exactly in 64 bits (`total64`, zeroed by the caller): the int
@@ -393,8 +409,8 @@ inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 
 }  // namespace
 
-void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
-                 const RenderSync& sync) {
+// Allocations of one view and the depth-order reuse decision (host only).
+bool prepare_view(const SceneDev& scene, ViewSlot& v, bool want_debug, const RenderSync& sync) {
     const int n = scene.n;
     v.n = n;
     v.W = v.cam.width;
@@ -418,14 +434,10 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     v.t_final.ensure(npx);
     v.last.ensure(npx);
     if (want_debug) v.entry64.ensure(kEntry64 * static_cast<size_t>(n));
-    int bits = 1;
-    while ((1 << bits) < v.T) ++bits;
     if (!v.sort_scratch) v.sort_scratch = new SortScratch();
-    SortScratch& sc = *static_cast<SortScratch*>(v.sort_scratch);
     v.depth_key_alt.ensure(n);
     v.order_alt.ensure(n);
     v.counters.ensure(6);  // [0] n, [1] P (int scan), [2] min(P, cap), [4..5] P as u64
-
     // The culled set (key 0xFFFFFFFF: behind the near plane) and the depth keys depend on the
     // positions and the camera only; a non-PD projected covariance is a step error.
     const bool keep_order = sync.pos_version != 0 && v.order_version == sync.pos_version && v.order_n == n &&
@@ -433,16 +445,42 @@ void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err
     v.order_version = sync.pos_version;
     v.order_cam = v.cam;
     v.order_n = n;
-    if (n > 0) {
+    v.keep_order = keep_order;
+    return keep_order;
+}
+
+void project_views(const SceneDev& scene, ViewSlot* const* views, int nv, bool want_debug, int* d_err,
+                   cudaStream_t s) {
+    const int n = scene.n;
+    if (n == 0 || nv == 0) return;
+    if (nv > kMaxSolveViews) throw Error(NGS_ERR_INTERNAL, "project_views: too many views");
+    for (int i = 0; i < nv; ++i) {
+        ViewSlot& v = *views[i];
+        const ProjOut o{v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr, v.pix.ptr, v.depth.ptr, v.rect.ptr,
+                        v.tiles_touched.ptr, v.flags.ptr, v.keep_order ? nullptr : v.depth_key.ptr,
+                        v.keep_order ? nullptr : v.order.ptr, want_debug ? v.entry64.ptr : nullptr};
         StageScope st(NGS_STAGE_PROJECT, s);
-        project_kernel_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr,
-                                                       v.pix.ptr, v.depth.ptr, v.rect.ptr, v.tiles_touched.ptr,
-                                                       v.flags.ptr, keep_order ? nullptr : v.depth_key.ptr,
-                                                       keep_order ? nullptr : v.order.ptr,
-                                                       want_debug ? v.entry64.ptr : nullptr, d_err);
+        project_view_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, o, d_err);
         CUDA_LAUNCH_CHECK();
     }
+}
+
+void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
+                 const RenderSync& sync) {
+    prepare_view(scene, v, want_debug, sync);
+    ViewSlot* one = &v;
+    project_views(scene, &one, 1, want_debug, d_err, s);
     if (sync.projected) CUDA_CHECK(cudaEventRecord(sync.projected, s));
+    bin_and_raster(scene, v, d_err, s, sync);
+}
+
+// K2-K6 of one view after its projection: depth order, tile binning, forward raster.
+void bin_and_raster(const SceneDev& scene, ViewSlot& v, int* d_err, cudaStream_t s, const RenderSync& sync) {
+    const int n = scene.n;
+    const bool keep_order = v.keep_order;
+    int bits = 1;
+    while ((1 << bits) < v.T) ++bits;
+    SortScratch& sc = *static_cast<SortScratch*>(v.sort_scratch);
     if (!v.raster.owns_rows()) {
         // Multi-GPU: another rank owns this view; only its projection (flags for the
         // replicated colour solve) is needed here. The depth order was not sorted.
