@@ -256,19 +256,51 @@ __global__ void emit_pairs_k(int n, int tiles_x, int cap, const int* order, cons
         if (pair_counter) atomicAdd(pair_counter, static_cast<unsigned long long>(total));
         counters[2] = total < cap ? total : cap;
     }
-    if (r >= n) return;
-    const int k = order[r];
-    if (tiles_touched[k] == 0) return;
-    const int4 rc = rect[k];
-    int o = offsets[r];
-    for (int ty = rc.y; ty <= rc.w; ++ty)
-        for (int tx = rc.x; tx <= rc.z; ++tx) {
-            if (o < cap) {
-                keys[o] = static_cast<unsigned int>(ty * tiles_x + tx);
-                vals[o] = k;
-            }
-            ++o;
+    // Warp-cooperative emission: the warp's 32 Gaussians (consecutive in depth order) own one
+    // contiguous run of pairs starting at offsets[r0]; lane l writes items l, l + 32, ... of
+    // that run, so every key / value store instruction is coalesced (one thread looping over
+    // its own rect wrote 32 scattered streams). Item e belongs to the first lane whose
+    // inclusive count exceeds e (5-step search over the shuffled counts).
+    const int lane = threadIdx.x & 31;
+    const int k = r < n ? order[r] : 0;
+    const int cnt = r < n ? tiles_touched[k] : 0;
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    const int warp_total = __shfl_sync(0xffffffffu, incl, 31);
+    if (warp_total == 0) return;
+    const int r0 = r - lane;
+    const int base = offsets[r0];
+    const int4 rc = cnt ? rect[k] : make_int4(0, 0, 0, 0);
+    const int rw = rc.z - rc.x + 1;
+    for (int e0 = 0; e0 < warp_total; e0 += 32) {
+        const int e = e0 + lane;
+        // owner = number of lanes whose inclusive count is <= e
+        int owner = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int probe = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+            if (probe <= e) owner += step;
         }
+        const int own_incl = __shfl_sync(0xffffffffu, incl, owner);
+        const int own_cnt = __shfl_sync(0xffffffffu, cnt, owner);
+        const int own_k = __shfl_sync(0xffffffffu, k, owner);
+        const int own_x0 = __shfl_sync(0xffffffffu, rc.x, owner);
+        const int own_y0 = __shfl_sync(0xffffffffu, rc.y, owner);
+        const int own_w = __shfl_sync(0xffffffffu, rw, owner);
+        if (e < warp_total) {
+            const int i = e - (own_incl - own_cnt);  // index inside the owner's rect, row-major
+            const int dy = i / own_w, dx = i - dy * own_w;
+            const int o = base + e;
+            if (o < cap) {
+                keys[o] = static_cast<unsigned int>((own_y0 + dy) * tiles_x + own_x0 + dx);
+                vals[o] = own_k;
+            }
+        }
+    }
 }
 
 // K5: per-tile [start, end) ranges from the tile-sorted key array.
