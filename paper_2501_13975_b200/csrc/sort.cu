@@ -30,6 +30,10 @@ constexpr int kDigits = 256;
 // ---------------------------------------------------------------------------
 
 constexpr int kMaxPasses = 4;
+#ifndef NGS_LOOKBACK
+#define NGS_LOOKBACK 4
+#endif
+constexpr int kLookBack = NGS_LOOKBACK;  // predecessors loaded per look-back round
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1;
 
 __global__ void __launch_bounds__(kThreads) radix_global_hist_k(const uint32_t* __restrict__ keys,
@@ -152,16 +156,18 @@ __global__ void __launch_bounds__(kThreads) radix_onesweep_k(const uint32_t* __r
         atomicExch(st, kFlagInc | bc);
     } else {
         atomicExch(st, kFlagAgg | bc);
-        // Walk back four predecessors per round (independent loads in flight), in order,
-        // re-polling only a status that is not published yet.
+        // Walk back kLookBack predecessors per round (independent loads in flight), in order,
+        // re-polling only a status that is not published yet. All tiles of a pass start in
+        // one wave, so early in the pass a tile sums many aggregates before it meets an
+        // inclusive prefix: the round count, not the load count, sets the latency.
         bool found = false;
-        for (int t = tile - 1; t >= 0 && !found; t -= 4) {
-            unsigned v[4];
+        for (int t = tile - 1; t >= 0 && !found; t -= kLookBack) {
+            unsigned v[kLookBack];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < kLookBack; ++q)
                 v[q] = t - q >= 0 ? *(const volatile unsigned*)(status + static_cast<size_t>(t - q) * kDigits + d) : 0u;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < kLookBack; ++q) {
                 if (found || t - q < 0) break;
                 const volatile unsigned* sp = status + static_cast<size_t>(t - q) * kDigits + d;
                 while ((v[q] & ~kCountMask) == 0) v[q] = *sp;
