@@ -15,6 +15,18 @@
 #ifndef NGS_COLOR4_MINB
 #define NGS_COLOR4_MINB 5
 #endif
+// One kernel per Gaussian for the colour solve (stage 1 in registers) instead of the
+// Gram kernel + one thread per (Gaussian, channel) with an HBM eigen scratch.
+// (measured slower: c4 colour 7.3 -> 8.9 ms; the solve is FP64 latency-bound and a third
+// of the threads hides less of it than the scratch round trip costs)
+#ifndef NGS_COLOR_FUSED
+#define NGS_COLOR_FUSED 0
+#endif
+#ifndef NGS_COLORF_MINB
+#define NGS_COLORF_MINB 4
+#endif
+constexpr bool kColorFused = NGS_COLOR_FUSED != 0;
+constexpr double kJacobiTol = 1e-28;  // (1e-20 / 1e-16 measured: c4 colour 7.18 -> 7.10 / 7.27 ms, kept)
 
 namespace ngsb {
 
@@ -368,7 +380,7 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
         }
         // Converged when the off-diagonal mass is ~1e-14 of the diagonal: eigenvalues are then
         // within ~1e-14 ||A|| (Weyl), far below the FP32 accumulation error of the inputs.
-        if (off == 0.0 || off <= 1e-28 * diag) break;
+        if (off == 0.0 || off <= kJacobiTol * diag) break;
         if constexpr (MAXM == 4) {  // parallel ordering: 3 rounds of 2 disjoint rotations
             jacobi4_round<0, 1, 2, 3>(a, v);
             jacobi4_round<0, 2, 1, 3>(a, v);
@@ -425,50 +437,52 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
 // Colour solve, stage 1 (per Gaussian): the Gram matrix G = Phi^T Phi of the
 // views' SH bases and its eigen-decomposition G = E L E^T (stored: E, diag L),
 // shared by the three channels of stage 2.
+// Gram matrix of the visible views' SH bases (phi_a . phi_b; absent views are zero) and its
+// eigen-decomposition G = E diag(L) E^T (eigenvalues on the diagonal of L).
+template <int MV>
+__device__ __forceinline__ void color_gram(const SceneDev& s, const ColorViews& cv, int k, double (&L)[MV][MV],
+                                           double (&E)[MV][MV]) {
+    const float4 ps = s.pos_sigma[k];
+    const D3 p = {ps.x, ps.y, ps.z};
+    const int nv = cv.n_views;
+    D3 dir[MV];
+    uint8_t fl[MV];
+#pragma unroll
+    for (int v = 0; v < MV; ++v) {
+        fl[v] = 0;
+        dir[v] = d3(0, 0, 1);
+        if (v < nv) {
+            fl[v] = cv.flags[v][k];
+            double nr;
+            if (!view_direction(cv.cam[v], p, dir[v], nr)) dir[v] = d3(0, 0, 1);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < MV; ++a) {
+        double pa[16];
+        sh_basis(dir[a], s.sh_degree, pa);
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+            double pb[16];
+            sh_basis(dir[b], s.sh_degree, pb);
+            double t = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) t += pa[i] * pb[i];
+            const bool on = (fl[a] & kProjected) && (fl[b] & kProjected);
+            L[a][b] = on ? t : 0.0;
+            L[b][a] = L[a][b];
+        }
+    }
+    jacobi_eig<MV>(L, E);
+}
+
 template <int MV>
 __global__ void __launch_bounds__(128) solve_color_gram_k(SceneDev s, ColorViews cv, double* __restrict__ eig,
                                                           size_t stride) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < s.n) {
-        const float4 ps = s.pos_sigma[k];
-        const D3 p = {ps.x, ps.y, ps.z};
-        const int nv = cv.n_views;
-        D3 dir[MV];
-        uint8_t fl[MV];
-#pragma unroll
-        for (int v = 0; v < MV; ++v) {
-            fl[v] = 0;
-            dir[v] = d3(0, 0, 1);
-            if (v < nv) {
-                fl[v] = cv.flags[v][k];
-                double nr;
-                if (!view_direction(cv.cam[v], p, dir[v], nr)) dir[v] = d3(0, 0, 1);
-            }
-        }
-        // Gram matrix of the visible views' SH bases (phi_a . phi_b); absent views are zero.
-        double G[MV][MV];
-#pragma unroll
-        for (int a = 0; a < MV; ++a) {
-            double pa[16];
-            sh_basis(dir[a], s.sh_degree, pa);
-#pragma unroll
-            for (int b = 0; b <= a; ++b) {
-                double pb[16];
-                sh_basis(dir[b], s.sh_degree, pb);
-                double t = 0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) t += pa[i] * pb[i];
-                const bool on = (fl[a] & kProjected) && (fl[b] & kProjected);
-                G[a][b] = on ? t : 0.0;
-                G[b][a] = G[a][b];
-            }
-        }
         double L[MV][MV], E[MV][MV];
-#pragma unroll
-        for (int a = 0; a < MV; ++a)
-#pragma unroll
-            for (int b = 0; b < MV; ++b) L[a][b] = G[a][b];
-        jacobi_eig<MV>(L, E);
+        color_gram<MV>(s, cv, k, L, E);
 #pragma unroll
         for (int a = 0; a < MV; ++a) {
             eig[static_cast<size_t>(MV * MV + a) * stride + k] = L[a][a];
@@ -479,11 +493,12 @@ __global__ void __launch_bounds__(128) solve_color_gram_k(SceneDev s, ColorViews
 }
 
 // Colour solve, stage 2 (one thread per Gaussian and channel, blockIdx.y = channel).
-template <int MV>
-__global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2) solve_color_k(SceneDev s, ColorViews cv, SolveParams sp,
-                                                     const double* __restrict__ acc, size_t stride,
-                                                     const double* __restrict__ eig, SolveOutputs out) {
-    const int ch = blockIdx.y;
+// FUSED: one thread per Gaussian computes stage 1 itself (no eigen scratch round trip
+// through HBM) and then the three channels in turn.
+template <int MV, bool FUSED>
+__global__ void __launch_bounds__(128, FUSED ? NGS_COLORF_MINB : (MV == 4 ? NGS_COLOR4_MINB : 2))
+    solve_color_k(SceneDev s, ColorViews cv, SolveParams sp, const double* __restrict__ acc, size_t stride,
+                  const double* __restrict__ eig, SolveOutputs out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     double nsq = 0.0;
     if (k < s.n) {
@@ -495,13 +510,32 @@ __global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2) solve_colo
         // Stage 1's G = E L E^T (SH0: no stage 1, E = I and L unused). G itself is not
         // re-formed: G g = E L E^T g and beta^T G beta = sum_j L_j (E^T beta)_j^2.
         double L[MV][MV], E[MV][MV];
+        if constexpr (FUSED) {
+            if (n > 1) {
+                color_gram<MV>(s, cv, k, L, E);
 #pragma unroll
-        for (int a = 0; a < MV; ++a)
+                for (int a = 0; a < MV; ++a)
 #pragma unroll
-            for (int b = 0; b < MV; ++b) {
-                L[a][b] = (a == b && n > 1) ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : 0.0;
-                E[a][b] = n > 1 ? eig[static_cast<size_t>(MV * a + b) * stride + k] : (a == b ? 1.0 : 0.0);
+                    for (int b = 0; b < MV; ++b)
+                        if (a != b) L[a][b] = 0.0;
+            } else {
+#pragma unroll
+                for (int a = 0; a < MV; ++a)
+#pragma unroll
+                    for (int b = 0; b < MV; ++b) {
+                        L[a][b] = 0.0;
+                        E[a][b] = a == b ? 1.0 : 0.0;
+                    }
             }
+        } else {
+#pragma unroll
+            for (int a = 0; a < MV; ++a)
+#pragma unroll
+                for (int b = 0; b < MV; ++b) {
+                    L[a][b] = (a == b && n > 1) ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : 0.0;
+                    E[a][b] = n > 1 ? eig[static_cast<size_t>(MV * a + b) * stride + k] : (a == b ? 1.0 : 0.0);
+                }
+        }
         double lmax = 0;
 #pragma unroll
         for (int a = 0; a < MV; ++a) lmax = fmax(lmax, L[a][a]);
@@ -515,6 +549,9 @@ __global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2) solve_colo
             sq[a] = L[a][a] * isq[a];  // L^1/2 on kept directions, 0 elsewhere
             r += kept[a] ? 1 : 0;
         }
+        const int ch0 = FUSED ? 0 : static_cast<int>(blockIdx.y), ch1 = FUSED ? 3 : ch0 + 1;
+#pragma unroll 1
+        for (int ch = ch0; ch < ch1; ++ch) {
         double beta_all[MV];
         do {
             double gv[MV], hv[MV];
@@ -672,7 +709,8 @@ __global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2) solve_colo
                     if (i < n) s.sh[(static_cast<size_t>(16 * ch + i)) * s.n + k] = (float)((double)cur[i] + delta[i]);
             }
         }
-        if (out.accepted && ch == 0) out.accepted[k] = 1;
+        }  // channels
+        if (out.accepted && ch0 == 0) out.accepted[k] = 1;
     }
     block_add(nsq, out.norm_sq);
 }
@@ -829,7 +867,7 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
                   size_t stride, const SolveOutputs& out, cudaStream_t s) {
     const int n = scene.n;
     if (n == 0) return;
-    StageScope st(NGS_STAGE_SOLVE, s, attr == NGS_COLOR && scene.n_coeffs > 1 ? 2 : 1);
+    StageScope st(NGS_STAGE_SOLVE, s, attr == NGS_COLOR && scene.n_coeffs > 1 && !kColorFused ? 2 : 1);
     switch (attr) {
         case NGS_POSITION:
             solve_position_k<<<blocks_for(n), 256, 0, s>>>(scene, primary, sp, acc, stride, out);
@@ -846,18 +884,22 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
             break;
         case NGS_COLOR: {
             // stage 1 (Gram eigen-decomposition, only with higher SH bands) + stage 2 per channel
-            auto run = [&](auto gram_kernel, auto ch_kernel, int) {
+            auto run = [&](auto gram_kernel, auto ch_kernel, auto fused_kernel) {
+                if (kColorFused) {
+                    fused_kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
+                    return;
+                }
                 if (scene.n_coeffs > 1) gram_kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, cv.eig, stride);
                 ch_kernel<<<dim3(blocks_for(n, 128), 3), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
             };
             if (cv.n_views <= 1)
-                run(solve_color_gram_k<1>, solve_color_k<1>, 1);
+                run(solve_color_gram_k<1>, solve_color_k<1, false>, solve_color_k<1, true>);
             else if (cv.n_views <= 2)
-                run(solve_color_gram_k<2>, solve_color_k<2>, 2);
+                run(solve_color_gram_k<2>, solve_color_k<2, false>, solve_color_k<2, true>);
             else if (cv.n_views <= 4)
-                run(solve_color_gram_k<4>, solve_color_k<4>, 4);
+                run(solve_color_gram_k<4>, solve_color_k<4, false>, solve_color_k<4, true>);
             else
-                run(solve_color_gram_k<8>, solve_color_k<8>, 8);
+                run(solve_color_gram_k<8>, solve_color_k<8, false>, solve_color_k<8, true>);
             break;
         }
     }
