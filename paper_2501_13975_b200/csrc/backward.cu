@@ -827,6 +827,13 @@ __global__ void limbs_to_double_k(const unsigned long long* __restrict__ limbs, 
     }
 }
 
+// Stage the per-view constant rows with TMA bulk copies (cp.async.bulk + mbarrier) instead
+// of 16-byte cp.async (LDGSTS) chunks spread over the block (A/B knob).
+#ifndef NGS_BWD_TMA
+#define NGS_BWD_TMA 0
+#endif
+constexpr bool kBwdTma = NGS_BWD_TMA != 0;
+
 // Per-warp record queue (ring of 64 entries) between the two phases.
 constexpr int kQ = 64;
 // Two float4 per record (one STS.128 / LDS.128 each, consecutive slots: conflict-free)
@@ -871,6 +878,7 @@ struct BackwardSmem {
     float4 lg[NT];                         // per-pixel loss derivatives (gl0, gl1, gl2, hl0)
     float2 lh[NT];                         // (hl1, hl2): two loads per record instead of six
     WarpQueue q[NW];
+    unsigned long long cst_bar[2];         // NGS_BWD_TMA: mbarriers of the bulk-copied constant rows
     int maxlast;
 };
 
@@ -1043,9 +1051,19 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
         }
         if constexpr (NC4 > 0) {
             const float4* src = reinterpret_cast<const float4*>(a.consts);
-            for (int i = tid; i < n * NC4; i += NT) {
-                const int j = i / NC4, c = i - j * NC4;
-                cp_async16(&S.cst[buf][j * CST + c], src + static_cast<size_t>(S.kid[buf][j]) * NC4 + c);
+            if constexpr (kBwdTma) {
+                // One TMA bulk copy (UBLKCP) per splat: its contiguous row of NC4 float4s.
+                if (tid == 0) mbar_expect_tx(&S.cst_bar[buf], static_cast<unsigned>(n * NC4 * 16));
+                if (tid < n) {
+                    fence_proxy_async();  // the generic-proxy reads of this buffer (two batches ago) are done
+                    bulk_copy_g2s(&S.cst[buf][tid * CST], src + static_cast<size_t>(S.kid[buf][tid]) * NC4,
+                                  NC4 * 16, &S.cst_bar[buf]);
+                }
+            } else {
+                for (int i = tid; i < n * NC4; i += NT) {
+                    const int j = i / NC4, c = i - j * NC4;
+                    cp_async16(&S.cst[buf][j * CST + c], src + static_cast<size_t>(S.kid[buf][j]) * NC4 + c);
+                }
             }
         }
     };
@@ -1053,6 +1071,13 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
     if (tid < B) {
         if (range.x + tid < end) S.kid[0][tid] = a.vals[range.x + tid];
         if (range.x + B + tid < end) kid_next = a.vals[range.x + B + tid];
+    }
+    if constexpr (kBwdTma && NC4 > 0) {
+        if (tid == 0) {
+            mbar_init(&S.cst_bar[0], 1);
+            mbar_init(&S.cst_bar[1], 1);
+            mbar_fence_init();
+        }
     }
     __syncthreads();
     if (range.x < end) issue(0, range.x);
@@ -1063,6 +1088,7 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
         const int cnt = min(B, end - base);
         s_const = S.cst[buf];
         cp_async_wait_all();
+        if constexpr (kBwdTma && NC4 > 0) mbar_wait(&S.cst_bar[buf], (it >> 1) & 1);
         __syncthreads();  // batch `it` staged by every thread; the previous batch's readers are done
         if (tid < B) {
             if (tid < cnt) {
