@@ -23,6 +23,7 @@
 #include "context.h"
 #include "solve.h"
 #include "ngs_b200_dist.h"
+#include "ngs_b200_ext.h"
 
 namespace ngsb {
 thread_local Profiler* g_prof = nullptr;
@@ -1250,6 +1251,14 @@ int32_t ngs_trainer_neighbors(ngs_context* ctx, int32_t view_id, int32_t* out, i
         const auto& nb = ctx->trainer.neighbors.at(view_id);
         *n_out = static_cast<int32_t>(nb.size());
         for (int i = 0; i < std::min<int>(capacity, static_cast<int>(nb.size())); ++i) out[i] = nb[i];
+    });
+}
+
+int32_t ngs_trainer_set_barrier_weight(ngs_context* ctx, double weight) {
+    return guarded([&] {
+        if (!ctx->trainer.active) throw Error(NGS_ERR_INVALID_INPUT, "trainer not configured");
+        if (!(weight >= 0.0) || !std::isfinite(weight)) throw Error(NGS_ERR_INVALID_INPUT, "barrier weight must be >= 0");
+        ctx->trainer.barrier_weight = weight;
     });
 }
 

@@ -20,7 +20,7 @@ def test_header_symbols_match_binding_list():
     assert sorted(capi.EXPORTED_SYMBOLS) == declared("ngs_b200.h")
 
 
-@pytest.mark.parametrize("header", ["ngs_b200.h", "ngs_b200_profile.h", "ngs_b200_dist.h"])
+@pytest.mark.parametrize("header", ["ngs_b200.h", "ngs_b200_profile.h", "ngs_b200_dist.h", "ngs_b200_ext.h"])
 def test_product_library_exports_every_declared_symbol(header):
     assert os.path.exists(capi.PRODUCT_LIB), "run __graft_entry__.build() first"
     lib = ctypes.CDLL(capi.PRODUCT_LIB)
