@@ -943,14 +943,14 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
 }
 
 ColorViews color_views(ngs_context* ctx, ViewSlot* const* views, int nv) {
-    if (nv > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "at most 8 views per Newton step are supported");
+    if (nv > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "at most 16 views per Newton step are supported");
     ColorViews cv{};
     cv.n_views = nv;
     for (int i = 0; i < nv; ++i) {
         cv.cam[i] = views[i]->cam;
         cv.flags[i] = views[i]->flags.ptr;
     }
-    const int mv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : 8;  // solve_color_k<MV> instantiation
+    const int mv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 16;  // solve_color_k<MV> instantiation
     ctx->color_eig.ensure(static_cast<size_t>(mv * mv + mv) * std::max(ctx->scene.n, 1));
     cv.eig = ctx->color_eig.ptr;
     return cv;
@@ -1142,7 +1142,7 @@ int32_t ngs_trainer_configure(ngs_context* ctx, const ngs_train_config* c, int32
         if (n_cameras <= 0) throw Error(NGS_ERR_INVALID_INPUT, "trainer: dataset has no cameras");
         if (n_train <= 0) throw Error(NGS_ERR_INVALID_INPUT, "trainer: no training views");
         if (ctx->scene.n <= 0) throw Error(NGS_ERR_INVALID_INPUT, "fit_bounding_sphere: empty scene");
-        if (1 + c->knn > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "knn > 7 unsupported");
+        if (1 + c->knn > kMaxSolveViews) throw Error(NGS_ERR_INVALID_INPUT, "knn > 15 unsupported");
         TrainerState& T = ctx->trainer;
         T.release();
         T.cfg = *c;

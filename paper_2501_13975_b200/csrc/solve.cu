@@ -884,22 +884,30 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
             break;
         case NGS_COLOR: {
             // stage 1 (Gram eigen-decomposition, only with higher SH bands) + stage 2 per channel
-            auto run = [&](auto gram_kernel, auto ch_kernel, auto fused_kernel) {
-                if (kColorFused) {
-                    fused_kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
-                    return;
-                }
+            auto run = [&](auto gram_kernel, auto ch_kernel) {
                 if (scene.n_coeffs > 1) gram_kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, cv.eig, stride);
                 ch_kernel<<<dim3(blocks_for(n, 128), 3), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
             };
-            if (cv.n_views <= 1)
-                run(solve_color_gram_k<1>, solve_color_k<1, false>, solve_color_k<1, true>);
-            else if (cv.n_views <= 2)
-                run(solve_color_gram_k<2>, solve_color_k<2, false>, solve_color_k<2, true>);
-            else if (cv.n_views <= 4)
-                run(solve_color_gram_k<4>, solve_color_k<4, false>, solve_color_k<4, true>);
-            else
-                run(solve_color_gram_k<8>, solve_color_k<8, false>, solve_color_k<8, true>);
+            if constexpr (kColorFused) {
+                auto fused = [&](auto kernel) {
+                    kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
+                };
+                if (cv.n_views <= 1) fused(solve_color_k<1, true>);
+                else if (cv.n_views <= 2) fused(solve_color_k<2, true>);
+                else if (cv.n_views <= 4) fused(solve_color_k<4, true>);
+                else if (cv.n_views <= 8) fused(solve_color_k<8, true>);
+                else fused(solve_color_k<16, true>);
+            } else if (cv.n_views <= 1) {
+                run(solve_color_gram_k<1>, solve_color_k<1, false>);
+            } else if (cv.n_views <= 2) {
+                run(solve_color_gram_k<2>, solve_color_k<2, false>);
+            } else if (cv.n_views <= 4) {
+                run(solve_color_gram_k<4>, solve_color_k<4, false>);
+            } else if (cv.n_views <= 8) {
+                run(solve_color_gram_k<8>, solve_color_k<8, false>);
+            } else {  // knn 8..15 (the reference's overshoot ablation uses knn = 8): spills, rarely used
+                run(solve_color_gram_k<16>, solve_color_k<16, false>);
+            }
             break;
         }
     }

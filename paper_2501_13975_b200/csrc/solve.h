@@ -5,7 +5,7 @@
 
 namespace ngsb {
 
-constexpr int kMaxSolveViews = 8;  // primary + up to 7 secondary views per step
+constexpr int kMaxSolveViews = 16;  // primary + up to 15 secondary views per step (reference knn has no cap)
 
 // NewtonOptions (newton.hpp:58-68) plus commit flag and FP32 opacity bounds.
 struct SolveParams {

@@ -71,3 +71,110 @@ def test_terms_match_finite_differences(gpu, seed, attr):
             errs.append(abs(fd - an) / max(abs(an), 1e-2 * mag.max()))
     print(f"FD {attr} seed {seed}: max rel err {max(errs):.2e} over {len(errs)} probes")
     assert max(errs) < 2e-2
+
+
+def _f32(a):
+    return np.asarray(a, np.float64).astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_scaling_terms_match_finite_differences(gpu, seed):
+    """solve_scaling_grad of check_derivatives (check.hpp:456-472): the scaling gradient is
+    dL/dlambda_i along the eigen-directions v_i v_i^T of the projected covariance. The
+    reference perturbs the 2D covariance directly (Cov2dOverride); the device has no such
+    override, so the 3D scale moves along the direction ds that changes Sigma_2D by exactly
+    h v_i v_i^T to first order: dSigma/ds_c = 2 s_c n_c n_c^T (n = J W R_q, newton.hpp:152-184,
+    from the float64 oracle), and the 3x3 map ds -> (v_0^T dS v_0, v_1^T dS v_1, v_0^T dS v_1)
+    is inverted for (h, 0, 0) / (0, h, 0). Scales are rounded to the device's FP32 and the
+    realised first-order change is used."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import ngs_oracle as O
+    scene, cam, target = check_fixture(seed)
+    for f in ("position", "scale", "quaternion", "sigma", "sh"):
+        setattr(scene, f, _f32(getattr(scene, f)))
+    ctx = gpu.context()
+    base = _loss(ctx, scene, cam, target)
+    g, _, vis = ctx.accumulate(capi.SCALING, 0)
+    ocam = O.Cam.of(cam)
+    mag = np.abs(g).max(axis=1)
+    errs = []
+    for k in [int(k) for k in np.argsort(-mag)[:6] if vis[k]]:
+        kern = dict(p=scene.position[k], s=scene.scale[k], q=scene.quaternion[k], sigma=scene.sigma[k],
+                    sh=scene.sh[k])
+        proj = O.project_kernel(ocam, kern)
+        vals_, vecs = O.sym2_eigen(proj["cov"])
+        if vals_[1] - vals_[0] <= 1e-6 * abs(vals_[1]):
+            continue  # degenerate subspace: the solve uses one direction
+        n = proj["J"] @ ocam.rot @ O.quaternion_to_rotation(kern["q"])
+        v0, v1 = vecs[:, 0], vecs[:, 1]
+        M = np.array([[2 * kern["s"][c] * (v0 @ n[:, c]) ** 2 for c in range(3)],
+                      [2 * kern["s"][c] * (v1 @ n[:, c]) ** 2 for c in range(3)],
+                      [2 * kern["s"][c] * (v0 @ n[:, c]) * (v1 @ n[:, c]) for c in range(3)]])
+        if np.linalg.cond(M) > 1e6:
+            continue
+        for i in range(2):
+            h = 1e-3 * float(np.max(np.abs(proj["cov"])))
+            e = np.zeros(3)
+            e[i] = h
+            ds = np.linalg.solve(M, e)
+            vals, dss = [], []
+            for sgn in (1, -1):
+                s = scene.copy()
+                s.scale = s.scale.copy()
+                s.scale[k] = _f32(scene.scale[k] + sgn * ds)
+                dss.append(s.scale[k] - scene.scale[k])
+                vals.append(_loss(ctx, s, cam, target))
+            dlam = M @ (dss[0] - dss[1])  # realised (dlambda_0, dlambda_1, doff), first order
+            pred = g[k, 0] * dlam[0] + g[k, 1] * dlam[1]
+            fd = vals[0] - vals[1]
+            errs.append(abs(fd - pred) / max(abs(pred), 1e-2 * mag.max() * 2 * h))
+    print(f"FD scaling seed {seed}: max rel err {max(errs):.2e} over {len(errs)} probes (loss {base:.6g})")
+    assert errs and max(errs) < 2e-2
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_loss_fields_match_finite_differences(gpu, seed):
+    """loss_grad / ssim_hess_diag of check_derivatives (check.hpp:384-411) on the GPU loss.
+    The GPU has no entry point that scores an arbitrary image, but total_loss_value is
+    symmetric in its two images (L2 and SSIM both are), so L(R_A + e d_x, R_B) =
+    L(R_B, R_A + e d_x): the GPU's fields at (R_A, R_B) (build_view of scene A with target
+    R_B) are checked against central differences of the GPU's own loss value of scene B's
+    render against the perturbed R_A (ngs_view_metrics). Steps as the reference: 2e-5 for
+    the gradient, 1e-4 for the second difference; floors 1e-7 / 1e-8."""
+    scene_a, cam, _ = check_fixture(seed)
+    scene_b, _, _ = check_fixture(seed + 10)
+    for s in (scene_a, scene_b):
+        for f in ("position", "scale", "quaternion", "sigma", "sh"):
+            setattr(s, f, _f32(getattr(s, f)))
+    if scene_b.count != scene_a.count:
+        scene_b = scene_a.copy()
+        scene_b.position = _f32(scene_a.position + 0.02)
+    ctx = gpu.context()
+    ctx.set_scene(scene_b)
+    r_b = ctx.render(cam)
+    ctx.set_scene(scene_a)
+    ctx.build_view(0, cam, r_b)
+    r_a = ctx.view_image(0)
+    ga, ha = ctx.view_loss_derivs(0)
+    ctx.set_scene(scene_b)
+    rng = np.random.default_rng(seed)
+    eg, eh = [], []
+    for _ in range(24):
+        x, y, ch = int(rng.integers(cam.width)), int(rng.integers(cam.height)), int(rng.integers(3))
+
+        def loss_at(v):
+            img = r_a.copy()
+            img[y, x, ch] += v
+            return ctx.view_metrics(cam, img).loss
+
+        l0, lp, lm = loss_at(0.0), loss_at(2e-5), loss_at(-2e-5)
+        fd_g = (lp - lm) / 4e-5
+        hp, hm = loss_at(1e-4), loss_at(-1e-4)
+        fd_h = (hp - 2 * l0 + hm) / 1e-8
+        eg.append(abs(ga[y, x, ch] - fd_g) / max(abs(ga[y, x, ch]), abs(fd_g), 1e-7))
+        eh.append(abs(ha[y, x, ch] - fd_h) / max(abs(ha[y, x, ch]), abs(fd_h), 1e-8))
+    print(f"FD loss fields seed {seed}: grad max rel {max(eg):.2e}, ssim/L2 hess diag max rel {max(eh):.2e}")
+    assert max(eg) < 1e-4  # measured <= 6.6e-6 (B200)
+    assert max(eh) < 1e-4  # measured <= 1.3e-6
