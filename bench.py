@@ -386,13 +386,20 @@ def ours_arm(args, cfg: Config):
     counters = main["stats"]
     pst = prof["stats"]
 
-    # Roofline of the dominant kernel (position backward, FP32 CUDA-core bound).
+    # Roofline of the dominant kernel: the primary view's position backward launch
+    # (backward_k<PositionUV, 16>), FP32 CUDA-core bound. Algorithmic work = 290 flop per
+    # contributing record x the primary's records; time = that launch alone (CUDA events on
+    # its stream in the profiled re-run).
     fp32_peak = ctx.microbench_fp32()
     fp64_peak = ctx.microbench_fp64()
-    bwd_ms = pst["ms"]["bwd_position"]
-    bwd_launches = max(pst["launches"]["bwd_position"], 1)
-    pairs = pst["contrib_pairs"][0]
+    bwd_ms = pst["primary_bwd_ms"][0]
+    bwd_launches = args.steps
+    pairs = pst["primary_contrib_pairs"][0]
     achieved = POSITION_FLOPS_PER_PAIR * pairs / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else 0.0
+    all_views = {"ms_per_step": pst["ms"]["bwd_position"] / args.steps,
+                 "records_per_step": pst["contrib_pairs"][0] / args.steps,
+                 "tflops": POSITION_FLOPS_PER_PAIR * pst["contrib_pairs"][0] / (pst["ms"]["bwd_position"] * 1e-3) / 1e12
+                 if pst["ms"]["bwd_position"] > 0 else 0.0}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (ncu numbers are never bench values; this only sizes traffic vs algorithmic bytes).
     traffic, traffic_src = None, None
@@ -443,12 +450,15 @@ def ours_arm(args, cfg: Config):
                 "d2h_bytes_per_step": 48},
         "gpu_launches": int(counters["total_launches"]),
         "allreduce_bytes_per_step": counters["allreduce_bytes"] / args.steps,
-        "roofline": {"bound": "fp32", "kernel": "backward_k<position>", "achieved": achieved,
+        "roofline": {"bound": "fp32", "kernel": "backward_k<PositionUV,16> (primary view, position pass)",
+                     "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
                      "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": "measured FFMA microbenchmark (ngs_microbench_fp32)",
                      "algorithmic": f"{POSITION_FLOPS_PER_PAIR} flop x {pairs} contributing records / "
-                                    f"{bwd_launches} launches"},
+                                    f"{bwd_launches} launches",
+                     "flop_crosscheck": _flop_crosscheck(),
+                     "all_views_position_backward": all_views},
         "profiled_pass": {"note": "same K steps re-run with views serialised and per-launch CUDA events; "
                                   "stage times below come from it", "ms_per_step": prof["device_ms"] / args.steps},
         "stage_ms_per_step": {k: round(v / args.steps, 4) for k, v in pst["ms"].items()},
@@ -461,6 +471,17 @@ def ours_arm(args, cfg: Config):
     }
     line.update(extras)
     print(json.dumps(line), flush=True)
+
+
+def _flop_crosscheck():
+    """Executed FP32 flops of the same launch from the committed ncu instruction counts
+    (2 FFMA + 4 FFMA2 + FMUL + 2 FMUL2 + FADD + 2 FADD2 per thread instruction), divided by
+    its contributing records: the check of the 290 flop/record constant."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r2_flops_backward.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
 
 
 def spawn_ranks(args):

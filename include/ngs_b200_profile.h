@@ -49,6 +49,10 @@ typedef struct {
      * and their payload bytes (accumulators, overflow votes). */
     int64_t allreduce_calls;
     int64_t allreduce_bytes;
+    /* The primary view's backward launch of each pass alone (the dominant kernel of the
+     * step): summed device time (profiling on) and contributing records (always). */
+    double primary_bwd_ms[4];
+    int64_t primary_contrib_pairs[4];
 } ngs_profile_stats;
 
 /* Timeline of the concurrent schedule (views NOT serialised): one row per stage

@@ -127,7 +127,8 @@ STAGES = ("project", "sort", "raster", "loss", "consts", "bwd_position", "bwd_ro
 class ngs_profile_stats(C.Structure):
     _fields_ = [("ms", C.c_double * 11), ("launches", C.c_int64 * 11), ("total_launches", C.c_int64),
                 ("contrib_pairs", C.c_int64 * 4), ("raster_pairs", C.c_int64), ("renders", C.c_int64),
-                ("group_ms", C.c_double * 6), ("allreduce_calls", C.c_int64), ("allreduce_bytes", C.c_int64)]
+                ("group_ms", C.c_double * 6), ("allreduce_calls", C.c_int64), ("allreduce_bytes", C.c_int64),
+                ("primary_bwd_ms", C.c_double * 4), ("primary_contrib_pairs", C.c_int64 * 4)]
 
 
 class ngs_terms(C.Structure):
@@ -491,6 +492,7 @@ class Context:
                     total_launches=st.total_launches, contrib_pairs=list(st.contrib_pairs),
                     raster_pairs=st.raster_pairs, renders=st.renders,
                     allreduce_calls=st.allreduce_calls, allreduce_bytes=st.allreduce_bytes,
+                    primary_bwd_ms=list(st.primary_bwd_ms), primary_contrib_pairs=list(st.primary_contrib_pairs),
                     # Trainer renders are chained per view into the following backward pass, so each
                     # pass group includes the render before it ("render" stays 0 in trainer steps).
                     group_ms=dict(zip(("render", "render+bwd_position", "render+bwd_rotation", "render+bwd_scaling",

@@ -1291,7 +1291,8 @@ void limbs_to_double(const unsigned long long* limbs, double* acc, size_t count,
 }
 
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
-                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs, int* err) {
+                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs, int* err,
+                     int primary_tag) {
     if (acc_limbs && !err) throw Error(NGS_ERR_INTERNAL, "launch_backward: deterministic mode needs the error flag");
     if (v.pairs == 0 || v.n == 0) return;
     BackwardArgs a;
@@ -1321,7 +1322,8 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     if (own1 <= own0) return;
     a.tile0 = own0 * v.cam.tiles_x;
     const int blocks = (own1 - own0) * v.cam.tiles_x;
-    StageScope st(NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV || pass == kPassGrad ? kPassPosition : pass), s);
+    StageScope st(NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV || pass == kPassGrad ? kPassPosition : pass), s, 1,
+                  primary_tag);
     const bool small = v.cam.tile == 8;
     const int threads = small ? 64 : 256;
     auto go = [&](auto kernel, auto smem_tag) {

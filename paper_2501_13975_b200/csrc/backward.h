@@ -103,6 +103,6 @@ void acc_from_f32(const float* in, double* acc, size_t count, cudaStream_t s);
 
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
                      unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs = nullptr,
-                     int* err = nullptr);
+                     int* err = nullptr, int primary_tag = -1);
 
 }  // namespace ngsb

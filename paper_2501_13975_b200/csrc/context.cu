@@ -598,9 +598,9 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), ctx->stream));
         ctx->err.ensure(1);
         ctx->norm.ensure(5 * kExactWords);
-        ctx->pairs.ensure(5);
+        ctx->pairs.ensure(9);  // [0..3] records per pass (secondary views), [4] raster pairs, [5..8] primary records
         CUDA_CHECK(cudaMemsetAsync(ctx->err.ptr, 0, sizeof(int), ctx->stream));
-        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 5 * sizeof(unsigned long long), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 9 * sizeof(unsigned long long), ctx->stream));
         ctx->scene.n = 0;
         ctx->scene.sh_degree = 0;
         ctx->scene.n_coeffs = 1;
@@ -906,10 +906,13 @@ void accumulate_pass(ngs_context* ctx, int pass, ViewSlot* const* views, int nv,
         compute_pass_consts(pass, ctx->scene, v, views[0]->cam, s);
         if (concurrent && chained) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->rev[i], 0));
         double* acc = ctx->acc.ptr + (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0);
-        unsigned long long* contrib = ctx->pairs.ptr + (pass == kPassPositionUV ? kPassPosition : pass);
+        const int pk = (pass == kPassPositionUV || pass == kPassGrad) ? kPassPosition : pass;
+        // the primary view's records are counted apart (slots 5..8): its launch is the step's dominant kernel
+        unsigned long long* contrib = ctx->pairs.ptr + (i == 0 && pk < 4 ? 5 + pk : pk);
         unsigned long long* vl =
             limbs ? limbs + 4 * (pass == kPassOpacityColor ? static_cast<size_t>(i) * kAccOpColor * stride : 0) : nullptr;
-        launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s, vl, ctx->err.ptr);
+        launch_backward(pass, ctx->scene, v, acc, stride, visible, contrib, s, vl, ctx->err.ptr,
+                        i == 0 && pk < 4 ? pk : -1);
     }
     if (concurrent) ctx->join(nv, ctx->vs.data());
     if (ctx->comm) {
@@ -1747,7 +1750,7 @@ int32_t ngs_profile_reset(ngs_context* ctx) {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         ctx->prof.reset();
-        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 5 * sizeof(unsigned long long), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 9 * sizeof(unsigned long long), ctx->stream));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -1757,10 +1760,13 @@ int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out) {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         ctx->prof.resolve();
-        unsigned long long p[5];
+        unsigned long long p[9];
         CUDA_CHECK(cudaMemcpy(p, ctx->pairs.ptr, sizeof(p), cudaMemcpyDeviceToHost));
         *out = ctx->prof.stats;
-        for (int i = 0; i < 4; ++i) out->contrib_pairs[i] = static_cast<int64_t>(p[i]);
+        for (int i = 0; i < 4; ++i) {
+            out->contrib_pairs[i] = static_cast<int64_t>(p[i] + p[5 + i]);
+            out->primary_contrib_pairs[i] = static_cast<int64_t>(p[5 + i]);
+        }
         out->raster_pairs = static_cast<int64_t>(p[4]);
     });
 }

@@ -153,6 +153,7 @@ struct Profiler {
         int stage;
         cudaEvent_t a, b;
         cudaStream_t s;
+        int tag;  // >= 0: the primary view's backward of pass `tag` (also summed into primary_bwd_ms)
     };
     std::vector<Rec> pending;
     std::vector<ngs_timeline_row> rows;
@@ -175,6 +176,7 @@ struct Profiler {
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
             stats.ms[r.stage] += ms;
+            if (r.tag >= 0 && r.tag < 4) stats.primary_bwd_ms[r.tag] += ms;
             if (timeline && origin) {
                 float t0 = 0, t1 = 0;
                 CUDA_CHECK(cudaEventElapsedTime(&t0, origin, r.a));
@@ -211,7 +213,8 @@ struct StageScope {
     int stage;
     cudaStream_t s;
     cudaEvent_t a = nullptr;
-    StageScope(int stage_, cudaStream_t s_, int launches = 1) : p(g_prof), stage(stage_), s(s_) {
+    int tag;
+    StageScope(int stage_, cudaStream_t s_, int launches = 1, int tag_ = -1) : p(g_prof), stage(stage_), s(s_), tag(tag_) {
         if (!p) return;
         p->stats.launches[stage] += launches;
         p->stats.total_launches += launches;
@@ -223,7 +226,7 @@ struct StageScope {
     ~StageScope() {
         if (!p || !a) return;
         cudaEvent_t b = p->get();
-        if (cudaEventRecord(b, s) == cudaSuccess) p->pending.push_back({stage, a, b, s});
+        if (cudaEventRecord(b, s) == cudaSuccess) p->pending.push_back({stage, a, b, s, tag});
     }
 };
 
