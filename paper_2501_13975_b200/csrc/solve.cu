@@ -15,17 +15,7 @@
 #ifndef NGS_COLOR4_MINB
 #define NGS_COLOR4_MINB 5
 #endif
-// One kernel per Gaussian for the colour solve (stage 1 in registers) instead of the
-// Gram kernel + one thread per (Gaussian, channel) with an HBM eigen scratch.
-// (measured slower: c4 colour 7.3 -> 8.9 ms; the solve is FP64 latency-bound and a third
-// of the threads hides less of it than the scratch round trip costs)
-#ifndef NGS_COLOR_FUSED
-#define NGS_COLOR_FUSED 0
-#endif
-#ifndef NGS_COLORF_MINB
-#define NGS_COLORF_MINB 4
-#endif
-constexpr bool kColorFused = NGS_COLOR_FUSED != 0;
+
 constexpr double kJacobiTol = 1e-28;  // (1e-20 / 1e-16 measured: c4 colour 7.18 -> 7.10 / 7.27 ms, kept)
 
 namespace ngsb {
@@ -493,10 +483,10 @@ __global__ void __launch_bounds__(128) solve_color_gram_k(SceneDev s, ColorViews
 }
 
 // Colour solve, stage 2 (one thread per Gaussian and channel, blockIdx.y = channel).
-// FUSED: one thread per Gaussian computes stage 1 itself (no eigen scratch round trip
-// through HBM) and then the three channels in turn.
-template <int MV, bool FUSED>
-__global__ void __launch_bounds__(128, FUSED ? NGS_COLORF_MINB : (MV == 4 ? NGS_COLOR4_MINB : 2))
+// (One thread per Gaussian with stage 1 in registers and the channels in turn, no eigen
+// scratch in HBM, measured slower: C4 colour 7.3 -> 8.9 ms.)
+template <int MV>
+__global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2)
     solve_color_k(SceneDev s, ColorViews cv, SolveParams sp, const double* __restrict__ acc, size_t stride,
                   const double* __restrict__ eig, SolveOutputs out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -510,32 +500,13 @@ __global__ void __launch_bounds__(128, FUSED ? NGS_COLORF_MINB : (MV == 4 ? NGS_
         // Stage 1's G = E L E^T (SH0: no stage 1, E = I and L unused). G itself is not
         // re-formed: G g = E L E^T g and beta^T G beta = sum_j L_j (E^T beta)_j^2.
         double L[MV][MV], E[MV][MV];
-        if constexpr (FUSED) {
-            if (n > 1) {
-                color_gram<MV>(s, cv, k, L, E);
 #pragma unroll
-                for (int a = 0; a < MV; ++a)
+        for (int a = 0; a < MV; ++a)
 #pragma unroll
-                    for (int b = 0; b < MV; ++b)
-                        if (a != b) L[a][b] = 0.0;
-            } else {
-#pragma unroll
-                for (int a = 0; a < MV; ++a)
-#pragma unroll
-                    for (int b = 0; b < MV; ++b) {
-                        L[a][b] = 0.0;
-                        E[a][b] = a == b ? 1.0 : 0.0;
-                    }
+            for (int b = 0; b < MV; ++b) {
+                L[a][b] = (a == b && n > 1) ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : 0.0;
+                E[a][b] = n > 1 ? eig[static_cast<size_t>(MV * a + b) * stride + k] : (a == b ? 1.0 : 0.0);
             }
-        } else {
-#pragma unroll
-            for (int a = 0; a < MV; ++a)
-#pragma unroll
-                for (int b = 0; b < MV; ++b) {
-                    L[a][b] = (a == b && n > 1) ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : 0.0;
-                    E[a][b] = n > 1 ? eig[static_cast<size_t>(MV * a + b) * stride + k] : (a == b ? 1.0 : 0.0);
-                }
-        }
         double lmax = 0;
 #pragma unroll
         for (int a = 0; a < MV; ++a) lmax = fmax(lmax, L[a][a]);
@@ -549,9 +520,7 @@ __global__ void __launch_bounds__(128, FUSED ? NGS_COLORF_MINB : (MV == 4 ? NGS_
             sq[a] = L[a][a] * isq[a];  // L^1/2 on kept directions, 0 elsewhere
             r += kept[a] ? 1 : 0;
         }
-        const int ch0 = FUSED ? 0 : static_cast<int>(blockIdx.y), ch1 = FUSED ? 3 : ch0 + 1;
-#pragma unroll 1
-        for (int ch = ch0; ch < ch1; ++ch) {
+        const int ch = blockIdx.y;
         double beta_all[MV];
         do {
             double gv[MV], hv[MV];
@@ -709,8 +678,7 @@ __global__ void __launch_bounds__(128, FUSED ? NGS_COLORF_MINB : (MV == 4 ? NGS_
                     if (i < n) s.sh[(static_cast<size_t>(16 * ch + i)) * s.n + k] = (float)((double)cur[i] + delta[i]);
             }
         }
-        }  // channels
-        if (out.accepted && ch0 == 0) out.accepted[k] = 1;
+        if (out.accepted && ch == 0) out.accepted[k] = 1;
     }
     block_add(nsq, out.norm_sq);
 }
@@ -867,7 +835,7 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
                   size_t stride, const SolveOutputs& out, cudaStream_t s) {
     const int n = scene.n;
     if (n == 0) return;
-    StageScope st(NGS_STAGE_SOLVE, s, attr == NGS_COLOR && scene.n_coeffs > 1 && !kColorFused ? 2 : 1);
+    StageScope st(NGS_STAGE_SOLVE, s, attr == NGS_COLOR && scene.n_coeffs > 1 ? 2 : 1);
     switch (attr) {
         case NGS_POSITION:
             solve_position_k<<<blocks_for(n), 256, 0, s>>>(scene, primary, sp, acc, stride, out);
@@ -888,25 +856,16 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
                 if (scene.n_coeffs > 1) gram_kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, cv.eig, stride);
                 ch_kernel<<<dim3(blocks_for(n, 128), 3), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
             };
-            if constexpr (kColorFused) {
-                auto fused = [&](auto kernel) {
-                    kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
-                };
-                if (cv.n_views <= 1) fused(solve_color_k<1, true>);
-                else if (cv.n_views <= 2) fused(solve_color_k<2, true>);
-                else if (cv.n_views <= 4) fused(solve_color_k<4, true>);
-                else if (cv.n_views <= 8) fused(solve_color_k<8, true>);
-                else fused(solve_color_k<16, true>);
-            } else if (cv.n_views <= 1) {
-                run(solve_color_gram_k<1>, solve_color_k<1, false>);
+            if (cv.n_views <= 1) {
+                run(solve_color_gram_k<1>, solve_color_k<1>);
             } else if (cv.n_views <= 2) {
-                run(solve_color_gram_k<2>, solve_color_k<2, false>);
+                run(solve_color_gram_k<2>, solve_color_k<2>);
             } else if (cv.n_views <= 4) {
-                run(solve_color_gram_k<4>, solve_color_k<4, false>);
+                run(solve_color_gram_k<4>, solve_color_k<4>);
             } else if (cv.n_views <= 8) {
-                run(solve_color_gram_k<8>, solve_color_k<8, false>);
+                run(solve_color_gram_k<8>, solve_color_k<8>);
             } else {  // knn 8..15 (the reference's overshoot ablation uses knn = 8): spills, rarely used
-                run(solve_color_gram_k<16>, solve_color_k<16, false>);
+                run(solve_color_gram_k<16>, solve_color_k<16>);
             }
             break;
         }
