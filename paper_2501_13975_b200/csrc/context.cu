@@ -175,6 +175,7 @@ struct ngs_context {
     // restores, first-order updates, every trainer step start): trainer renders with an
     // unchanged version and camera keep their slot's depth order (RenderSync::pos_version).
     unsigned long long pos_version = 1;
+    unsigned long long sh_version = 1;  // bumped whenever the SH coefficients may change (RenderSync::sh_version)
     bool order_reuse = true;  // NGS_ORDER_REUSE=0 disables it (tests compare both)
 
     ~ngs_context() {
@@ -631,6 +632,7 @@ int32_t ngs_set_scene(ngs_context* ctx, const ngs_scene* s) {
             for (int c = 0; c < 48; ++c) sh[static_cast<size_t>(c) * n + k] = static_cast<float>(s->sh[48 * k + c]);
         }
         ++ctx->pos_version;
+        ++ctx->sh_version;
         ctx->pos_sigma.ensure(std::max(n, 1));
         ctx->scale.ensure(std::max(n, 1));
         ctx->quat.ensure(std::max(n, 1));
@@ -1339,6 +1341,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         rs.pair_counter = ctx->pairs.ptr + 4;
         if (concurrent && !join) rs.projected = ctx->pev[i];
         rs.pos_version = ctx->order_reuse ? ctx->pos_version : 0;
+        rs.sh_version = ctx->order_reuse ? ctx->sh_version : 0;
         render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
         if (v.raster.owns_rows()) {
             if (upload_targets && concurrent) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->tev[i], 0));
@@ -1357,6 +1360,7 @@ float first_order_step(ngs_context* ctx, int view_id, double norms[5]) {
     const size_t stride = static_cast<size_t>(std::max(n, 1));
     cudaStream_t s = ctx->stream;
     ++ctx->pos_version;  // every first-order step moves the positions
+    ++ctx->sh_version;   // ... and the colours
     const bool adam = T.cfg.optimizer == NGS_OPT_ADAM;
     if (adam && T.adam_n != n) {
         // Moments are sized for (and belong to) one scene: (re)start them whenever the scene
@@ -1477,6 +1481,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                 marks.emplace_back(ge++, group);
             };
             ++ctx->pos_version;  // step start / snapshot restore
+            ++ctx->sh_version;
             CUDA_CHECK(cudaEventRecord(ctx->ev0, s));
             CUDA_CHECK(cudaMemsetAsync(ctx->norm.ptr, 0, 5 * kExactWords * sizeof(unsigned long long), s));
             CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), s));
@@ -1498,6 +1503,7 @@ extern "C" int32_t ngs_trainer_step(ngs_context* ctx, int32_t view_id, ngs_itera
                 }
                 SolveOutputs so{nullptr, nullptr, nullptr, ctx->norm.ptr + attr * kExactWords, ctx->err.ptr};
                 if (attr == NGS_POSITION) ++ctx->pos_version;  // the next renders re-sort by depth
+                if (attr == NGS_COLOR) ++ctx->sh_version;      // ... and re-evaluate the view colours
                 launch_solve(attr, ctx->scene, views[0]->cam, views[0]->raster.lambda_lp, views[0]->flags.ptr,
                              color_views(ctx, views.data(), nv), base, ctx->acc.ptr, stride, so, s);
                 mark(5);

@@ -95,6 +95,8 @@ struct ViewSlot {
     CameraDev cam{};
     unsigned long long order_version = 0;  // RenderSync::pos_version of the last depth sort (0: not reusable)
     bool keep_order = false;               // this render reuses the sorted depth order (prepare_view)
+    unsigned long long color_sh_version = 0;  // RenderSync::sh_version of the slot's view colours
+    bool keep_color = false;               // this render reuses the view colours (same positions, camera, SH)
     CameraDev order_cam{};
     int order_n = -1;
     int W = 0, H = 0, T = 0;
@@ -241,6 +243,9 @@ struct RenderSync {
     // function of the positions and the camera only, so a slot re-rendered with the same
     // camera and version keeps its sorted order and skips K2.
     unsigned long long pos_version = 0;
+    // SH version of the scene (0 = unknown): with the same position version and camera as well,
+    // the view colours (SH evaluation, clamp flags) of the slot's last projection still hold.
+    unsigned long long sh_version = 0;
 };
 void render_view(const SceneDev& scene, ViewSlot& v, bool want_debug, int* d_err, cudaStream_t s,
                  const RenderSync& sync = RenderSync{});

@@ -113,6 +113,10 @@ struct ProjOut {
     unsigned int* depth_key;
     int* ids;
     double* entry64;
+    // The slot's view colours (c~ in rb.zw / rc.x) and clamp flags are still those of the
+    // current positions, SH coefficients and camera (ProjOut-level cache, prepare_view):
+    // skip the SH evaluation and leave them in place.
+    bool keep_color;
 };
 
 // K1: per-kernel projection, SH colour and tile extent (FP64 math, coalesced
@@ -135,26 +139,28 @@ __device__ __forceinline__ void project_one(const SceneDev& s, int k, const Came
         o.depth[k] = 0;
         return;
     }
-    D3 r;
-    double rn;
-    if (!view_direction(cam, p, r, rn)) {
-        atomicOr(err, kErrDegenerate);  // DegenerateGeometry
-        r = d3(0, 0, 1);
-    }
-    double basis[16];
-    sh_basis(r, s.sh_degree, basis);
-    double col[3];
+    double col[3] = {0.0, 0.0, 0.0};
     uint8_t f = kProjected;
+    if (!o.keep_color) {
+        D3 r;
+        double rn;
+        if (!view_direction(cam, p, r, rn)) {
+            atomicOr(err, kErrDegenerate);  // DegenerateGeometry
+            r = d3(0, 0, 1);
+        }
+        double basis[16];
+        sh_basis(r, s.sh_degree, basis);
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-        double v = 0;
+        for (int ch = 0; ch < 3; ++ch) {
+            double v = 0;
 #pragma unroll
-        for (int i = 0; i < 16; ++i)  // fully unrolled (basis in registers, loads issued together)
-            if (i < s.n_coeffs) v += basis[i] * static_cast<double>(s.sh[(16 * ch + i) * s.n + k]);
-        v += kColorOffset;
-        const bool clamped = v <= 0.0;
-        col[ch] = clamped ? 0.0 : v;
-        if (clamped) f |= static_cast<uint8_t>(kClamp0 << ch);
+            for (int i = 0; i < 16; ++i)  // fully unrolled (basis in registers, loads issued together)
+                if (i < s.n_coeffs) v += basis[i] * static_cast<double>(s.sh[(16 * ch + i) * s.n + k]);
+            v += kColorOffset;
+            const bool clamped = v <= 0.0;
+            col[ch] = clamped ? 0.0 : v;
+            if (clamped) f |= static_cast<uint8_t>(kClamp0 << ch);
+        }
     }
     const double qa = pr.s11 / det, qb = -pr.s01 / det, qc = pr.s00 / det;
     double x0, y0, x1, y1;
@@ -184,14 +190,22 @@ __device__ __forceinline__ void project_one(const SceneDev& s, int k, const Came
     off = off || ty0 > ty1;
     o.rect[k] = off ? make_int4(1, 1, 0, 0) : make_int4(tx0, ty0, tx1, ty1);
     o.tiles_touched[k] = off ? 0 : (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-    o.flags[k] = f;
     o.depth[k] = pr.depth;
     if (o.depth_key) o.depth_key[k] = depth_sort_key(pr.depth);
     o.pix[k] = make_double2(pr.px, pr.py);
     o.ra[k] = make_float4(0.f, 0.f, static_cast<float>(qa), static_cast<float>(qb));
-    o.rb[k] = make_float4(static_cast<float>(qc), ps.w, static_cast<float>(col[0]), static_cast<float>(col[1]));
-    o.rc[k] = make_float4(static_cast<float>(col[2]), static_cast<float>(pr.s00), static_cast<float>(pr.s01),
-                          static_cast<float>(pr.s11));
+    if (o.keep_color) {  // colours and clamp flags stay; the geometry halves are rewritten
+        reinterpret_cast<float2*>(o.rb)[2 * static_cast<size_t>(k)] = make_float2(static_cast<float>(qc), ps.w);
+        float* rc = reinterpret_cast<float*>(o.rc + k);
+        rc[1] = static_cast<float>(pr.s00);
+        rc[2] = static_cast<float>(pr.s01);
+        rc[3] = static_cast<float>(pr.s11);
+    } else {
+        o.flags[k] = f;
+        o.rb[k] = make_float4(static_cast<float>(qc), ps.w, static_cast<float>(col[0]), static_cast<float>(col[1]));
+        o.rc[k] = make_float4(static_cast<float>(col[2]), static_cast<float>(pr.s00), static_cast<float>(pr.s01),
+                              static_cast<float>(pr.s11));
+    }
     if (o.entry64) {
         double* e = o.entry64 + kEntry64 * static_cast<size_t>(k);
         e[0] = pr.px;
@@ -478,6 +492,9 @@ bool prepare_view(const SceneDev& scene, ViewSlot& v, bool want_debug, const Ren
     v.order_cam = v.cam;
     v.order_n = n;
     v.keep_order = keep_order;
+    // View colours depend on the positions, the camera and the SH coefficients only.
+    v.keep_color = keep_order && !want_debug && sync.sh_version != 0 && v.color_sh_version == sync.sh_version;
+    v.color_sh_version = sync.sh_version;
     return keep_order;
 }
 
@@ -490,7 +507,7 @@ void project_views(const SceneDev& scene, ViewSlot* const* views, int nv, bool w
         ViewSlot& v = *views[i];
         const ProjOut o{v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr, v.pix.ptr, v.depth.ptr, v.rect.ptr,
                         v.tiles_touched.ptr, v.flags.ptr, v.keep_order ? nullptr : v.depth_key.ptr,
-                        v.keep_order ? nullptr : v.order.ptr, want_debug ? v.entry64.ptr : nullptr};
+                        v.keep_order ? nullptr : v.order.ptr, want_debug ? v.entry64.ptr : nullptr, v.keep_color};
         StageScope st(NGS_STAGE_PROJECT, s);
         project_view_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, o, d_err);
         CUDA_LAUNCH_CHECK();
@@ -517,6 +534,7 @@ void bin_and_raster(const SceneDev& scene, ViewSlot& v, int* d_err, cudaStream_t
         // Multi-GPU: another rank owns this view; only its projection (flags for the
         // replicated colour solve) is needed here. The depth order was not sorted.
         v.order_version = 0;
+        v.color_sh_version = 0;
         v.pairs = 0;
         v.valid = true;
         return;
