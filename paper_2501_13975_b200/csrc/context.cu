@@ -1315,14 +1315,18 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
             v.raster = to_raster(&T.cfg.raster);
             apply_shard(plan[i], v.raster);
             v.loss = to_loss(&T.cfg.loss);
+            v.target_ext = nullptr;
             if (!v.raster.owns_rows()) continue;  // projection only: no target, no loss
+            if (!T.cfg.host_targets) {  // device-resident targets: the loss reads them in place
+                v.target_ext = (i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr;
+                if (concurrent) CUDA_CHECK(cudaEventRecord(ctx->tev[i], ctx->cs));
+                continue;
+            }
             const size_t npx = static_cast<size_t>(cam.width) * cam.height;
             v.target.ensure(3 * npx);
             cudaStream_t s = concurrent ? ctx->cs : ctx->stream;
-            const double* src = T.cfg.host_targets ? ((i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id])
-                                                   : ((i == 0) ? T.targets[cam_id].ptr : T.down_targets[cam_id].ptr);
-            CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx,
-                                       T.cfg.host_targets ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+            const double* src = (i == 0) ? T.host_targets[cam_id] : T.host_down_targets[cam_id];
+            CUDA_CHECK(cudaMemcpyAsync(v.target.ptr, src, sizeof(double) * 3 * npx, cudaMemcpyHostToDevice, s));
             if (concurrent) CUDA_CHECK(cudaEventRecord(ctx->tev[i], s));
         }
     }

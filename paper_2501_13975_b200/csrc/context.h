@@ -125,7 +125,6 @@ struct ViewSlot {
     DevBuf<int> pair_val, pair_val_alt;
     DevBuf<int2> ranges;
     DevBuf<int> counters;    // [0] entries n, [1] pairs P, [2] min(P, capacity)
-    int n_host = 0;          // pinned-lifetime source of the counters[0] upload
     void* sort_scratch = nullptr;
     // K6 forward raster outputs (planar [3][H][W])
     DevBuf<double> image;   // FP64 (see raster_forward_k)
@@ -133,6 +132,9 @@ struct ViewSlot {
     DevBuf<int> last;       // index into the tile list of the last contributing splat, -1 if none
     // K7 loss fields
     DevBuf<double> target;  // planar [3][H][W], FP64 like the reference Image
+    // Device-resident trainer targets are read in place (no per-step D2D copy into `target`).
+    const double* target_ext = nullptr;
+    const double* target_ptr() const { return target_ext ? target_ext : target.ptr; }
     DevBuf<double> fields;  // 9 center fields x 3 channels x H x W
     DevBuf<float> loss_grad, loss_hess;  // planar [3][H][W]
     DevBuf<unsigned long long> loss_sums;  // exact sums (kExactWords each): [0] sum d^2, [1] sum ssim

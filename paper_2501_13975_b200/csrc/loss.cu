@@ -599,11 +599,11 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     auto run = [&](auto fields_kernel, auto derivs_kernel) {
         if (ssim) {
             v.fields.ensure(27 * npx);
-            fields_kernel<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
+            fields_kernel<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target_ptr(), win, L.c1, L.c2, v.fields.ptr,
                                                v.loss_sums.ptr, row0, own0, own1);
             CUDA_LAUNCH_CHECK();
         }
-        derivs_kernel<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.lambda,
+        derivs_kernel<<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target_ptr(), win, L.lambda,
                                            ssim ? v.fields.ptr : nullptr, v.loss_grad.ptr, v.loss_hess.ptr,
                                            v.loss_sums.ptr, row0, own0, own1);
         CUDA_LAUNCH_CHECK();
@@ -616,11 +616,11 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
         ensure_dynamic_smem(reinterpret_cast<const void*>(ssim_derivs32_k), sm_d);
         if (ssim) {
             v.fields.ensure(27 * npx);
-            ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, v.fields.ptr,
+            ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target_ptr(), win, L.c1, L.c2, v.fields.ptr,
                                                    v.loss_sums.ptr, r32a, own0, own1);
             CUDA_LAUNCH_CHECK();
         }
-        ssim_derivs32_k<<<g32, 256, ssim ? sm_d : 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.lambda,
+        ssim_derivs32_k<<<g32, 256, ssim ? sm_d : 0, s>>>(v.W, v.H, v.image.ptr, v.target_ptr(), win, L.lambda,
                                                            ssim ? v.fields.ptr : nullptr, v.loss_grad.ptr,
                                                            v.loss_hess.ptr, v.loss_sums.ptr, r32a, own0, own1);
         CUDA_LAUNCH_CHECK();
@@ -653,18 +653,18 @@ void compute_loss_value(ViewSlot& v, cudaStream_t s) {
     v.loss_sums.ensure(2 * kExactWords);
     CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * kExactWords * sizeof(unsigned long long), s));
     StageScope st(NGS_STAGE_LOSS, s, 2);
-    l2_sum_k<<<std::min<size_t>((3 * npx + 255) / 256, 4 * 148), 256, 0, s>>>(v.image.ptr, v.target.ptr, 3 * npx,
+    l2_sum_k<<<std::min<size_t>((3 * npx + 255) / 256, 4 * 148), 256, 0, s>>>(v.image.ptr, v.target_ptr(), 3 * npx,
                                                                            v.loss_sums.ptr);
     CUDA_LAUNCH_CHECK();
     if (win.half == kFH) {
         const dim3 g32((v.W + kFT - 1) / kFT, (v.H + kFT - 1) / kFT, 3);
         const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1);
         ensure_dynamic_smem(reinterpret_cast<const void*>(ssim_fields32_k), sm_f);
-        ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, nullptr,
+        ssim_fields32_k<<<g32, 256, sm_f, s>>>(v.W, v.H, v.image.ptr, v.target_ptr(), win, L.c1, L.c2, nullptr,
                                                v.loss_sums.ptr, 0, 0, v.H);
     } else {
         const dim3 grid((v.W + kLT - 1) / kLT, (v.H + kLT - 1) / kLT, 3);
-        ssim_fields_k<0><<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target.ptr, win, L.c1, L.c2, nullptr,
+        ssim_fields_k<0><<<grid, 256, 0, s>>>(v.W, v.H, v.image.ptr, v.target_ptr(), win, L.c1, L.c2, nullptr,
                                               v.loss_sums.ptr, 0, 0, v.H);
     }
     CUDA_LAUNCH_CHECK();

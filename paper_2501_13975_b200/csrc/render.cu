@@ -224,8 +224,12 @@ __device__ __forceinline__ void project_one(const SceneDev& s, int k, const Came
 }
 
 // One launch per view (a fused all-views launch measured slower: DESIGN.md §6).
-__global__ void __launch_bounds__(256) project_view_k(SceneDev s, CameraDev cam, RasterParams rp, ProjOut o, int* err) {
+// Also publishes the entry count for the device-side sort (`n_out`, the slot's counters[0]):
+// no host->device copy per render.
+__global__ void __launch_bounds__(256) project_view_k(SceneDev s, CameraDev cam, RasterParams rp, ProjOut o, int* err,
+                                                      int* n_out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0) *n_out = s.n;
     if (k < s.n) project_one(s, k, cam, rp, o, err);
 }
 
@@ -509,7 +513,7 @@ void project_views(const SceneDev& scene, ViewSlot* const* views, int nv, bool w
                         v.tiles_touched.ptr, v.flags.ptr, v.keep_order ? nullptr : v.depth_key.ptr,
                         v.keep_order ? nullptr : v.order.ptr, want_debug ? v.entry64.ptr : nullptr, v.keep_color};
         StageScope st(NGS_STAGE_PROJECT, s);
-        project_view_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, o, d_err);
+        project_view_k<<<blocks_for(n), 256, 0, s>>>(scene, v.cam, v.raster, o, d_err, v.counters.ptr);
         CUDA_LAUNCH_CHECK();
     }
 }
@@ -543,8 +547,6 @@ void bin_and_raster(const SceneDev& scene, ViewSlot& v, int* d_err, cudaStream_t
         StageScope st(NGS_STAGE_SORT, s, keep_order ? 4 : 11);  // sort 2 + 4 passes, fix-up, gather, scan 3
         // K2: global depth order, exactly (FP64 depth, kernel id): 4-pass radix sort of the
         // FP32 depth key (stable over the id-ordered input) + fix-up of equal-key runs.
-        v.n_host = n;
-        CUDA_CHECK(cudaMemcpyAsync(v.counters.ptr, &v.n_host, sizeof(int), cudaMemcpyHostToDevice, s));
         if (!keep_order) {
             radix_sort_pairs(v.depth_key.ptr, v.order.ptr, v.depth_key_alt.ptr, v.order_alt.ptr, v.counters.ptr, n, 32,
                              sc, s);
