@@ -3,7 +3,8 @@ downsample 4) and a C2-shaped slice (30K Gaussians, 256x256, SH3, c2's footprint
 law), the CUDA library (libngs_b200.so) against the compiled reference
 (oracle/_ref/libngs_ref.so) through the same C-ABI.
 
-Fixture: the reference's own ``synth_scene`` (synth.hpp:71-154) generates the
+A third fixture, c3slice, is C3-shaped (16:9 at 320x180 with ragged edge tiles, SH3,
+c3's footprint law). Fixture: the reference's own ``synth_scene`` (synth.hpp:71-154) generates the
 scenes and cameras. Its images are rendered at 16x16 only to keep the
 generator's single-threaded ``render_reference`` cheap: the RNG stream, the
 kernels, the jittered init and the view/proj matrices do not depend on the
@@ -81,13 +82,18 @@ def box_downsample(img, f):
     return img[: h // f * f, : w // f * f].reshape(h // f, f, w // f, f, 3).mean(axis=(1, 3))
 
 
-def make_fixture(kernels, sh_degree, scale_mul, seed):
-    p = dict(seed=seed, kernels=kernels, views=16, probe_views=4, width=16, height=16, sh_degree=sh_degree,
-             secondary_downsample=1)
+def make_fixture(kernels, sh_degree, scale_mul, seed, width=256, height=256):
+    # synth_scene's images are rendered small (16x16, or 1/10 of a 16:9 size): the aspect fixes the projection
+    # matrix (synth.hpp:108-110); the RNG stream and the scene do not depend on the size.
+    aspect = width / height
+    sw, sh = (16, 16) if width == height else (width // 10, height // 10)  # 320x180 -> 32x18: same aspect
+    p = dict(seed=seed, kernels=kernels, views=16, probe_views=4, width=sw, height=sh,
+             sh_degree=sh_degree, secondary_downsample=1)
     if scale_mul != 1.0:
         p.update(kernel_scale_min=0.05 * scale_mul, kernel_scale_max=0.12 * scale_mul)
     d = synth(**p)
-    cams = [capi.Camera(c.view, c.proj, 256, 256) for c in d["cameras"]]
+    assert abs(d["cameras"][0].width / d["cameras"][0].height - aspect) < 1e-12
+    cams = [capi.Camera(c.view, c.proj, width, height) for c in d["cameras"]]
     r = ref().context()
     r.set_scene(d["truth"])
     ro = ref().default_raster()
@@ -102,11 +108,19 @@ def make_fixture(kernels, sh_degree, scale_mul, seed):
 C2_SLICE_SCALE = (100.0 / 300_000) ** (1.0 / 3.0) * 800.0 / 256.0
 
 
-@pytest.fixture(scope="module", params=["c1", "c2slice"])
+# C3's 16:9 aspect with ragged edge tiles (320x180: 20 x 11.25 tiles; secondaries 80x45
+# with 8x8 tiles), SH3, the c3 footprint law at this width (3M at 1920 -> 20K at 320 keeps
+# the splats per pixel).
+C3_SLICE_SCALE = (100.0 / 3_000_000) ** (1.0 / 3.0) * 1920.0 / 320.0
+
+
+@pytest.fixture(scope="module", params=["c1", "c2slice", "c3slice"])
 def fixture(request):
     if request.param == "c1":
         return request.param, make_fixture(10_000, 0, 1.0, 1000)
-    return request.param, make_fixture(30_000, 3, C2_SLICE_SCALE, 1001)
+    if request.param == "c2slice":
+        return request.param, make_fixture(30_000, 3, C2_SLICE_SCALE, 1001)
+    return request.param, make_fixture(20_000, 3, C3_SLICE_SCALE, 1002, 320, 180)
 
 
 @pytest.fixture(scope="module")
