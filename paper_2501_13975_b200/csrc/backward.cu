@@ -883,7 +883,7 @@ struct BackwardSmem {
 };
 
 template <int PASS, int TILE>
-__global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k(BackwardArgs a) {
+__device__ __forceinline__ void backward_body(const BackwardArgs& a, const int block) {
     using TR = PassTraits<PASS>;
     using SM = BackwardSmem<PASS, TILE>;
     constexpr int NT = TILE * TILE, NW = NT / 32;
@@ -904,7 +904,7 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
     auto& s_maxlast = S.maxlast;
     unsigned long long block_pairs = 0;
 
-    const int tile = a.tile0 + blockIdx.x;  // owned tile rows only (multi-GPU shard)
+    const int tile = a.tile0 + block;  // owned tile rows only (multi-GPU shard)
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int lx, ly;
     WarpBox<TILE>::pixel(threadIdx.x, lx, ly);
@@ -1209,6 +1209,27 @@ __global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k
     if (a.contrib_pairs && lane == 0 && block_pairs) atomicAdd(a.contrib_pairs, block_pairs);
 }
 
+template <int PASS, int TILE>
+__global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_k(BackwardArgs a) {
+    backward_body<PASS, TILE>(a, blockIdx.x);
+}
+
+// The small (8x8-tile) secondary views of a pass in ONE launch: a view's blocks follow the
+// previous view's (block_end: inclusive prefix of the per-view block counts). Each view alone
+// is 625 blocks of 2 warps at c2 (~10 % occupancy, latency-bound); together they fill the SMs.
+template <int PASS, int TILE>
+__global__ void __maxnreg__(TILE == 16 ? PassTraits<PASS>::R16 : 128) backward_batch_k(BackwardBatch b) {
+    const int bid = blockIdx.x;
+    int v = 0;
+#pragma unroll
+    for (int i = 0; i < kBackwardBatch - 1; ++i)
+        if (i + 1 < b.nv && bid >= b.block_end[i]) v = i + 1;
+    const int first = v == 0 ? 0 : b.block_end[v == 1 ? 0 : v == 2 ? 1 : 2];
+    // static-index selects (a dynamic index into the kernel parameters would copy them to local memory)
+    const BackwardArgs& a = v == 0 ? b.a[0] : v == 1 ? b.a[1] : v == 2 ? b.a[2] : b.a[3];
+    backward_body<PASS, TILE>(a, bid - first);
+}
+
 }  // namespace
 
 void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s,
@@ -1290,12 +1311,13 @@ void limbs_to_double(const unsigned long long* limbs, double* acc, size_t count,
     CUDA_LAUNCH_CHECK();
 }
 
-void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
-                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs, int* err,
-                     int primary_tag) {
-    if (acc_limbs && !err) throw Error(NGS_ERR_INTERNAL, "launch_backward: deterministic mode needs the error flag");
-    if (v.pairs == 0 || v.n == 0) return;
-    BackwardArgs a;
+namespace {
+
+// Kernel arguments of one view's backward; false when the view has nothing to traverse.
+bool make_backward_args(const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
+                        unsigned long long* contrib_pairs, unsigned long long* acc_limbs, int* err, BackwardArgs& a,
+                        int& blocks) {
+    if (v.pairs == 0 || v.n == 0) return false;
     a.tiles_x = v.cam.tiles_x;
     a.W = v.W;
     a.H = v.H;
@@ -1319,44 +1341,77 @@ void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, 
     a.contrib_pairs = contrib_pairs;
     a.err = err;
     const int own0 = std::max(0, v.raster.own_y0), own1 = std::min(v.cam.tiles_y, v.raster.own_y1);
-    if (own1 <= own0) return;
+    if (own1 <= own0) return false;
     a.tile0 = own0 * v.cam.tiles_x;
-    const int blocks = (own1 - own0) * v.cam.tiles_x;
-    StageScope st(NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV || pass == kPassGrad ? kPassPosition : pass), s, 1,
-                  primary_tag);
-    const bool small = v.cam.tile == 8;
-    const int threads = small ? 64 : 256;
-    auto go = [&](auto kernel, auto smem_tag) {
-        using SM = typename decltype(smem_tag)::type;
-        ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), sizeof(SM));
-        kernel<<<blocks, threads, sizeof(SM), s>>>(a);
-    };
-    switch (pass) {
-        case kPassPosition:
-            if (small) go(backward_k<kPassPosition, 8>, SmemTag<BackwardSmem<kPassPosition, 8>>{});
-            else go(backward_k<kPassPosition, 16>, SmemTag<BackwardSmem<kPassPosition, 16>>{});
-            break;
-        case kPassPositionUV:
-            if (small) go(backward_k<kPassPositionUV, 8>, SmemTag<BackwardSmem<kPassPositionUV, 8>>{});
-            else go(backward_k<kPassPositionUV, 16>, SmemTag<BackwardSmem<kPassPositionUV, 16>>{});
-            break;
-        case kPassGrad:
-            if (small) go(backward_k<kPassGrad, 8>, SmemTag<BackwardSmem<kPassGrad, 8>>{});
-            else go(backward_k<kPassGrad, 16>, SmemTag<BackwardSmem<kPassGrad, 16>>{});
-            break;
-        case kPassRotation:
-            if (small) go(backward_k<kPassRotation, 8>, SmemTag<BackwardSmem<kPassRotation, 8>>{});
-            else go(backward_k<kPassRotation, 16>, SmemTag<BackwardSmem<kPassRotation, 16>>{});
-            break;
-        case kPassScaling:
-            if (small) go(backward_k<kPassScaling, 8>, SmemTag<BackwardSmem<kPassScaling, 8>>{});
-            else go(backward_k<kPassScaling, 16>, SmemTag<BackwardSmem<kPassScaling, 16>>{});
-            break;
-        case kPassOpacityColor:
-            if (small) go(backward_k<kPassOpacityColor, 8>, SmemTag<BackwardSmem<kPassOpacityColor, 8>>{});
-            else go(backward_k<kPassOpacityColor, 16>, SmemTag<BackwardSmem<kPassOpacityColor, 16>>{});
-            break;
+    blocks = (own1 - own0) * v.cam.tiles_x;
+    return true;
+}
+
+template <int PASS, int TILE>
+struct BackwardKernels {
+    using SM = BackwardSmem<PASS, TILE>;
+    static void single(const BackwardArgs& a, int blocks, cudaStream_t s) {
+        ensure_dynamic_smem(reinterpret_cast<const void*>(backward_k<PASS, TILE>), sizeof(SM));
+        backward_k<PASS, TILE><<<blocks, TILE * TILE, sizeof(SM), s>>>(a);
     }
+    static void batch(const BackwardBatch& b, int blocks, cudaStream_t s) {
+        ensure_dynamic_smem(reinterpret_cast<const void*>(backward_batch_k<PASS, TILE>), sizeof(SM));
+        backward_batch_k<PASS, TILE><<<blocks, TILE * TILE, sizeof(SM), s>>>(b);
+    }
+};
+
+template <template <int, int> class K, typename F>
+void dispatch_pass(int pass, bool small, F&& f) {
+    switch (pass) {
+        case kPassPosition: small ? f(K<kPassPosition, 8>{}) : f(K<kPassPosition, 16>{}); break;
+        case kPassPositionUV: small ? f(K<kPassPositionUV, 8>{}) : f(K<kPassPositionUV, 16>{}); break;
+        case kPassGrad: small ? f(K<kPassGrad, 8>{}) : f(K<kPassGrad, 16>{}); break;
+        case kPassRotation: small ? f(K<kPassRotation, 8>{}) : f(K<kPassRotation, 16>{}); break;
+        case kPassScaling: small ? f(K<kPassScaling, 8>{}) : f(K<kPassScaling, 16>{}); break;
+        default: small ? f(K<kPassOpacityColor, 8>{}) : f(K<kPassOpacityColor, 16>{}); break;
+    }
+}
+
+int stage_of(int pass) {
+    return NGS_STAGE_BWD_POSITION + (pass == kPassPositionUV || pass == kPassGrad ? kPassPosition : pass);
+}
+
+}  // namespace
+
+void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
+                     unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs, int* err,
+                     int primary_tag) {
+    if (acc_limbs && !err) throw Error(NGS_ERR_INTERNAL, "launch_backward: deterministic mode needs the error flag");
+    BackwardArgs a;
+    int blocks = 0;
+    if (!make_backward_args(scene, v, acc, acc_stride, visible, contrib_pairs, acc_limbs, err, a, blocks)) return;
+    StageScope st(stage_of(pass), s, 1, primary_tag);
+    dispatch_pass<BackwardKernels>(pass, v.cam.tile == 8, [&](auto k) { decltype(k)::single(a, blocks, s); });
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_backward_batch(int pass, const SceneDev& scene, ViewSlot* const* views, int nv, double* const* acc,
+                           size_t acc_stride, uint8_t* visible, unsigned long long* contrib_pairs, cudaStream_t s,
+                           unsigned long long* const* acc_limbs, int* err) {
+    if (nv > kBackwardBatch) throw Error(NGS_ERR_INTERNAL, "launch_backward_batch: too many views");
+    BackwardBatch b{};
+    int total = 0, tile = 0;
+    for (int i = 0; i < nv; ++i) {
+        if (acc_limbs && acc_limbs[i] && !err)
+            throw Error(NGS_ERR_INTERNAL, "launch_backward: deterministic mode needs the error flag");
+        int blocks = 0;
+        if (!make_backward_args(scene, *views[i], acc[i], acc_stride, visible, contrib_pairs,
+                                acc_limbs ? acc_limbs[i] : nullptr, err, b.a[b.nv], blocks))
+            continue;
+        if (tile != 0 && views[i]->cam.tile != tile) throw Error(NGS_ERR_INTERNAL, "backward batch: mixed tile sizes");
+        tile = views[i]->cam.tile;
+        total += blocks;
+        b.block_end[b.nv++] = total;
+    }
+    if (b.nv == 0) return;
+    for (int i = b.nv; i < kBackwardBatch; ++i) b.block_end[i] = total;
+    StageScope st(stage_of(pass), s, 1);
+    dispatch_pass<BackwardKernels>(pass, tile == 8, [&](auto k) { decltype(k)::batch(b, total, s); });
     CUDA_LAUNCH_CHECK();
 }
 

@@ -86,6 +86,14 @@ struct BackwardArgs {
     int* err;                            // device error flag (kErrFixedRange in deterministic mode)
 };
 
+// Up to kBackwardBatch views of one pass in one launch (launch_backward_batch).
+constexpr int kBackwardBatch = 4;
+struct BackwardBatch {
+    int nv;
+    int block_end[kBackwardBatch];
+    BackwardArgs a[kBackwardBatch];
+};
+
 void compute_pass_consts(int pass, const SceneDev& scene, ViewSlot& v, const CameraDev& primary, cudaStream_t s,
                          float* out = nullptr);  // out: destination (default v.consts)
 // Deterministic accumulation: each FP32 partial is converted exactly to a 128-bit
@@ -104,5 +112,10 @@ void acc_from_f32(const float* in, double* acc, size_t count, cudaStream_t s);
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
                      unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs = nullptr,
                      int* err = nullptr, int primary_tag = -1);
+// The same for nv <= kBackwardBatch views with the same tile size in ONE launch (the small
+// secondary views of a pass); per-view accumulator and counter pointers.
+void launch_backward_batch(int pass, const SceneDev& scene, ViewSlot* const* views, int nv, double* const* acc,
+                           size_t acc_stride, uint8_t* visible, unsigned long long* contrib_pairs, cudaStream_t s,
+                           unsigned long long* const* acc_limbs, int* err);
 
 }  // namespace ngsb
