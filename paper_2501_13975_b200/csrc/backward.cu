@@ -17,6 +17,8 @@
 // by the *_consts kernels and staged through shared memory per batch.
 #include <algorithm>
 
+#include <cstdio>
+
 #include "backward.h"
 #include "geometry.cuh"
 #include "splat.cuh"
@@ -834,6 +836,10 @@ __global__ void limbs_to_double_k(const unsigned long long* __restrict__ limbs, 
 #endif
 constexpr bool kBwdTma = NGS_BWD_TMA != 0;
 
+#ifdef NGS_COUNT_CANDIDATES
+__device__ unsigned long long g_cand[6][6];
+#endif
+
 // Per-warp record queue (ring of 64 entries) between the two phases.
 constexpr int kQ = 64;
 // Two float4 per record (one STS.128 / LDS.128 each, consecutive slots: conflict-free)
@@ -1160,6 +1166,14 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
                     }
                 }
                 const unsigned ballot = __ballot_sync(0xffffffffu, contrib);
+#ifdef NGS_COUNT_CANDIDATES
+                if (lane == 0) {  // debug: [PASS][0] candidates, [1] with >= 1 record, [2] records; [3] = TILE 8
+                    const int t = TILE == 8 ? 3 : 0;
+                    atomicAdd(&g_cand[PASS][t + 0], 1ull);
+                    if (ballot) atomicAdd(&g_cand[PASS][t + 1], 1ull);
+                    atomicAdd(&g_cand[PASS][t + 2], static_cast<unsigned long long>(__popc(ballot)));
+                }
+#endif
                 if (ballot) {
                     if (contrib) {
                         const int slot = (qhead + qcount + __popc(ballot & ((1u << lane) - 1u))) & (kQ - 1);
@@ -1377,6 +1391,18 @@ int stage_of(int pass) {
 }
 
 }  // namespace
+
+#ifdef NGS_COUNT_CANDIDATES
+void dump_candidates() {
+    unsigned long long h[6][6];
+    cudaMemcpyFromSymbol(h, g_cand, sizeof(h));
+    for (int p = 0; p < 6; ++p)
+        fprintf(stderr, "[candidates] pass %d: 16x16 iters %llu with-record %llu records %llu | 8x8 iters %llu with-record %llu records %llu\n",
+                p, h[p][0], h[p][1], h[p][2], h[p][3], h[p][4], h[p][5]);
+    unsigned long long z[6][6] = {};
+    cudaMemcpyToSymbol(g_cand, z, sizeof(z));
+}
+#endif
 
 void launch_backward(int pass, const SceneDev& scene, ViewSlot& v, double* acc, size_t acc_stride, uint8_t* visible,
                      unsigned long long* contrib_pairs, cudaStream_t s, unsigned long long* acc_limbs, int* err,

@@ -86,6 +86,10 @@ struct BackwardArgs {
     int* err;                            // device error flag (kErrFixedRange in deterministic mode)
 };
 
+#ifdef NGS_COUNT_CANDIDATES
+void dump_candidates();  // debug build: phase-1 candidate statistics
+#endif
+
 // Up to kBackwardBatch views of one pass in one launch (launch_backward_batch).
 constexpr int kBackwardBatch = 4;
 struct BackwardBatch {

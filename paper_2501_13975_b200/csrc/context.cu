@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -1812,6 +1813,9 @@ int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out) {
         ctx->prof.resolve();
         unsigned long long p[9];
         CUDA_CHECK(cudaMemcpy(p, ctx->pairs.ptr, sizeof(p), cudaMemcpyDeviceToHost));
+#ifdef NGS_COUNT_CANDIDATES
+        ngsb::dump_candidates();
+#endif
         *out = ctx->prof.stats;
         for (int i = 0; i < 4; ++i) {
             out->contrib_pairs[i] = static_cast<int64_t>(p[i] + p[5 + i]);
