@@ -27,27 +27,27 @@ ctx.set_scene(init)
 ctx.trainer_configure(lib.default_train(), cams, targets, list(range(cfg.views)))
 order = [int(v) for v in np.random.default_rng(7).permutation(cfg.views)]
 for i in range(3):
-    ctx.trainer_step(order[i])
+    ctx.trainer_step(order[(i) % len(order)])
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-rep = ctx.trainer_step(order[3])
+rep = ctx.trainer_step(order[(3) % len(order)])
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print(f"{cfg.name}: profiled step {rep.dt_ms:.3f} ms")
 ctx.profile_reset()
 ctx.profile_enable(True)
-dts = [ctx.trainer_step(order[4 + i]).dt_ms for i in range(steps)]
+dts = [ctx.trainer_step(order[(4 + i) % len(order)]).dt_ms for i in range(steps)]
 p = ctx.profile_read()
 print(f"{cfg.name}: serialised steps {np.mean(dts):.3f} ms; stage ms/step",
       {k: round(v / steps, 3) for k, v in p["ms"].items()}, "pairs", [x / steps for x in p["contrib_pairs"]],
       "raster pairs", p["raster_pairs"] / steps)
 ctx.profile_enable(False)
-dts = [ctx.trainer_step(order[10 + i]).dt_ms for i in range(steps)]
+dts = [ctx.trainer_step(order[(10 + i) % len(order)]).dt_ms for i in range(steps)]
 print(f"{cfg.name}: concurrent steps {np.mean(dts):.3f} ms")
 
 # Timeline of one concurrent step (per-launch events, views NOT serialised).
 ctx.profile_timeline(True)
-rep = ctx.trainer_step(order[20])
+rep = ctx.trainer_step(order[(20) % len(order)])
 rows = ctx.read_timeline()
 ctx.profile_timeline(False)
 streams = {}
