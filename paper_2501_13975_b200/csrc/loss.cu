@@ -14,6 +14,7 @@
 #include <algorithm>
 
 #include "context.h"
+#include "splat.cuh"
 
 // Minimum resident blocks per SM of the 32-bit SSIM kernels (build-time knobs for A/B runs).
 #ifndef NGS_SSIMD_MINB
@@ -33,10 +34,12 @@ constexpr int kMaxHalf = 10;  // window <= 21
 struct Window {
     double w[2 * kMaxHalf + 1];
     double w2[2 * kMaxHalf + 1];
+    double full;  // sum of all taps in the device loop's order (window wholly inside the image)
     int half;
 };
 
 __device__ __forceinline__ double axis_norm(int x, int n, const Window& win) {
+    if (x >= win.half && x + win.half < n) return win.full;  // same sum, no loop
     const int i0 = max(-win.half, -x), i1 = min(win.half, n - 1 - x);
     double s = 0;
     for (int i = i0; i <= i1; ++i) s += win.w[i + win.half];
@@ -352,6 +355,13 @@ constexpr int kFT = 32;              // output tile edge
 constexpr int kFH = 5;               // window half-width (11 taps)
 constexpr int kFS = kFT + 2 * kFH;   // 42 rows / columns incl. halo
 constexpr int kFR = 4;               // outputs per task (both passes)
+// Derivative-field halo tiles: rows of kFS + 2 doubles from global column ox - kFH - 1
+// (16-byte aligned when W is even), row stride kBS (16-byte aligned rows); logical column
+// cc (global ox - kFH + cc) lives at index cc + 1.
+constexpr int kBS = kFS + 4;
+constexpr int kHW = 6;                          // derivative horizontal pass: outputs per task
+constexpr int kHG = (kFT + kHW - 1) / kHW;      // ... and tasks per row
+constexpr unsigned kBulkRow = sizeof(double) * (kFS + 2);
 
 template <int NF, class Load>
 __device__ __forceinline__ void hpass32(const Window& win, unsigned w2mask, Load load, double (*s_h)[kFS][kFT + 1]) {
@@ -465,45 +475,82 @@ __global__ void __launch_bounds__(256, NGS_SSIMF_MINB) ssim_fields32_k(int W, in
     if (threadIdx.x == 0) exact_add(sums + kExactWords, tot);
 }
 
+// Horizontal pass of one staged derivative field: kFS rows x kHG groups of kHW outputs
+// (252 tasks, one per thread; the last group overlaps its neighbour and both write the
+// same values). W2 selects the weights at compile time (constant-bank operands).
+template <bool W2>
+__device__ __forceinline__ void hpass_field(const Window& win, const double (*s_fb)[kBS], double (*s_h0)[kFT + 1]) {
+    for (int task = threadIdx.x; task < kFS * kHG; task += blockDim.x) {
+        const int cg = task / kFS, r = task - cg * kFS, c0 = min(cg * kHW, kFT - kHW);
+        double acc[kHW] = {};
+#pragma unroll
+        for (int k = 0; k < kHW + 2 * kFH; ++k) {
+            const double v = s_fb[r][c0 + k + 1];
+#pragma unroll
+            for (int o = 0; o < kHW; ++o)
+                if (k - o >= 0 && k - o <= 2 * kFH) acc[o] += (W2 ? win.w2[k - o] : win.w[k - o]) * v;
+        }
+#pragma unroll
+        for (int o = 0; o < kHW; ++o) s_h0[r][c0 + o] = acc[o];
+    }
+}
+
 __global__ void __launch_bounds__(256, NGS_SSIMD_MINB) ssim_derivs32_k(int W, int H, const double* __restrict__ image,
                                                        const double* __restrict__ target, Window win, double lambda,
                                                        const double* __restrict__ fields, float* __restrict__ grad,
                                                        float* __restrict__ hess, unsigned long long* __restrict__ sums, int row0,
                                                        int own_y0, int own_y1) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [1][kFS][kFT + 1], then s_f [2][kFS][kFS + 1]
+    auto s_h = reinterpret_cast<double (*)[kFS][kFT + 1]>(smem_raw);  // [1][kFS][kFT + 1], then s_f [2][kFS][kBS]
     __shared__ double red[8];
+    __shared__ unsigned long long fbar[2];
     const int ch = blockIdx.z;
     const int ox = blockIdx.x * kFT, oy = (row0 + blockIdx.y) * kFT;
     const size_t plane = static_cast<size_t>(W) * H;
     const int c = threadIdx.x % kFT, r0 = (threadIdx.x / kFT) * kFR;
     const int x = ox + c;
     const double inv3n = 1.0 / (3.0 * static_cast<double>(plane));
-    double cv[kFR], ctv[kFR];
-#pragma unroll
-    for (int o = 0; o < kFR; ++o) {
+    // The thread's own pixels are re-read where needed (L1) rather than held across the
+    // nine rounds: registers go to the horizontal pass.
+    auto pix = [&](const double* a, int o) {
         const int y = oy + r0 + o;
-        cv[o] = ctv[o] = 0.0;
-        if (x < W && y < H) {
-            cv[o] = image[ch * plane + static_cast<size_t>(y) * W + x];
-            ctv[o] = target[ch * plane + static_cast<size_t>(y) * W + x];
-        }
-    }
+        return (x < W && y < H) ? __ldg(a + ch * plane + static_cast<size_t>(y) * W + x) : 0.0;
+    };
     double g_ssim[kFR] = {}, h_ssim[kFR] = {};
     if (lambda != 0.0) {
         // One field per round, double-buffered: the halo tile of field f+1 streams in
-        // (cp.async) while field f is convolved. Horizontal tasks are row-major so a
-        // warp's lanes read different rows (row stride 43 doubles: conflict-free).
-        auto s_f = reinterpret_cast<double (*)[kFS][kFS + 1]>(smem_raw + sizeof(double) * kFS * (kFT + 1));
+        // while field f is convolved. Interior tiles (W even) move it as one TMA bulk copy
+        // per row completing on an mbarrier; edge tiles per element (cp.async, zeros
+        // outside the image). Horizontal tasks are row-major so a warp's lanes read
+        // different rows.
+        auto s_f = reinterpret_cast<double (*)[kFS][kBS]>(smem_raw + sizeof(double) * kFS * (kFT + 1));
+        const bool bulk = (W % 2 == 0) && ox >= kFH + 1 && ox + kFT + kFH + 1 <= W && oy >= kFH &&
+                          oy + kFT + kFH <= H;
+        if (bulk) {
+            if (threadIdx.x == 0) {
+                mbar_init(&fbar[0], 1);
+                mbar_init(&fbar[1], 1);
+                mbar_fence_init();
+            }
+            __syncthreads();
+        }
         auto issue = [&](int f, int buf) {
             const double* field = fields + (static_cast<size_t>(f) * 3 + ch) * plane;
+            if (bulk) {
+                if (threadIdx.x == 0) mbar_expect_tx(&fbar[buf], kFS * kBulkRow);
+                if (threadIdx.x < kFS)
+                    bulk_copy_g2s(&s_f[buf][threadIdx.x][0],
+                                  field + static_cast<size_t>(oy - kFH + threadIdx.x) * W + (ox - kFH - 1), kBulkRow,
+                                  &fbar[buf]);
+                return;
+            }
             for (int i = threadIdx.x; i < kFS * kFS; i += blockDim.x) {
                 const int r = i / kFS, cc = i - r * kFS;
                 const int gx = ox - kFH + cc, gy = oy - kFH + r;
                 if (gx >= 0 && gx < W && gy >= 0 && gy < H)
-                    cp_async8(&s_f[buf][r][cc], field + static_cast<size_t>(gy) * W + gx);
+                    cp_async8(&s_f[buf][r][cc + 1], field + static_cast<size_t>(gy) * W + gx);
                 else
-                    s_f[buf][r][cc] = 0.0;
+                    s_f[buf][r][cc + 1] = 0.0;
             }
             cp_async_commit_l();
         };
@@ -511,26 +558,30 @@ __global__ void __launch_bounds__(256, NGS_SSIMD_MINB) ssim_derivs32_k(int W, in
 #pragma unroll 1
         for (int f = 0; f < 9; ++f) {
             const int buf = f & 1;
-            cp_async_wait_all_l();
+            if (bulk)
+                mbar_wait(&fbar[buf], (f >> 1) & 1);
+            else
+                cp_async_wait_all_l();
             __syncthreads();  // tile f visible; previous round's readers of s_h and s_f[buf ^ 1] done
             if (f + 1 < 9) issue(f + 1, buf ^ 1);
             const bool w2 = f >= 4;  // fp, fq, fr, fkw use w; the rest w^2
-            for (int task = threadIdx.x; task < kFS * (kFT / kFR); task += blockDim.x) {
-                const int cg = task / kFS, r = task - cg * kFS, c0 = cg * kFR;
-                double acc[kFR] = {};
-#pragma unroll
-                for (int k = 0; k < kFR + 2 * kFH; ++k) {
-                    const double v = s_f[buf][r][c0 + k];
-#pragma unroll
-                    for (int o = 0; o < kFR; ++o)
-                        if (k - o >= 0 && k - o <= 2 * kFH) acc[o] += (w2 ? win.w2[k - o] : win.w[k - o]) * v;
-                }
-#pragma unroll
-                for (int o = 0; o < kFR; ++o) s_h[0][r][c0 + o] = acc[o];
-            }
+            if (w2)
+                hpass_field<true>(win, s_f[buf], s_h[0]);
+            else
+                hpass_field<false>(win, s_f[buf], s_h[0]);
             __syncthreads();
+            const bool need_c = f == 2 || f == 5 || f == 7 || f == 8, need_t = f == 1 || f == 6 || f == 7;
+            double cv[kFR], ctv[kFR];
+#pragma unroll
+            for (int o = 0; o < kFR; ++o) {
+                cv[o] = need_c ? pix(image, o) : 0.0;
+                ctv[o] = need_t ? pix(target, o) : 0.0;
+            }
             double sv[kFR];
-            vpass32(win, w2, s_h[0], c, r0, sv);
+            if (w2)
+                vpass32(win, true, s_h[0], c, r0, sv);
+            else
+                vpass32(win, false, s_h[0], c, r0, sv);
 #pragma unroll
             for (int o = 0; o < kFR; ++o) {  // loss.hpp:323-327
                 const double cf = f == 1 ? ctv[o] : f == 2 ? cv[o] : f == 5 ? cv[o] : f == 6 ? ctv[o]
@@ -545,7 +596,7 @@ __global__ void __launch_bounds__(256, NGS_SSIMD_MINB) ssim_derivs32_k(int W, in
     for (int o = 0; o < kFR; ++o) {
         const int y = oy + r0 + o;
         if (x >= W || y >= H) continue;
-        const double d = cv[o] - ctv[o];
+        const double d = pix(image, o) - pix(target, o);
         if (y >= own_y0 && y < own_y1) dsq_own += d * d;
         double gg = inv3n * d, hh = inv3n;
         if (lambda != 0.0) {
@@ -560,17 +611,8 @@ __global__ void __launch_bounds__(256, NGS_SSIMD_MINB) ssim_derivs32_k(int W, in
     if (threadIdx.x == 0) exact_add(sums, tot);
 }
 
-}  // namespace
-
-void compute_loss(ViewSlot& v, cudaStream_t s) {
-    const LossParams& L = v.loss;
-    if (L.lambda < 0.0) throw Error(NGS_ERR_INVALID_INPUT, "loss: lambda must be >= 0");
-    if (L.window < 3 || L.window % 2 == 0) throw Error(NGS_ERR_INVALID_INPUT, "loss: window must be odd and >= 3");
-    if (L.window > 2 * kMaxHalf + 1) throw Error(NGS_ERR_INVALID_INPUT, "loss: window larger than 21 unsupported");
-    const bool ssim = L.lambda != 0.0;
-    if (ssim && (v.W < L.window || v.H < L.window))
-        throw Error(NGS_ERR_INVALID_INPUT, "ssim stats: image smaller than the filter window");
-    // gaussian_window_1d, loss.hpp:66-77
+// gaussian_window_1d, loss.hpp:66-77
+Window make_window(const LossParams& L) {
     Window win{};
     win.half = L.window / 2;
     double sum = 0;
@@ -583,6 +625,22 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
         win.w[i] /= sum;
         win.w2[i] = win.w[i] * win.w[i];
     }
+    win.full = 0;
+    for (int i = 0; i < L.window; ++i) win.full += win.w[i];  // axis_norm's order: i0 = -half .. half
+    return win;
+}
+
+}  // namespace
+
+void compute_loss(ViewSlot& v, cudaStream_t s) {
+    const LossParams& L = v.loss;
+    if (L.lambda < 0.0) throw Error(NGS_ERR_INVALID_INPUT, "loss: lambda must be >= 0");
+    if (L.window < 3 || L.window % 2 == 0) throw Error(NGS_ERR_INVALID_INPUT, "loss: window must be odd and >= 3");
+    if (L.window > 2 * kMaxHalf + 1) throw Error(NGS_ERR_INVALID_INPUT, "loss: window larger than 21 unsupported");
+    const bool ssim = L.lambda != 0.0;
+    if (ssim && (v.W < L.window || v.H < L.window))
+        throw Error(NGS_ERR_INVALID_INPUT, "ssim stats: image smaller than the filter window");
+    const Window win = make_window(L);
     const size_t npx = static_cast<size_t>(v.W) * v.H;
     v.loss_grad.ensure(3 * npx);
     v.loss_hess.ensure(3 * npx);
@@ -611,7 +669,7 @@ void compute_loss(ViewSlot& v, cudaStream_t s) {
     if (win.half == kFH) {  // the reference default (window 11): 32x32 register-blocked tiles
         const int r32a = band_px0 / kFT, r32b = (band_px1 + kFT - 1) / kFT;
         const dim3 g32((v.W + kFT - 1) / kFT, r32b - r32a, 3);
-        const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1), sm_d = sizeof(double) * kFS * (kFT + 1 + 2 * (kFS + 1));
+        const size_t sm_f = sizeof(double) * 5 * kFS * (kFT + 1), sm_d = sizeof(double) * kFS * (kFT + 1 + 2 * kBS);
         ensure_dynamic_smem(reinterpret_cast<const void*>(ssim_fields32_k), sm_f);
         ensure_dynamic_smem(reinterpret_cast<const void*>(ssim_derivs32_k), sm_d);
         if (ssim) {
@@ -637,18 +695,7 @@ void compute_loss_value(ViewSlot& v, cudaStream_t s) {
     if (L.window > 2 * kMaxHalf + 1) throw Error(NGS_ERR_INVALID_INPUT, "loss: window larger than 21 unsupported");
     if (v.W < L.window || v.H < L.window)
         throw Error(NGS_ERR_INVALID_INPUT, "ssim stats: image smaller than the filter window");
-    Window win{};
-    win.half = L.window / 2;
-    double sum = 0;
-    for (int i = 0; i < L.window; ++i) {
-        const double d = i - win.half;
-        win.w[i] = std::exp(-d * d / (2.0 * L.window_sigma * L.window_sigma));
-        sum += win.w[i];
-    }
-    for (int i = 0; i < L.window; ++i) {
-        win.w[i] /= sum;
-        win.w2[i] = win.w[i] * win.w[i];
-    }
+    const Window win = make_window(L);
     const size_t npx = static_cast<size_t>(v.W) * v.H;
     v.loss_sums.ensure(2 * kExactWords);
     CUDA_CHECK(cudaMemsetAsync(v.loss_sums.ptr, 0, 2 * kExactWords * sizeof(unsigned long long), s));
