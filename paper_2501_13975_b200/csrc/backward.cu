@@ -910,7 +910,8 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
     auto& s_maxlast = S.maxlast;
     unsigned long long block_pairs = 0;
 
-    const int tile = a.tile0 + block;  // owned tile rows only (multi-GPU shard)
+    const int chunk = a.chunks > 1 ? block % a.chunks : 0;
+    const int tile = a.tile0 + (a.chunks > 1 ? block / a.chunks : block);  // owned tile rows only (multi-GPU shard)
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     int lx, ly;
     WarpBox<TILE>::pixel(threadIdx.x, lx, ly);
@@ -918,7 +919,11 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
     const bool inside = x < a.W && y < a.H;
     const float fx = lx + 0.5f, fy = ly + 0.5f;
     const double ox = tx * TILE, oy = ty * TILE;
-    const int2 range = a.ranges[tile];
+    const int2 range_all = a.ranges[tile];
+    // this block's part of the tile's list (the whole list when chunks == 1)
+    const int2 range = a.chunks > 1 ? make_int2(chunk_begin(range_all, chunk, a.chunks),
+                                                chunk_begin(range_all, chunk + 1, a.chunks))
+                                    : range_all;
     const size_t plane = static_cast<size_t>(a.W) * a.H;
     const size_t pidx = static_cast<size_t>(y) * a.W + x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -955,6 +960,11 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
 
     float T = 1.0f;
     double P[3] = {0.0, 0.0, 0.0};
+    if (chunk > 0 && inside) {  // the forward's state before list entry range.x
+        T = a.ck_t[(chunk - 1) * plane + pidx];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) P[c] = a.ck_p[(3 * (chunk - 1) + c) * plane + pidx];
+    }
     int qhead = 0, qcount = 0;  // warp-uniform ring state
 
     const float4* s_const = S.cst[0];  // constants of the batch being traversed
@@ -1357,7 +1367,10 @@ bool make_backward_args(const SceneDev& scene, ViewSlot& v, double* acc, size_t 
     const int own0 = std::max(0, v.raster.own_y0), own1 = std::min(v.cam.tiles_y, v.raster.own_y1);
     if (own1 <= own0) return false;
     a.tile0 = own0 * v.cam.tiles_x;
-    blocks = (own1 - own0) * v.cam.tiles_x;
+    a.chunks = v.cam.tile == 8 ? std::max(1, v.ck_chunks) : 1;
+    a.ck_t = v.ck_t.ptr;
+    a.ck_p = v.ck_p.ptr;
+    blocks = (own1 - own0) * v.cam.tiles_x * a.chunks;
     return true;
 }
 

@@ -76,6 +76,11 @@ struct BackwardArgs {
     const float* loss_grad;
     const float* loss_hess;
     const float* consts;
+    // Chunked traversal (8x8 tiles): block = (tile, chunk); chunk c > 0 starts from the
+    // forward's checkpoint c (ck_t / ck_p, see ViewSlot). chunks == 1: whole lists.
+    int chunks;
+    const float* ck_t;
+    const double* ck_p;
     float cutoff;
     float bg[3];
     double* acc;

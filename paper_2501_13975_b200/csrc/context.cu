@@ -176,6 +176,8 @@ struct ngs_context {
     ncclComm_t comm = nullptr;
     int stream_policy = 0;  // 0: secondaries first, high priority; 1: primary first+high; 2: none, sec first; 3: none, primary first
     int tile_policy = 0;  // 0 auto (8x8 tiles for small views), else forced 8 or 16
+    int bwd_chunks = 0;   // list chunks per 8x8 tile in the trainer's backward (0: auto, 1: whole lists)
+    int sm_count = 148;
     unsigned long long contrib_pairs_total = 0;
     // Bumped whenever the positions may change (set_scene, position commits, snapshot
     // restores, first-order updates, every trainer step start): trainer renders with an
@@ -589,6 +591,8 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         if (const char* e = getenv("NGS_STREAM_POLICY")) ctx->stream_policy = atoi(e);  // experiments only
         if (const char* e = getenv("NGS_TILE_POLICY")) ctx->tile_policy = atoi(e);      // experiments only
+        CUDA_CHECK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device));
+        if (const char* e = getenv("NGS_BWD_CHUNKS")) ctx->bwd_chunks = std::max(0, std::min(64, atoi(e)));  // A/B
         if (const char* e = getenv("NGS_ORDER_REUSE")) ctx->order_reuse = atoi(e) != 0;  // tests only
         if (const char* e = getenv("NGS_BATCH_SECONDARIES")) ctx->batch_secondaries = atoi(e) != 0;  // A/B only
         for (int i = 0; i < kMaxSolveViews; ++i) {
@@ -1324,6 +1328,19 @@ namespace {
 // on the device and handled by the caller).
 // join = false leaves the views in flight on their streams (recording rev[i]); the
 // next accumulate_pass(chained = true) picks each view up where its render ends.
+// List chunks per 8x8 tile of a view's backward (policy > 0: forced, for A/B runs). A
+// primary view with fewer tiles than the GPU holds resident backward blocks (~8 per SM) is
+// one latency-bound wave whose deepest lists set the step's critical path: split them
+// (c1). Secondary views overlap the primary's work on other streams, so splitting theirs
+// only adds per-block overhead (c2 +2 %, c3 +2 % with every 8x8 view split).
+int backward_chunks(int policy, int sm_count, const ngs_camera& cam, int tile, bool primary) {
+    if (policy > 0) return policy;
+    const int tiles = ((cam.width + tile - 1) / tile) * ((cam.height + tile - 1) / tile);
+    const int resident = 8 * sm_count;
+    if (!primary || tiles >= resident) return 1;
+    return std::max(1, std::min(16, 4 * resident / std::max(tiles, 1)));
+}
+
 void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nbrs, bool upload_targets,
                        bool join = true) {
     TrainerState& T = ctx->trainer;
@@ -1353,6 +1370,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
             const int cam_id = (i == 0) ? view_id : nbrs[i - 1];
             const ngs_camera& cam = (i == 0) ? T.cameras[cam_id] : T.down_cameras[cam_id];
             upload_camera(cam, v.cam, ts[i]);
+            v.chunks = ts[i] == 8 ? backward_chunks(ctx->bwd_chunks, ctx->sm_count, cam, ts[i], i == 0) : 1;
             v.raster = to_raster(&T.cfg.raster);
             apply_shard(plan[i], v.raster);
             v.loss = to_loss(&T.cfg.loss);

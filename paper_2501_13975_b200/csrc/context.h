@@ -130,6 +130,12 @@ struct ViewSlot {
     DevBuf<double> image;   // FP64 (see raster_forward_k)
     DevBuf<float> t_final;
     DevBuf<int> last;       // index into the tile list of the last contributing splat, -1 if none
+    // Chunked backward of 8x8-tile views: per-pixel compositing state at the chunk starts
+    // ([chunk-1][H][W] T, [chunk-1][3][H][W] FP64 colour prefix), written by the forward.
+    int chunks = 1;         // requested for the next render (trainer secondaries)
+    int ck_chunks = 1;      // what the last render wrote (the backward's block split)
+    DevBuf<float> ck_t;
+    DevBuf<double> ck_p;
     // K7 loss fields
     DevBuf<double> target;  // planar [3][H][W], FP64 like the reference Image
     // Device-resident trainer targets are read in place (no per-step D2D copy into `target`).

@@ -347,13 +347,17 @@ struct RasterSmem {
     unsigned char wmask[N];
 };
 
-template <int TILE>
+// CK: also write each pixel's compositing state (T, FP64 colour prefix) at the chunk
+// boundaries chunk_begin(range, c, chunks), c = 1 .. chunks-1, of its tile's list: the
+// backward of deep small-tile lists then runs one block per (tile, chunk) from there.
+template <int TILE, bool CK>
 __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int W, int H, const int2* __restrict__ ranges,
                                                         const int* __restrict__ vals, const double2* __restrict__ pix,
                                                         const float4* __restrict__ ra, const float4* __restrict__ rb,
                                                         const float4* __restrict__ rc, float bg0, float bg1, float bg2,
                                                         float cutoff, float tmin, double* __restrict__ image,
-                                                        float* __restrict__ t_final, int* __restrict__ last_out) {
+                                                        float* __restrict__ t_final, int* __restrict__ last_out,
+                                                        int chunks, float* __restrict__ ck_t, double* __restrict__ ck_p) {
     constexpr int kRasterBatch = TILE * TILE;  // one splat per thread per batch
     // Dynamic shared memory (> 48 KB for 16x16 tiles): RasterSmem<TILE>.
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -375,6 +379,16 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
     double C0 = 0.0, C1 = 0.0, C2 = 0.0;  // FP64 colour sums: the image feeds the cancelling (c - c^t) loss terms
     int last = -1;
     bool done = !inside;
+    const size_t npx = static_cast<size_t>(W) * H, pidx = static_cast<size_t>(y) * W + x;
+    int nc = 1, bnd = CK ? chunk_begin(range, 1, chunks) : 0;  // next checkpoint and its list index
+    auto save = [&](int c) {
+        if (inside) {
+            ck_t[(c - 1) * npx + pidx] = T;
+            ck_p[(3 * (c - 1) + 0) * npx + pidx] = C0;
+            ck_p[(3 * (c - 1) + 1) * npx + pidx] = C1;
+            ck_p[(3 * (c - 1) + 2) * npx + pidx] = C2;
+        }
+    };
     const float tmin_eff = tmin > 0.f ? tmin : -1.0f;  // T < tmin_eff: early termination (none when tmin = 0)
     // Software pipeline: thread t stages splat t of the next batch with cp.async
     // (into its own slot, so only its own wait is needed) while the current batch
@@ -429,6 +443,12 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
             while (m) {
                 const int j = c32 + __ffs(m) - 1;
                 m &= m - 1;
+                if constexpr (CK) {
+                    while (nc < chunks && base + j >= bnd) {  // state before list entry bnd
+                        save(nc);
+                        bnd = chunk_begin(range, ++nc, chunks);
+                    }
+                }
                 const SplatSh sp = s_sp[j];
                 SplatEval e;
                 if (eval_splat_bf(sp, fx, fy, cutoff, e) && !done) {
@@ -444,6 +464,8 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
         }
     }
     cp_async_wait_all();
+    if constexpr (CK)
+        for (; nc < chunks; ++nc) save(nc);  // boundaries past the last entry this warp saw
     if (inside) {
         const size_t plane = static_cast<size_t>(W) * H;
         const size_t idx = static_cast<size_t>(y) * W + x;
@@ -603,17 +625,27 @@ void bin_and_raster(const SceneDev& scene, ViewSlot& v, int* d_err, cudaStream_t
     }
     if (g_prof) g_prof->stats.renders += 1;
     StageScope st(NGS_STAGE_RASTER, s);
+    // Chunked backward (8x8 tiles): checkpoints of the compositing state at the chunk starts.
+    const int chunks = v.cam.tile == 8 ? std::max(1, v.chunks) : 1;
+    v.ck_chunks = chunks;
+    if (chunks > 1) {
+        const size_t npx = static_cast<size_t>(v.W) * v.H;
+        v.ck_t.ensure(static_cast<size_t>(chunks - 1) * npx);
+        v.ck_p.ensure(static_cast<size_t>(chunks - 1) * 3 * npx);
+    }
     auto launch = [&](auto kernel, int threads, size_t smem) {
         ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
         kernel<<<v.T, threads, smem, s>>>(v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val.ptr : nullptr,
                                        v.pix.ptr, v.rec_a.ptr, v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1],
                                        scene.bg[2], v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
-                                       v.last.ptr);
+                                       v.last.ptr, chunks, v.ck_t.ptr, v.ck_p.ptr);
     };
-    if (v.cam.tile == 8)
-        launch(raster_forward_k<8>, 64, sizeof(RasterSmem<8>));
+    if (v.cam.tile == 8 && chunks > 1)
+        launch(raster_forward_k<8, true>, 64, sizeof(RasterSmem<8>));
+    else if (v.cam.tile == 8)
+        launch(raster_forward_k<8, false>, 64, sizeof(RasterSmem<8>));
     else
-        launch(raster_forward_k<16>, 256, sizeof(RasterSmem<16>));
+        launch(raster_forward_k<16, false>, 256, sizeof(RasterSmem<16>));
     CUDA_LAUNCH_CHECK();
     v.valid = true;
 }

@@ -125,6 +125,12 @@ __device__ __forceinline__ float reject_bound(float sigma, float cutoff) {
 
 // A splat as staged in shared memory for a tile batch: one 48-byte record so
 // every visit is a single broadcast base address.
+// First list index of chunk c of a tile's list [range.x, range.y) split into `chunks`
+// near-equal parts (c = chunks gives range.y): the chunked backward's block split.
+__device__ __forceinline__ int chunk_begin(int2 range, int c, int chunks) {
+    return range.x + static_cast<int>(static_cast<long long>(range.y - range.x) * c / chunks);
+}
+
 struct SplatSh {
     float4 g0;  // (px, py, Q00, Q01) in tile coordinates
     float4 g1;  // (Q11, sigma, qmax, c0)
