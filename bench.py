@@ -424,6 +424,7 @@ def ours_arm(args, cfg: Config):
         solve_mb = {"gaussians": mb_n, "ms_per_attr": dict(zip(("position", "rotation", "scaling", "opacity", "color"),
                                                                 [round(x, 4) for x in ms5])),
                     "gaussian_updates_per_s": upd_s, "algorithmic_bytes_per_update": bytes_per_update,
+                    "color_fast_path_frac": getattr(ctx, "last_color_fast_frac", None),
                     "achieved_GBps": upd_s * bytes_per_update / 1e9, "hbm_frac": upd_s * bytes_per_update / 1e9 / hbm,
                     "commits": "every timed launch commits all parameters (restored between launches, untimed)"}
 

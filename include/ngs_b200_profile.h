@@ -53,6 +53,10 @@ typedef struct {
      * step): summed device time (profiling on) and contributing records (always). */
     double primary_bwd_ms[4];
     int64_t primary_contrib_pairs[4];
+    /* Colour solves (SH degree >= 1, always counted): channel systems solved, and those
+     * that took the no-repair fast path (no eigen-decomposition, solve.cu). */
+    int64_t color_channels;
+    int64_t color_fast_channels;
 } ngs_profile_stats;
 
 /* Timeline of the concurrent schedule (views NOT serialised): one row per stage
@@ -81,11 +85,12 @@ int32_t ngs_microbench_fp64(ngs_context* ctx, double* tflops);
 /* Newton-solve microbenchmark (BASELINE config 4): n synthetic
  * Gaussians (SH degree sh_degree) with random SPD accumulator blocks for every
  * attribute group (position/scaling 2x2, rotation/opacity 1x1, colour rank-`views`
- * per channel), solved without commit `reps` times; ms_out[attr] = mean device
- * time of solve_<attr> over all n Gaussians. Scratch buffers only (the context's
- * scene is untouched). */
+ * per channel), solved AND committed `reps` times (parameters restored between the
+ * timed launches); ms_out[attr] = mean device time of solve_<attr> over all n
+ * Gaussians; color_fast_frac (nullable) = fraction of the colour channel solves that
+ * took the no-repair fast path. Scratch buffers only (the context's scene is untouched). */
 int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int32_t views, int32_t reps,
-                             double ms_out[5]);
+                             double ms_out[5], double* color_fast_frac);
 
 #ifdef __cplusplus
 }

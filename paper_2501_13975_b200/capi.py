@@ -128,7 +128,8 @@ class ngs_profile_stats(C.Structure):
     _fields_ = [("ms", C.c_double * 11), ("launches", C.c_int64 * 11), ("total_launches", C.c_int64),
                 ("contrib_pairs", C.c_int64 * 4), ("raster_pairs", C.c_int64), ("renders", C.c_int64),
                 ("group_ms", C.c_double * 6), ("allreduce_calls", C.c_int64), ("allreduce_bytes", C.c_int64),
-                ("primary_bwd_ms", C.c_double * 4), ("primary_contrib_pairs", C.c_int64 * 4)]
+                ("primary_bwd_ms", C.c_double * 4), ("primary_contrib_pairs", C.c_int64 * 4),
+                ("color_channels", C.c_int64), ("color_fast_channels", C.c_int64)]
 
 
 class ngs_terms(C.Structure):
@@ -493,6 +494,7 @@ class Context:
                     raster_pairs=st.raster_pairs, renders=st.renders,
                     allreduce_calls=st.allreduce_calls, allreduce_bytes=st.allreduce_bytes,
                     primary_bwd_ms=list(st.primary_bwd_ms), primary_contrib_pairs=list(st.primary_contrib_pairs),
+                    color_channels=st.color_channels, color_fast_channels=st.color_fast_channels,
                     # Trainer renders are chained per view into the following backward pass, so each
                     # pass group includes the render before it ("render" stays 0 in trainer steps).
                     group_ms=dict(zip(("render", "render+bwd_position", "render+bwd_rotation", "render+bwd_scaling",
@@ -526,10 +528,13 @@ class Context:
         return v.value
 
     def microbench_solve(self, n: int, sh_degree: int = 3, views: int = 4, reps: int = 5) -> list:
-        """Mean ms of solve_<attr> over n synthetic Gaussians (ngs_microbench_solve)."""
+        """Mean ms of solve_<attr> over n synthetic Gaussians (ngs_microbench_solve);
+        self.last_color_fast_frac = the colour channel solves that took the fast path."""
         out = (C.c_double * 5)()
+        frac = C.c_double()
         self._call("ngs_microbench_solve", C.c_int32(n), C.c_int32(sh_degree), C.c_int32(views), C.c_int32(reps),
-                   out)
+                   out, C.byref(frac))
+        self.last_color_fast_frac = frac.value
         return list(out)
 
     # multi-GPU sharding (include/ngs_b200_dist.h; CUDA library only)

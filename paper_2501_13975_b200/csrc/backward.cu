@@ -971,6 +971,12 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
 
     // Phase 2 over queue entries [qhead, qhead + n), n <= 32.
     auto drain = [&](int n) {
+#ifdef NGS_SKIP_PHASE2  // debug A/B only: phase-1 cost alone (results are wrong)
+        if (lane == 0) block_pairs += n;
+        qhead = (qhead + n) & (kQ - 1);
+        qcount -= n;
+        return;
+#endif
         const bool valid = lane < n;
         const int e = (qhead + lane) & (kQ - 1);
         const unsigned jp = valid ? Q.jp[e] : 0xFFFFu;

@@ -178,6 +178,7 @@ struct ngs_context {
     int tile_policy = 0;  // 0 auto (8x8 tiles for small views), else forced 8 or 16
     int bwd_chunks = 0;   // list chunks per 8x8 tile in the trainer's backward (0: auto, 1: whole lists)
     int sm_count = 148;
+    bool color_fused = false;  // one-launch colour solve with the no-repair fast path (NGS_COLOR_FUSED=1)
     unsigned long long contrib_pairs_total = 0;
     // Bumped whenever the positions may change (set_scene, position commits, snapshot
     // restores, first-order updates, every trainer step start): trainer renders with an
@@ -592,6 +593,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         if (const char* e = getenv("NGS_STREAM_POLICY")) ctx->stream_policy = atoi(e);  // experiments only
         if (const char* e = getenv("NGS_TILE_POLICY")) ctx->tile_policy = atoi(e);      // experiments only
         CUDA_CHECK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device));
+        if (const char* e = getenv("NGS_COLOR_FUSED")) ctx->color_fused = atoi(e) != 0;  // A/B
         if (const char* e = getenv("NGS_BWD_CHUNKS")) ctx->bwd_chunks = std::max(0, std::min(64, atoi(e)));  // A/B
         if (const char* e = getenv("NGS_ORDER_REUSE")) ctx->order_reuse = atoi(e) != 0;  // tests only
         if (const char* e = getenv("NGS_BATCH_SECONDARIES")) ctx->batch_secondaries = atoi(e) != 0;  // A/B only
@@ -613,9 +615,11 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         CUDA_CHECK(cudaMemsetAsync(ctx->overflow.ptr, 0, sizeof(int), ctx->stream));
         ctx->err.ensure(1);
         ctx->norm.ensure(5 * kExactWords);
-        ctx->pairs.ensure(9);  // [0..3] records per pass (secondary views), [4] raster pairs, [5..8] primary records
+        // [0..3] records per pass (secondary views), [4] raster pairs, [5..8] primary records,
+        // [9] colour channel solves on the fast path
+        ctx->pairs.ensure(10);
         CUDA_CHECK(cudaMemsetAsync(ctx->err.ptr, 0, sizeof(int), ctx->stream));
-        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 9 * sizeof(unsigned long long), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 10 * sizeof(unsigned long long), ctx->stream));
         ctx->scene.n = 0;
         ctx->scene.sh_degree = 0;
         ctx->scene.n_coeffs = 1;
@@ -1000,9 +1004,14 @@ ColorViews color_views(ngs_context* ctx, ViewSlot* const* views, int nv) {
         cv.cam[i] = views[i]->cam;
         cv.flags[i] = views[i]->flags.ptr;
     }
-    const int mv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 16;  // solve_color_k<MV> instantiation
-    ctx->color_eig.ensure(static_cast<size_t>(mv * mv + mv) * std::max(ctx->scene.n, 1));
-    cv.eig = ctx->color_eig.ptr;
+    cv.fused = ctx->color_fused ? 1 : 0;
+    cv.fast_count = ctx->pairs.ptr + 9;
+    if (!cv.fused) {
+        const int mv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 16;  // solve_color_k<MV> instantiation
+        ctx->color_eig.ensure(static_cast<size_t>(mv * mv + mv) * std::max(ctx->scene.n, 1));
+        cv.eig = ctx->color_eig.ptr;
+    }
+    if (ctx->scene.n_coeffs > 1) ctx->prof.stats.color_channels += 3 * static_cast<int64_t>(ctx->scene.n);
     return cv;
 }
 
@@ -1819,7 +1828,7 @@ int32_t ngs_profile_reset(ngs_context* ctx) {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         ctx->prof.reset();
-        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 9 * sizeof(unsigned long long), ctx->stream));
+        CUDA_CHECK(cudaMemsetAsync(ctx->pairs.ptr, 0, 10 * sizeof(unsigned long long), ctx->stream));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -1829,7 +1838,7 @@ int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out) {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         ctx->prof.resolve();
-        unsigned long long p[9];
+        unsigned long long p[10];
         CUDA_CHECK(cudaMemcpy(p, ctx->pairs.ptr, sizeof(p), cudaMemcpyDeviceToHost));
 #ifdef NGS_COUNT_CANDIDATES
         ngsb::dump_candidates();
@@ -1840,6 +1849,7 @@ int32_t ngs_profile_read(ngs_context* ctx, ngs_profile_stats* out) {
             out->primary_contrib_pairs[i] = static_cast<int64_t>(p[5 + i]);
         }
         out->raster_pairs = static_cast<int64_t>(p[4]);
+        out->color_fast_channels = static_cast<int64_t>(p[9]);
     });
 }
 
@@ -1940,7 +1950,7 @@ int32_t ngs_set_deterministic(ngs_context* ctx, int32_t on) {
 }
 
 int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int32_t views, int32_t reps,
-                             double ms_out[5]) {
+                             double ms_out[5], double* color_fast_frac) {
     return guarded([&] {
         CUDA_CHECK(cudaSetDevice(ctx->device));
         if (n <= 0 || views < 1 || views > kMaxSolveViews || sh_degree < 0 || sh_degree > 3 || reps < 1)
@@ -1979,8 +1989,13 @@ int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int
         ColorViews cv{};
         cv.n_views = views;
         DevBuf<double> eig;
-        eig.ensure(static_cast<size_t>(8 * 8 + 8) * stride);
-        cv.eig = eig.ptr;
+        DevBuf<unsigned long long> fast;
+        fast.ensure(1);
+        cv.fused = ctx->color_fused ? 1 : 0;
+        if (!cv.fused) {
+            eig.ensure(static_cast<size_t>(8 * 8 + 8) * stride);
+            cv.eig = eig.ptr;
+        }
         for (int v = 0; v < views; ++v) {
             upload_camera(mb_camera(v, std::max(views, 2)), cv.cam[v]);
             cv.flags[v] = flags.ptr + static_cast<size_t>(v) * stride;
@@ -2024,6 +2039,16 @@ int32_t ngs_microbench_solve(ngs_context* ctx, int32_t n, int32_t sh_degree, int
             ms_out[a] = total / reps;
         }
         restore();
+        if (color_fast_frac) {  // one more colour launch, counting the fast-path channel solves
+            CUDA_CHECK(cudaMemsetAsync(fast.ptr, 0, sizeof(unsigned long long), s));
+            cv.fast_count = fast.ptr;
+            launch_solve(4, sd, cv.cam[0], 0.3, cv.flags[0], cv, sp, accs[4], stride, so, s);
+            restore();
+            unsigned long long f = 0;
+            CUDA_CHECK(cudaMemcpyAsync(&f, fast.ptr, sizeof(f), cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaStreamSynchronize(s));
+            *color_fast_frac = sd.n_coeffs > 1 && cv.fused ? static_cast<double>(f) / (3.0 * n) : 0.0;
+        }
         ctx->check_err();
     });
 }

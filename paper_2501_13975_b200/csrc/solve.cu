@@ -15,6 +15,9 @@
 #ifndef NGS_COLOR4_MINB
 #define NGS_COLOR4_MINB 5
 #endif
+#ifndef NGS_COLORF4_MINB  // ... and of the fused one-launch colour solve
+#define NGS_COLORF4_MINB 3
+#endif
 
 constexpr double kJacobiTol = 1e-28;  // (1e-20 / 1e-16 measured: c4 colour 7.18 -> 7.10 / 7.27 ms, kept)
 
@@ -430,8 +433,7 @@ __device__ inline void jacobi_eig(double (&a)[MAXM][MAXM], double (&v)[MAXM][MAX
 // Gram matrix of the visible views' SH bases (phi_a . phi_b; absent views are zero) and its
 // eigen-decomposition G = E diag(L) E^T (eigenvalues on the diagonal of L).
 template <int MV>
-__device__ __forceinline__ void color_gram(const SceneDev& s, const ColorViews& cv, int k, double (&L)[MV][MV],
-                                           double (&E)[MV][MV]) {
+__device__ __forceinline__ void color_gram_matrix(const SceneDev& s, const ColorViews& cv, int k, double (&L)[MV][MV]) {
     const float4 ps = s.pos_sigma[k];
     const D3 p = {ps.x, ps.y, ps.z};
     const int nv = cv.n_views;
@@ -463,6 +465,43 @@ __device__ __forceinline__ void color_gram(const SceneDev& s, const ColorViews& 
             L[b][a] = L[a][b];
         }
     }
+}
+
+// The same Gram matrix from the addition theorem of the orthonormal real SH basis
+// (sum_m Y_lm(a) Y_lm(b) = (2l+1)/(4 pi) P_l(a.b)): G_ab = sum_{l <= degree}
+// (2l+1)/(4 pi) P_l(d_a . d_b), equal to the explicit dot products up to rounding, from
+// the view directions alone (also returned, for the commit).
+template <int MV>
+__device__ __forceinline__ void color_gram_addition(const SceneDev& s, const ColorViews& cv, int k,
+                                                    const uint8_t (&fl)[MV], double (&G)[MV][MV], D3 (&dir)[MV]) {
+    const float4 ps = s.pos_sigma[k];
+    const D3 p = {ps.x, ps.y, ps.z};
+    const int nv = cv.n_views, deg = s.sh_degree;
+    constexpr double k4pi = 0.07957747154594767;  // 1 / (4 pi)
+#pragma unroll
+    for (int v = 0; v < MV; ++v) {
+        dir[v] = d3(0, 0, 1);
+        double nr;
+        if (v < nv && !view_direction(cv.cam[v], p, dir[v], nr)) dir[v] = d3(0, 0, 1);
+    }
+#pragma unroll
+    for (int a = 0; a < MV; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+            const double t = dir[a].x * dir[b].x + dir[a].y * dir[b].y + dir[a].z * dir[b].z;
+            double g = 1.0;                                  // l = 0
+            if (deg >= 1) g += 3.0 * t;                      // l = 1
+            if (deg >= 2) g += 5.0 * (1.5 * t * t - 0.5);    // l = 2
+            if (deg >= 3) g += 7.0 * (2.5 * t * t - 1.5) * t;  // l = 3
+            const bool on = (fl[a] & kProjected) && (fl[b] & kProjected);
+            G[a][b] = G[b][a] = on ? g * k4pi : 0.0;
+        }
+}
+
+template <int MV>
+__device__ __forceinline__ void color_gram(const SceneDev& s, const ColorViews& cv, int k, double (&L)[MV][MV],
+                                           double (&E)[MV][MV]) {
+    color_gram_matrix<MV>(s, cv, k, L);
     jacobi_eig<MV>(L, E);
 }
 
@@ -482,7 +521,294 @@ __global__ void __launch_bounds__(128) solve_color_gram_k(SceneDev s, ColorViews
     }
 }
 
-// Colour solve, stage 2 (one thread per Gaussian and channel, blockIdx.y = channel).
+// This channel's per-view compact accumulators (colour_terms): views that are projected
+// and not colour-clamped in the channel; false when no view contributes.
+template <int MV>
+__device__ __forceinline__ bool color_channel_terms(const double* __restrict__ acc, size_t stride, int k, int nv,
+                                                    const uint8_t (&fl)[MV], int ch, double (&gv)[MV],
+                                                    double (&hv)[MV]) {
+    bool any = false;
+#pragma unroll
+    for (int v = 0; v < MV; ++v) {
+        gv[v] = 0.0;
+        hv[v] = 0.0;
+        if (v < nv && (fl[v] & kProjected) && !(fl[v] & (kClamp0 << ch))) {
+            const double* a = acc + static_cast<size_t>(v) * kAccOpColor * stride;
+            gv[v] = a[(2 + ch) * stride + k];
+            hv[v] = a[(5 + ch) * stride + k];
+            any = true;
+        }
+    }
+    return any;
+}
+
+// The exact psd_safeguard solve of one channel in view space from the Gram
+// eigen-decomposition G = E diag(L) E^T (n > 1): beta and |delta|^2 = beta^T G beta.
+template <int MV>
+__device__ __forceinline__ void color_channel_eigen(int n, const double (&L)[MV][MV], const double (&E)[MV][MV],
+                                                    const double (&gv)[MV], const double (&hv)[MV],
+                                                    const SolveParams& sp, double (&beta)[MV], double& nrm2) {
+    double lmax = 0;
+#pragma unroll
+    for (int a = 0; a < MV; ++a) lmax = fmax(lmax, L[a][a]);
+    bool kept[MV];
+    double isq[MV], sq[MV];  // L^-1/2 on kept directions
+    int r = 0;
+#pragma unroll
+    for (int a = 0; a < MV; ++a) {
+        kept[a] = L[a][a] > 1e-13 * lmax && L[a][a] > 0.0;
+        isq[a] = kept[a] ? rsqrt_pos(L[a][a]) : 0.0;
+        sq[a] = L[a][a] * isq[a];  // L^1/2 on kept directions, 0 elsewhere
+        r += kept[a] ? 1 : 0;
+    }
+#pragma unroll
+    for (int a = 0; a < MV; ++a) beta[a] = 0.0;
+    nrm2 = 0;
+    // K = L^1/2 E^T D E L^1/2 on the kept directions.
+    double K[MV][MV], W[MV][MV];
+#pragma unroll
+    for (int i = 0; i < MV; ++i)
+#pragma unroll
+        for (int j = i; j < MV; ++j) {
+            double t = 0;
+#pragma unroll
+            for (int v = 0; v < MV; ++v) t += E[v][i] * hv[v] * E[v][j];
+            K[i][j] = K[j][i] = t * sq[i] * sq[j];  // 0 unless both directions are kept
+        }
+    jacobi_eig<MV>(K, W);
+    // Eigenvectors y_e = Phi c_e with c_e = E L^-1/2 W_e; those living in the
+    // dropped subspace have c_e = 0.
+    double c[MV][MV];
+    bool live[MV];
+    double lam_abs_max = 0, lam_min = 1e300;
+#pragma unroll
+    for (int e = 0; e < MV; ++e) {
+        double wk = 0;
+#pragma unroll
+        for (int j = 0; j < MV; ++j) wk += kept[j] ? W[j][e] * W[j][e] : 0.0;
+        live[e] = wk > 0.5;
+#pragma unroll
+        for (int v = 0; v < MV; ++v) {
+            double t = 0;
+#pragma unroll
+            for (int j = 0; j < MV; ++j) t += E[v][j] * isq[j] * W[j][e];
+            c[e][v] = live[e] ? t : 0.0;
+        }
+        if (live[e]) {
+            lam_abs_max = fmax(lam_abs_max, fabs(K[e][e]));
+            lam_min = fmin(lam_min, K[e][e]);
+        }
+    }
+    if (r < n) lam_min = fmin(lam_min, 0.0);  // zero eigenvalues outside range(Phi)
+    const double mu = fmax(sp.mu_min, sp.eig_floor_rel * lam_abs_max);
+    const bool keep_h = lam_min >= mu;  // newton.hpp:231: PD input solved unmodified
+    double Gg[MV], Etg[MV];
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+        double t = 0;
+#pragma unroll
+        for (int v = 0; v < MV; ++v) t += E[v][j] * gv[v];
+        Etg[j] = L[j][j] * t;
+    }
+#pragma unroll
+    for (int a = 0; a < MV; ++a) {
+        double t = 0;
+#pragma unroll
+        for (int j = 0; j < MV; ++j) t += E[a][j] * Etg[j];
+        Gg[a] = t;
+    }
+#pragma unroll
+    for (int e = 0; e < MV; ++e) {
+        if (!live[e]) continue;
+        double yg = 0;
+#pragma unroll
+        for (int v = 0; v < MV; ++v) yg += c[e][v] * Gg[v];
+        const double lam = K[e][e];
+        const double l = keep_h ? lam : fmax(fabs(lam), mu);
+#pragma unroll
+        for (int v = 0; v < MV; ++v) beta[v] -= (yg / l) * c[e][v];
+    }
+    if (!keep_h) {
+        // range(Phi) directions with a vanishing Gram eigenvalue: eigenvalue ~0 -> mu.
+#pragma unroll
+        for (int a = 0; a < MV; ++a) {
+            if (kept[a] || !(L[a][a] > 0.0)) continue;
+            double eg = 0;
+#pragma unroll
+            for (int v = 0; v < MV; ++v) eg += E[v][a] * gv[v];
+#pragma unroll
+            for (int v = 0; v < MV; ++v) beta[v] -= E[v][a] * eg / mu;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+        double t = 0;
+#pragma unroll
+        for (int a = 0; a < MV; ++a) t += E[a][j] * beta[a];
+        nrm2 += L[j][j] * t * t;
+    }
+}
+
+// In-place lower Cholesky factor of a symmetric MV x MV matrix; false unless every pivot
+// is positive (the matrix is numerically positive definite).
+template <int MV>
+__device__ __forceinline__ bool cholesky(double (&a)[MV][MV]) {
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+        double d = a[j][j];
+#pragma unroll
+        for (int q = 0; q < j; ++q) d -= a[j][q] * a[j][q];
+        if (!(d > 0.0)) return false;
+        const double inv = rsqrt_pos(d);
+        a[j][j] = d * inv;
+#pragma unroll
+        for (int i = j + 1; i < MV; ++i) {
+            double t = a[i][j];
+#pragma unroll
+            for (int q = 0; q < j; ++q) t -= a[i][q] * a[j][q];
+            a[i][j] = t * inv;
+        }
+    }
+    return true;
+}
+
+// Fast path of color_channel_eigen when the safeguard provably leaves the spectrum
+// alone. On the views P that carry terms (the rest have zero Gram rows and beta_v = 0):
+// if every Gram eigenvalue is kept (G_P - 1e-13 |G_P|_F I is PD, |G_P|_F >= lambda_max)
+// and every eigenvalue of K ~ M = D^1/2 G_P D^1/2 (D = diag h_v > 0) is at least
+// mu = max(mu_min, rel * lambda_max) (M - max(mu_min, rel |M|_F) I is PD), the repaired
+// system is the unmodified one and the solution collapses to
+// beta_P = -G_P^-1 (g_v / h_v): two Cholesky tests and one Cholesky solve, no Jacobi.
+// Otherwise false (the caller runs the eigen path).
+template <int MV>
+__device__ __forceinline__ bool color_channel_fast(const double (&G)[MV][MV], const double (&gv)[MV],
+                                                   const double (&hv)[MV], const bool (&in)[MV],
+                                                   const SolveParams& sp, double (&beta)[MV], double& nrm2) {
+    double gf = 0, mf = 0;
+#pragma unroll
+    for (int a = 0; a < MV; ++a) {
+        if (in[a] && !(hv[a] > 0.0)) return false;
+#pragma unroll
+        for (int b = 0; b < MV; ++b)
+            if (in[a] && in[b]) {
+                gf += G[a][b] * G[a][b];
+                mf += (hv[a] * G[a][b] * hv[b]) * G[a][b];  // M_ab^2 = h_a h_b G_ab^2
+            }
+    }
+    gf = sqrt(gf);
+    const double mu_hi = fmax(sp.mu_min, sp.eig_floor_rel * sqrt(mf));
+    double A[MV][MV], C[MV][MV], F[MV][MV];
+    double sh[MV];
+#pragma unroll
+    for (int a = 0; a < MV; ++a) sh[a] = in[a] ? sqrt(hv[a]) : 1.0;
+#pragma unroll
+    for (int a = 0; a < MV; ++a)
+#pragma unroll
+        for (int b = 0; b < MV; ++b) {
+            const bool on = in[a] && in[b];
+            const double off = a == b ? 1.0 : 0.0;  // identity outside P
+            A[a][b] = on ? G[a][b] - (a == b ? 1e-13 * gf : 0.0) : off * (gf + 1.0);
+            C[a][b] = on ? sh[a] * G[a][b] * sh[b] - (a == b ? mu_hi : 0.0) : off * (mu_hi + 1.0);
+            F[a][b] = on ? G[a][b] : off;
+        }
+    if (!cholesky<MV>(A) || !cholesky<MV>(C) || !cholesky<MV>(F)) return false;
+    // F F^T beta = -(g / h) on P (zero right-hand side outside P: beta_v = 0 there)
+    double y[MV];
+#pragma unroll
+    for (int i = 0; i < MV; ++i) {
+        double t = in[i] ? -gv[i] / hv[i] : 0.0;
+#pragma unroll
+        for (int q = 0; q < i; ++q) t -= F[i][q] * y[q];
+        y[i] = t / F[i][i];
+    }
+#pragma unroll
+    for (int i = MV - 1; i >= 0; --i) {
+        double t = y[i];
+#pragma unroll
+        for (int q = i + 1; q < MV; ++q) t -= F[q][i] * beta[q];
+        beta[i] = t / F[i][i];
+    }
+    // |delta|^2 = beta^T G beta = |F^T beta|^2
+    nrm2 = 0;
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+        double t = 0;
+#pragma unroll
+        for (int i = j; i < MV; ++i) t += F[i][j] * beta[i];
+        nrm2 += t * t;
+    }
+    return true;
+}
+
+// Colour cap (newton.hpp:801-804), then delta_ch = sum_v beta_v phi_v (SH0: beta_0);
+// written to out.delta and / or committed.
+template <int MV>
+__device__ __forceinline__ void color_channel_commit(const SceneDev& s, const ColorViews& cv, const SolveParams& sp,
+                                                     const SolveOutputs& out, int k, int ch, bool any,
+                                                     const double (&beta)[MV], double nrm2, double& nsq,
+                                                     const D3* dirs = nullptr) {
+    const int n = s.n_coeffs, nv = cv.n_views;
+    double beta_all[MV];
+    double scale = 1.0;
+    if (any && sp.color_cap > 0.0 && sqrt(nrm2) > sp.color_cap) scale = sp.color_cap / sqrt(nrm2);
+    if (any) nsq += nrm2 * scale * scale;
+#pragma unroll
+    for (int a = 0; a < MV; ++a) beta_all[a] = any ? beta[a] * scale : 0.0;
+    double delta[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) delta[i] = 0.0;
+    if (n == 1) {
+        delta[0] = beta_all[0];
+    } else {
+        const float4 ps = s.pos_sigma[k];
+        const D3 p = {ps.x, ps.y, ps.z};
+#pragma unroll
+        for (int v = 0; v < MV; ++v) {
+            D3 dir = d3(0, 0, 1);
+            if (dirs) {
+                dir = dirs[v];
+            } else {
+                double nr;
+                if (v < nv && !view_direction(cv.cam[v], p, dir, nr)) dir = d3(0, 0, 1);
+            }
+            double ph[16];
+            sh_basis(dir, s.sh_degree, ph);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) delta[i] += beta_all[v] * ph[i];
+        }
+    }
+    if (out.delta)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) out.delta[48 * static_cast<size_t>(k) + 16 * ch + i] = i < n ? delta[i] : 0.0;
+    if (sp.commit) {  // all loads of the channel first, then the stores (no load-store serialisation)
+        float cur[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cur[i] = i < n ? s.sh[(static_cast<size_t>(16 * ch + i)) * s.n + k] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (i < n) s.sh[(static_cast<size_t>(16 * ch + i)) * s.n + k] = (float)((double)cur[i] + delta[i]);
+    }
+    if (out.accepted && ch == 0) out.accepted[k] = 1;
+}
+
+// Scalar system (psd_safeguard n = 1, SH0): phi = kSH0 for every view.
+template <int MV>
+__device__ __forceinline__ void color_channel_sh0(const double (&gv)[MV], const double (&hv)[MV],
+                                                  const SolveParams& sp, double (&beta)[MV], double& nrm2) {
+    double g = 0, h = 0;
+#pragma unroll
+    for (int a = 0; a < MV; ++a) {
+        g += gv[a] * kSH0;
+        h += hv[a] * kSH0 * kSH0;
+        beta[a] = 0.0;
+    }
+    const double d = solve1(h, g, sp);  // coefficient delta
+    beta[0] = d;
+    nrm2 = d * d;
+}
+
+// Colour solve, stage 2 (one thread per Gaussian and channel, blockIdx.y = channel), from
+// stage 1's Gram eigen-decomposition in the eig scratch.
 // (One thread per Gaussian with stage 1 in registers and the channels in turn, no eigen
 // scratch in HBM, measured slower: C4 colour 7.3 -> 8.9 ms.)
 template <int MV>
@@ -494,191 +820,83 @@ __global__ void __launch_bounds__(128, MV == 4 ? NGS_COLOR4_MINB : 2)
     if (k < s.n) {
         const int n = s.n_coeffs;
         const int nv = cv.n_views;
+        const int ch = blockIdx.y;
         uint8_t fl[MV];
 #pragma unroll
         for (int v = 0; v < MV; ++v) fl[v] = v < nv ? cv.flags[v][k] : 0;
-        // Stage 1's G = E L E^T (SH0: no stage 1, E = I and L unused). G itself is not
-        // re-formed: G g = E L E^T g and beta^T G beta = sum_j L_j (E^T beta)_j^2.
-        double L[MV][MV], E[MV][MV];
+        double gv[MV], hv[MV], beta[MV], nrm2 = 0.0;
+        const bool any = color_channel_terms<MV>(acc, stride, k, nv, fl, ch, gv, hv);
+        if (any) {
+            if (n == 1) {
+                color_channel_sh0<MV>(gv, hv, sp, beta, nrm2);
+            } else {
+                // Stage 1's G = E L E^T. G itself is not re-formed: G g = E L E^T g and
+                // beta^T G beta = sum_j L_j (E^T beta)_j^2.
+                double L[MV][MV], E[MV][MV];
 #pragma unroll
-        for (int a = 0; a < MV; ++a)
+                for (int a = 0; a < MV; ++a)
 #pragma unroll
-            for (int b = 0; b < MV; ++b) {
-                L[a][b] = (a == b && n > 1) ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : 0.0;
-                E[a][b] = n > 1 ? eig[static_cast<size_t>(MV * a + b) * stride + k] : (a == b ? 1.0 : 0.0);
+                    for (int b = 0; b < MV; ++b) {
+                        L[a][b] = a == b ? eig[static_cast<size_t>(MV * MV + a) * stride + k] : 0.0;
+                        E[a][b] = eig[static_cast<size_t>(MV * a + b) * stride + k];
+                    }
+                color_channel_eigen<MV>(n, L, E, gv, hv, sp, beta, nrm2);
             }
-        double lmax = 0;
-#pragma unroll
-        for (int a = 0; a < MV; ++a) lmax = fmax(lmax, L[a][a]);
-        bool kept[MV];
-        double isq[MV], sq[MV];  // L^-1/2 on kept directions
-        int r = 0;
-#pragma unroll
-        for (int a = 0; a < MV; ++a) {
-            kept[a] = L[a][a] > 1e-13 * lmax && L[a][a] > 0.0;
-            isq[a] = kept[a] ? rsqrt_pos(L[a][a]) : 0.0;
-            sq[a] = L[a][a] * isq[a];  // L^1/2 on kept directions, 0 elsewhere
-            r += kept[a] ? 1 : 0;
         }
+        color_channel_commit<MV>(s, cv, sp, out, k, ch, any, beta, nrm2, nsq);
+    }
+    block_add(nsq, out.norm_sq);
+}
+
+// Colour solve in ONE launch (one thread per Gaussian and channel): the Gram matrix of
+// the views' SH bases is formed in registers; the fast path (color_channel_fast) solves
+// without any eigen-decomposition, and only the channels that fail its tests
+// eigen-decompose G themselves and run the exact repair. No eig scratch in HBM.
+template <int MV>
+__global__ void __launch_bounds__(128, MV == 4 ? NGS_COLORF4_MINB : 2)
+    solve_color_fused_k(SceneDev s, ColorViews cv, SolveParams sp, const double* __restrict__ acc, size_t stride,
+                        SolveOutputs out, unsigned long long* __restrict__ fast_count) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    double nsq = 0.0;
+    bool fast = false;
+    if (k < s.n) {
+        const int n = s.n_coeffs;
+        const int nv = cv.n_views;
         const int ch = blockIdx.y;
-        double beta_all[MV];
-        do {
-            double gv[MV], hv[MV];
-            bool any = false;
+        uint8_t fl[MV];
 #pragma unroll
-            for (int v = 0; v < MV; ++v) {
-                gv[v] = 0.0;
-                hv[v] = 0.0;
-                beta_all[v] = 0.0;
-                if (v < nv && (fl[v] & kProjected) && !(fl[v] & (kClamp0 << ch))) {
-                    const double* a = acc + static_cast<size_t>(v) * kAccOpColor * stride;
-                    gv[v] = a[(2 + ch) * stride + k];
-                    hv[v] = a[(5 + ch) * stride + k];
-                    any = true;
-                }
-            }
-            if (!any) break;
-            double beta[MV];
-#pragma unroll
-            for (int a = 0; a < MV; ++a) beta[a] = 0.0;
-            double nrm2 = 0;
+        for (int v = 0; v < MV; ++v) fl[v] = v < nv ? cv.flags[v][k] : 0;
+        double gv[MV], hv[MV], beta[MV], nrm2 = 0.0;
+        D3 dir[MV];
+        const bool any = color_channel_terms<MV>(acc, stride, k, nv, fl, ch, gv, hv);
+        if (any) {
             if (n == 1) {
-                // Scalar system (psd_safeguard n = 1); phi = kSH0 for every view.
-                double g = 0, h = 0;
-#pragma unroll
-                for (int a = 0; a < MV; ++a) {
-                    g += gv[a] * kSH0;
-                    h += hv[a] * kSH0 * kSH0;
-                }
-                const double d = solve1(h, g, sp);  // coefficient delta
-                beta[0] = d;
-                nrm2 = d * d;
+                color_channel_sh0<MV>(gv, hv, sp, beta, nrm2);
             } else {
-                // K = L^1/2 E^T D E L^1/2 on the kept directions.
-                double K[MV][MV], W[MV][MV];
-#pragma unroll
-                for (int i = 0; i < MV; ++i)
-#pragma unroll
-                    for (int j = i; j < MV; ++j) {
-                        double t = 0;
-#pragma unroll
-                        for (int v = 0; v < MV; ++v) t += E[v][i] * hv[v] * E[v][j];
-                        K[i][j] = K[j][i] = t * sq[i] * sq[j];  // 0 unless both directions are kept
-                    }
-                jacobi_eig<MV>(K, W);
-                // Eigenvectors y_e = Phi c_e with c_e = E L^-1/2 W_e; those living in the
-                // dropped subspace have c_e = 0.
-                double c[MV][MV];
-                bool live[MV];
-                double lam_abs_max = 0, lam_min = 1e300;
-#pragma unroll
-                for (int e = 0; e < MV; ++e) {
-                    double wk = 0;
-#pragma unroll
-                    for (int j = 0; j < MV; ++j) wk += kept[j] ? W[j][e] * W[j][e] : 0.0;
-                    live[e] = wk > 0.5;
-#pragma unroll
-                    for (int v = 0; v < MV; ++v) {
-                        double t = 0;
-#pragma unroll
-                        for (int j = 0; j < MV; ++j) t += E[v][j] * isq[j] * W[j][e];
-                        c[e][v] = live[e] ? t : 0.0;
-                    }
-                    if (live[e]) {
-                        lam_abs_max = fmax(lam_abs_max, fabs(K[e][e]));
-                        lam_min = fmin(lam_min, K[e][e]);
-                    }
-                }
-                if (r < n) lam_min = fmin(lam_min, 0.0);  // zero eigenvalues outside range(Phi)
-                const double mu = fmax(sp.mu_min, sp.eig_floor_rel * lam_abs_max);
-                const bool keep_h = lam_min >= mu;  // newton.hpp:231: PD input solved unmodified
-                double Gg[MV], Etg[MV];
-#pragma unroll
-                for (int j = 0; j < MV; ++j) {
-                    double t = 0;
-#pragma unroll
-                    for (int v = 0; v < MV; ++v) t += E[v][j] * gv[v];
-                    Etg[j] = L[j][j] * t;
-                }
-#pragma unroll
-                for (int a = 0; a < MV; ++a) {
-                    double t = 0;
-#pragma unroll
-                    for (int j = 0; j < MV; ++j) t += E[a][j] * Etg[j];
-                    Gg[a] = t;
-                }
-#pragma unroll
-                for (int e = 0; e < MV; ++e) {
-                    if (!live[e]) continue;
-                    double yg = 0;
-#pragma unroll
-                    for (int v = 0; v < MV; ++v) yg += c[e][v] * Gg[v];
-                    const double lam = K[e][e];
-                    const double l = keep_h ? lam : fmax(fabs(lam), mu);
-#pragma unroll
-                    for (int v = 0; v < MV; ++v) beta[v] -= (yg / l) * c[e][v];
-                }
-                if (!keep_h) {
-                    // range(Phi) directions with a vanishing Gram eigenvalue: eigenvalue ~0 -> mu.
-#pragma unroll
-                    for (int a = 0; a < MV; ++a) {
-                        if (kept[a] || !(L[a][a] > 0.0)) continue;
-                        double eg = 0;
-#pragma unroll
-                        for (int v = 0; v < MV; ++v) eg += E[v][a] * gv[v];
-#pragma unroll
-                        for (int v = 0; v < MV; ++v) beta[v] -= E[v][a] * eg / mu;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < MV; ++j) {
-                    double t = 0;
-#pragma unroll
-                    for (int a = 0; a < MV; ++a) t += E[a][j] * beta[a];
-                    nrm2 += L[j][j] * t * t;
-                }
-            }
-            // Colour cap (newton.hpp:801-804) on |delta| = sqrt(beta^T G beta).
-            double scale = 1.0;
-            if (sp.color_cap > 0.0 && sqrt(nrm2) > sp.color_cap) scale = sp.color_cap / sqrt(nrm2);
-            nsq += nrm2 * scale * scale;
-#pragma unroll
-            for (int a = 0; a < MV; ++a) beta_all[a] = beta[a] * scale;
-        } while (false);
-        // delta_ch = sum_v beta_v phi_v (SH0: delta = beta_0); write / commit.
-        {
-            double delta[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) delta[i] = 0.0;
-            if (n == 1) {
-                delta[0] = beta_all[0];
-            } else {
-                const float4 ps = s.pos_sigma[k];
-                const D3 p = {ps.x, ps.y, ps.z};
+                double L[MV][MV], E[MV][MV];
+                color_gram_addition<MV>(s, cv, k, fl, L, dir);
+                // P = the projected views (the nonzero Gram rows); a projected view whose
+                // colour is clamped in this channel carries h_v = 0 (a zero eigenvalue the
+                // repair floors): eigen path.
+                bool in[MV], clamped = false;
 #pragma unroll
                 for (int v = 0; v < MV; ++v) {
-                    D3 dir = d3(0, 0, 1);
-                    double nr;
-                    if (v < nv && !view_direction(cv.cam[v], p, dir, nr)) dir = d3(0, 0, 1);
-                    double ph[16];
-                    sh_basis(dir, s.sh_degree, ph);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) delta[i] += beta_all[v] * ph[i];
+                    in[v] = v < nv && (fl[v] & kProjected);
+                    clamped |= in[v] && (fl[v] & (kClamp0 << ch));
+                }
+                fast = !clamped && color_channel_fast<MV>(L, gv, hv, in, sp, beta, nrm2);
+                if (!fast) {  // the explicit Gram (as the two-stage kernels) and the exact repair
+                    color_gram_matrix<MV>(s, cv, k, L);
+                    jacobi_eig<MV>(L, E);
+                    color_channel_eigen<MV>(n, L, E, gv, hv, sp, beta, nrm2);
                 }
             }
-            if (out.delta)
-#pragma unroll
-                for (int i = 0; i < 16; ++i) out.delta[48 * static_cast<size_t>(k) + 16 * ch + i] = i < n ? delta[i] : 0.0;
-            if (sp.commit) {  // all loads of the channel first, then the stores (no load-store serialisation)
-                float cur[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) cur[i] = i < n ? s.sh[(static_cast<size_t>(16 * ch + i)) * s.n + k] : 0.f;
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (i < n) s.sh[(static_cast<size_t>(16 * ch + i)) * s.n + k] = (float)((double)cur[i] + delta[i]);
-            }
         }
-        if (out.accepted && ch == 0) out.accepted[k] = 1;
+        color_channel_commit<MV>(s, cv, sp, out, k, ch, any, beta, nrm2, nsq, any && n > 1 ? dir : nullptr);
+    }
+    if (fast_count) {
+        const unsigned b = __ballot_sync(0xffffffffu, fast);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(fast_count, static_cast<unsigned long long>(__popc(b)));
     }
     block_add(nsq, out.norm_sq);
 }
@@ -835,7 +1053,7 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
                   size_t stride, const SolveOutputs& out, cudaStream_t s) {
     const int n = scene.n;
     if (n == 0) return;
-    StageScope st(NGS_STAGE_SOLVE, s, attr == NGS_COLOR && scene.n_coeffs > 1 ? 2 : 1);
+    StageScope st(NGS_STAGE_SOLVE, s, attr == NGS_COLOR && scene.n_coeffs > 1 && !cv.fused ? 2 : 1);
     switch (attr) {
         case NGS_POSITION:
             solve_position_k<<<blocks_for(n), 256, 0, s>>>(scene, primary, sp, acc, stride, out);
@@ -851,21 +1069,28 @@ void launch_solve(int attr, const SceneDev& scene, const CameraDev& primary, dou
             solve_opacity_k<<<blocks_for(n), 256, 0, s>>>(scene, sp, acc, stride, cv.n_views, out);
             break;
         case NGS_COLOR: {
-            // stage 1 (Gram eigen-decomposition, only with higher SH bands) + stage 2 per channel
-            auto run = [&](auto gram_kernel, auto ch_kernel) {
+            // fused: one launch, Gram in registers, fast path / in-thread eigen repair;
+            // otherwise stage 1 (Gram eigen-decomposition, only with higher SH bands) +
+            // stage 2 per channel
+            auto run = [&](auto gram_kernel, auto ch_kernel, auto fused_kernel) {
+                if (cv.fused) {
+                    fused_kernel<<<dim3(blocks_for(n, 128), 3), 128, 0, s>>>(scene, cv, sp, acc, stride, out,
+                                                                              cv.fast_count);
+                    return;
+                }
                 if (scene.n_coeffs > 1) gram_kernel<<<blocks_for(n, 128), 128, 0, s>>>(scene, cv, cv.eig, stride);
                 ch_kernel<<<dim3(blocks_for(n, 128), 3), 128, 0, s>>>(scene, cv, sp, acc, stride, cv.eig, out);
             };
             if (cv.n_views <= 1) {
-                run(solve_color_gram_k<1>, solve_color_k<1>);
+                run(solve_color_gram_k<1>, solve_color_k<1>, solve_color_fused_k<1>);
             } else if (cv.n_views <= 2) {
-                run(solve_color_gram_k<2>, solve_color_k<2>);
+                run(solve_color_gram_k<2>, solve_color_k<2>, solve_color_fused_k<2>);
             } else if (cv.n_views <= 4) {
-                run(solve_color_gram_k<4>, solve_color_k<4>);
+                run(solve_color_gram_k<4>, solve_color_k<4>, solve_color_fused_k<4>);
             } else if (cv.n_views <= 8) {
-                run(solve_color_gram_k<8>, solve_color_k<8>);
+                run(solve_color_gram_k<8>, solve_color_k<8>, solve_color_fused_k<8>);
             } else {  // knn 8..15 (the reference's overshoot ablation uses knn = 8): spills, rarely used
-                run(solve_color_gram_k<16>, solve_color_k<16>);
+                run(solve_color_gram_k<16>, solve_color_k<16>, solve_color_fused_k<16>);
             }
             break;
         }

@@ -30,6 +30,8 @@ struct ColorViews {
     CameraDev cam[kMaxSolveViews];
     const uint8_t* flags[kMaxSolveViews];
     double* eig;  // colour-solve scratch: (MV^2 + MV) doubles per Gaussian (Gram eigen-decomposition)
+    int fused;    // 1: one-launch colour solve with the no-repair fast path (no eig scratch)
+    unsigned long long* fast_count;  // optional: channel solves that took the fast path
 };
 
 // First-order baselines (first_order_step, trainer.hpp:419-509).

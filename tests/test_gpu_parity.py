@@ -223,6 +223,36 @@ def test_newton_step(gpu, newton_fixture, attr):
         assert e < TOL, f
 
 
+def test_fused_color_solve(gpu, monkeypatch):
+    """Opt-in one-launch colour solve (NGS_COLOR_FUSED=1): with widely separated views
+    the Gram and view-space systems pass the no-repair tests, and the fast path
+    beta = -G^-1 (g / h) must reproduce the reference's eigen-repaired solve; channels
+    that fail the tests run the exact repair in the same launch."""
+    scene, cam, target = check_fixture(7)
+    r0 = ref().context()
+    r0.set_scene(scene)
+    secs = []
+    for eye in [(3.0, 0.4, 0.3), (-2.9, 0.6, -0.4), (0.3, 3.0, -0.6)]:
+        c = test_camera(eye, 32, 32)
+        secs.append((c, r0.render(c)))
+    fx = (scene, cam, target, secs)
+    monkeypatch.setenv("NGS_COLOR_FUSED", "1")  # read at context creation
+    g, r = pair(gpu, scene)
+    sec = _views(g, fx)
+    _views(r, fx)
+    g.profile_reset()
+    dg = g.newton_step(capi.COLOR, 0, sec)
+    dr = r.newton_step(capi.COLOR, 0, sec)
+    prof = g.profile_read()
+    e = qerr(dg["delta"], dr["delta"])
+    print(f"fused colour solve: delta {e:.2e}, fast-path channels {prof['color_fast_channels']}/{prof['color_channels']}")
+    assert prof["color_fast_channels"] > 0
+    assert e < TOL_DELTA
+    assert np.array_equal(dg["accepted"], dr["accepted"])
+    e = qerr(g.get_scene().sh, r.get_scene().sh)
+    assert e < TOL, e
+
+
 # ---------------------------------------------------------------------------
 # Trainer::step
 # ---------------------------------------------------------------------------
