@@ -870,6 +870,7 @@ struct BackwardSmem {
     float4 raw[2][4][B];                   // staged records (pix as double2, ra, rb, rc), double-buffered
     float4 cst[2][(CST > 0 ? CST : 1) * B];  // staged per-view constants, double-buffered
     SplatSh sp[B];                         // staged splats of the batch
+    double cold[3][B];                     // their colours widened to FP64 once (the FP64 prefix operand)
     unsigned char wmask[B];                // bit w: the splat's cutoff ellipse reaches warp w's pixel rows
     // Per-warp sums (segment tails are unique within a drain), as NA / 4 float4 planes
     // plus a float2 and / or a float plane for the remainder: a segment tail adds its NA
@@ -1125,6 +1126,9 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
                 sp.g2 = make_float2(rb.w, rc.x);
                 sp.pad = make_float2(0.f, 0.f);
                 s_sp[tid] = sp;
+                S.cold[0][tid] = rb.z;
+                S.cold[1][tid] = rb.w;
+                S.cold[2][tid] = rc.x;
                 S.wmask[tid] = static_cast<unsigned char>(
                     WarpBox<TILE>::mask_exact(px, py, ellipse_half_extent(qmax, rc.y), ellipse_half_extent(qmax, rc.w),
                                               ra.z, ra.w, rb.x, qmax));
@@ -1146,41 +1150,9 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
             while (m) {
                 const int j = c32 + __ffs(m) - 1;
                 m &= m - 1;
-                bool contrib = false;
-                float G = 0.f, q0 = 0.f, q1 = 0.f, Tr = 0.f, wa = 0.f, ac0 = 0.f, ac1 = 0.f, ac2 = 0.f;
                 const SplatSh sp = s_sp[j];
                 SplatEval ev;
-                const bool cand = eval_splat_bf(sp, fx, fy, a.cutoff, ev);
-                {
-                    if (cand && base + j <= last) {
-                        contrib = true;
-                        const float col[3] = {sp.g1.w, sp.g2.x, sp.g2.y};
-                        const float Ti = T;
-                        const float w = blend_weight(Ti, ev.alpha);
-                        const float Tn = next_transmittance(Ti, ev.alpha);
-                        const bool is_last = (base + j == last);
-                        float inv_tn;  // behind is a derived quantity (not re-composited): approximate 1/T is enough
-                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_tn) : "f"(Tn));
-                        float ac[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const double Pn = __fma_rn(static_cast<double>(w), static_cast<double>(col[c]), P[c]);
-                            const float behind =
-                                is_last ? a.bg[c] : __double2float_rn(__dsub_rn(Cf[c], Pn)) * inv_tn;
-                            ac[c] = col[c] - behind;
-                            P[c] = Pn;
-                        }
-                        T = Tn;
-                        G = ev.g;
-                        q0 = ev.qd0;
-                        q1 = ev.qd1;
-                        Tr = Ti;
-                        wa = sp.g1.y * Ti;
-                        ac0 = ac[0];
-                        ac1 = ac[1];
-                        ac2 = ac[2];
-                    }
-                }
+                const bool contrib = eval_splat_bf(sp, fx, fy, a.cutoff, ev) && base + j <= last;
                 const unsigned ballot = __ballot_sync(0xffffffffu, contrib);
 #ifdef NGS_COUNT_CANDIDATES
                 if (lane == 0) {  // debug: [PASS][0] candidates, [1] with >= 1 record, [2] records; [3] = TILE 8
@@ -1191,10 +1163,29 @@ __device__ __forceinline__ void backward_body(const BackwardArgs& a, const int b
                 }
 #endif
                 if (ballot) {
-                    if (contrib) {
+                    if (contrib) {  // the record, straight into the warp's queue
+                        const float col[3] = {sp.g1.w, sp.g2.x, sp.g2.y};
+                        const float Ti = T;
+                        const float w = blend_weight(Ti, ev.alpha);
+                        const float Tn = next_transmittance(Ti, ev.alpha);
+                        const bool is_last = (base + j == last);
+                        float inv_tn;  // behind is a derived quantity (not re-composited): approximate 1/T is enough
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_tn) : "f"(Tn));
+                        const double wd = static_cast<double>(w);
+                        float ac[3];  // c~ - behind, behind = (C_final - prefix) / T_next (bg for the last record)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            // colours widened once per splat at staging (S.cold), not per record
+                            const double Pn = __fma_rn(wd, S.cold[c][j], P[c]);
+                            const float behind =
+                                is_last ? a.bg[c] : __double2float_rn(__dsub_rn(Cf[c], Pn)) * inv_tn;
+                            ac[c] = col[c] - behind;
+                            P[c] = Pn;
+                        }
+                        T = Tn;
                         const int slot = (qhead + qcount + __popc(ballot & ((1u << lane) - 1u))) & (kQ - 1);
-                        Q.r0[slot] = make_float4(G, q0, q1, Tr);
-                        Q.r1[slot] = make_float4(wa, ac0, ac1, ac2);
+                        Q.r0[slot] = make_float4(ev.g, ev.qd0, ev.qd1, Ti);
+                        Q.r1[slot] = make_float4(sp.g1.y * Ti, ac[0], ac[1], ac[2]);
                         Q.jp[slot] = static_cast<unsigned short>(j | (lane << 8));
                     }
                     qcount += __popc(ballot);
