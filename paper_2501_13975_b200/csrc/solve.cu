@@ -31,6 +31,9 @@ __device__ __forceinline__ void block_add(double v, unsigned long long* target) 
     __shared__ double red[8];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // a previous block_add's thread 0 may still be reading red[] (first_order_k calls this
+    // once per attribute back to back): overwrite only after it is done
+    __syncthreads();
     if (lane == 0) red[warp] = v;
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -126,3 +126,27 @@ def test_adam_moments_follow_the_scene(gpu):
     r2 = fresh.trainer_step(big["train"][0])
     for a, b in zip(r1.delta_norms, r2.delta_norms):
         assert abs(a - b) <= 1e-6 * max(abs(b), 1e-12)
+
+
+def test_first_order_reported_norms_match_the_update(gpu):
+    """The first-order kernel reduces five per-attribute norms with back-to-back block
+    reductions; the reported |delta| of position and colour must equal the parameter change
+    actually committed (a shared-memory reuse race there once corrupted the first step's
+    report). Held to the FP32 parameter storage rounding (2e-3 relative)."""
+    d = synth(seed=32, kernels=200, views=4, probe_views=0, width=48, height=48, perturbation=0.5,
+              secondary_downsample=2)
+    for opt in (capi.OPT_ADAM, capi.OPT_GD):
+        ctx = gpu.context()
+        ctx.set_scene(d["init"])
+        cfg = gpu.default_train()
+        cfg.optimizer = opt
+        ctx.trainer_configure(cfg, d["cameras"], d["targets"], d["train"])
+        for v in d["train"][:3]:
+            before = ctx.get_scene()
+            rep = ctx.trainer_step(v)
+            after = ctx.get_scene()
+            for a, f in ((capi.POSITION, "position"), (capi.COLOR, "sh")):
+                moved = float(np.linalg.norm(getattr(after, f) - getattr(before, f)))
+                got = rep.delta_norms[a]
+                assert abs(got - moved) <= 2e-3 * max(moved, 1e-9), (opt, v, f, got, moved)
+        ctx.close()
