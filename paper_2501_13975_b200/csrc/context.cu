@@ -1402,11 +1402,7 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     // fused projection launch for all views was measured slower: it serialises the views'
     // chains behind one kernel and re-reads the SH planes per view anyway.)
     if (concurrent) ctx->fork(nv, ctx->vr.data());
-    for (int ii = 0; ii < nv; ++ii) {
-        const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
-        const int i = concurrent && sec_first ? nv - 1 - ii : ii;  // secondaries first (see ngs_context_create)
-        ViewSlot& v = T.views[i];
-        cudaStream_t s = concurrent ? ctx->vr[i] : ctx->stream;
+    auto sync_of = [&](int i) {
         RenderSync rs;
         rs.exact = false;
         rs.overflow = ctx->overflow.ptr;
@@ -1414,7 +1410,28 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
         if (concurrent && !join) rs.projected = ctx->pev[i];
         rs.pos_version = ctx->order_reuse ? ctx->pos_version : 0;
         rs.sh_version = ctx->order_reuse ? ctx->sh_version : 0;
-        render_view(ctx->scene, v, false, ctx->err.ptr, s, rs);
+        return rs;
+    };
+    const bool sec_first = ctx->stream_policy == 0 || ctx->stream_policy == 2;
+    auto view_at = [&](int ii) { return concurrent && sec_first ? nv - 1 - ii : ii; };  // see ngs_context_create
+    // Every view's projection is enqueued before any view's binning chain: enqueueing the
+    // views one whole chain after another (~11 launches each) started the last view's
+    // projection ~0.25 ms after the first on the device.
+    for (int ii = 0; ii < nv; ++ii) {
+        const int i = view_at(ii);
+        ViewSlot& v = T.views[i];
+        cudaStream_t s = concurrent ? ctx->vr[i] : ctx->stream;
+        const RenderSync rs = sync_of(i);
+        prepare_view(ctx->scene, v, false, rs);
+        ViewSlot* one = &v;
+        project_views(ctx->scene, &one, 1, false, ctx->err.ptr, s);
+        if (rs.projected) CUDA_CHECK(cudaEventRecord(rs.projected, s));
+    }
+    for (int ii = 0; ii < nv; ++ii) {
+        const int i = view_at(ii);
+        ViewSlot& v = T.views[i];
+        cudaStream_t s = concurrent ? ctx->vr[i] : ctx->stream;
+        bin_and_raster(ctx->scene, v, ctx->err.ptr, s, sync_of(i));
         if (v.raster.owns_rows()) {
             if (upload_targets && concurrent) CUDA_CHECK(cudaStreamWaitEvent(s, ctx->tev[i], 0));
             compute_loss(v, s);
