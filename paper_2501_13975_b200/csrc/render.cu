@@ -341,14 +341,19 @@ __global__ void tile_ranges_k(const int* d_pairs, int T, const unsigned int* key
 // (__syncthreads_count = block-wide ballot). Pixel centres and splat centres
 // are expressed relative to the tile origin so the FP32 offsets carry
 // full precision at 4K resolutions.
-template <int TILE>
-struct RasterSmem {
-    static constexpr int N = TILE * TILE;
+template <int N_>
+struct RasterSmemB {
+    static constexpr int N = N_;
     float4 raw[2][4][N];  // staged records (pix as double2, ra, rb, rc), double-buffered
     double col[3][N];
     SplatSh sp[N];
     unsigned char wmask[N];
 };
+template <int TILE>
+using RasterSmem = RasterSmemB<TILE * TILE>;
+#ifndef NGS_RASTER2_BATCH
+#define NGS_RASTER2_BATCH 128
+#endif
 
 // CK: also write each pixel's compositing state (T, FP64 colour prefix) at the chunk
 // boundaries chunk_begin(range, c, chunks), c = 1 .. chunks-1, of its tile's list: the
@@ -480,9 +485,144 @@ __global__ void __launch_bounds__(TILE * TILE) raster_forward_k(int tiles_x, int
     }
 }
 
+// The 16x16-tile forward with TWO pixels per lane: 4 warps, each an 8x8 box, lane l
+// owning pixels (l % 8, l / 8) and (l % 8, l / 8 + 4) of it. Per splat a warp loads the
+// record and walks the mask loop once for 64 pixels and evaluates both on packed f32x2
+// (eval_splat_bf2: bit-identical to the scalar evaluation), so the per-pixel results —
+// image, T and last contributor — are the one-pixel-per-lane kernel's, bit for bit.
+template <int TILE, int B>
+__global__ void __launch_bounds__(TILE * TILE / 2) raster_forward2_k(
+    int tiles_x, int W, int H, const int2* __restrict__ ranges, const int* __restrict__ vals,
+    const double2* __restrict__ pix, const float4* __restrict__ ra, const float4* __restrict__ rb,
+    const float4* __restrict__ rc, float bg0, float bg1, float bg2, float cutoff, float tmin,
+    double* __restrict__ image, float* __restrict__ t_final, int* __restrict__ last_out) {
+    using WB = WarpBoxT<TILE, 8>;
+    constexpr int NT = TILE * TILE / 2, HPT = B / NT;  // B staged splats per batch, HPT per thread
+    static_assert(B % NT == 0, "whole splats per thread");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RasterSmemB<B>& S = *reinterpret_cast<RasterSmemB<B>*>(smem_raw);
+    const int tile = blockIdx.x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int lx = (warp % WB::ACROSS) * WB::BW + (lane & 7), ly = (warp / WB::ACROSS) * WB::BH + (lane >> 3);
+    const int x = tx * TILE + lx, y0 = ty * TILE + ly, y1 = y0 + 4;
+    const bool in0 = x < W && y0 < H, in1 = x < W && y1 < H;
+    const float fx = lx + 0.5f, fy0 = ly + 0.5f, fy1 = ly + 4.5f;
+    const double ox = tx * TILE, oy = ty * TILE;
+    const int2 range = ranges[tile];
+    float T0 = 1.0f, T1 = 1.0f;
+    double C0[3] = {0.0, 0.0, 0.0}, C1[3] = {0.0, 0.0, 0.0};
+    int last0 = -1, last1 = -1;
+    bool done0 = !in0, done1 = !in1;
+    const float tmin_eff = tmin > 0.f ? tmin : -1.0f;
+    auto issue = [&](int buf, int slot, int k) {
+        cp_async16(&S.raw[buf][0][slot], pix + k);
+        cp_async16(&S.raw[buf][1][slot], ra + k);
+        cp_async16(&S.raw[buf][2][slot], rb + k);
+        cp_async16(&S.raw[buf][3][slot], rc + k);
+    };
+#pragma unroll
+    for (int h = 0; h < HPT; ++h)
+        if (range.x + t + h * NT < range.y) issue(0, t + h * NT, vals[range.x + t + h * NT]);
+    cp_async_commit();
+    int kn[HPT];
+#pragma unroll
+    for (int h = 0; h < HPT; ++h) kn[h] = range.x + B + t + h * NT < range.y ? vals[range.x + B + t + h * NT] : 0;
+    int it = 0;
+    for (int base = range.x; base < range.y; base += B, ++it) {
+        const int buf = it & 1;
+        if (__syncthreads_count(done0 && done1) == NT) break;
+        cp_async_wait_all();
+#pragma unroll
+        for (int h = 0; h < HPT; ++h) {
+            const int slot = t + h * NT, i = base + slot;
+            if (i < range.y) {
+                const double2 p = reinterpret_cast<const double2*>(S.raw[buf][0])[slot];
+                const float4 a = S.raw[buf][1][slot], b = S.raw[buf][2][slot], c = S.raw[buf][3][slot];
+                const float qmax = reject_bound(b.y, cutoff);
+                const float py = static_cast<float>(p.y - oy);
+                const float px = static_cast<float>(p.x - ox);
+                SplatSh sp;
+                sp.g0 = make_float4(px, py, a.z, a.w);
+                sp.g1 = make_float4(b.x, b.y, qmax, b.z);
+                sp.g2 = make_float2(b.w, c.x);
+                sp.pad = make_float2(0.f, 0.f);
+                S.sp[slot] = sp;
+                S.col[0][slot] = b.z;
+                S.col[1][slot] = b.w;
+                S.col[2][slot] = c.x;
+                S.wmask[slot] = static_cast<unsigned char>(WB::mask_exact(
+                    px, py, ellipse_half_extent(qmax, c.y), ellipse_half_extent(qmax, c.w), a.z, a.w, b.x, qmax));
+            } else {
+                S.wmask[slot] = 0;
+            }
+            if (i + B < range.y) issue(buf ^ 1, slot, kn[h]);
+        }
+        cp_async_commit();
+#pragma unroll
+        for (int h = 0; h < HPT; ++h) {
+            const int i2 = base + t + h * NT + 2 * B;
+            kn[h] = i2 < range.y ? vals[i2] : 0;
+        }
+        __syncthreads();
+        const int cnt = min(B, range.y - base);
+        for (int c32 = 0; c32 < cnt && !__all_sync(0xffffffffu, done0 && done1); c32 += 32) {
+            unsigned m = __ballot_sync(0xffffffffu, (S.wmask[c32 + lane] >> warp) & 1u);
+            while (m) {
+                const int j = c32 + __ffs(m) - 1;
+                m &= m - 1;
+                const SplatSh sp = S.sp[j];
+                SplatEval e0, e1;
+                bool k0, k1;
+                eval_splat_bf2(sp, fx, fy0, fy1, cutoff, e0, e1, k0, k1);
+                if (k0 && !done0) {
+                    const double w = blend_weight(T0, e0.alpha);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) C0[q] = __fma_rn(w, S.col[q][j], C0[q]);
+                    T0 = next_transmittance(T0, e0.alpha);
+                    last0 = base + j;
+                    if (T0 < tmin_eff) done0 = true;
+                }
+                if (k1 && !done1) {
+                    const double w = blend_weight(T1, e1.alpha);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) C1[q] = __fma_rn(w, S.col[q][j], C1[q]);
+                    T1 = next_transmittance(T1, e1.alpha);
+                    last1 = base + j;
+                    if (T1 < tmin_eff) done1 = true;
+                }
+            }
+        }
+    }
+    cp_async_wait_all();
+    const size_t plane = static_cast<size_t>(W) * H;
+    if (in0) {
+        const size_t idx = static_cast<size_t>(y0) * W + x;
+        image[idx] = __fma_rn(T0, bg0, C0[0]);
+        image[plane + idx] = __fma_rn(T0, bg1, C0[1]);
+        image[2 * plane + idx] = __fma_rn(T0, bg2, C0[2]);
+        t_final[idx] = T0;
+        last_out[idx] = last0;
+    }
+    if (in1) {
+        const size_t idx = static_cast<size_t>(y1) * W + x;
+        image[idx] = __fma_rn(T1, bg0, C1[0]);
+        image[plane + idx] = __fma_rn(T1, bg1, C1[1]);
+        image[2 * plane + idx] = __fma_rn(T1, bg2, C1[2]);
+        t_final[idx] = T1;
+        last_out[idx] = last1;
+    }
+}
+
 inline int blocks_for(int n, int b = 256) { return (n + b - 1) / b; }
 
 }  // namespace
+
+// 16x16 tiles: two pixels per lane in the forward (NGS_RASTER2=0: one pixel per lane, A/B).
+static const bool g_raster2 = [] {
+    const char* e = getenv("NGS_RASTER2");
+    return !e || atoi(e) != 0;
+}();
 
 // Allocations of one view and the depth-order reuse decision (host only).
 bool prepare_view(const SceneDev& scene, ViewSlot& v, bool want_debug, const RenderSync& sync) {
@@ -644,12 +784,20 @@ void bin_and_raster(const SceneDev& scene, ViewSlot& v, int* d_err, cudaStream_t
                                        scene.bg[2], v.raster.alpha_cutoff, v.raster.t_min, v.image.ptr, v.t_final.ptr,
                                        v.last.ptr, chunks, v.ck_t.ptr, v.ck_p.ptr);
     };
-    if (v.cam.tile == 8 && chunks > 1)
+    if (v.cam.tile == 8 && chunks > 1) {
         launch(raster_forward_k<8, true>, 64, sizeof(RasterSmem<8>));
-    else if (v.cam.tile == 8)
+    } else if (v.cam.tile == 8) {
         launch(raster_forward_k<8, false>, 64, sizeof(RasterSmem<8>));
-    else
+    } else if (g_raster2) {
+        constexpr int B2 = NGS_RASTER2_BATCH;
+        ensure_dynamic_smem(reinterpret_cast<const void*>(raster_forward2_k<16, B2>), sizeof(RasterSmemB<B2>));
+        raster_forward2_k<16, B2><<<v.T, 128, sizeof(RasterSmemB<B2>), s>>>(
+            v.cam.tiles_x, v.W, v.H, v.ranges.ptr, cap > 0 ? v.pair_val.ptr : nullptr, v.pix.ptr, v.rec_a.ptr,
+            v.rec_b.ptr, v.rec_c.ptr, scene.bg[0], scene.bg[1], scene.bg[2], v.raster.alpha_cutoff, v.raster.t_min,
+            v.image.ptr, v.t_final.ptr, v.last.ptr);
+    } else {
         launch(raster_forward_k<16, false>, 256, sizeof(RasterSmem<16>));
+    }
     CUDA_LAUNCH_CHECK();
     v.valid = true;
 }

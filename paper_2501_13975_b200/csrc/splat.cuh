@@ -26,9 +26,9 @@ struct SplatEval {
 // Pixel <-> thread map of a tile block: each warp owns an 8x4 pixel box (two
 // boxes across a 16-wide tile), tighter than a 16x2 strip for the warp-level
 // overlap masks built below.
-template <int TILE>
-struct WarpBox {
-    static constexpr int BW = 8, BH = 4, ACROSS = TILE / BW, NW = TILE * TILE / 32;
+template <int TILE, int BH_ = 4>
+struct WarpBoxT {
+    static constexpr int BW = 8, BH = BH_, ACROSS = TILE / BW, NW = TILE * TILE / (BW * BH);
     __device__ static void pixel(int tid, int& lx, int& ly) {
         const int warp = tid >> 5, lane = tid & 31;
         lx = (warp % ACROSS) * BW + (lane % BW);
@@ -74,6 +74,9 @@ struct WarpBox {
         return m;
     }
 };
+
+template <int TILE>
+using WarpBox = WarpBoxT<TILE, 4>;
 
 // Half-extents of the cutoff ellipse {q <= qmax}: |dx| <= sqrt(qmax Sigma00),
 // |dy| <= sqrt(qmax Sigma11); widened so the warp-level skip never drops a
@@ -157,6 +160,50 @@ __device__ __forceinline__ bool eval_splat_bf(const SplatSh& sp, float x, float 
     e.g = exp_neg_half(q);
     e.alpha = __fmul_rn(e.g, sp.g1.y);
     return q <= sp.g1.z && !(e.alpha < cutoff);
+}
+
+// eval_splat_bf for two pixels of one column (x, y0) and (x, y1) on packed f32x2
+// arithmetic: each half of FFMA2 / FMUL2 / FADD2 rounds exactly like the scalar op, so
+// both results are bit-identical to eval_splat_bf (the backward recomputes them that way).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void unpk2(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long fma2rn(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long mul2rn(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ void eval_splat_bf2(const SplatSh& sp, float x, float y0, float y1, float cutoff,
+                                               SplatEval& e0, SplatEval& e1, bool& c0, bool& c1) {
+    const float dx = __fsub_rn(sp.g0.x, x);
+    const float dy0 = __fsub_rn(sp.g0.y, y0), dy1 = __fsub_rn(sp.g0.y, y1);
+    const unsigned long long DX = pk2(dx, dx), DY = pk2(dy0, dy1);
+    const unsigned long long qd0 = fma2rn(pk2(sp.g0.z, sp.g0.z), DX, mul2rn(pk2(sp.g0.w, sp.g0.w), DY));
+    const unsigned long long qd1 = fma2rn(pk2(sp.g0.w, sp.g0.w), DX, mul2rn(pk2(sp.g1.x, sp.g1.x), DY));
+    const unsigned long long q = fma2rn(DX, qd0, mul2rn(DY, qd1));
+    float q0, q1;
+    unpk2(q, q0, q1);
+    e0.dx = e1.dx = dx;
+    e0.dy = dy0;
+    e1.dy = dy1;
+    unpk2(qd0, e0.qd0, e1.qd0);
+    unpk2(qd1, e0.qd1, e1.qd1);
+    e0.g = exp_neg_half(q0);
+    e1.g = exp_neg_half(q1);
+    e0.alpha = __fmul_rn(e0.g, sp.g1.y);
+    e1.alpha = __fmul_rn(e1.g, sp.g1.y);
+    c0 = q0 <= sp.g1.z && !(e0.alpha < cutoff);
+    c1 = q1 <= sp.g1.z && !(e1.alpha < cutoff);
 }
 
 // T <- T * (1 - alpha), C <- C + T * alpha * c (rasterizer.hpp:287-288).
