@@ -11,7 +11,8 @@ from paper_2501_13975_b200.workload import CONFIGS, cameras_for, make_scenes  # 
 
 libs = [capi.NgsLibrary(p) for p in sys.argv[1:3]]
 ok = True
-for name, (w, h) in (("c2", (800, 800)), ("c2", (801, 603)), ("c2", (962, 540)), ("c1", (256, 256))):
+for name, (w, h) in (("c2", (800, 800)), ("c2", (801, 603)), ("c2", (962, 540)), ("c1", (256, 256)),
+                     ("c2", (200, 200))):
     cfg = CONFIGS[name]
     truth, init = make_scenes(cfg)
     cam = cameras_for(cfg)[0]
