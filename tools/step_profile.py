@@ -41,7 +41,7 @@ p = ctx.profile_read()
 print(f"{cfg.name}: serialised steps {np.mean(dts):.3f} ms; stage ms/step",
       {k: round(v / steps, 3) for k, v in p["ms"].items()}, "pairs", [x / steps for x in p["contrib_pairs"]],
       "raster pairs", p["raster_pairs"] / steps)
-if p.get("color_channels"):
+if p.get("color_channels") and os.environ.get("NGS_COLOR_FUSED", "0") != "0":  # fused colour solve only
     print(f"{cfg.name}: colour channel solves on the fast path {p['color_fast_channels'] / p['color_channels']:.4f}")
 ctx.profile_enable(False)
 dts = [ctx.trainer_step(order[(10 + i) % len(order)]).dt_ms for i in range(steps)]
