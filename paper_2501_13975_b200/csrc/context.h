@@ -61,6 +61,8 @@ inline void apply_shard(const ShardRows& r, RasterParams& rp) {
 // Views with fewer 16x16 tiles than this render with 8x8 tiles: their per-tile
 // lists are deep (secondaries at 1/4 resolution) and 16x16 leaves the GPU idle.
 constexpr int kSmallViewTiles = 4 * 148;
+// Secondary views: 8x8 tiles only below this many 16x16 tiles (tile_for).
+constexpr int kTinyViewTiles = 64;
 
 struct LossParams {
     double lambda, c1, c2;
