@@ -179,7 +179,7 @@ struct ngs_context {
     int tile_policy = 0;  // 0 auto (8x8 tiles for small views), else forced 8 or 16
     int bwd_chunks = 0;   // list chunks per 8x8 tile in the trainer's backward (0: auto, 1: whole lists)
     int sm_count = 148;
-    bool render_priority = true;  // render_step_views: primary render first when N <= its pixels (NGS_RENDER_PRIORITY=0: off)
+    int render_priority = 1;  // render_step_views: primary render first when N <= its pixels (NGS_RENDER_PRIORITY=0: off, 2: always)
     bool color_fused = false;  // one-launch colour solve with the no-repair fast path (NGS_COLOR_FUSED=1)
     unsigned long long contrib_pairs_total = 0;
     // Bumped whenever the positions may change (set_scene, position commits, snapshot
@@ -602,7 +602,7 @@ int32_t ngs_context_create(int32_t device, ngs_context** out) {
         if (const char* e = getenv("NGS_TILE_POLICY")) ctx->tile_policy = atoi(e);      // experiments only
         CUDA_CHECK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device));
         if (const char* e = getenv("NGS_COLOR_FUSED")) ctx->color_fused = atoi(e) != 0;  // A/B
-        if (const char* e = getenv("NGS_RENDER_PRIORITY")) ctx->render_priority = atoi(e) != 0;  // A/B
+        if (const char* e = getenv("NGS_RENDER_PRIORITY")) ctx->render_priority = atoi(e);  // A/B
         if (const char* e = getenv("NGS_BWD_CHUNKS")) ctx->bwd_chunks = std::max(0, std::min(64, atoi(e)));  // A/B
         if (const char* e = getenv("NGS_ORDER_REUSE")) ctx->order_reuse = atoi(e) != 0;  // tests only
         if (const char* e = getenv("NGS_BATCH_SECONDARIES")) ctx->batch_secondaries = atoi(e) != 0;  // A/B only
@@ -1418,9 +1418,10 @@ void render_step_views(ngs_context* ctx, int view_id, const std::vector<int>& nb
     // chain (whose backward ends the pass) goes first: c2 9.52 -> 9.39 ms. With more Gaussians
     // than primary pixels (c3: 3M vs 2.1M) the secondaries' depth sorts are as long as the
     // primary's, and ranking them lower leaves their backward as the pass's tail (c3 +2 %).
-    const bool primary_prio = ctx->stream_policy == 0 && ctx->render_priority &&
-                              static_cast<int64_t>(ctx->scene.n) <= static_cast<int64_t>(T.views[0].cam.width) *
-                                                                        T.views[0].cam.height;
+    const bool primary_prio = ctx->stream_policy == 0 && ctx->render_priority != 0 &&
+                              (ctx->render_priority == 2 ||  // forced (A/B)
+                               static_cast<int64_t>(ctx->scene.n) <= static_cast<int64_t>(T.views[0].cam.width) *
+                                                                         T.views[0].cam.height);
     auto& vr = primary_prio ? ctx->vrp : ctx->vr;
     if (concurrent) ctx->fork(nv, vr.data());
     auto sync_of = [&](int i) {
